@@ -1,0 +1,170 @@
+/*
+ * hd.h — C-ABI of the B200-native Householder Dice (HD) hot path.
+ *
+ * Drop-in boundary for the reference's probe-operator interface
+ * (/root/reference/proj/include/lazymat/operators.hpp:29-49) and its
+ * callers. Plain pointers and sizes only; no C++, Eigen or torch types.
+ * Every entry point names the reference interface it replaces.
+ *
+ * Error model (types.hpp:32-43, 67-69; dynamics.hpp:50-51,65-66): every
+ * function returns an hd_status; on failure hd_last_error() returns the
+ * reference's message text (thread-local). HD_ERR_INVALID_ARGUMENT maps
+ * std::invalid_argument (Python ValueError), HD_ERR_BUDGET_EXHAUSTED maps
+ * BudgetExhausted, HD_ERR_RESOURCE_CAP maps ResourceCapExceeded,
+ * HD_ERR_RUNTIME maps std::runtime_error (non-finite iterate). A failed
+ * probe leaves the operator state untouched, like the reference.
+ *
+ * Threading: one handle per thread, no internal locking (
+ * parallel.hpp:13-16). Determinism: the same config (seed, stream, draw
+ * mode) and inputs give bit-identical outputs on the same GPU model.
+ */
+#ifndef HD_B200_H_
+#define HD_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum hd_status {
+  HD_OK = 0,
+  HD_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument (types.hpp:67-69) */
+  HD_ERR_BUDGET_EXHAUSTED = 2, /* BudgetExhausted (types.hpp:32-35)       */
+  HD_ERR_RESOURCE_CAP = 3,     /* ResourceCapExceeded (types.hpp:39-43)   */
+  HD_ERR_RUNTIME = 4,          /* std::runtime_error (dynamics.hpp:65-66) */
+  HD_ERR_CUDA = 5,
+  HD_ERR_NCCL = 6
+} hd_status;
+
+typedef enum hd_ensemble { HD_GINIBRE = 0, HD_HAAR = 1, HD_GOE = 2 } hd_ensemble;
+typedef enum hd_side { HD_RIGHT = 0, HD_LEFT = 1 } hd_side; /* types.hpp:26 */
+typedef enum hd_dtype { HD_F64 = 0, HD_F32 = 1 } hd_dtype;
+/* Gaussian draws: device Philox4x32-10 keyed by (seed, stream) with counter
+ * (row, probe) — production; or the caller injects them in probe order
+ * (parity mode: e.g. the reference RandomSource(seed).normals(len) stream). */
+typedef enum hd_draw_mode { HD_DRAWS_PHILOX = 0, HD_DRAWS_INJECTED = 1 } hd_draw_mode;
+/* reflect.hpp:33 SignRule; FaultFlags operators.hpp:16-22 */
+typedef enum hd_sign_rule {
+  HD_SIGN_STABLE = 0,
+  HD_SIGN_NEGATIVE_AT_ZERO = 1,
+  HD_SIGN_ZERO_WHEN_NEGATIVE = 2
+} hd_sign_rule;
+
+typedef struct hd_config {
+  int32_t ensemble;      /* hd_ensemble                                      */
+  int32_t dtype;         /* hd_dtype (storage + streaming precision)        */
+  int64_t m, n;          /* Ginibre: m x n; Haar/GOE: n x n (m ignored)      */
+  double sigma;          /* Ginibre entry std (ginibre.hpp:31); GOE inner σ  */
+  uint64_t seed;         /* RandomSource(seed, stream) (random.hpp:130)      */
+  uint64_t stream;
+  int64_t capacity;      /* max probes this handle will serve (panel width);
+                            0 = the full budget min(m,n) / n / floor(n/2)    */
+  int32_t draw_mode;     /* hd_draw_mode                                     */
+  int32_t skip_reflector;/* FaultFlags::skip_reflector                       */
+  int32_t sign_rule;     /* FaultFlags::sign_rule                            */
+  int32_t device;        /* CUDA device ordinal                              */
+} hd_config;
+
+typedef struct hd_op hd_op;
+
+/* Replaces the constructors GinibreOperator(m, n, sigma, RandomSource, faults)
+ * (ginibre.hpp:31-42), HaarOperator(n, RandomSource, faults) (haar.hpp:24-31),
+ * GOEOperator(n, RandomSource, faults) / GOEOperator(unique_ptr<Ginibre>)
+ * (ensembles.hpp:100-109) and the bindings (module.cpp:68-111). */
+int hd_create(const hd_config* cfg, hd_op** out);
+int hd_destroy(hd_op* op);
+
+/* ProbeOperator::rows/cols/remaining_probes (operators.hpp:33-40). */
+int hd_shape(const hd_op* op, int64_t* rows, int64_t* cols);
+int hd_remaining(const hd_op* op, int64_t* remaining);
+/* GinibreOperator::probe_counts (ginibre.hpp:53) / HaarOperator::probe_count
+ * (haar.hpp:37; returned as right = t, left = 0) and chain sizes. */
+int hd_counts(const hd_op* op, int64_t* right, int64_t* left);
+int hd_chain_sizes(const hd_op* op, int64_t* right_chain, int64_t* left_chain);
+
+/* ProbeOperator::probe(x, side) (operators.hpp:41): y = Q x (right) or
+ * Q^T x (left). x/y are host pointers (on_device = 0) or device pointers of
+ * the operator's dtype (on_device = 1). Validation order follows
+ * check_probe_input then the budget check (operators.hpp:44-48,
+ * ginibre.hpp:59-62). Synchronous: returns after y is written. `stream` is a
+ * cudaStream_t or NULL for the handle's own stream. */
+int hd_probe(hd_op* op, const void* x, int64_t x_len, void* y, int64_t y_len, int32_t side, int32_t on_device,
+             void* stream);
+
+/* Parity mode: append caller-supplied N(0,1) draws (fp64) to the handle's
+ * draw queue; each probe consumes one vector of its draw length (Ginibre
+ * right: m, left: n; Haar: n; GOE: n per inner probe). */
+int hd_push_draws(hd_op* op, const double* g, int64_t len, int32_t on_device);
+
+/* Reset to the freshly constructed state (counters, chains, queue). */
+int hd_reset(hd_op* op);
+
+/* ---------------------------------------------------------------------------
+ * Device-resident dynamics (replaces run_dynamics, dynamics.hpp:42-76, for the
+ * built-in update maps of the BASELINE configs). */
+typedef enum hd_update {
+  HD_UPDATE_IDENTITY = 0,  /* x_{t+1} = y_t                                   */
+  HD_UPDATE_NORMALIZE = 1, /* x_{t+1} = y_t / ||y_t|| (bench.cpp:25-28)       */
+  HD_UPDATE_TANH_MIX = 2   /* x_{t+1} = tanh(2 y_t) + 0.1 x_{t-1} (depth 1)   */
+} hd_update;
+
+typedef enum hd_side_rule {
+  HD_SIDES_ALTERNATE = 0, /* right on odd t, left on even t (bench.cpp:22-24) */
+  HD_SIDES_RIGHT = 1,
+  HD_SIDES_LEFT = 2
+} hd_side_rule;
+
+typedef struct hd_run_args {
+  int32_t update;      /* hd_update                                          */
+  int32_t side_rule;   /* hd_side_rule                                       */
+  int64_t iterations;  /* T                                                  */
+  const void* x1;      /* newest initial iterate                             */
+  const void* x0;      /* older iterate for depth-1 maps (NULL = zeros)      */
+  int32_t on_device;   /* pointers are device pointers of the op's dtype     */
+  int32_t use_graph;   /* capture the T-step launch sequence in a CUDA graph */
+  void* traj;          /* optional (T+1) x dim iterates x_1..x_{T+1}         */
+  void* final_out;     /* optional x_{T+1}                                   */
+  void* stream;        /* cudaStream_t or NULL                               */
+} hd_run_args;
+
+/* run_dynamics(op, spec): validation messages and the non-finite abort
+ * ("run_dynamics: non-finite iterate at step N") follow dynamics.hpp:44-67. */
+int hd_run(hd_op* op, const hd_run_args* args);
+
+/* User update map on device memory: called once per step after the probe
+ * with y_t and the history window newest first (device pointers of the op's
+ * dtype, each dim elements); must write x_{t+1} into `next` on `stream`.
+ * Return non-zero to abort. (DynamicsSpec::update, dynamics.hpp:21-32.) */
+typedef int (*hd_update_fn)(void* user, int64_t t, const void* y, const void* const* history, int32_t depth,
+                            void* next, int64_t dim, void* stream);
+typedef int32_t (*hd_side_fn)(void* user, int64_t t);
+
+int hd_run_callback(hd_op* op, int64_t iterations, int32_t depth, const void* const* initial_dev,
+                    hd_side_fn side_of, hd_update_fn update, void* user, void* final_out_dev);
+
+/* ---------------------------------------------------------------------------
+ * Instrumentation: per-kernel-kind launch counts, device time (CUDA events
+ * on the handle's stream) and algorithmic bytes. Off by default. */
+typedef struct hd_kernel_stats {
+  char name[32];
+  int64_t launches;
+  double ms;
+  double alg_bytes;
+} hd_kernel_stats;
+
+int hd_set_profiling(hd_op* op, int32_t enabled);
+int hd_get_stats(hd_op* op, hd_kernel_stats* out, int32_t max, int32_t* count);
+int hd_reset_stats(hd_op* op);
+/* Number of kernels this library launched on behalf of the handle. */
+int hd_launch_count(const hd_op* op, int64_t* count);
+
+const char* hd_last_error(void);
+const char* hd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HD_B200_H_ */

@@ -1,0 +1,121 @@
+"""ctypes binding of the C-ABI in include/hd.h (libhd_b200.so, built in-tree).
+
+This is the only way the Python layer reaches the device path: there is no
+CPU fallback. If the shared library is missing the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libhd_b200.so")
+
+HD_OK = 0
+HD_ERR_INVALID_ARGUMENT = 1
+HD_ERR_BUDGET_EXHAUSTED = 2
+HD_ERR_RESOURCE_CAP = 3
+HD_ERR_RUNTIME = 4
+HD_ERR_CUDA = 5
+HD_ERR_NCCL = 6
+
+HD_GINIBRE, HD_HAAR, HD_GOE = 0, 1, 2
+HD_RIGHT, HD_LEFT = 0, 1
+HD_F64, HD_F32 = 0, 1
+HD_DRAWS_PHILOX, HD_DRAWS_INJECTED = 0, 1
+SIGN_RULES = {"stable": 0, "negative_at_zero": 1, "zero_when_negative": 2}
+UPDATES = {"identity": 0, "normalize": 1, "tanh_mix": 2}
+SIDE_RULES = {"alternate": 0, "right": 1, "left": 2}
+
+# Every symbol include/hd.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "hd_create", "hd_destroy", "hd_shape", "hd_remaining", "hd_counts", "hd_chain_sizes", "hd_probe",
+    "hd_push_draws", "hd_reset", "hd_run", "hd_run_callback", "hd_set_profiling", "hd_get_stats",
+    "hd_reset_stats", "hd_launch_count", "hd_last_error", "hd_version",
+)
+
+
+class hd_config(C.Structure):
+    _fields_ = [
+        ("ensemble", C.c_int32), ("dtype", C.c_int32), ("m", C.c_int64), ("n", C.c_int64),
+        ("sigma", C.c_double), ("seed", C.c_uint64), ("stream", C.c_uint64), ("capacity", C.c_int64),
+        ("draw_mode", C.c_int32), ("skip_reflector", C.c_int32), ("sign_rule", C.c_int32),
+        ("device", C.c_int32),
+    ]
+
+
+class hd_run_args(C.Structure):
+    _fields_ = [
+        ("update", C.c_int32), ("side_rule", C.c_int32), ("iterations", C.c_int64), ("x1", C.c_void_p),
+        ("x0", C.c_void_p), ("on_device", C.c_int32), ("use_graph", C.c_int32), ("traj", C.c_void_p),
+        ("final_out", C.c_void_p), ("stream", C.c_void_p),
+    ]
+
+
+class hd_kernel_stats(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("ms", C.c_double), ("alg_bytes", C.c_double)]
+
+
+UPDATE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(C.c_void_p), C.c_int32, C.c_void_p,
+                        C.c_int64, C.c_void_p)
+SIDE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_int64)
+
+_lib = None
+
+
+class BudgetExhausted(RuntimeError):
+    """types.hpp:32-35 (registered by module.cpp:42)."""
+
+
+class ResourceCapExceeded(RuntimeError):
+    """types.hpp:39-43 (registered by module.cpp:43)."""
+
+
+class HDCudaError(RuntimeError):
+    pass
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"libhd_b200.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+        L.hd_last_error.restype = C.c_char_p
+        L.hd_version.restype = C.c_char_p
+        L.hd_create.argtypes = [C.POINTER(hd_config), C.POINTER(vp)]
+        L.hd_destroy.argtypes = [vp]
+        L.hd_shape.argtypes = [vp, C.POINTER(i64), C.POINTER(i64)]
+        L.hd_remaining.argtypes = [vp, C.POINTER(i64)]
+        L.hd_counts.argtypes = [vp, C.POINTER(i64), C.POINTER(i64)]
+        L.hd_chain_sizes.argtypes = [vp, C.POINTER(i64), C.POINTER(i64)]
+        L.hd_probe.argtypes = [vp, vp, i64, vp, i64, i32, i32, vp]
+        L.hd_push_draws.argtypes = [vp, vp, i64, i32]
+        L.hd_reset.argtypes = [vp]
+        L.hd_run.argtypes = [vp, C.POINTER(hd_run_args)]
+        L.hd_run_callback.argtypes = [vp, i64, i32, C.POINTER(vp), SIDE_FN, UPDATE_FN, vp, vp]
+        L.hd_set_profiling.argtypes = [vp, i32]
+        L.hd_get_stats.argtypes = [vp, C.POINTER(hd_kernel_stats), i32, C.POINTER(i32)]
+        L.hd_reset_stats.argtypes = [vp]
+        L.hd_launch_count.argtypes = [vp, C.POINTER(i64)]
+        for name in EXPORTS:
+            if name not in ("hd_last_error", "hd_version"):
+                getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == HD_OK:
+        return
+    msg = lib().hd_last_error().decode()
+    if rc == HD_ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if rc == HD_ERR_BUDGET_EXHAUSTED:
+        raise BudgetExhausted(msg)
+    if rc == HD_ERR_RESOURCE_CAP:
+        raise ResourceCapExceeded(msg)
+    if rc == HD_ERR_CUDA:
+        raise HDCudaError(msg)
+    raise RuntimeError(msg)

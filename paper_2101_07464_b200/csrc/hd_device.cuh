@@ -1,0 +1,188 @@
+// Device-side building blocks of the Householder Dice hot path on sm_100a.
+//
+// Data layout: every reflector chain, and the Ginibre basis
+// stores, live in HBM as tall-skinny panels in TILE-MAJOR order
+//   element (row i, column j) -> P[(i / 256) * (K * 256) + j * 256 + (i % 256)]
+// so the j used columns of a 256-row tile are one contiguous j*2 KB block
+// (fp64) and appending a column writes 2 KB contiguous per tile. K is the
+// column capacity fixed at operator creation (hd_config.capacity).
+//
+// Column j of a chain panel holds the Householder vector up to an exact
+// power-of-two / per-column scale: w_j = sig[j] * P[:, j], where w_j is the
+// reference's normalised reflection vector (reflect.hpp:168-174).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hd {
+
+constexpr int kTile = 256;       // panel tile height (rows)
+constexpr int kTileShift = 8;
+
+__host__ __device__ __forceinline__ size_t paddr(int64_t i, int64_t j, int64_t K) {
+  return (size_t)(i >> kTileShift) * (size_t)(K << kTileShift) + (size_t)(j << kTileShift) + (size_t)(i & (kTile - 1));
+}
+
+// ------------------------------------------------------------ Philox4x32-10
+// Counter-based generator (Salmon et al., SC'11). Keyed by the operator seed;
+// counter = (row-pair index lo/hi, probe index, stream) so any row of any
+// probe's draw can be regenerated independently, in any kernel, any number
+// of times (generated twice per Ginibre probe instead of stored).
+struct Philox {
+  uint32_t k0, k1;
+};
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+  constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
+    const uint32_t hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    k0 += W0;
+    k1 += W1;
+  }
+  return c;
+}
+
+// Two N(0,1) draws for rows (2q, 2q+1) of probe `probe` (Box-Muller on two
+// 53-bit uniforms, computed in fp64 for every dtype).
+__device__ __forceinline__ double2 philox_normal_pair(uint64_t seed, uint32_t stream, uint32_t probe, uint64_t q) {
+  const uint4 w = philox4x32_10(make_uint4((uint32_t)q, (uint32_t)(q >> 32), probe, stream), (uint32_t)seed,
+                                (uint32_t)(seed >> 32));
+  const uint64_t a = ((uint64_t)w.x << 32) | w.y;
+  const uint64_t b = ((uint64_t)w.z << 32) | w.w;
+  const double u1 = ((double)(a >> 11) + 1.0) * 0x1.0p-53;  // (0, 1]
+  const double u2 = (double)(b >> 11) * 0x1.0p-53;          // [0, 1)
+  const double r = sqrt(-2.0 * log(u1));
+  double s, c;
+  sincospi(2.0 * u2, &s, &c);
+  return make_double2(r * c, r * s);
+}
+
+// ------------------------------------------------------------ vector source
+// Where a streamed right-hand side comes from: a dense device vector (the
+// iterate, optionally times a device scalar), fresh Philox normals, or draws
+// injected by the caller (parity mode). Rows < mask_begin read as zero
+// (ginibre.hpp:73 `g.head(l).setZero()`, and the Haar tail restriction); the
+// optional D factor is the chain's cumulative-sign diagonal.
+enum SrcKind : int { kSrcNone = 0, kSrcVec = 1, kSrcPhilox = 2, kSrcInjected = 3 };
+
+template <typename T>
+struct Src {
+  int kind = kSrcNone;
+  const T* x = nullptr;
+  const double* xscale = nullptr;  // device scalar or null
+  uint64_t seed = 0;
+  uint32_t stream = 0;
+  uint32_t probe = 0;
+  const double* inj = nullptr;  // this probe's injected draws (length n)
+  int64_t mask_begin = 0;
+  const double* D = nullptr;    // D(i) = i < Dlen ? D[i] : *Dtail
+  const double* Dtail = nullptr;
+  int64_t Dlen = 0;
+};
+
+template <typename T>
+__device__ __forceinline__ double dvalue(const Src<T>& s, int64_t i) {
+  if (s.D == nullptr) return 1.0;
+  return i < s.Dlen ? s.D[i] : *s.Dtail;
+}
+
+// Values of rows (i, i+1), i even; rows >= n read as zero.
+template <typename T>
+__device__ __forceinline__ double2 src_pair(const Src<T>& s, int64_t i, int64_t n) {
+  double2 v = make_double2(0.0, 0.0);
+  if (s.kind == kSrcVec) {
+    if (i + 1 < n) {
+      if constexpr (sizeof(T) == 8) {
+        v = *reinterpret_cast<const double2*>(s.x + i);
+      } else {
+        const float2 f = *reinterpret_cast<const float2*>(s.x + i);
+        v = make_double2(f.x, f.y);
+      }
+    } else if (i < n) {
+      v.x = (double)s.x[i];
+    }
+    if (s.xscale) {
+      const double sc = *s.xscale;
+      v.x *= sc;
+      v.y *= sc;
+    }
+  } else if (s.kind == kSrcPhilox) {
+    if (i < n) {
+      v = philox_normal_pair(s.seed, s.stream, s.probe, (uint64_t)(i >> 1));
+      if constexpr (sizeof(T) == 4) {  // fp32 path consumes fp32-rounded draws
+        v.x = (double)(float)v.x;
+        v.y = (double)(float)v.y;
+      }
+      if (i + 1 >= n) v.y = 0.0;
+    }
+  } else if (s.kind == kSrcInjected) {
+    if (i < n) v.x = s.inj[i];
+    if (i + 1 < n) v.y = s.inj[i + 1];
+    if constexpr (sizeof(T) == 4) {
+      v.x = (double)(float)v.x;
+      v.y = (double)(float)v.y;
+    }
+  }
+  if (i < s.mask_begin) v.x = 0.0;
+  if (i + 1 < s.mask_begin) v.y = 0.0;
+  if (s.D) {
+    v.x *= dvalue(s, i);
+    v.y *= dvalue(s, i + 1);
+  }
+  return v;
+}
+
+// Load two consecutive panel entries as doubles.
+template <typename T>
+__device__ __forceinline__ double2 ld_pair(const T* p) {
+  if constexpr (sizeof(T) == 8) {
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+  } else {
+    float2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "l"(p));
+    return make_double2(r.x, r.y);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void st_pair(T* p, double a, double b) {
+  if constexpr (sizeof(T) == 8) {
+    *reinterpret_cast<double2*>(p) = make_double2(a, b);
+  } else {
+    *reinterpret_cast<float2*>(p) = make_float2((float)a, (float)b);
+  }
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block sum (fixed tree); result valid in all threads.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (w == 0) {
+    t = (l < NT / 32) ? sh[l] : 0.0;
+    t = warp_sum(t);
+    if (l == 0) sh[0] = t;
+  }
+  __syncthreads();
+  t = sh[0];
+  __syncthreads();
+  return t;
+}
+
+}  // namespace hd

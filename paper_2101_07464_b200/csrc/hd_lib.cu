@@ -1,0 +1,1482 @@
+// Host side of the B200 Householder Dice library: operator state, the
+// per-probe launch sequences, device dynamics, CUDA-graph
+// replay, instrumentation and the C-ABI declared in include/hd.h.
+//
+// Reference semantics restated here (file:line into /root/reference/proj):
+//   GinibreOperator::probe   include/lazymat/ginibre.hpp:58-106
+//   HaarOperator::probe      include/lazymat/haar.hpp:40-67
+//   GOEOperator::probe       include/lazymat/ensembles.hpp:117-127
+//   run_dynamics             include/lazymat/dynamics.hpp:42-76
+//   check_probe_input        include/lazymat/operators.hpp:44-48
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hd.h"
+#include "hd_kernels.cuh"
+
+using namespace hd;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct HdError : std::runtime_error {
+  int code;
+  HdError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void require(bool cond, const std::string& msg) {
+  if (!cond) throw HdError(HD_ERR_INVALID_ARGUMENT, msg);
+}
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw HdError(HD_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+template <typename P>
+P* dmalloc(size_t count) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  ck(cudaMalloc(&p, count * sizeof(P)), "cudaMalloc");
+  return static_cast<P*>(p);
+}
+
+// ----------------------------------------------------------------- chains
+struct Panel {
+  void* P = nullptr;  // tile-major, dtype bytes esz
+  int64_t K = 0;      // column capacity
+  int64_t count = 0;  // columns in use
+};
+
+struct Chain {
+  Panel pan;
+  int pend = -1;  // column whose Gram/T column is not yet known
+  ChainDev dev;   // K-sized small state
+};
+
+struct KStat {
+  int64_t launches = 0;
+  double ms = 0.0;
+  double bytes = 0.0;
+};
+
+struct PendingEv {
+  cudaEvent_t a, b;
+  std::string kind;
+};
+
+// host-side counters, snapshotted per step so a failed probe / aborted run
+// can restore the exact reference state (operators.hpp:44-48: a failed probe
+// leaves the operator untouched)
+struct Counters {
+  int64_t r = 0, l = 0, t = 0;  // Ginibre right/left; Haar probes
+  int64_t rc_count = 0, lc_count = 0, u_count = 0, v_count = 0;
+  int rc_pend = -1, lc_pend = -1;
+  uint32_t probe_index = 0;
+  int64_t inj_pos = 0;
+};
+
+}  // namespace
+
+struct hd_op {
+  hd_config cfg{};
+  int ens = 0;
+  bool f32 = false;
+  size_t esz = 8;
+  int64_t m = 0, n = 0;  // inner Ginibre m x n (Haar/GOE: n x n)
+  int64_t rows_pad_m = 0, rows_pad_n = 0;
+  int64_t budget = 0;    // inner probes
+  Chain R, L;            // right chain (dim n), left chain (dim m)
+  Panel U, V;            // Ginibre basis stores: U (m) right probes, V (n) left probes
+  Counters c;
+  // scratch
+  double* partials = nullptr;
+  size_t partials_cap = 0;
+  double* partials2 = nullptr;  // per-tile partials of update kernels
+  double* red = nullptr;
+  size_t red_cap = 0;
+  double* scal = nullptr;
+  int* status = nullptr;
+  double *beta1 = nullptr, *beta3 = nullptr, *tmp = nullptr, *tmp2 = nullptr, *coefS = nullptr;
+  double *head = nullptr, *zbuf = nullptr, *csp = nullptr;
+  int64_t small_cap = 0;  // length of the K-sized scratch above
+  void* xbuf = nullptr;   // dtype, rows_pad(max)
+  void* ybuf[3] = {nullptr, nullptr, nullptr};
+  void* gtmp = nullptr;   // GOE right-probe partial output
+  int64_t io_len = 0;
+  double* inj = nullptr;
+  int64_t inj_cap = 0, inj_size = 0;
+  cudaStream_t stream = nullptr;
+  int nsm = 148;
+  std::map<int, int> dots_bps;  // smem bytes -> blocks/SM
+  // graph cache (hd_run from a fresh state)
+  cudaGraphExec_t graph = nullptr;
+  std::string graph_key;
+  std::vector<Counters> graph_snaps;  // per-step host state recorded at capture
+  int64_t graph_launches = 0;         // kernels inside the captured graph
+  // instrumentation
+  bool prof = false;
+  std::map<std::string, KStat> stats;
+  std::vector<PendingEv> evq;
+  std::vector<cudaEvent_t> evpool;
+  int64_t launches = 0;
+};
+
+namespace {
+
+// ============================================================ allocation
+void alloc_chain(hd_op* op, Chain& ch, int64_t rows_pad, int64_t K) {
+  ch.pan.K = K;
+  ch.pan.count = 0;
+  ch.pend = -1;
+  ch.pan.P = dmalloc<unsigned char>((size_t)rows_pad * K * op->esz);
+  ck(cudaMemsetAsync(ch.pan.P, 0, (size_t)rows_pad * K * op->esz, op->stream), "memset panel");
+  ch.dev.K = K;
+  ch.dev.Dlen = K;
+  ch.dev.sig = dmalloc<double>(K);
+  ch.dev.c = dmalloc<double>(K);
+  ch.dev.s = dmalloc<double>(K);
+  ch.dev.G = dmalloc<double>((size_t)K * K);
+  ch.dev.Tm = dmalloc<double>((size_t)K * K);
+  ch.dev.Drow = dmalloc<double>(K);
+  ch.dev.Dtail = dmalloc<double>(1);
+  ck(cudaMemsetAsync(ch.dev.G, 0, sizeof(double) * K * K, op->stream), "memset");
+  ck(cudaMemsetAsync(ch.dev.Tm, 0, sizeof(double) * K * K, op->stream), "memset");
+}
+
+void free_chain(Chain& ch) {
+  cudaFree(ch.pan.P);
+  cudaFree(ch.dev.sig);
+  cudaFree(ch.dev.c);
+  cudaFree(ch.dev.s);
+  cudaFree(ch.dev.G);
+  cudaFree(ch.dev.Tm);
+  cudaFree(ch.dev.Drow);
+  cudaFree(ch.dev.Dtail);
+  ch = Chain{};
+}
+
+void alloc_store(hd_op* op, Panel& p, int64_t rows_pad, int64_t K) {
+  p.K = K;
+  p.count = 0;
+  p.P = dmalloc<unsigned char>((size_t)rows_pad * K * op->esz);
+  ck(cudaMemsetAsync(p.P, 0, (size_t)rows_pad * K * op->esz, op->stream), "memset store");
+}
+
+__global__ void k_fill(double* p, int64_t n, const double* v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = *v;
+}
+
+// Grow a panel's column capacity (tile-major re-layout via pitched copy).
+void grow_panel(hd_op* op, Panel& p, int64_t rows_pad, int64_t Knew) {
+  void* np = dmalloc<unsigned char>((size_t)rows_pad * Knew * op->esz);
+  ck(cudaMemsetAsync(np, 0, (size_t)rows_pad * Knew * op->esz, op->stream), "memset");
+  const int64_t ntiles = rows_pad / kTile;
+  if (p.count > 0)
+    ck(cudaMemcpy2DAsync(np, (size_t)Knew * kTile * op->esz, p.P, (size_t)p.K * kTile * op->esz,
+                         (size_t)p.count * kTile * op->esz, (size_t)ntiles, cudaMemcpyDeviceToDevice, op->stream),
+       "grow copy");
+  ck(cudaStreamSynchronize(op->stream), "sync");
+  cudaFree(p.P);
+  p.P = np;
+  p.K = Knew;
+}
+
+void grow_chain(hd_op* op, Chain& ch, int64_t rows_pad, int64_t Knew) {
+  const int64_t Kold = ch.pan.K;
+  grow_panel(op, ch.pan, rows_pad, Knew);
+  auto grow_vec = [&](double*& v) {
+    double* nv = dmalloc<double>(Knew);
+    ck(cudaMemcpyAsync(nv, v, sizeof(double) * Kold, cudaMemcpyDeviceToDevice, op->stream), "grow");
+    ck(cudaStreamSynchronize(op->stream), "sync");
+    cudaFree(v);
+    v = nv;
+  };
+  auto grow_mat = [&](double*& M) {
+    double* nm = dmalloc<double>((size_t)Knew * Knew);
+    ck(cudaMemsetAsync(nm, 0, sizeof(double) * Knew * Knew, op->stream), "memset");
+    ck(cudaMemcpy2DAsync(nm, sizeof(double) * Knew, M, sizeof(double) * Kold, sizeof(double) * Kold, Kold,
+                         cudaMemcpyDeviceToDevice, op->stream),
+       "grow mat");
+    ck(cudaStreamSynchronize(op->stream), "sync");
+    cudaFree(M);
+    M = nm;
+  };
+  grow_vec(ch.dev.sig);
+  grow_vec(ch.dev.c);
+  grow_vec(ch.dev.s);
+  grow_vec(ch.dev.Drow);
+  grow_mat(ch.dev.G);
+  grow_mat(ch.dev.Tm);
+  // rows [Kold, Knew) lie beyond every existing offset: D = Dtail there
+  k_fill<<<(unsigned)ceil_div(Knew - Kold, 256), 256, 0, op->stream>>>(ch.dev.Drow + Kold, Knew - Kold, ch.dev.Dtail);
+  ck(cudaGetLastError(), "k_fill");
+  ch.dev.K = Knew;
+  ch.dev.Dlen = Knew;
+}
+
+void ensure_small(hd_op* op, int64_t K) {
+  if (K <= op->small_cap) return;
+  for (double** p : {&op->beta1, &op->beta3, &op->tmp, &op->tmp2, &op->coefS, &op->head, &op->zbuf, &op->csp}) {
+    cudaFree(*p);
+    *p = dmalloc<double>(K + 8);
+  }
+  op->small_cap = K;
+}
+
+void ensure_red(hd_op* op, size_t nslots, size_t nblk) {
+  if (nslots * nblk > op->partials_cap) {
+    cudaFree(op->partials);
+    op->partials_cap = nslots * nblk * 2;
+    op->partials = dmalloc<double>(op->partials_cap);
+  }
+  if (nslots > op->red_cap) {
+    cudaFree(op->red);
+    op->red_cap = nslots * 2;
+    op->red = dmalloc<double>(op->red_cap);
+  }
+}
+
+// Capacity for `nr` more right and `nl` more left inner probes (Haar: both
+// chains gain one column per probe; Ginibre: R/U per right, L/V per left).
+void ensure_capacity(hd_op* op, int64_t nr, int64_t nl) {
+  auto target = [&](int64_t K, int64_t need) {
+    int64_t k = std::max<int64_t>(K, 1);
+    while (k < need) k *= 2;
+    return std::min(std::max(k, need), std::max<int64_t>(op->budget, 1));
+  };
+  int64_t total;
+  if (op->ens == HD_HAAR) {
+    total = std::min(op->c.t + nr + nl, op->budget);
+    if (op->R.pan.K < total) grow_chain(op, op->R, op->rows_pad_n, target(op->R.pan.K, total));
+    if (op->L.pan.K < total) grow_chain(op, op->L, op->rows_pad_n, target(op->L.pan.K, total));
+  } else {
+    total = std::min(op->c.r + op->c.l + nr + nl, op->budget);
+    const int64_t needR = std::min(op->c.r + nr, op->budget), needL = std::min(op->c.l + nl, op->budget);
+    if (op->R.pan.K < needR) grow_chain(op, op->R, op->rows_pad_n, target(op->R.pan.K, needR));
+    if (op->U.K < needR) grow_panel(op, op->U, op->rows_pad_m, target(op->U.K, needR));
+    if (op->L.pan.K < needL) grow_chain(op, op->L, op->rows_pad_m, target(op->L.pan.K, needL));
+    if (op->V.K < needL) grow_panel(op, op->V, op->rows_pad_n, target(op->V.K, needL));
+  }
+  const int64_t K = std::max({op->R.pan.K, op->L.pan.K, op->U.K, op->V.K});
+  ensure_small(op, std::max<int64_t>(K, total) + 1);
+}
+
+// ========================================================= instrumentation
+cudaEvent_t get_event(hd_op* op) {
+  if (!op->evpool.empty()) {
+    cudaEvent_t e = op->evpool.back();
+    op->evpool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  ck(cudaEventCreate(&e), "event");
+  return e;
+}
+
+struct LaunchScope {
+  hd_op* op;
+  cudaStream_t s;
+  const char* kind;
+  double bytes;
+  cudaEvent_t a = nullptr;
+  LaunchScope(hd_op* o, cudaStream_t st, const char* k, double b) : op(o), s(st), kind(k), bytes(b) {
+    op->launches++;
+    if (op->prof) {
+      a = get_event(op);
+      cudaEventRecord(a, s);
+    }
+  }
+  ~LaunchScope() {
+    if (op->prof) {
+      cudaEvent_t b = get_event(op);
+      cudaEventRecord(b, s);
+      op->evq.push_back({a, b, kind});
+      KStat& st = op->stats[kind];
+      st.launches++;
+      st.bytes += bytes;
+    }
+  }
+};
+
+void drain_events(hd_op* op) {
+  if (op->evq.empty()) return;
+  cudaStreamSynchronize(op->stream);
+  for (auto& e : op->evq) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    op->stats[e.kind].ms += ms;
+    op->evpool.push_back(e.a);
+    op->evpool.push_back(e.b);
+  }
+  op->evq.clear();
+}
+
+void check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw HdError(HD_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// =========================================================== launchers
+template <typename T>
+int dots_grid(hd_op* op, int smem, int64_t ntiles) {
+  auto it = op->dots_bps.find(smem);
+  int bps;
+  if (it == op->dots_bps.end()) {
+    if (smem > 48 * 1024)
+      ck(cudaFuncSetAttribute(k_dots<T, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dots<T, 8>, 256, smem), "occupancy");
+    bps = std::max(1, bps);
+    op->dots_bps[smem] = bps;
+  } else {
+    bps = it->second;
+  }
+  const int64_t want = ceil_div(ntiles, 8);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)op->nsm * bps));
+}
+
+template <typename T>
+int launch_dots(hd_op* op, cudaStream_t s, DotArgs<T>& a, double bytes) {
+  // slot layout: per job [dot: ncols][pend: pend+1][sumsq: 1]
+  int slot = 0;
+  for (int jb = 0; jb < a.njobs; ++jb) {
+    DotJob<T>& J = a.job[jb];
+    J.slot_dot = slot;
+    slot += J.ncols;
+    if (J.pend >= 0) {
+      J.slot_pend = slot;
+      slot += J.pend + 1;
+    }
+    J.slot_sumsq = slot++;
+  }
+  a.nslots = slot;
+  const int smem = 8 * a.nslots * (int)sizeof(double);
+  if (smem > 200 * 1024) throw HdError(HD_ERR_RESOURCE_CAP, "hd: chain too long for the dots kernel");
+  const int grid = dots_grid<T>(op, smem, a.ntiles);
+  ensure_red(op, a.nslots, grid);
+  a.partials = op->partials;
+  a.status = op->status;
+  {
+    LaunchScope ls(op, s, "dots", bytes);
+    k_dots<T, 8><<<grid, 256, smem, s>>>(a);
+  }
+  check_launch("k_dots");
+  return grid;
+}
+
+template <typename T>
+Src<T> vec_src(const void* x, const double* xscale) {
+  Src<T> s;
+  s.kind = kSrcVec;
+  s.x = static_cast<const T*>(x);
+  s.xscale = xscale;
+  return s;
+}
+
+// The fresh draw of the current inner probe (ginibre.hpp:67/86, haar.hpp:48).
+template <typename T>
+Src<T> draw_src(hd_op* op, int64_t len) {
+  Src<T> s;
+  if (op->cfg.draw_mode == HD_DRAWS_INJECTED) {
+    if (op->inj_size - op->c.inj_pos < len)
+      throw HdError(HD_ERR_INVALID_ARGUMENT, "hd: injected draws exhausted (push one vector per probe)");
+    s.kind = kSrcInjected;
+    s.inj = op->inj + op->c.inj_pos;
+    op->c.inj_pos += len;
+  } else {
+    s.kind = kSrcPhilox;
+    s.seed = op->cfg.seed;
+    s.stream = (uint32_t)op->cfg.stream;
+    s.probe = op->c.probe_index;
+  }
+  op->c.probe_index++;
+  return s;
+}
+
+double bytes_of(hd_op* op, double elems) { return elems * (double)op->esz; }
+
+// --------------------------------------------------------------- Haar
+// haar.hpp:40-67. fold = chain of the probed side, other = the opposite.
+template <typename T>
+void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cudaStream_t s) {
+  const int64_t n = op->n;
+  const int64_t ntiles = op->rows_pad_n / kTile;
+  const bool first = (op->c.t == 0);
+  op->c.t += 1;
+  const int64_t off = op->c.t - 1;
+  Chain& F = (side == HD_RIGHT) ? op->R : op->L;
+  Chain& O = (side == HD_RIGHT) ? op->L : op->R;
+  const bool append_fold = !(op->cfg.skip_reflector && first);
+  Src<T> g = draw_src<T>(op, n);
+  g.mask_begin = off;
+
+  // K1: a = P_F^T x, P_O^T g[off:], pending Gram columns, ||x||^2, ||g_tail||^2
+  DotArgs<T> da;
+  da.njobs = 2;
+  da.n = n;
+  da.ntiles = ntiles;
+  da.job[0].P = static_cast<const T*>(F.pan.P);
+  da.job[0].K = F.pan.K;
+  da.job[0].ncols = (int)F.pan.count;
+  da.job[0].pend = F.pend;
+  da.job[0].rhs = xsrc;
+  da.job[0].check_finite = 1;
+  da.job[1].P = static_cast<const T*>(O.pan.P);
+  da.job[1].K = O.pan.K;
+  da.job[1].ncols = (int)O.pan.count;
+  da.job[1].pend = O.pend;
+  da.job[1].rhs = g;
+  da.job[1].wcol = static_cast<T*>(O.pan.P);
+  da.job[1].wK = O.pan.K;
+  da.job[1].wj = O.pan.count;
+  da.job[1].pivot_out = op->scal + kScPivotG;
+  da.job[1].pivot_row = off;
+  const double b1 = bytes_of(op, (double)n * (F.pan.count + O.pan.count + (F.pend >= 0) + (O.pend >= 0) + 2)) +
+                    (g.kind == kSrcInjected ? 8.0 * n : 0.0);
+  const int grid = launch_dots<T>(op, s, da, b1);
+
+  SmallArgs sa;
+  sa.partials = op->partials;
+  sa.nblk = grid;
+  sa.nslots = da.nslots;
+  sa.red = op->red;
+  sa.scal = op->scal;
+  sa.status = op->status;
+  sa.chA = F.dev;
+  sa.chB = O.dev;
+  sa.PA = F.pan.P;
+  sa.PB = O.pan.P;
+  sa.kA = (int)F.pan.count;
+  sa.kB = (int)O.pan.count;
+  sa.pendA = F.pend;
+  sa.pendB = O.pend;
+  sa.slotA_dot = da.job[0].slot_dot;
+  sa.slotA_pend = da.job[0].slot_pend;
+  sa.slotA_ss = da.job[0].slot_sumsq;
+  sa.slotB_dot = da.job[1].slot_dot;
+  sa.slotB_pend = da.job[1].slot_pend;
+  sa.slotB_ss = da.job[1].slot_sumsq;
+  sa.off = off;
+  sa.rule = op->cfg.sign_rule;
+  sa.beta1 = op->beta1;
+  sa.beta3 = op->beta3;
+  sa.tmp = op->tmp;
+  sa.tmp2 = op->tmp2;
+  sa.head = op->head;
+  sa.zbuf = op->zbuf;
+  sa.csp = op->csp;
+  sa.coefS = op->coefS;
+  sa.is_haar = 1;
+  {
+    LaunchScope ls(op, s, "small_dots", 0.0);
+    k_small_dots<T><<<1, kSmallThreads, 0, s>>>(sa);
+  }
+  check_launch("k_small_dots");
+  F.pend = -1;
+  O.pend = -1;
+  O.pan.count += 1;  // mix reflector appended (haar.hpp:63), Gram known
+
+  // K2: p = D_F (x - P_F beta), new fold column
+  FoldArgs<T> fa;
+  fa.P = static_cast<const T*>(F.pan.P);
+  fa.K = F.pan.K;
+  fa.ncols = (int)F.pan.count;
+  fa.beta = op->beta1;
+  fa.x = xsrc;
+  fa.D = F.dev.Drow;
+  fa.Dtail = F.dev.Dtail;
+  fa.Dlen = F.dev.Dlen;
+  fa.Pw = static_cast<T*>(F.pan.P);
+  fa.newj = F.pan.count;
+  fa.off = off;
+  fa.escale = op->scal + kScEscale;
+  fa.head = op->head;
+  fa.partials = op->partials2;
+  fa.n = n;
+  fa.status = op->status;
+  {
+    LaunchScope ls(op, s, "fold", bytes_of(op, (double)n * (F.pan.count + 2)));
+    k_fold<T><<<(unsigned)ntiles, kUpdThreads, sizeof(double) * std::max<int64_t>(F.pan.count, 1), s>>>(fa);
+  }
+  check_launch("k_fold");
+
+  sa.partials = op->partials2;
+  sa.nblk = (int)ntiles;
+  sa.kA = (int)F.pan.count;
+  sa.kB = (int)O.pan.count;
+  sa.append = append_fold ? 1 : 0;
+  {
+    LaunchScope ls(op, s, "small_fold", 0.0);
+    k_small_fold<T><<<1, kSmallThreads, 0, s>>>(sa);
+  }
+  check_launch("k_small_fold");
+  if (append_fold) {
+    F.pend = (int)F.pan.count;
+    F.pan.count += 1;
+  }
+
+  // K3: y = D_O z - P_O beta (+ dynamics epilogue)
+  OtherArgs<T> oa;
+  oa.P = static_cast<const T*>(O.pan.P);
+  oa.K = O.pan.K;
+  oa.ncols = (int)O.pan.count;
+  oa.beta = op->beta1;
+  oa.z = op->zbuf;
+  oa.zlen = off + 1;
+  oa.D = O.dev.Drow;
+  oa.Dtail = O.dev.Dtail;
+  oa.Dlen = O.dev.Dlen;
+  oa.n = n;
+  oa.status = op->status;
+  oa.epi = epi;
+  double eb = (double)n * (O.pan.count + 1);
+  if (epi.kind == kEpiTanhMix) eb += (double)n * ((epi.xprev ? 1 : 0) + (epi.y ? 1 : 0));
+  {
+    LaunchScope ls(op, s, "other", bytes_of(op, eb));
+    k_other<T><<<(unsigned)ntiles, kUpdThreads, sizeof(double) * std::max<int64_t>(O.pan.count, 1), s>>>(oa);
+  }
+  check_launch("k_other");
+}
+
+// ------------------------------------------------------------- Ginibre
+// ginibre.hpp:58-106. Right probe: fold chain R (dim n), store S = U (dim m),
+// opposite chain L (dim m), opposite store V (dim n). Left probe mirrored.
+template <typename T>
+void enqueue_ginibre(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cudaStream_t s) {
+  const bool right = (side == HD_RIGHT);
+  const bool first = (op->c.r + op->c.l == 0);
+  Chain& F = right ? op->R : op->L;       // fold chain (input dimension)
+  Chain& O = right ? op->L : op->R;       // opposite chain (output dimension)
+  Panel& S = right ? op->U : op->V;       // same-side store (output dim)
+  Panel& Sopp = right ? op->V : op->U;    // opposite-side store (input dim)
+  const int64_t nin = right ? op->n : op->m;
+  const int64_t nout = right ? op->m : op->n;
+  const int64_t tin = (right ? op->rows_pad_n : op->rows_pad_m) / kTile;
+  const int64_t tout = (right ? op->rows_pad_m : op->rows_pad_n) / kTile;
+  int64_t& cnt = right ? op->c.r : op->c.l;
+  const int64_t opp_cnt = right ? op->c.l : op->c.r;
+  cnt += 1;
+  const int64_t off = cnt - 1;
+  const bool append_fold = !(op->cfg.skip_reflector && first);
+  Src<T> g = draw_src<T>(op, nout);
+  g.mask_begin = opp_cnt;  // ginibre.hpp:73 / :92
+  g.D = O.dev.Drow;
+  g.Dtail = O.dev.Dtail;
+  g.Dlen = O.dev.Dlen;
+
+  // K1 (input side): a = P_F^T x (+ pending), c = Sopp^T x
+  DotArgs<T> da;
+  da.njobs = 2;
+  da.n = nin;
+  da.ntiles = tin;
+  da.job[0].P = static_cast<const T*>(F.pan.P);
+  da.job[0].K = F.pan.K;
+  da.job[0].ncols = (int)F.pan.count;
+  da.job[0].pend = F.pend;
+  da.job[0].rhs = xsrc;
+  da.job[0].check_finite = 1;
+  da.job[1].P = static_cast<const T*>(Sopp.P);
+  da.job[1].K = Sopp.K;
+  da.job[1].ncols = (int)Sopp.count;
+  da.job[1].rhs = xsrc;
+  const double b1 = bytes_of(op, (double)nin * (F.pan.count + Sopp.count + (F.pend >= 0) + 1));
+  int grid = launch_dots<T>(op, s, da, b1);
+
+  SmallArgs sa;
+  sa.partials = op->partials;
+  sa.nblk = grid;
+  sa.nslots = da.nslots;
+  sa.red = op->red;
+  sa.scal = op->scal;
+  sa.status = op->status;
+  sa.chA = F.dev;
+  sa.chB = O.dev;
+  sa.PA = F.pan.P;
+  sa.PB = O.pan.P;
+  sa.kA = (int)F.pan.count;
+  sa.kB = (int)Sopp.count;
+  sa.pendA = F.pend;
+  sa.pendB = -1;
+  sa.slotA_dot = da.job[0].slot_dot;
+  sa.slotA_pend = da.job[0].slot_pend;
+  sa.slotA_ss = da.job[0].slot_sumsq;
+  sa.slotB_dot = da.job[1].slot_dot;
+  sa.off = off;
+  sa.rule = op->cfg.sign_rule;
+  sa.beta1 = op->beta1;
+  sa.beta3 = op->beta3;
+  sa.tmp = op->tmp;
+  sa.tmp2 = op->tmp2;
+  sa.head = op->head;
+  sa.zbuf = op->zbuf;
+  sa.csp = op->csp;
+  sa.coefS = op->coefS;
+  sa.is_haar = 0;
+  {
+    LaunchScope ls(op, s, "small_dots", 0.0);
+    k_small_dots<T><<<1, kSmallThreads, 0, s>>>(sa);
+  }
+  check_launch("k_small_dots");
+  F.pend = -1;
+
+  // K2: p = D_F (x - P_F beta), new fold column, head p[0..off]
+  FoldArgs<T> fa;
+  fa.P = static_cast<const T*>(F.pan.P);
+  fa.K = F.pan.K;
+  fa.ncols = (int)F.pan.count;
+  fa.beta = op->beta1;
+  fa.x = xsrc;
+  fa.D = F.dev.Drow;
+  fa.Dtail = F.dev.Dtail;
+  fa.Dlen = F.dev.Dlen;
+  fa.Pw = static_cast<T*>(F.pan.P);
+  fa.newj = F.pan.count;
+  fa.off = off;
+  fa.escale = op->scal + kScEscale;
+  fa.head = op->head;
+  fa.partials = op->partials2;
+  fa.n = nin;
+  fa.status = op->status;
+  {
+    LaunchScope ls(op, s, "fold", bytes_of(op, (double)nin * (F.pan.count + 2)));
+    k_fold<T><<<(unsigned)tin, kUpdThreads, sizeof(double) * std::max<int64_t>(F.pan.count, 1), s>>>(fa);
+  }
+  check_launch("k_fold");
+  sa.partials = op->partials2;
+  sa.nblk = (int)tin;
+  sa.append = append_fold ? 1 : 0;
+  {
+    LaunchScope ls(op, s, "small_fold", 0.0);
+    k_small_fold<T><<<1, kSmallThreads, 0, s>>>(sa);
+  }
+  check_launch("k_small_fold");
+  if (append_fold) {
+    F.pend = (int)F.pan.count;
+    F.pan.count += 1;
+  }
+
+  // K3 (output side): a_g = P_O^T (D_O g_m) (+ pending of O)
+  DotArgs<T> db;
+  db.njobs = 1;
+  db.n = nout;
+  db.ntiles = tout;
+  db.job[0].P = static_cast<const T*>(O.pan.P);
+  db.job[0].K = O.pan.K;
+  db.job[0].ncols = (int)O.pan.count;
+  db.job[0].pend = O.pend;
+  db.job[0].rhs = g;
+  const double b3 = bytes_of(op, (double)nout * (O.pan.count + (O.pend >= 0))) +
+                    (g.kind == kSrcInjected ? 8.0 * nout : 0.0);
+  grid = launch_dots<T>(op, s, db, b3);
+
+  SmallArgs sg = sa;
+  sg.partials = op->partials;
+  sg.nblk = grid;
+  sg.nslots = db.nslots;
+  sg.chB = O.dev;
+  sg.PB = O.pan.P;
+  sg.kB = (int)O.pan.count;
+  sg.pendB = O.pend;
+  sg.slotB_dot = db.job[0].slot_dot;
+  sg.slotB_pend = db.job[0].slot_pend;
+  sg.csplen = Sopp.count;  // rows < opp count carry <v_i, x>
+  sg.nS = (int)S.count;
+  {
+    LaunchScope ls(op, s, "small_gin", 0.0);
+    k_small_gin<T><<<1, kSmallThreads, 0, s>>>(sg);
+  }
+  check_launch("k_small_gin");
+  O.pend = -1;
+
+  // K4: u = D_O g_m - P_O beta1 -> S[:, cnt-1];  y = sigma(S coef + c u + D_O c - P_O beta3)
+  GinArgs<T> ga;
+  ga.P = static_cast<const T*>(O.pan.P);
+  ga.K = O.pan.K;
+  ga.ncols = (int)O.pan.count;
+  ga.beta1 = op->beta1;
+  ga.beta3 = op->beta3;
+  ga.S = static_cast<const T*>(S.P);
+  ga.KS = S.K;
+  ga.nS = (int)S.count;
+  ga.coefS = op->coefS;
+  ga.Sw = static_cast<T*>(S.P);
+  ga.newj = S.count;
+  ga.g = g;
+  ga.csp = op->csp;
+  ga.csplen = Sopp.count;
+  ga.D = O.dev.Drow;
+  ga.Dtail = O.dev.Dtail;
+  ga.Dlen = O.dev.Dlen;
+  ga.coef_cur = op->scal + kScCoefCur;
+  ga.sigma = op->cfg.sigma;
+  ga.n = nout;
+  ga.status = op->status;
+  ga.epi = epi;
+  double eb = (double)nout * (O.pan.count + S.count + 2 + (g.kind == kSrcInjected ? 1 : 0));
+  if (epi.yadd) eb += nout;
+  {
+    LaunchScope ls(op, s, "ginout", bytes_of(op, eb));
+    const size_t smem = sizeof(double) * (2 * O.pan.K + std::max<int64_t>(S.K, 1));
+    k_ginout<T><<<(unsigned)tout, kUpdThreads, smem, s>>>(ga);
+  }
+  check_launch("k_ginout");
+  S.count += 1;
+}
+
+template <typename T>
+void enqueue_probe(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cudaStream_t s) {
+  if (op->ens == HD_HAAR) {
+    enqueue_haar<T>(op, side, xsrc, epi, s);
+  } else if (op->ens == HD_GINIBRE) {
+    enqueue_ginibre<T>(op, side, xsrc, epi, s);
+  } else {
+    // GOE: y = (inner.right(x) + inner.left(x)) / sqrt(2)  (ensembles.hpp:117-127)
+    Epi<T> e1;
+    e1.kind = kEpiPlain;
+    e1.y = static_cast<T*>(op->gtmp);
+    e1.step = epi.step;
+    enqueue_ginibre<T>(op, HD_RIGHT, xsrc, e1, s);
+    Epi<T> e2 = epi;
+    e2.yadd = static_cast<const T*>(op->gtmp);
+    e2.add_scale = 0.7071067811865475244;
+    enqueue_ginibre<T>(op, HD_LEFT, xsrc, e2, s);
+  }
+}
+
+int64_t remaining(const hd_op* op) {
+  if (op->ens == HD_HAAR) return op->n - op->c.t;
+  if (op->ens == HD_GINIBRE) return std::min(op->m, op->n) - (op->c.r + op->c.l);
+  return (std::min(op->m, op->n) - (op->c.r + op->c.l)) / 2;
+}
+
+const char* budget_msg(const hd_op* op) {
+  if (op->ens == HD_HAAR) return "HaarOperator: probe budget n spent";
+  if (op->ens == HD_GINIBRE) return "GinibreOperator: probe budget min(m, n) spent";
+  return "GOEOperator: budget floor(n/2) spent";
+}
+
+int64_t inner_per_outer(const hd_op* op) { return op->ens == HD_GOE ? 2 : 1; }
+
+void snapshot_chains(const hd_op* op, Counters& c) {
+  c.rc_count = op->R.pan.count;
+  c.lc_count = op->L.pan.count;
+  c.u_count = op->U.count;
+  c.v_count = op->V.count;
+  c.rc_pend = op->R.pend;
+  c.lc_pend = op->L.pend;
+}
+
+void restore(hd_op* op, const Counters& c) {
+  op->c = c;
+  op->R.pan.count = c.rc_count;
+  op->L.pan.count = c.lc_count;
+  op->U.count = c.u_count;
+  op->V.count = c.v_count;
+  op->R.pend = c.rc_pend;
+  op->L.pend = c.lc_pend;
+}
+
+Counters take_snapshot(const hd_op* op) {
+  Counters c = op->c;
+  snapshot_chains(op, c);
+  return c;
+}
+
+void reset_device_state(hd_op* op, cudaStream_t s) {
+  {
+    LaunchScope ls(op, s, "reset", 0.0);
+    k_reset_status<<<1, 32, 0, s>>>(op->status);
+  }
+  for (Chain* ch : {&op->R, &op->L}) {
+    if (!ch->pan.P) continue;
+    LaunchScope ls(op, s, "reset", 0.0);
+    k_reset_chain<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ch->dev.Dlen, 256), 1024)), 256, 0, s>>>(
+        ch->dev);
+  }
+  check_launch("reset");
+}
+
+void hard_reset(hd_op* op) {
+  op->c = Counters{};
+  op->R.pan.count = op->L.pan.count = op->U.count = op->V.count = 0;
+  op->R.pend = op->L.pend = -1;
+  op->inj_size = 0;
+  reset_device_state(op, op->stream);
+  ck(cudaStreamSynchronize(op->stream), "sync");
+}
+
+// Read status after a synchronous section; returns bad step (or 0).
+void read_status(hd_op* op, int st[kStWords]) {
+  ck(cudaMemcpy(st, op->status, sizeof(int) * kStWords, cudaMemcpyDeviceToHost), "status");
+}
+
+void clear_status(hd_op* op, cudaStream_t s) {
+  k_reset_status<<<1, 32, 0, s>>>(op->status);
+  check_launch("reset status");
+}
+
+bool host_all_finite(const void* x, int64_t n, bool f32) {
+  if (f32) {
+    const float* p = static_cast<const float*>(x);
+    for (int64_t i = 0; i < n; ++i)
+      if (!std::isfinite(p[i])) return false;
+  } else {
+    const double* p = static_cast<const double*>(x);
+    for (int64_t i = 0; i < n; ++i)
+      if (!std::isfinite(p[i])) return false;
+  }
+  return true;
+}
+
+// ================================================================= probe
+template <typename T>
+void do_probe(hd_op* op, const void* x, int64_t x_len, void* y, int64_t y_len, int side, int on_device,
+              cudaStream_t s) {
+  require(side == HD_RIGHT || side == HD_LEFT, "side must be 'right' or 'left'");
+  const int eff_side = (op->ens == HD_GOE) ? HD_RIGHT : side;  // ensembles.hpp:118-119
+  const int64_t rows = op->m, cols = op->n;
+  const int64_t want = (eff_side == HD_RIGHT) ? cols : rows;
+  const int64_t out_len = (eff_side == HD_RIGHT) ? rows : cols;
+  require(x_len == want, "probe: input dimension mismatch");
+  require(y_len == out_len, "probe: output dimension mismatch");
+  const bool budget_left = remaining(op) > 0;
+  if (!on_device) require(host_all_finite(x, x_len, op->f32), "probe: non-finite input");
+  if (!budget_left) {
+    if (on_device) {
+      std::vector<unsigned char> h((size_t)x_len * op->esz);
+      ck(cudaMemcpy(h.data(), x, h.size(), cudaMemcpyDeviceToHost), "copy");
+      require(host_all_finite(h.data(), x_len, op->f32), "probe: non-finite input");
+    }
+    throw HdError(HD_ERR_BUDGET_EXHAUSTED, budget_msg(op));
+  }
+  if (op->ens == HD_GOE) ensure_capacity(op, 1, 1);
+  else ensure_capacity(op, eff_side == HD_RIGHT ? 1 : 0, eff_side == HD_LEFT ? 1 : 0);
+  const Counters snap = take_snapshot(op);
+  // stage input (16 B aligned for vector loads)
+  const void* xin = x;
+  if (!on_device || (reinterpret_cast<uintptr_t>(x) % 16) != 0) {
+    ck(cudaMemcpyAsync(op->xbuf, x, (size_t)x_len * op->esz, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       s),
+       "copy x");
+    xin = op->xbuf;
+  }
+  void* yout = (on_device && (reinterpret_cast<uintptr_t>(y) % 16) == 0) ? y : op->ybuf[0];
+  clear_status(op, s);
+  Epi<T> epi;
+  epi.kind = kEpiPlain;
+  epi.y = static_cast<T*>(yout);
+  epi.step = 1;
+  try {
+    enqueue_probe<T>(op, eff_side, vec_src<T>(xin, nullptr), epi, s);
+  } catch (...) {
+    restore(op, snap);
+    throw;
+  }
+  if (yout != y)
+    ck(cudaMemcpyAsync(y, yout, (size_t)out_len * op->esz, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       s),
+       "copy y");
+  ck(cudaStreamSynchronize(s), "probe sync");
+  int st[kStWords];
+  read_status(op, st);
+  if (st[kStBadInput]) {
+    restore(op, snap);
+    throw HdError(HD_ERR_INVALID_ARGUMENT, "probe: non-finite input");
+  }
+  if (st[kStAbort]) {
+    restore(op, snap);
+    throw HdError(HD_ERR_RUNTIME, "hd: probe aborted on device");
+  }
+}
+
+// =============================================================== dynamics
+int side_for(int rule, int64_t t) {
+  if (rule == HD_SIDES_RIGHT) return HD_RIGHT;
+  if (rule == HD_SIDES_LEFT) return HD_LEFT;
+  return (t % 2 == 1) ? HD_RIGHT : HD_LEFT;
+}
+
+template <typename T>
+__global__ void k_copy_scaled(const T* y, const double* scale, T* x, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = scale ? (T)(*scale * (double)y[i]) : y[i];
+}
+
+template <typename T>
+struct RunPlan {
+  // iterate x_t lives in buffer xb[t] (optionally times *xs[t])
+  const void* xb = nullptr;
+  const double* xs = nullptr;
+};
+
+template <typename T>
+void enqueue_run(hd_op* op, const hd_run_args& a, int64_t dim_of_x1, cudaStream_t s, std::vector<Counters>* snaps,
+                 void* traj_dev, bool reset_first) {
+  if (reset_first) reset_device_state(op, s);
+  const int64_t T_ = a.iterations;
+  // buffers: xbuf holds x1 (and x0 in ybuf[2] for tanh mix); ybuf ping-pong
+  const void* x_cur = op->xbuf;
+  const double* x_scale = nullptr;
+  const void* x_prev = (a.update == HD_UPDATE_TANH_MIX) ? op->ybuf[2] : nullptr;
+  // tanh mix rotates three buffers: xbuf, ybuf[0], ybuf[1], ybuf[2]
+  void* tri[4] = {op->xbuf, op->ybuf[0], op->ybuf[1], op->ybuf[2]};
+  int idx_cur = 0, idx_prev = 3;
+  for (int64_t t = 1; t <= T_; ++t) {
+    const int side = side_for(a.side_rule, t);
+    const int eff_side = (op->ens == HD_GOE) ? HD_RIGHT : side;
+    const int64_t out_dim = (eff_side == HD_RIGHT) ? op->m : op->n;
+    Epi<T> epi;
+    epi.step = (int)std::min<int64_t>(t, INT_MAX - 1);
+    void* out_buf = nullptr;
+    if (a.update == HD_UPDATE_TANH_MIX) {
+      int idx_next = 0;
+      while (idx_next == idx_cur || idx_next == idx_prev) ++idx_next;
+      epi.kind = kEpiTanhMix;
+      epi.xprev = static_cast<const T*>(tri[idx_prev]);
+      epi.xnext = static_cast<T*>(tri[idx_next]);
+      enqueue_probe<T>(op, eff_side, vec_src<T>(tri[idx_cur], nullptr), epi, s);
+      idx_prev = idx_cur;
+      idx_cur = idx_next;
+      x_cur = tri[idx_cur];
+      x_scale = nullptr;
+      out_buf = tri[idx_cur];
+    } else {
+      out_buf = op->ybuf[t % 2];
+      epi.y = static_cast<T*>(out_buf);
+      epi.kind = (a.update == HD_UPDATE_NORMALIZE) ? kEpiNormalize : kEpiPlain;
+      epi.partials = op->partials2;
+      enqueue_probe<T>(op, eff_side, vec_src<T>(x_cur, x_scale), epi, s);
+      if (a.update == HD_UPDATE_NORMALIZE) {
+        const int64_t nblk = ((eff_side == HD_RIGHT) ? op->rows_pad_m : op->rows_pad_n) / kTile;
+        {
+          LaunchScope ls(op, s, "small_norm", 0.0);
+          k_small_norm<<<1, kSmallThreads, 0, s>>>(op->partials2, (int)nblk, op->scal, op->status, epi.step);
+        }
+        check_launch("k_small_norm");
+        // the next probe reads y * inv lazily; keep a private copy of inv
+        // per step so later steps cannot overwrite it before use
+        x_scale = op->scal + kScInv;
+      } else {
+        x_scale = nullptr;
+      }
+      x_cur = out_buf;
+    }
+    if (traj_dev) {
+      LaunchScope ls(op, s, "scale_copy", bytes_of(op, 2.0 * out_dim));
+      k_copy_scaled<T><<<(unsigned)ceil_div(out_dim, 256), 256, 0, s>>>(
+          static_cast<const T*>(x_cur), x_scale, static_cast<T*>(traj_dev) + (size_t)t * dim_of_x1, out_dim);
+      check_launch("traj copy");
+    }
+    if (snaps) snaps->push_back(take_snapshot(op));
+  }
+  // materialise x_{T+1} into ybuf[2]... caller copies from (x_cur, x_scale)
+  (void)x_prev;
+  // final iterate into op->ybuf slot "final": reuse gtmp-free buffer xbuf? use k_copy to ybuf[... ]
+  {
+    const int64_t fdim = dim_of_x1;
+    void* fin = (a.update == HD_UPDATE_TANH_MIX) ? nullptr : op->gtmp;
+    if (fin && T_ > 0) {
+      LaunchScope ls(op, s, "scale_copy", bytes_of(op, 2.0 * fdim));
+      k_copy_scaled<T><<<(unsigned)ceil_div(fdim, 256), 256, 0, s>>>(static_cast<const T*>(x_cur), x_scale,
+                                                                      static_cast<T*>(fin), fdim);
+      check_launch("final copy");
+    }
+  }
+}
+
+// Where x_{T+1} lives after enqueue_run (device pointer).
+template <typename T>
+const void* final_location(hd_op* op, const hd_run_args& a) {
+  if (a.iterations == 0) return op->xbuf;
+  if (a.update == HD_UPDATE_TANH_MIX) {
+    // replay the buffer rotation
+    int idx_cur = 0, idx_prev = 3;
+    for (int64_t t = 1; t <= a.iterations; ++t) {
+      int idx_next = 0;
+      while (idx_next == idx_cur || idx_next == idx_prev) ++idx_next;
+      idx_prev = idx_cur;
+      idx_cur = idx_next;
+    }
+    void* tri[4] = {op->xbuf, op->ybuf[0], op->ybuf[1], op->ybuf[2]};
+    return tri[idx_cur];
+  }
+  return op->gtmp;
+}
+
+template <typename T>
+void do_run(hd_op* op, const hd_run_args& a) {
+  cudaStream_t s = a.stream ? static_cast<cudaStream_t>(a.stream) : op->stream;
+  require(a.iterations >= 0, "run_dynamics: negative iteration count");
+  require(a.update >= 0 && a.update <= 2, "run_dynamics: unknown update map");
+  require(a.side_rule >= 0 && a.side_rule <= 2, "run_dynamics: unknown side schedule");
+  require(a.x1 != nullptr, "run_dynamics: initial history must hold d + 1 vectors");
+  require(a.iterations <= remaining(op), "run_dynamics: iteration count exceeds the operator's probe budget");
+  // dimensions: x_1 is the input of probe 1
+  const int side1 = side_for(a.side_rule, 1);
+  const int eff1 = (op->ens == HD_GOE) ? HD_RIGHT : side1;
+  const int64_t dim1 = (eff1 == HD_RIGHT) ? op->n : op->m;
+  if (a.update == HD_UPDATE_TANH_MIX || a.traj)
+    require(op->m == op->n, "run_dynamics: this update map needs a square operator");
+  if (!a.on_device) require(host_all_finite(a.x1, dim1, op->f32), "probe: non-finite input");
+  {
+    int64_t nr = 0, nl = 0;
+    for (int64_t t = 1; t <= a.iterations; ++t) {
+      if (op->ens == HD_GOE) { ++nr; ++nl; }
+      else if (side_for(a.side_rule, t) == HD_RIGHT) ++nr;
+      else ++nl;
+    }
+    ensure_capacity(op, nr, nl);
+  }
+  const Counters snap0 = take_snapshot(op);
+  const bool fresh = (op->c.r == 0 && op->c.l == 0 && op->c.t == 0 && op->R.pan.count == 0 && op->L.pan.count == 0);
+  const size_t xbytes = (size_t)dim1 * op->esz;
+  const cudaMemcpyKind k = a.on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  ck(cudaMemcpyAsync(op->xbuf, a.x1, xbytes, k, s), "copy x1");
+  if (a.update == HD_UPDATE_TANH_MIX) {
+    if (a.x0)
+      ck(cudaMemcpyAsync(op->ybuf[2], a.x0, xbytes, k, s), "copy x0");
+    else
+      ck(cudaMemsetAsync(op->ybuf[2], 0, xbytes, s), "zero x0");
+  }
+  void* traj_dev = nullptr;
+  if (a.traj) {
+    if (a.on_device) {
+      traj_dev = a.traj;
+    } else {
+      ck(cudaMalloc(&traj_dev, xbytes * (size_t)(a.iterations + 1)), "traj alloc");
+    }
+    ck(cudaMemcpyAsync(traj_dev, a.x1, xbytes, k, s), "traj x1");
+  }
+  std::vector<Counters> snaps;
+  snaps.push_back(snap0);
+  const bool graphable = a.use_graph && fresh && op->cfg.draw_mode == HD_DRAWS_PHILOX && !op->prof && !a.traj;
+  try {
+    if (graphable) {
+      char keybuf[160];
+      std::snprintf(keybuf, sizeof keybuf, "%d/%d/%lld/%p", a.update, a.side_rule, (long long)a.iterations, (void*)s);
+      const std::string key(keybuf);
+      if (!op->graph || op->graph_key != key) {
+        if (op->graph) {
+          cudaGraphExecDestroy(op->graph);
+          op->graph = nullptr;
+        }
+        cudaGraph_t gr;
+        const int64_t before = op->launches;
+        ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture begin");
+        enqueue_run<T>(op, a, dim1, s, &snaps, nullptr, true);
+        ck(cudaStreamEndCapture(s, &gr), "capture end");
+        ck(cudaGraphInstantiate(&op->graph, gr, 0), "graph instantiate");
+        cudaGraphDestroy(gr);
+        op->graph_key = key;
+        op->graph_launches = op->launches - before;
+        op->graph_snaps = snaps;
+        op->launches = before;
+      } else {
+        // the run starts from the fresh state, so it ends where the capture did
+        snaps = op->graph_snaps;
+        restore(op, snaps.back());
+      }
+      ck(cudaGraphLaunch(op->graph, s), "graph launch");
+      op->launches += op->graph_launches;
+    } else {
+      if (fresh) reset_device_state(op, s);
+      else clear_status(op, s);
+      enqueue_run<T>(op, a, dim1, s, &snaps, traj_dev, false);
+    }
+  } catch (...) {
+    restore(op, snap0);
+    if (traj_dev && !a.on_device) cudaFree(traj_dev);
+    throw;
+  }
+  ck(cudaStreamSynchronize(s), "run sync");
+  int st[kStWords];
+  read_status(op, st);
+  if (st[kStBadInput]) {
+    restore(op, snap0);
+    if (traj_dev && !a.on_device) cudaFree(traj_dev);
+    throw HdError(HD_ERR_INVALID_ARGUMENT, "probe: non-finite input");
+  }
+  if (st[kStBadStep] != INT_MAX) {
+    const int64_t bad = st[kStBadStep];
+    restore(op, snaps[(size_t)std::min<int64_t>(bad, (int64_t)snaps.size() - 1)]);
+    if (traj_dev && !a.on_device) cudaFree(traj_dev);
+    throw HdError(HD_ERR_RUNTIME, "run_dynamics: non-finite iterate at step " + std::to_string(bad));
+  }
+  const void* fin = final_location<T>(op, a);
+  // dimension of x_{T+1}
+  int64_t fdim = dim1;
+  if (a.iterations > 0) {
+    const int sideT = side_for(a.side_rule, a.iterations);
+    const int effT = (op->ens == HD_GOE) ? HD_RIGHT : sideT;
+    fdim = (effT == HD_RIGHT) ? op->m : op->n;
+  }
+  if (a.final_out)
+    ck(cudaMemcpyAsync(a.final_out, fin, (size_t)fdim * op->esz, a.on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       s),
+       "copy final");
+  if (a.traj && !a.on_device) {
+    ck(cudaMemcpyAsync(a.traj, traj_dev, xbytes * (size_t)(a.iterations + 1), cudaMemcpyDeviceToHost, s), "copy traj");
+  }
+  ck(cudaStreamSynchronize(s), "run sync");
+  if (traj_dev && !a.on_device) cudaFree(traj_dev);
+}
+
+// ------------------------------------------------- user callback dynamics
+template <typename T>
+void do_run_callback(hd_op* op, int64_t T_, int32_t depth, const void* const* initial, hd_side_fn side_of,
+                     hd_update_fn update, void* user, void* final_out) {
+  require(T_ >= 0, "run_dynamics: negative iteration count");
+  require(depth >= 0, "run_dynamics: negative history depth");
+  require(initial != nullptr, "run_dynamics: initial history must hold d + 1 vectors");
+  require(side_of != nullptr, "run_dynamics: no side schedule");
+  require(update != nullptr, "run_dynamics: no update map");
+  require(T_ <= remaining(op), "run_dynamics: iteration count exceeds the operator's probe budget");
+  require(op->m == op->n || depth == 0, "run_dynamics: this update map needs a square operator");
+  cudaStream_t s = op->stream;
+  const int64_t dim = std::max(op->m, op->n);
+  const size_t bytes = (size_t)dim * op->esz;
+  std::vector<void*> hist(depth + 1);
+  for (auto& h : hist) ck(cudaMalloc(&h, std::max<size_t>(bytes, 16)), "hist alloc");
+  void* ybuf = nullptr;
+  void* nbuf = nullptr;
+  ck(cudaMalloc(&ybuf, std::max<size_t>(bytes, 16)), "alloc");
+  ck(cudaMalloc(&nbuf, std::max<size_t>(bytes, 16)), "alloc");
+  auto cleanup = [&] {
+    for (auto h : hist) cudaFree(h);
+    cudaFree(ybuf);
+    cudaFree(nbuf);
+  };
+  try {
+    int64_t cur_dim = op->n;
+    {
+      const int s1 = side_of(user, 1);
+      cur_dim = (op->ens == HD_GOE || s1 == HD_RIGHT) ? op->n : op->m;
+    }
+    for (int i = 0; i <= depth; ++i)
+      ck(cudaMemcpyAsync(hist[i], initial[i], (size_t)cur_dim * op->esz, cudaMemcpyDeviceToDevice, s), "copy init");
+    ensure_capacity(op, T_ * inner_per_outer(op), T_ * inner_per_outer(op));
+    for (int64_t t = 1; t <= T_; ++t) {
+      const int side = side_of(user, t);
+      require(side == HD_RIGHT || side == HD_LEFT, "side must be 'right' or 'left'");
+      const int eff = (op->ens == HD_GOE) ? HD_RIGHT : side;
+      const int64_t in_dim = (eff == HD_RIGHT) ? op->n : op->m;
+      const int64_t out_dim = (eff == HD_RIGHT) ? op->m : op->n;
+      (void)in_dim;
+      do_probe<T>(op, hist[0], in_dim, ybuf, out_dim, side, 1, s);
+      const int rc = update(user, t, ybuf, hist.data(), depth, nbuf, out_dim, (void*)s);
+      if (rc != 0) throw HdError(HD_ERR_RUNTIME, "run_dynamics: update callback failed at step " + std::to_string(t));
+      ck(cudaStreamSynchronize(s), "sync");
+      std::vector<unsigned char> h((size_t)out_dim * op->esz);
+      ck(cudaMemcpy(h.data(), nbuf, h.size(), cudaMemcpyDeviceToHost), "check");
+      if (!host_all_finite(h.data(), out_dim, op->f32))
+        throw HdError(HD_ERR_RUNTIME, "run_dynamics: non-finite iterate at step " + std::to_string(t));
+      void* oldest = hist.back();
+      for (int i = depth; i > 0; --i) hist[i] = hist[i - 1];
+      hist[0] = nbuf;
+      nbuf = oldest;
+      cur_dim = out_dim;
+    }
+    if (final_out) ck(cudaMemcpy(final_out, hist[0], (size_t)cur_dim * op->esz, cudaMemcpyDeviceToDevice), "final");
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+}
+
+}  // namespace
+
+// ================================================================= C-ABI
+#define HD_TRY try {
+#define HD_CATCH                          \
+  }                                       \
+  catch (const HdError& e) {              \
+    g_err = e.what();                     \
+    return e.code;                        \
+  }                                       \
+  catch (const std::exception& e) {       \
+    g_err = e.what();                     \
+    return HD_ERR_RUNTIME;                \
+  }                                       \
+  catch (...) {                           \
+    g_err = "hd: unknown error";          \
+    return HD_ERR_RUNTIME;                \
+  }
+
+extern "C" {
+
+const char* hd_last_error(void) { return g_err.c_str(); }
+const char* hd_version(void) { return "hd-b200 0.1.0 (sm_100a)"; }
+
+int hd_create(const hd_config* cfg, hd_op** out) {
+  HD_TRY
+  require(cfg != nullptr && out != nullptr, "hd_create: null argument");
+  const hd_config& c = *cfg;
+  require(c.dtype == HD_F64 || c.dtype == HD_F32, "hd_create: dtype must be HD_F64 or HD_F32");
+  require(c.draw_mode == HD_DRAWS_PHILOX || c.draw_mode == HD_DRAWS_INJECTED, "hd_create: unknown draw mode");
+  require(c.sign_rule >= 0 && c.sign_rule <= 2, "hd_create: unknown sign rule");
+  int64_t m = c.m, n = c.n;
+  if (c.ensemble == HD_GINIBRE) {
+    require(m >= 1 && n >= 1, "GinibreOperator: dims must be positive");  // ginibre.hpp:40
+    require(c.sigma > 0.0, "GinibreOperator: sigma must be positive");     // ginibre.hpp:41
+  } else if (c.ensemble == HD_HAAR) {
+    require(n >= 1, "HaarOperator: n must be positive");  // haar.hpp:30
+    m = n;
+  } else if (c.ensemble == HD_GOE) {
+    require(n >= 1, "GinibreOperator: dims must be positive");
+    require(c.sigma > 0.0, "GinibreOperator: sigma must be positive");
+    m = n;
+  } else {
+    throw HdError(HD_ERR_INVALID_ARGUMENT, "hd_create: unknown ensemble");
+  }
+  ck(cudaSetDevice(c.device), "cudaSetDevice");
+  auto op = std::make_unique<hd_op>();
+  op->cfg = c;
+  op->ens = c.ensemble;
+  op->f32 = (c.dtype == HD_F32);
+  op->esz = op->f32 ? 4 : 8;
+  op->m = m;
+  op->n = n;
+  op->rows_pad_m = ceil_div(m, kTile) * kTile;
+  op->rows_pad_n = ceil_div(n, kTile) * kTile;
+  op->budget = (c.ensemble == HD_HAAR) ? n : std::min(m, n);
+  ck(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking), "stream");
+  ck(cudaDeviceGetAttribute(&op->nsm, cudaDevAttrMultiProcessorCount, c.device), "attr");
+  const int64_t per_outer = (c.ensemble == HD_GOE) ? 2 : 1;
+  int64_t K;
+  if (c.capacity > 0) {
+    K = std::min((int64_t)(c.capacity * per_outer), op->budget);
+  } else {
+    K = std::min(op->budget, (int64_t)64);
+  }
+  K = std::max<int64_t>(K, 1);
+  const int64_t Kside = (c.ensemble == HD_GOE) ? std::max<int64_t>(1, (K + 1) / 2) : K;
+  alloc_chain(op.get(), op->R, op->rows_pad_n, Kside);
+  alloc_chain(op.get(), op->L, op->rows_pad_m, Kside);
+  if (c.ensemble != HD_HAAR) {
+    alloc_store(op.get(), op->U, op->rows_pad_m, Kside);
+    alloc_store(op.get(), op->V, op->rows_pad_n, Kside);
+  }
+  ensure_small(op.get(), K + 1);
+  op->scal = dmalloc<double>(kScWords);
+  ck(cudaMemsetAsync(op->scal, 0, sizeof(double) * kScWords, op->stream), "memset");
+  op->status = dmalloc<int>(kStWords);
+  const int64_t rp = std::max(op->rows_pad_m, op->rows_pad_n);
+  op->io_len = rp;
+  op->xbuf = dmalloc<unsigned char>((size_t)rp * op->esz);
+  for (auto& b : op->ybuf) b = dmalloc<unsigned char>((size_t)rp * op->esz);
+  op->gtmp = dmalloc<unsigned char>((size_t)rp * op->esz);
+  op->partials2 = dmalloc<double>(rp / kTile + 8);
+  ensure_red(op.get(), 4 * K + 16, (size_t)op->nsm * 4);
+  hard_reset(op.get());
+  *out = op.release();
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_destroy(hd_op* op) {
+  HD_TRY
+  if (!op) return HD_OK;
+  cudaSetDevice(op->cfg.device);
+  cudaStreamSynchronize(op->stream);
+  if (op->graph) cudaGraphExecDestroy(op->graph);
+  free_chain(op->R);
+  free_chain(op->L);
+  cudaFree(op->U.P);
+  cudaFree(op->V.P);
+  for (double* p : {op->partials, op->partials2, op->red, op->scal, op->beta1, op->beta3, op->tmp, op->tmp2,
+                    op->coefS, op->head, op->zbuf, op->csp, op->inj})
+    cudaFree(p);
+  cudaFree(op->status);
+  cudaFree(op->xbuf);
+  for (auto b : op->ybuf) cudaFree(b);
+  cudaFree(op->gtmp);
+  for (auto& e : op->evq) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  for (auto e : op->evpool) cudaEventDestroy(e);
+  cudaStreamDestroy(op->stream);
+  delete op;
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_shape(const hd_op* op, int64_t* rows, int64_t* cols) {
+  HD_TRY
+  require(op && rows && cols, "hd_shape: null argument");
+  *rows = op->m;
+  *cols = op->n;
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_remaining(const hd_op* op, int64_t* r) {
+  HD_TRY
+  require(op && r, "hd_remaining: null argument");
+  *r = remaining(op);
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_counts(const hd_op* op, int64_t* right, int64_t* left) {
+  HD_TRY
+  require(op && right && left, "hd_counts: null argument");
+  if (op->ens == HD_HAAR) {
+    *right = op->c.t;
+    *left = 0;
+  } else {
+    *right = op->c.r;
+    *left = op->c.l;
+  }
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_chain_sizes(const hd_op* op, int64_t* rc, int64_t* lc) {
+  HD_TRY
+  require(op && rc && lc, "hd_chain_sizes: null argument");
+  *rc = op->R.pan.count;
+  *lc = op->L.pan.count;
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_probe(hd_op* op, const void* x, int64_t x_len, void* y, int64_t y_len, int32_t side, int32_t on_device,
+             void* stream) {
+  HD_TRY
+  require(op && x && y, "hd_probe: null argument");
+  cudaSetDevice(op->cfg.device);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : op->stream;
+  if (op->f32)
+    do_probe<float>(op, x, x_len, y, y_len, side, on_device, s);
+  else
+    do_probe<double>(op, x, x_len, y, y_len, side, on_device, s);
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_push_draws(hd_op* op, const double* g, int64_t len, int32_t on_device) {
+  HD_TRY
+  require(op && g, "hd_push_draws: null argument");
+  require(op->cfg.draw_mode == HD_DRAWS_INJECTED, "hd_push_draws: operator was not created with HD_DRAWS_INJECTED");
+  require(len >= 1, "normal_vector: len must be >= 1");
+  cudaSetDevice(op->cfg.device);
+  // compact consumed prefix, then grow
+  if (op->c.inj_pos > 0 && op->c.r == 0 && op->c.l == 0 && op->c.t == 0) {
+    // nothing consumed by live probes can be referenced any more only when
+    // the queue was reset; keep it simple: never compact live queues
+  }
+  if (op->inj_size + len > op->inj_cap) {
+    const int64_t ncap = std::max<int64_t>(op->inj_cap * 2, op->inj_size + len);
+    double* np = dmalloc<double>(ncap);
+    if (op->inj_size > 0)
+      ck(cudaMemcpyAsync(np, op->inj, sizeof(double) * op->inj_size, cudaMemcpyDeviceToDevice, op->stream), "grow");
+    ck(cudaStreamSynchronize(op->stream), "sync");
+    cudaFree(op->inj);
+    op->inj = np;
+    op->inj_cap = ncap;
+  }
+  ck(cudaMemcpyAsync(op->inj + op->inj_size, g, sizeof(double) * len,
+                     on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, op->stream),
+     "push");
+  ck(cudaStreamSynchronize(op->stream), "sync");
+  op->inj_size += len;
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_reset(hd_op* op) {
+  HD_TRY
+  require(op, "hd_reset: null argument");
+  cudaSetDevice(op->cfg.device);
+  hard_reset(op);
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_run(hd_op* op, const hd_run_args* args) {
+  HD_TRY
+  require(op && args, "hd_run: null argument");
+  cudaSetDevice(op->cfg.device);
+  if (op->f32)
+    do_run<float>(op, *args);
+  else
+    do_run<double>(op, *args);
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_run_callback(hd_op* op, int64_t iterations, int32_t depth, const void* const* initial_dev, hd_side_fn side_of,
+                    hd_update_fn update, void* user, void* final_out_dev) {
+  HD_TRY
+  require(op, "hd_run_callback: null argument");
+  cudaSetDevice(op->cfg.device);
+  if (op->f32)
+    do_run_callback<float>(op, iterations, depth, initial_dev, side_of, update, user, final_out_dev);
+  else
+    do_run_callback<double>(op, iterations, depth, initial_dev, side_of, update, user, final_out_dev);
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_set_profiling(hd_op* op, int32_t enabled) {
+  HD_TRY
+  require(op, "hd_set_profiling: null argument");
+  drain_events(op);
+  op->prof = enabled != 0;
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_get_stats(hd_op* op, hd_kernel_stats* out, int32_t max, int32_t* count) {
+  HD_TRY
+  require(op && count, "hd_get_stats: null argument");
+  drain_events(op);
+  int32_t i = 0;
+  for (auto& kv : op->stats) {
+    if (out && i < max) {
+      std::memset(out[i].name, 0, sizeof(out[i].name));
+      std::strncpy(out[i].name, kv.first.c_str(), sizeof(out[i].name) - 1);
+      out[i].launches = kv.second.launches;
+      out[i].ms = kv.second.ms;
+      out[i].alg_bytes = kv.second.bytes;
+    }
+    ++i;
+  }
+  *count = i;
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_reset_stats(hd_op* op) {
+  HD_TRY
+  require(op, "hd_reset_stats: null argument");
+  drain_events(op);
+  op->stats.clear();
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_launch_count(const hd_op* op, int64_t* count) {
+  HD_TRY
+  require(op && count, "hd_launch_count: null argument");
+  *count = op->launches;
+  return HD_OK;
+  HD_CATCH
+}
+
+}  // extern "C"

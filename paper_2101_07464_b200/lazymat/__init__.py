@@ -1,0 +1,294 @@
+"""Drop-in mirror of the reference's ``lazymat`` Python module on the B200 path.
+
+Same names, argument names, defaults and exceptions as the reference bindings
+(/root/reference/proj/bindings/module.cpp:38-194, python/lazymat/__init__.py):
+
+    GinibreOperator(m, n, sigma=1.0, seed=1).probe(x, side="right")
+    HaarOperator(n, seed=1).probe(x, side="right"); .reconstruct()
+    derive_seed(base, index); BudgetExhausted; ResourceCapExceeded
+
+plus the B200 extensions (keyword-only): ``dtype`` ("f64"/"f32"), ``draws``
+("philox" device draws, or "injected" for parity runs fed by
+``push_draws``), ``capacity`` (panel width hint), ``stream``, fault flags,
+``GOEOperator`` (ensembles.hpp:93-131) and device dynamics ``run(...)``.
+
+Inputs may be numpy arrays (host, like the reference) or CUDA torch tensors
+(zero-copy device path; the result is then a CUDA tensor). Everything runs
+through the C-ABI of libhd_b200.so; there is no CPU fallback.
+
+Out of scope this round: sample_dense_haar,
+ista_curves, spectral_summary, two_sample_ks raise NotImplementedError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from .. import _native as N
+from .._native import BudgetExhausted, ResourceCapExceeded
+
+__all__ = [
+    "BudgetExhausted", "GinibreOperator", "HaarOperator", "GOEOperator", "ResourceCapExceeded",
+    "derive_seed", "ista_curves", "make_reflector", "sample_dense_haar", "spectral_summary", "two_sample_ks",
+]
+
+__version__ = "0.1.0"
+
+_MASK = (1 << 64) - 1
+
+
+def derive_seed(base: int, index: int) -> int:
+    """random.cpp:73-76: splitmix64(base + index * golden_gamma)."""
+    z = (base + index * 0x9E3779B97F4A7C15 + 0x9E3779B97F4A7C15) & _MASK
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _MASK
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _MASK
+    return z ^ (z >> 31)
+
+
+def _side(side: str) -> int:
+    if side == "right":
+        return N.HD_RIGHT
+    if side == "left":
+        return N.HD_LEFT
+    raise ValueError("side must be 'right' or 'left'")  # module.cpp:24-28
+
+
+def _is_torch_cuda(x) -> bool:
+    return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
+
+
+class _Operator:
+    _ensemble = -1
+
+    def __init__(self, m: int, n: int, sigma: float, seed: int, *, dtype: str = "f64", draws: str = "philox",
+                 capacity: int = 0, stream: int = 0, skip_reflector: bool = False, sign_rule: str = "stable",
+                 device: int = 0):
+        cfg = N.hd_config()
+        cfg.ensemble = self._ensemble
+        cfg.dtype = {"f64": N.HD_F64, "f32": N.HD_F32}[dtype]
+        cfg.m, cfg.n = int(m), int(n)
+        cfg.sigma = float(sigma)
+        cfg.seed = int(seed) & _MASK
+        cfg.stream = int(stream)
+        cfg.capacity = int(capacity)
+        cfg.draw_mode = {"philox": N.HD_DRAWS_PHILOX, "injected": N.HD_DRAWS_INJECTED}[draws]
+        cfg.skip_reflector = int(bool(skip_reflector))
+        cfg.sign_rule = N.SIGN_RULES[sign_rule]
+        cfg.device = int(device)
+        h = C.c_void_p()
+        N.check(N.lib().hd_create(C.byref(cfg), C.byref(h)))
+        self._h = h
+        self._np_dtype = np.float64 if dtype == "f64" else np.float32
+        self.dtype = dtype
+        self.device = int(device)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                N.lib().hd_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # ProbeOperator interface (operators.hpp:29-49)
+    @property
+    def rows(self) -> int:
+        r, c = C.c_int64(), C.c_int64()
+        N.check(N.lib().hd_shape(self._h, C.byref(r), C.byref(c)))
+        return r.value
+
+    @property
+    def cols(self) -> int:
+        r, c = C.c_int64(), C.c_int64()
+        N.check(N.lib().hd_shape(self._h, C.byref(r), C.byref(c)))
+        return c.value
+
+    @property
+    def remaining_probes(self) -> int:
+        v = C.c_int64()
+        N.check(N.lib().hd_remaining(self._h, C.byref(v)))
+        return v.value
+
+    def probe_counts(self):
+        r, l = C.c_int64(), C.c_int64()
+        N.check(N.lib().hd_counts(self._h, C.byref(r), C.byref(l)))
+        return r.value, l.value
+
+    def chain_sizes(self):
+        r, l = C.c_int64(), C.c_int64()
+        N.check(N.lib().hd_chain_sizes(self._h, C.byref(r), C.byref(l)))
+        return r.value, l.value
+
+    def _out_len(self, side: int) -> int:
+        return self.rows if side == N.HD_RIGHT else self.cols
+
+    def probe(self, x, side: str = "right"):
+        """Q @ x ('right') or Q.T @ x ('left'), revealing only the randomness
+        the probe requires (module.cpp:79-87)."""
+        s = _side(side)
+        if _is_torch_cuda(x):
+            import torch
+
+            xt = x.contiguous()
+            want = torch.float64 if self.dtype == "f64" else torch.float32
+            if xt.dtype != want:
+                xt = xt.to(want)
+            out = torch.empty(self._out_len(s if self._ensemble != N.HD_GOE else N.HD_RIGHT), dtype=want,
+                              device=xt.device)
+            stream = torch.cuda.current_stream(xt.device).cuda_stream
+            N.check(N.lib().hd_probe(self._h, C.c_void_p(xt.data_ptr()), xt.numel(), C.c_void_p(out.data_ptr()),
+                                     out.numel(), s, 1, C.c_void_p(stream)))
+            return out
+        xa = np.ascontiguousarray(np.asarray(x, dtype=self._np_dtype).reshape(-1))
+        out_len = self._out_len(s if self._ensemble != N.HD_GOE else N.HD_RIGHT)
+        y = np.empty(out_len, dtype=self._np_dtype)
+        N.check(N.lib().hd_probe(self._h, xa.ctypes.data_as(C.c_void_p), xa.size, y.ctypes.data_as(C.c_void_p),
+                                 y.size, s, 0, None))
+        return y
+
+    # parity mode
+    def push_draws(self, g) -> None:
+        ga = np.ascontiguousarray(np.asarray(g, dtype=np.float64).reshape(-1))
+        N.check(N.lib().hd_push_draws(self._h, ga.ctypes.data_as(C.c_void_p), ga.size, 0))
+
+    def reset(self) -> None:
+        N.check(N.lib().hd_reset(self._h))
+
+    # device dynamics (run_dynamics, dynamics.hpp:42-76, built-in maps)
+    def run(self, x1, iterations: int, update: str = "normalize", sides: str = "alternate", x0=None,
+            keep_trajectory: bool = False, use_graph: bool = False):
+        a = N.hd_run_args()
+        a.update = N.UPDATES[update]
+        a.side_rule = N.SIDE_RULES[sides]
+        a.iterations = int(iterations)
+        a.use_graph = int(bool(use_graph))
+        if _is_torch_cuda(x1):
+            import torch
+
+            want = torch.float64 if self.dtype == "f64" else torch.float32
+            x1t = x1.contiguous().to(want)
+            a.x1 = x1t.data_ptr()
+            x0t = None
+            if x0 is not None:
+                x0t = x0.contiguous().to(want)
+                a.x0 = x0t.data_ptr()
+            a.on_device = 1
+            fdim = self._final_dim(iterations, sides, x1t.numel())
+            fin = torch.empty(fdim, dtype=want, device=x1t.device)
+            a.final_out = fin.data_ptr()
+            traj = None
+            if keep_trajectory:
+                traj = torch.empty((iterations + 1, x1t.numel()), dtype=want, device=x1t.device)
+                a.traj = traj.data_ptr()
+            a.stream = torch.cuda.current_stream(x1t.device).cuda_stream
+            N.check(N.lib().hd_run(self._h, C.byref(a)))
+            return traj if keep_trajectory else fin
+        x1a = np.ascontiguousarray(np.asarray(x1, dtype=self._np_dtype).reshape(-1))
+        a.x1 = x1a.ctypes.data
+        x0a = None
+        if x0 is not None:
+            x0a = np.ascontiguousarray(np.asarray(x0, dtype=self._np_dtype).reshape(-1))
+            a.x0 = x0a.ctypes.data
+        fdim = self._final_dim(iterations, sides, x1a.size)
+        fin = np.empty(fdim, dtype=self._np_dtype)
+        a.final_out = fin.ctypes.data
+        traj = None
+        if keep_trajectory:
+            traj = np.empty((iterations + 1, x1a.size), dtype=self._np_dtype)
+            a.traj = traj.ctypes.data
+        N.check(N.lib().hd_run(self._h, C.byref(a)))
+        return traj if keep_trajectory else fin
+
+    def _final_dim(self, iterations: int, sides: str, dim1: int) -> int:
+        if iterations == 0:
+            return dim1
+        if self._ensemble == N.HD_GOE:
+            return self.rows
+        last = iterations
+        right = sides == "right" or (sides == "alternate" and last % 2 == 1)
+        return self.rows if right else self.cols
+
+    # instrumentation
+    def set_profiling(self, on: bool = True) -> None:
+        N.check(N.lib().hd_set_profiling(self._h, int(on)))
+
+    def kernel_stats(self):
+        cnt = C.c_int32()
+        N.check(N.lib().hd_get_stats(self._h, None, 0, C.byref(cnt)))
+        arr = (N.hd_kernel_stats * max(cnt.value, 1))()
+        N.check(N.lib().hd_get_stats(self._h, arr, cnt.value, C.byref(cnt)))
+        return {arr[i].name.decode(): {"launches": arr[i].launches, "ms": arr[i].ms, "alg_bytes": arr[i].alg_bytes}
+                for i in range(cnt.value)}
+
+    def reset_stats(self) -> None:
+        N.check(N.lib().hd_reset_stats(self._h))
+
+    def launch_count(self) -> int:
+        v = C.c_int64()
+        N.check(N.lib().hd_launch_count(self._h, C.byref(v)))
+        return v.value
+
+
+class GinibreOperator(_Operator):
+    """Lazy m x n Gaussian matrix, entries N(0, sigma^2) (ginibre.hpp:26-118)."""
+
+    _ensemble = N.HD_GINIBRE
+
+    def __init__(self, m: int, n: int, sigma: float = 1.0, seed: int = 1, **kw):
+        super().__init__(m, n, sigma, seed, **kw)
+
+
+class HaarOperator(_Operator):
+    """Lazy n x n Haar-orthogonal matrix (haar.hpp:21-76)."""
+
+    _ensemble = N.HD_HAAR
+
+    def __init__(self, n: int, seed: int = 1, **kw):
+        super().__init__(n, n, 1.0, seed, **kw)
+
+    def reconstruct(self):
+        """Materialise Q by right-probing the natural basis; consumes the whole
+        budget (haar.hpp:80-91, module.cpp:105-111)."""
+        r, _ = self.probe_counts()
+        if r != 0:
+            raise ValueError("reconstruct: operator already probed")
+        n = self.rows
+        q = np.empty((n, n), dtype=self._np_dtype)
+        for j in range(n):
+            e = np.zeros(n, dtype=self._np_dtype)
+            e[j] = 1.0
+            q[:, j] = self.probe(e, "right")
+        return q
+
+
+class GOEOperator(_Operator):
+    """Lazy symmetric Gaussian matrix: (inner right + inner left probe)/sqrt(2)
+    over a square Ginibre of entry std ``sigma`` (ensembles.hpp:93-131)."""
+
+    _ensemble = N.HD_GOE
+
+    def __init__(self, n: int, seed: int = 1, sigma: float = 1.0, **kw):
+        super().__init__(n, n, sigma, seed, **kw)
+
+
+def make_reflector(p, offset: int = 0):
+    raise NotImplementedError("make_reflector: standalone reflector utility is served inside the operators "
+                              "this round (SURVEY.md §8a a5); see DESIGN.md")
+
+
+def sample_dense_haar(n: int, seed: int = 1):
+    raise NotImplementedError("sample_dense_haar: dense oracle is out of scope (SURVEY.md §8f f4)")
+
+
+def ista_curves(*args, **kwargs):
+    raise NotImplementedError("ista_curves: application driver is out of scope (SURVEY.md §8f f3)")
+
+
+def spectral_summary(*args, **kwargs):
+    raise NotImplementedError("spectral_summary: application driver is out of scope (SURVEY.md §8f f3)")
+
+
+def two_sample_ks(a, b):
+    raise NotImplementedError("two_sample_ks: statistics harness is out of scope (SURVEY.md §8f f4)")
