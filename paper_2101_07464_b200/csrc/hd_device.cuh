@@ -165,6 +165,22 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Four warp sums at once (fixed butterfly, 6 shuffles instead of 20).
+// Returns the full sum of d[(lane >> 3) & 3] in every lane.
+__device__ __forceinline__ double warp_sum4(double d0, double d1, double d2, double d3, int lane) {
+  const bool hi = lane & 16;
+  const double k0 = hi ? d2 : d0, k1 = hi ? d3 : d1;
+  const double s0 = hi ? d0 : d2, s1 = hi ? d1 : d3;
+  const double e0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 16);
+  const double e1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 16);
+  const bool hb = lane & 8;
+  double f = (hb ? e1 : e0) + __shfl_xor_sync(0xffffffffu, hb ? e0 : e1, 8);
+  f += __shfl_xor_sync(0xffffffffu, f, 4);
+  f += __shfl_xor_sync(0xffffffffu, f, 2);
+  f += __shfl_xor_sync(0xffffffffu, f, 1);
+  return f;
+}
+
 // Deterministic block sum (fixed tree); result valid in all threads.
 template <int NT>
 __device__ __forceinline__ double block_sum(double v, double* sh) {
@@ -183,6 +199,56 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   t = sh[0];
   __syncthreads();
   return t;
+}
+
+// ------------------------------------------- TMA bulk copies + mbarriers
+// The streaming kernels stage panel chunks global -> shared with
+// cp.async.bulk (SASS UBLKCP) completing on an mbarrier transaction count;
+// a single producer thread keeps a ring of stages in flight while the
+// consumer warps compute.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// global -> shared bulk copy (bytes % 16 == 0, 16 B aligned), evict-first
+// in L2: every panel byte is streamed exactly once per pass.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .b64 pol;\n"
+      "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n"
+      "}\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 }  // namespace hd

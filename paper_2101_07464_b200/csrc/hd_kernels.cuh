@@ -19,6 +19,83 @@
 
 namespace hd {
 
+
+// Cross-CTA reduction of a CTA's slot row acc[nslots] (shared memory):
+// groups of kGroup consecutive CTAs — each CTA parks its row in `scratch`,
+// and the last CTA of the group to arrive (fence + atomic ticket) adds the
+// group's rows in fixed CTA order, so one partial per group reaches the
+// single-CTA kernels and results stay bitwise deterministic:
+//   partials[s * ngroups + group].
+// Kernels using this never return early (every CTA must take a ticket).
+constexpr int kGroup = 8;
+
+struct Flush {
+  double* partials = nullptr;  // [nslots][ngroups]
+  double* scratch = nullptr;   // [gridDim.x][nslots]
+  int* counters = nullptr;     // [ngroups], zero between launches
+};
+
+__device__ __forceinline__ void flush_row(const double* acc, int nslots, const Flush& f) {
+  __shared__ int s_last;
+  __syncthreads();
+  double* row = f.scratch + (size_t)blockIdx.x * nslots;
+  for (int s = threadIdx.x; s < nslots; s += blockDim.x) row[s] = acc[s];
+  __threadfence();
+  __syncthreads();
+  const int grp = blockIdx.x / kGroup;
+  const int b0 = grp * kGroup;
+  const int gsz = min(kGroup, (int)gridDim.x - b0);
+  if (threadIdx.x == 0) s_last = (atomicAdd(f.counters + grp, 1) == gsz - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int ng = ((int)gridDim.x + kGroup - 1) / kGroup;
+  for (int s = threadIdx.x; s < nslots; s += blockDim.x) {
+    double v = 0.0;
+    for (int b = 0; b < gsz; ++b) v += __ldcg(f.scratch + (size_t)(b0 + b) * nslots + s);
+    f.partials[(size_t)s * ng + grp] = v;
+  }
+  if (threadIdx.x == 0) f.counters[grp] = 0;
+}
+
+// ------------------------------------------- TMA-pipelined streaming warps
+// Each warp streams its own contiguous run of 256-row tiles through a
+// private ring of kRing shared-memory stages: lane 0 keeps kRing chunks
+// (kCW columns of one tile = kCW x 2 KB contiguous in the tile-major panel)
+// in flight with cp.async.bulk, the whole warp consumes a chunk and lane 0
+// refills the slot. No inter-warp synchronisation in the streaming loop;
+// per-warp slot rows keep the GEMV-T sums deterministic.
+constexpr int kCW = 4;
+constexpr int kRing = 3;
+constexpr int kMaxWarps = 8;
+
+template <typename T>
+__device__ __forceinline__ double2 lds_pair(const T* p) {
+  if constexpr (sizeof(T) == 8) {
+    return *reinterpret_cast<const double2*>(p);
+  } else {
+    const float2 f = *reinterpret_cast<const float2*>(p);
+    return make_double2(f.x, f.y);
+  }
+}
+
+// Stage `it` of a warp's stream -> (tile, job, chunk) given per-job chunk
+// counts; the stream is tile-major, then job, then chunk.
+struct StreamPos {
+  int64_t tile;
+  int job, chunk;
+};
+
+__device__ __forceinline__ StreamPos stream_pos(int64_t t0, uint32_t it, int nch0, int nch1) {
+  const int per = nch0 + nch1;
+  StreamPos p;
+  p.tile = t0 + it / per;
+  const int r = (int)(it % per);
+  p.job = (r < nch0) ? 0 : 1;
+  p.chunk = (r < nch0) ? r : r - nch0;
+  return p;
+}
+
 // ------------------------------------------------------------------ status
 // status[0]: abort (non-zero: every later kernel of this op returns at once)
 // status[1]: first non-finite dynamics step (INT_MAX = none)
@@ -63,137 +140,120 @@ struct DotArgs {
   DotJob<T> job[2];
   int njobs = 1;
   int64_t n = 0, ntiles = 0;
-  double* partials = nullptr;  // [gridDim.x][nslots]
+  Flush out;
   int nslots = 0;
   int* status = nullptr;
 };
 
-// Each warp owns a contiguous run of 256-row tiles and streams every panel
-// column of its tile once (4 x 16 B loads per lane per column, coalesced
-// 2 KB per warp); per-column lane partials are warp-reduced and accumulated
-// into the warp's own shared-memory slots, so no atomics are involved and
-// the result is bitwise deterministic for a fixed grid.
-template <typename T, int NW>
-__global__ void __launch_bounds__(NW * 32) k_dots(const __grid_constant__ DotArgs<T> a) {
-  extern __shared__ double acc_s[];
-  if (aborted(a.status)) return;
+// Shared-memory carve-up of the streaming kernels (per warp: ring + slots).
+template <typename T>
+__host__ __device__ constexpr size_t ring_bytes() {
+  return (size_t)kRing * kCW * kTile * sizeof(T);
+}
+
+// GEMV-T a = P^T v (k_dots). Lane l holds rows 2(l + 32q) + {0, 1} of the
+// current tile's right-hand side(s); each 4-column chunk costs 16 LDS.128,
+// 32 (or 64 with a pending column) DFMA and one 4-way butterfly.
+template <typename T>
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) k_dots(const __grid_constant__ DotArgs<T> a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int nw = blockDim.x >> 5;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* acc = acc_s + (size_t)w * a.nslots;
-  for (int s = lane; s < a.nslots; s += 32) acc[s] = 0.0;
+  const int nsl = (a.nslots + 1) & ~1;
+  unsigned char* ring = smem + (size_t)w * ring_bytes<T>();
+  double* accs = reinterpret_cast<double*>(smem + (size_t)nw * ring_bytes<T>());
+  double* acc = accs + (size_t)w * nsl;
+  uint64_t* full = reinterpret_cast<uint64_t*>(accs + (size_t)nw * nsl) + w * kRing;
+  for (int s = lane; s < nsl; s += 32) acc[s] = 0.0;
+  if (lane == 0) {
+    for (int s = 0; s < kRing; ++s) mbar_init(full + s, 1);
+    mbar_fence_init();
+  }
   __syncwarp();
+  const bool skip = aborted(a.status);
+  const int64_t W = (int64_t)gridDim.x * nw;
+  const int64_t gw = (int64_t)blockIdx.x * nw + w;
+  const int64_t t0 = gw * a.ntiles / W, t1 = skip ? t0 : (gw + 1) * a.ntiles / W;
+  const int nch0 = (a.job[0].ncols + kCW - 1) / kCW;
+  const int nch1 = (a.njobs > 1) ? (a.job[1].ncols + kCW - 1) / kCW : 0;
+  const uint32_t nst = (uint32_t)((t1 - t0) * (nch0 + nch1));
+  auto issue = [&](uint32_t it) {
+    const StreamPos p = stream_pos(t0, it, nch0, nch1);
+    const DotJob<T>& J = a.job[p.job];
+    const int nc = min(kCW, J.ncols - p.chunk * kCW);
+    const uint32_t bytes = (uint32_t)(nc * kTile * sizeof(T));
+    const int s = it % kRing;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the slot precede the refill
+    mbar_arrive_expect_tx(full + s, bytes);
+    bulk_g2s(ring + (size_t)s * kCW * kTile * sizeof(T),
+             J.P + (size_t)p.tile * (size_t)(J.K << kTileShift) + (size_t)p.chunk * kCW * kTile, bytes, full + s);
+  };
+  if (lane == 0)
+    for (uint32_t it = 0; it < (uint32_t)kRing && it < nst; ++it) issue(it);
 
-  const int64_t W = (int64_t)gridDim.x * NW;
-  const int64_t gw = (int64_t)blockIdx.x * NW + w;
-  const int64_t t0 = gw * a.ntiles / W, t1 = (gw + 1) * a.ntiles / W;
-  double ss[2] = {0.0, 0.0};
+  double ss0 = 0.0, ss1 = 0.0;
   bool bad = false;
-
+  double2 x[4], pv[4];
+  uint32_t it = 0;
   for (int64_t tile = t0; tile < t1; ++tile) {
     for (int jb = 0; jb < a.njobs; ++jb) {
       const DotJob<T>& J = a.job[jb];
-      double2 x[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int64_t i = tile * kTile + 2 * (lane + 32 * q);
         x[q] = src_pair(J.rhs, i, a.n);
-        ss[jb] += x[q].x * x[q].x + x[q].y * x[q].y;
+        const double sq = x[q].x * x[q].x + x[q].y * x[q].y;
+        if (jb == 0) ss0 += sq;
+        else ss1 += sq;
         if (J.check_finite) bad |= !(isfinite(x[q].x) && isfinite(x[q].y));
         if (J.pivot_out && (i == J.pivot_row || i + 1 == J.pivot_row)) *J.pivot_out = (i == J.pivot_row) ? x[q].x : x[q].y;
         if (J.wcol) st_pair(J.wcol + paddr(i, J.wj, J.wK), x[q].x, x[q].y);
+        pv[q] = (J.pend >= 0) ? ld_pair(J.P + paddr(i, J.pend, J.K)) : make_double2(0.0, 0.0);
       }
-      const T* base = J.P + (size_t)tile * (size_t)(J.K << kTileShift) + 2 * lane;
-      if (J.pend >= 0) {
-        double2 pv[4];
+      const int nch = (J.ncols + kCW - 1) / kCW;
+      for (int c = 0; c < nch; ++c, ++it) {
+        const int s = it % kRing;
+        mbar_wait(full + s, (it / kRing) & 1);
+        const T* sp = reinterpret_cast<const T*>(ring + (size_t)s * kCW * kTile * sizeof(T)) + 2 * lane;
+        double d[kCW], e[kCW];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) pv[q] = ld_pair(base + (size_t)J.pend * kTile + 64 * q);
-        int j = 0;
-        for (; j + 2 <= J.ncols; j += 2) {
-          double2 w0[4], w1[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            w0[q] = ld_pair(base + (size_t)j * kTile + 64 * q);
-            w1[q] = ld_pair(base + (size_t)(j + 1) * kTile + 64 * q);
-          }
-          double d0 = 0, d1 = 0, e0 = 0, e1 = 0;
+        for (int u = 0; u < kCW; ++u) {
+          d[u] = 0.0;
+          e[u] = 0.0;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            d0 += w0[q].x * x[q].x + w0[q].y * x[q].y;
-            d1 += w1[q].x * x[q].x + w1[q].y * x[q].y;
-            e0 += w0[q].x * pv[q].x + w0[q].y * pv[q].y;
-            e1 += w1[q].x * pv[q].x + w1[q].y * pv[q].y;
-          }
-          d0 = warp_sum(d0);
-          d1 = warp_sum(d1);
-          e0 = warp_sum(e0);
-          e1 = warp_sum(e1);
-          if (lane == 0) {
-            acc[J.slot_dot + j] += d0;
-            acc[J.slot_dot + j + 1] += d1;
-            if (j <= J.pend) acc[J.slot_pend + j] += e0;
-            if (j + 1 <= J.pend) acc[J.slot_pend + j + 1] += e1;
+            const double2 wv = lds_pair(sp + u * kTile + 64 * q);
+            d[u] += wv.x * x[q].x + wv.y * x[q].y;
+            e[u] += wv.x * pv[q].x + wv.y * pv[q].y;
           }
         }
-        for (; j < J.ncols; ++j) {
-          double d0 = 0, e0 = 0;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const double2 w0 = ld_pair(base + (size_t)j * kTile + 64 * q);
-            d0 += w0.x * x[q].x + w0.y * x[q].y;
-            e0 += w0.x * pv[q].x + w0.y * pv[q].y;
-          }
-          d0 = warp_sum(d0);
-          e0 = warp_sum(e0);
-          if (lane == 0) {
-            acc[J.slot_dot + j] += d0;
-            if (j <= J.pend) acc[J.slot_pend + j] += e0;
-          }
-        }
-      } else {
-        int j = 0;
-        for (; j + 4 <= J.ncols; j += 4) {
-          double2 w[4][4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) w[u][q] = ld_pair(base + (size_t)(j + u) * kTile + 64 * q);
-          double d[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            d[u] = 0.0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) d[u] += w[u][q].x * x[q].x + w[u][q].y * x[q].y;
-            d[u] = warp_sum(d[u]);
-          }
-          if (lane == 0) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) acc[J.slot_dot + j + u] += d[u];
-          }
-        }
-        for (; j < J.ncols; ++j) {
-          double d0 = 0;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const double2 w0 = ld_pair(base + (size_t)j * kTile + 64 * q);
-            d0 += w0.x * x[q].x + w0.y * x[q].y;
-          }
-          d0 = warp_sum(d0);
-          if (lane == 0) acc[J.slot_dot + j] += d0;
+        __syncwarp();
+        if (lane == 0 && it + kRing < nst) issue(it + kRing);
+        const int col0 = c * kCW;
+        const double f = warp_sum4(d[0], d[1], d[2], d[3], lane);
+        const int u = lane >> 3;
+        if ((lane & 7) == 0 && col0 + u < J.ncols) acc[J.slot_dot + col0 + u] += f;
+        if (J.pend >= 0 && col0 <= J.pend) {
+          const double g = warp_sum4(e[0], e[1], e[2], e[3], lane);
+          if ((lane & 7) == 0 && col0 + u <= J.pend) acc[J.slot_pend + col0 + u] += g;
         }
       }
     }
   }
-  for (int jb = 0; jb < a.njobs; ++jb) {
-    const double v = warp_sum(ss[jb]);
-    if (lane == 0 && a.job[jb].slot_sumsq >= 0) acc[a.job[jb].slot_sumsq] += v;
+  ss0 = warp_sum(ss0);
+  ss1 = warp_sum(ss1);
+  if (lane == 0) {
+    if (a.job[0].slot_sumsq >= 0) acc[a.job[0].slot_sumsq] += ss0;
+    if (a.njobs > 1 && a.job[1].slot_sumsq >= 0) acc[a.job[1].slot_sumsq] += ss1;
   }
   if (bad) atomicOr(a.status + kStBadInput, 1);
   __syncthreads();
-  for (int s = threadIdx.x; s < a.nslots; s += NW * 32) {
+  for (int s = threadIdx.x; s < a.nslots; s += blockDim.x) {
     double v = 0.0;
-#pragma unroll
-    for (int u = 0; u < NW; ++u) v += acc_s[(size_t)u * a.nslots + s];
-    a.partials[(size_t)blockIdx.x * a.nslots + s] = v;
+    for (int u = 0; u < nw; ++u) v += accs[(size_t)u * nsl + s];
+    accs[s] = v;  // row 0 (each slot owned by one thread here)
   }
+  flush_row(accs, a.nslots, a.out);
 }
 
 // ============================================================ GEMV-N core
@@ -306,91 +366,188 @@ __device__ __forceinline__ void epilogue(const Epi<T>& e, int* status, int64_t i
   }
 }
 
-// ============================================================== k_fold
-// p = D (x - P beta): the forward chain application of ginibre.hpp:68 /
-// haar.hpp:55 in compact-WY form. Also writes the new reflector column
-// (p[off:] times an exact power of two; the pivot is fixed once ||p[off:]||
-// is known), keeps p[0..off] and the per-block sums of p[off:]^2.
+// ============================================================= k_apply
+// GEMV-N on the TMA ring: warp w accumulates P[:, 8c + w] beta_{8c+w} into
+// its 8 rows-per-lane registers over all chunks of the tile; the 8 warps'
+// row partials are combined through shared memory (fixed order) and the
+// tile epilogue runs on 128 threads x 2 rows. The same column loads can also
+// feed a GEMV-T against the NEXT probe's fresh draw (regenerated on-chip
+// from Philox, or read from the injected queue): the Gram dots the next Haar
+// mix reflector needs (haar.hpp:57,63), so no extra pass over the other
+// chain is required.
+//   FOLD : p = D (x - acc)  -> new column p[off:] * 2^-e, head p[0..off],
+//          ||p[off:]||^2
+//   OTHER: y = D z - acc    -> epilogue (output / dynamics), ||y||^2
+enum ApplyMode : int { kApplyFold = 0, kApplyOther = 1 };
+
 template <typename T>
-struct FoldArgs {
+struct ApplyArgs {
   const T* P = nullptr;
   int64_t K = 0;
   int ncols = 0;
   const double* beta = nullptr;
-  Src<T> x;
+  int64_t n = 0, ntiles = 0;
   const double* D = nullptr;
   const double* Dtail = nullptr;
   int64_t Dlen = 0;
-  T* Pw = nullptr;       // panel receiving the new column (== P for the fold chain)
-  int64_t newj = 0;
-  int64_t off = 0;
-  const double* escale = nullptr;  // 2^-e
-  double* head = nullptr;          // p[0..off]
-  double* partials = nullptr;      // [gridDim.x]
-  int64_t n = 0;
-  int* status = nullptr;
-};
-
-template <typename T>
-__global__ void __launch_bounds__(kUpdThreads) k_fold(const __grid_constant__ FoldArgs<T> a) {
-  extern __shared__ double beta_s[];
-  __shared__ double red_s[32];
-  if (aborted(a.status)) return;
-  for (int j = threadIdx.x; j < a.ncols; j += kUpdThreads) beta_s[j] = a.beta[j];
-  __syncthreads();
-  const int64_t tile = blockIdx.x;
-  const int64_t i = tile * kTile + 2 * threadIdx.x;
-  const double* bp[1] = {beta_s};
-  double2 acc[1];
-  panel_accumulate<T, 1>(a.P, a.K, a.ncols, tile, threadIdx.x, bp, acc);
-  const double2 xv = src_pair(a.x, i, a.n);
-  double p0 = 0.0, p1 = 0.0;
-  if (i < a.n) p0 = dval(a.D, a.Dtail, a.Dlen, i) * (xv.x - acc[0].x);
-  if (i + 1 < a.n) p1 = dval(a.D, a.Dtail, a.Dlen, i + 1) * (xv.y - acc[0].y);
-  const double es = *a.escale;
-  const double c0 = (i >= a.off) ? p0 : 0.0, c1 = (i + 1 >= a.off) ? p1 : 0.0;
-  st_pair(a.Pw + paddr(i, a.newj, a.K), c0 * es, c1 * es);
-  if (i <= a.off) a.head[i] = p0;
-  if (i + 1 <= a.off) a.head[i + 1] = p1;
-  const double t = block_sum<kUpdThreads>(c0 * c0 + c1 * c1, red_s);
-  if (threadIdx.x == 0) a.partials[blockIdx.x] = t;
-}
-
-// ============================================================= k_other
-// y = D z - P beta with z supported on rows < zlen: the reverse-adjoint
-// application of the other chain to the folded iterate (haar.hpp:65).
-template <typename T>
-struct OtherArgs {
-  const T* P = nullptr;
-  int64_t K = 0;
-  int ncols = 0;
-  const double* beta = nullptr;
+  // fold
+  Src<T> x;
+  T* Pw = nullptr;
+  int64_t newj = 0, off = 0;
+  const double* escale = nullptr;
+  double* head = nullptr;
+  // other
   const double* z = nullptr;
   int64_t zlen = 0;
-  const double* D = nullptr;
-  const double* Dtail = nullptr;
-  int64_t Dlen = 0;
-  int64_t n = 0;
-  int* status = nullptr;
   Epi<T> epi;
+  // speculative dots with the next draw (kind kSrcNone = off; OTHER only)
+  Src<T> spec;
+  int slot_spec = 0;  // [ncols]
+  int slot_ss = 0;    // fold: ||p[off:]||^2; other: ||y||^2
+  Flush out;
+  int nslots = 0;
+  int* status = nullptr;
 };
 
-template <typename T>
-__global__ void __launch_bounds__(kUpdThreads) k_other(const __grid_constant__ OtherArgs<T> a) {
-  extern __shared__ double beta_s[];
-  __shared__ double red_s[32];
-  if (aborted(a.status)) return;
-  for (int j = threadIdx.x; j < a.ncols; j += kUpdThreads) beta_s[j] = a.beta[j];
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_constant__ ApplyArgs<T> a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int nw = blockDim.x >> 5;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nsl = (a.nslots + 1) & ~1;
+  const int nb = (a.ncols + 1) & ~1;
+  unsigned char* ring = smem + (size_t)w * ring_bytes<T>();
+  double* beta_s = reinterpret_cast<double*>(smem + (size_t)nw * ring_bytes<T>());
+  double* accs = beta_s + nb;
+  double* acc = accs + (size_t)w * nsl;
+  uint64_t* full = reinterpret_cast<uint64_t*>(accs + (size_t)nw * nsl) + w * kRing;
+  for (int j = threadIdx.x; j < a.ncols; j += blockDim.x) beta_s[j] = a.beta[j];
+  for (int s = lane; s < nsl; s += 32) acc[s] = 0.0;
+  if (lane == 0) {
+    for (int s = 0; s < kRing; ++s) mbar_init(full + s, 1);
+    mbar_fence_init();
+  }
   __syncthreads();
-  const int64_t tile = blockIdx.x;
-  const int64_t i = tile * kTile + 2 * threadIdx.x;
-  const double* bp[1] = {beta_s};
-  double2 acc[1];
-  panel_accumulate<T, 1>(a.P, a.K, a.ncols, tile, threadIdx.x, bp, acc);
-  double z0 = 0.0, z1 = 0.0;
-  if (i < a.zlen) z0 = dval(a.D, a.Dtail, a.Dlen, i) * a.z[i];
-  if (i + 1 < a.zlen) z1 = dval(a.D, a.Dtail, a.Dlen, i + 1) * a.z[i + 1];
-  epilogue(a.epi, a.status, i, a.n, make_double2(z0 - acc[0].x, z1 - acc[0].y), red_s);
+  const bool skip = aborted(a.status);
+  const bool spec = (a.spec.kind != kSrcNone);
+  const int64_t W = (int64_t)gridDim.x * nw;
+  const int64_t gw = (int64_t)blockIdx.x * nw + w;
+  const int64_t t0 = gw * a.ntiles / W, t1 = skip ? t0 : (gw + 1) * a.ntiles / W;
+  const int nch = (a.ncols + kCW - 1) / kCW;
+  const uint32_t nst = (uint32_t)((t1 - t0) * nch);
+  auto issue = [&](uint32_t it) {
+    const int64_t tile = t0 + it / nch;
+    const int c = (int)(it % nch);
+    const int nc = min(kCW, a.ncols - c * kCW);
+    const uint32_t bytes = (uint32_t)(nc * kTile * sizeof(T));
+    const int s = it % kRing;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive_expect_tx(full + s, bytes);
+    bulk_g2s(ring + (size_t)s * kCW * kTile * sizeof(T),
+             a.P + (size_t)tile * (size_t)(a.K << kTileShift) + (size_t)c * kCW * kTile, bytes, full + s);
+  };
+  if (lane == 0)
+    for (uint32_t it = 0; it < (uint32_t)kRing && it < nst; ++it) issue(it);
+
+  double ss = 0.0;
+  bool bad = false;
+  uint32_t it = 0;
+  for (int64_t tile = t0; tile < t1; ++tile) {
+    double2 g[4], r[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      g[q] = spec ? src_pair(a.spec, tile * kTile + 2 * (lane + 32 * q), a.n) : make_double2(0.0, 0.0);
+      r[q] = make_double2(0.0, 0.0);
+    }
+    for (int c = 0; c < nch; ++c, ++it) {
+      const int s = it % kRing;
+      mbar_wait(full + s, (it / kRing) & 1);
+      const T* sp = reinterpret_cast<const T*>(ring + (size_t)s * kCW * kTile * sizeof(T)) + 2 * lane;
+      const int col0 = c * kCW;
+      double d[kCW];
+#pragma unroll
+      for (int u = 0; u < kCW; ++u) {
+        const double b = (col0 + u < a.ncols) ? beta_s[col0 + u] : 0.0;
+        d[u] = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          double2 wv = lds_pair(sp + u * kTile + 64 * q);
+          if (col0 + u >= a.ncols) wv = make_double2(0.0, 0.0);
+          r[q].x += wv.x * b;
+          r[q].y += wv.y * b;
+          d[u] += wv.x * g[q].x + wv.y * g[q].y;
+        }
+      }
+      __syncwarp();
+      if (lane == 0 && it + kRing < nst) issue(it + kRing);
+      if (spec) {
+        const double f = warp_sum4(d[0], d[1], d[2], d[3], lane);
+        const int u = lane >> 3;
+        if ((lane & 7) == 0 && col0 + u < a.ncols) acc[a.slot_spec + col0 + u] += f;
+      }
+    }
+    // epilogue on the lane's 8 rows
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = tile * kTile + 2 * (lane + 32 * q);
+      const double d0 = (i < a.Dlen) ? a.D[i] : *a.Dtail;
+      const double d1 = (i + 1 < a.Dlen) ? a.D[i + 1] : *a.Dtail;
+      if constexpr (MODE == kApplyFold) {
+        const double2 xv = src_pair(a.x, i, a.n);
+        const double p0 = (i < a.n) ? d0 * (xv.x - r[q].x) : 0.0;
+        const double p1 = (i + 1 < a.n) ? d1 * (xv.y - r[q].y) : 0.0;
+        const double c0 = (i >= a.off) ? p0 : 0.0, c1 = (i + 1 >= a.off) ? p1 : 0.0;
+        const double es = *a.escale;
+        st_pair(a.Pw + paddr(i, a.newj, a.K), c0 * es, c1 * es);
+        if (i <= a.off) a.head[i] = p0;
+        if (i + 1 <= a.off) a.head[i + 1] = p1;
+        ss += c0 * c0 + c1 * c1;
+      } else {
+        double z0 = 0.0, z1 = 0.0;
+        if (i < a.zlen) z0 = d0 * a.z[i];
+        if (i + 1 < a.zlen) z1 = d1 * a.z[i + 1];
+        double2 y = make_double2(z0 - r[q].x, z1 - r[q].y);
+        const Epi<T>& e = a.epi;
+        if (i < a.n) {
+          if (i + 1 >= a.n) y.y = 0.0;
+          if (e.kind == kEpiTanhMix) {
+            double2 xp = make_double2(0.0, 0.0);
+            if (e.xprev) {
+              xp.x = (double)e.xprev[i];
+              if (i + 1 < a.n) xp.y = (double)e.xprev[i + 1];
+              if (e.xprev_scale) {
+                xp.x *= *e.xprev_scale;
+                xp.y *= *e.xprev_scale;
+              }
+            }
+            const double o0 = tanh(2.0 * y.x) + 0.1 * xp.x;
+            const double o1 = (i + 1 < a.n) ? tanh(2.0 * y.y) + 0.1 * xp.y : 0.0;
+            st_pair_guard(e.xnext, i, a.n, o0, o1);
+            bad |= !(isfinite(o0) && isfinite(o1));
+          } else {
+            bad |= !(isfinite(y.x) && isfinite(y.y));
+            ss += y.x * y.x + y.y * y.y;
+          }
+          if (e.y) st_pair_guard(e.y, i, a.n, y.x, y.y);
+        }
+      }
+    }
+  }
+  ss = warp_sum(ss);
+  if (lane == 0) acc[a.slot_ss] += ss;
+  if constexpr (MODE == kApplyOther) {
+    if (bad) {
+      atomicMin(a.status + kStBadStep, a.epi.step);
+      atomicOr(a.status + kStAbort, 1);
+    }
+  }
+  __syncthreads();
+  for (int s = threadIdx.x; s < a.nslots; s += blockDim.x) {
+    double v = 0.0;
+    for (int u = 0; u < nw; ++u) v += accs[(size_t)u * nsl + s];
+    accs[s] = v;
+  }
+  flush_row(accs, a.nslots, a.out);
 }
 
 // ============================================================ k_ginout
@@ -471,10 +628,26 @@ __device__ void sm_reduce(const double* partials, int nblk, int nslots, double* 
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int s = w; s < nslots; s += kSmallThreads / 32) {
     double v = 0.0;
-    for (int b = lane; b < nblk; b += 32) v += partials[(size_t)b * nslots + s];
+    const double* ps = partials + (size_t)s * nblk;
+    for (int b = lane; b < nblk; b += 32) v += ps[b];
     v = warp_sum(v);
     if (lane == 0) red[s] = v;
   }
+  __syncthreads();
+}
+
+// T_new[:k, k] = -c_k T[:k, :k] g  (g = G[:k, k]); warp per row, lanes
+// split the reduction so every load is independent (no serial chains).
+__device__ void sm_T_column(const ChainDev& ch, int k, double ck) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* g = ch.G + (int64_t)k * ch.K;
+  for (int i = w; i < k; i += kSmallThreads / 32) {
+    double v = 0.0;
+    for (int l = i + lane; l < k; l += 32) v += ch.Tm[i + (int64_t)l * ch.K] * g[l];
+    v = warp_sum(v);
+    if (lane == 0) ch.Tm[i + (int64_t)k * ch.K] = -ck * v;
+  }
+  if (threadIdx.x == 0) ch.Tm[k + (int64_t)k * ch.K] = ck;
   __syncthreads();
 }
 
@@ -485,14 +658,7 @@ __device__ void sm_finalize_pending(const ChainDev& ch, int pend, const double* 
   const double sp = ch.sig[pend];
   for (int j = threadIdx.x; j <= pend; j += kSmallThreads) ch.G[j + pend * K] = ch.sig[j] * sp * rdots[j];
   __syncthreads();
-  const double cp = ch.c[pend];
-  for (int i = threadIdx.x; i < pend; i += kSmallThreads) {
-    double v = 0.0;
-    for (int l = i; l < pend; ++l) v += ch.Tm[i + l * K] * ch.G[l + pend * K];
-    ch.Tm[i + pend * K] = -cp * v;
-  }
-  if (threadIdx.x == 0) ch.Tm[pend + pend * K] = cp;
-  __syncthreads();
+  sm_T_column(ch, pend, ch.c[pend]);
 }
 
 // out = T^T a (k x k upper T): warp per output column.
@@ -507,12 +673,14 @@ __device__ void sm_Tt(const ChainDev& ch, int k, const double* a, double* out) {
   __syncthreads();
 }
 
-// out = T a: thread per output row.
+// out = T a: warp per output row, lanes split the row.
 __device__ void sm_T(const ChainDev& ch, int k, const double* a, double* out) {
-  for (int i = threadIdx.x; i < k; i += kSmallThreads) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = w; i < k; i += kSmallThreads / 32) {
     double v = 0.0;
-    for (int j = i; j < k; ++j) v += ch.Tm[i + (int64_t)j * ch.K] * a[j];
-    out[i] = v;
+    for (int j = i + lane; j < k; j += 32) v += ch.Tm[i + (int64_t)j * ch.K] * a[j];
+    v = warp_sum(v);
+    if (lane == 0) out[i] = v;
   }
   __syncthreads();
 }
@@ -576,14 +744,7 @@ __device__ double sm_make_reflector(const ChainDev& ch, T* P, int j, int64_t off
 __device__ void sm_append_known_gram(const ChainDev& ch, int k, const double* G_col /*[k+1]*/) {
   for (int j = threadIdx.x; j <= k; j += kSmallThreads) ch.G[j + (int64_t)k * ch.K] = G_col[j];
   __syncthreads();
-  const double ck = ch.c[k];
-  for (int i = threadIdx.x; i < k; i += kSmallThreads) {
-    double v = 0.0;
-    for (int l = i; l < k; ++l) v += ch.Tm[i + l * ch.K] * ch.G[l + (int64_t)k * ch.K];
-    ch.Tm[i + (int64_t)k * ch.K] = -ck * v;
-  }
-  if (threadIdx.x == 0) ch.Tm[k + (int64_t)k * ch.K] = ck;
-  __syncthreads();
+  sm_T_column(ch, k, ch.c[k]);
 }
 
 // Scratch words shared between the small kernels of one probe.
@@ -626,7 +787,31 @@ struct SmallArgs {
   double* coefS = nullptr;
   int nS = 0;
   int is_haar = 0;
+  // Haar mix Gram dots P_B^T g[off:]: from k_dots (red + slotB_dot) or from
+  // the speculative pass of the previous probe (spec buffer)
+  const double* mix_dots = nullptr;
+  // reduce a previous k_apply(OTHER)'s speculative slots into spec_dst
+  const double* spec_parts = nullptr;
+  int spec_nblk = 0, spec_slot0 = 0, spec_count = 0;
+  double* spec_dst = nullptr;
+  // k_small_fold: ||p[off:]||^2 slot and speculative slots of k_apply(FOLD)
+  int fold_slot_ss = 0;
+  int fold_slot_spec = -1;
+  double* fold_spec_dst = nullptr;
 };
+
+// dst[s] = sum_b parts[(slot0 + s) * nblk + b] for s < count (fixed order).
+__device__ void sm_reduce_slots(const double* parts, int nblk, int slot0, int count, double* dst) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int s = w; s < count; s += kSmallThreads / 32) {
+    const double* ps = parts + (size_t)(slot0 + s) * nblk;
+    double v = 0.0;
+    for (int b = lane; b < nblk; b += 32) v += ps[b];
+    v = warp_sum(v);
+    if (lane == 0) dst[s] = v;
+  }
+  __syncthreads();
+}
 
 // After k_dots of a probe (Haar and Ginibre "fold" side): finalise pending
 // columns, the Haar mix reflector (chain B), the forward coefficients
@@ -635,6 +820,7 @@ struct SmallArgs {
 template <typename T>
 __global__ void __launch_bounds__(kSmallThreads) k_small_dots(const __grid_constant__ SmallArgs a) {
   if (aborted(a.status)) return;
+  if (a.spec_parts) sm_reduce_slots(a.spec_parts, a.spec_nblk, a.spec_slot0, a.spec_count, a.spec_dst);
   sm_reduce(a.partials, a.nblk, a.nslots, a.red);
   if (threadIdx.x == 0 && *(volatile int*)(a.status + kStBadInput)) *(volatile int*)(a.status + kStAbort) = 1;
   __syncthreads();
@@ -663,7 +849,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_dots(const __grid_const
     const T* PB = (const T*)a.PB;
     for (int j = threadIdx.x; j < a.kB; j += kSmallThreads) {
       a.tmp[j] = (nrm == 0.0) ? 0.0
-                              : a.chB.sig[j] * (a.red[a.slotB_dot + j] / nrm + sign * (double)PB[paddr(a.off, j, a.chB.K)]);
+                              : a.chB.sig[j] * (a.mix_dots[j] / nrm + sign * (double)PB[paddr(a.off, j, a.chB.K)]);
     }
     if (threadIdx.x == 0) a.tmp[a.kB] = (nrm == 0.0) ? 0.0 : 2.0 / a.chB.c[a.kB];
     __syncthreads();
@@ -685,8 +871,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_fold(const __grid_const
   {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     __shared__ double ws[kSmallThreads / 32];
+    const double* ps = a.partials + (size_t)a.fold_slot_ss * a.nblk;
     double v = 0.0;
-    for (int b = threadIdx.x; b < a.nblk; b += kSmallThreads) v += a.partials[b];
+    for (int b = threadIdx.x; b < a.nblk; b += kSmallThreads) v += ps[b];
     v = warp_sum(v);
     if (lane == 0) ws[w] = v;
     __syncthreads();
@@ -697,6 +884,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_fold(const __grid_const
     }
     __syncthreads();
   }
+  if (a.fold_slot_spec >= 0) sm_reduce_slots(a.partials, a.nblk, a.fold_slot_spec, a.kA + 1, a.fold_spec_dst);
   const double nrm = s_nrm;
   const double piv = a.head[a.off];
   double sign;

@@ -66,6 +66,12 @@ struct Chain {
   ChainDev dev;   // K-sized small state
 };
 
+struct FlushBufs {
+  double* partials = nullptr;
+  double* scratch = nullptr;
+  int* counters = nullptr;
+};
+
 struct KStat {
   int64_t launches = 0;
   double ms = 0.0;
@@ -86,6 +92,12 @@ struct Counters {
   int rc_pend = -1, lc_pend = -1;
   uint32_t probe_index = 0;
   int64_t inj_pos = 0;
+  // speculative mix-Gram dots left by the previous Haar k_apply(OTHER):
+  // chain (0 = R, 1 = L) dotted with the draw of probe `spec_probe`
+  int spec_chain = -1;
+  uint32_t spec_probe = 0;
+  int64_t spec_inj = -1;
+  int spec_count = 0, spec_nblk = 0, spec_slot0 = 0;
 };
 
 }  // namespace
@@ -103,8 +115,13 @@ struct hd_op {
   Counters c;
   // scratch
   double* partials = nullptr;
-  size_t partials_cap = 0;
   double* partials2 = nullptr;  // per-tile partials of update kernels
+  double* partsF = nullptr;     // k_apply(FOLD) partials [slot][block]
+  double* partsO = nullptr;     // k_apply(OTHER) partials (live until next probe)
+  size_t partsF_cap = 0, partsO_cap = 0;
+  double* specbuf = nullptr;    // [K] reduced speculative dots
+  FlushBufs fbD, fbF, fbO;      // group partials / per-CTA scratch / tickets
+  size_t flush_slots = 0;       // slot capacity of the buffers above
   double* red = nullptr;
   size_t red_cap = 0;
   double* scal = nullptr;
@@ -120,7 +137,9 @@ struct hd_op {
   int64_t inj_cap = 0, inj_size = 0;
   cudaStream_t stream = nullptr;
   int nsm = 148;
-  std::map<int, int> dots_bps;  // smem bytes -> blocks/SM
+  std::map<long, int> dots_bps;  // smem bytes -> co-resident clusters
+  std::map<long, int> apply_bps;
+  int last_other_grid = 0, last_other_slot_ss = 0;  // normalize partials of k_apply(OTHER)
   // graph cache (hd_run from a fresh state)
   cudaGraphExec_t graph = nullptr;
   std::string graph_key;
@@ -230,19 +249,15 @@ void grow_chain(hd_op* op, Chain& ch, int64_t rows_pad, int64_t Knew) {
 
 void ensure_small(hd_op* op, int64_t K) {
   if (K <= op->small_cap) return;
-  for (double** p : {&op->beta1, &op->beta3, &op->tmp, &op->tmp2, &op->coefS, &op->head, &op->zbuf, &op->csp}) {
+  for (double** p : {&op->beta1, &op->beta3, &op->tmp, &op->tmp2, &op->coefS, &op->head, &op->zbuf, &op->csp,
+                     &op->specbuf}) {
     cudaFree(*p);
     *p = dmalloc<double>(K + 8);
   }
   op->small_cap = K;
 }
 
-void ensure_red(hd_op* op, size_t nslots, size_t nblk) {
-  if (nslots * nblk > op->partials_cap) {
-    cudaFree(op->partials);
-    op->partials_cap = nslots * nblk * 2;
-    op->partials = dmalloc<double>(op->partials_cap);
-  }
+void ensure_red(hd_op* op, size_t nslots) {
   if (nslots > op->red_cap) {
     cudaFree(op->red);
     op->red_cap = nslots * 2;
@@ -273,6 +288,32 @@ void ensure_capacity(hd_op* op, int64_t nr, int64_t nl) {
   }
   const int64_t K = std::max({op->R.pan.K, op->L.pan.K, op->U.K, op->V.K});
   ensure_small(op, std::max<int64_t>(K, total) + 1);
+  // partial buffers sized for the widest launch (<= 8 CTAs of 256 per SM), so
+  // nothing is allocated inside a captured CUDA graph. fbO.partials may hold
+  // the previous probe's speculative dots: preserved across growth.
+  const size_t blocks = (size_t)op->nsm;
+  const size_t groups = ceil_div((int64_t)blocks, kGroup);
+  const size_t slots = (size_t)(4 * K + 16);
+  if (slots > op->flush_slots) {
+    for (FlushBufs* fb : {&op->fbD, &op->fbF, &op->fbO}) {
+      double* np = dmalloc<double>(slots * groups);
+      if (fb->partials && fb == &op->fbO)
+        ck(cudaMemcpy(np, fb->partials, sizeof(double) * op->flush_slots * groups, cudaMemcpyDeviceToDevice), "keep");
+      cudaFree(fb->partials);
+      fb->partials = np;
+      cudaFree(fb->scratch);
+      fb->scratch = dmalloc<double>(slots * blocks);
+      if (!fb->counters) {
+        fb->counters = dmalloc<int>(groups);
+        ck(cudaMemset(fb->counters, 0, sizeof(int) * groups), "memset");
+      }
+    }
+    op->flush_slots = slots;
+  }
+  op->partials = op->fbD.partials;
+  op->partsF = op->fbF.partials;
+  op->partsO = op->fbO.partials;
+  ensure_red(op, slots);
 }
 
 // ========================================================= instrumentation
@@ -331,21 +372,29 @@ void check_launch(const char* what) {
 }
 
 // =========================================================== launchers
-template <typename T>
-int dots_grid(hd_op* op, int smem, int64_t ntiles) {
-  auto it = op->dots_bps.find(smem);
-  int bps;
-  if (it == op->dots_bps.end()) {
-    if (smem > 48 * 1024)
-      ck(cudaFuncSetAttribute(k_dots<T, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dots<T, 8>, 256, smem), "occupancy");
-    bps = std::max(1, bps);
-    op->dots_bps[smem] = bps;
-  } else {
-    bps = it->second;
-  }
-  const int64_t want = ceil_div(ntiles, 8);
-  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)op->nsm * bps));
+// Persistent launch of a streaming kernel: grid = SMs x co-resident CTAs
+// (at most one warp-tile per warp); partial sums leave through Flush in
+// groups of kGroup CTAs. Returns the number of partial rows (groups).
+// Persistent launch of a per-warp TMA streaming kernel: up to kMaxWarps
+// warps per CTA (as many as the per-warp ring + slot rows fit in the opt-in
+// shared memory), one CTA per SM; partial sums leave through Flush in groups
+// of kGroup CTAs. Returns the number of partial rows.
+template <typename Args>
+int launch_tma(hd_op* op, cudaStream_t s, void (*kernel)(Args), Args& args, size_t shared_fixed, size_t per_warp,
+               int64_t ntiles, const FlushBufs& fb) {
+  int optin = 0;
+  ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, op->cfg.device), "attr");
+  const size_t budget = (size_t)optin - 1024;
+  if (shared_fixed + per_warp > budget) throw HdError(HD_ERR_RESOURCE_CAP, "hd: chain too long for one CTA");
+  const int nw = (int)std::min<size_t>(kMaxWarps, (budget - shared_fixed) / per_warp);
+  const size_t smem = shared_fixed + (size_t)nw * per_warp;
+  ck(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ntiles, nw), op->nsm));
+  args.out.partials = fb.partials;
+  args.out.scratch = fb.scratch;
+  args.out.counters = fb.counters;
+  kernel<<<grid, nw * 32, smem, s>>>(args);
+  return (int)ceil_div(grid, kGroup);
 }
 
 template <typename T>
@@ -363,17 +412,35 @@ int launch_dots(hd_op* op, cudaStream_t s, DotArgs<T>& a, double bytes) {
     J.slot_sumsq = slot++;
   }
   a.nslots = slot;
-  const int smem = 8 * a.nslots * (int)sizeof(double);
-  if (smem > 200 * 1024) throw HdError(HD_ERR_RESOURCE_CAP, "hd: chain too long for the dots kernel");
-  const int grid = dots_grid<T>(op, smem, a.ntiles);
-  ensure_red(op, a.nslots, grid);
-  a.partials = op->partials;
   a.status = op->status;
+  const size_t per_warp = ring_bytes<T>() + sizeof(double) * ((a.nslots + 1) & ~1) + 8 * kRing;
+  int grid;
   {
     LaunchScope ls(op, s, "dots", bytes);
-    k_dots<T, 8><<<grid, 256, smem, s>>>(a);
+    grid = launch_tma(op, s, k_dots<T>, a, 0, per_warp, a.ntiles, op->fbD);
   }
   check_launch("k_dots");
+  return grid;
+}
+
+template <typename T, int MODE>
+int launch_apply(hd_op* op, cudaStream_t s, ApplyArgs<T>& a, bool fold_buffer, double bytes, const char* kind) {
+  int slot = 0;
+  if (a.spec.kind != kSrcNone) {
+    a.slot_spec = slot;
+    slot += a.ncols + (MODE == kApplyFold ? 1 : 0);
+  }
+  a.slot_ss = slot++;
+  a.nslots = slot;
+  a.status = op->status;
+  const size_t per_warp = ring_bytes<T>() + sizeof(double) * ((a.nslots + 1) & ~1) + 8 * kRing;
+  int grid;
+  {
+    LaunchScope ls(op, s, kind, bytes);
+    grid = launch_tma(op, s, k_apply<T, MODE>, a, sizeof(double) * ((a.ncols + 1) & ~1), per_warp, a.ntiles,
+                      fold_buffer ? op->fbF : op->fbO);
+  }
+  check_launch("k_apply");
   return grid;
 }
 
@@ -410,6 +477,11 @@ double bytes_of(hd_op* op, double elems) { return elems * (double)op->esz; }
 
 // --------------------------------------------------------------- Haar
 // haar.hpp:40-67. fold = chain of the probed side, other = the opposite.
+// Passes over HBM per probe: GEMV-T over fold (k_dots), GEMV-N over fold
+// (k_apply FOLD), GEMV-N over other (k_apply OTHER). The other chain's Gram
+// dots with this probe's draw come from the previous probe's OTHER pass
+// when both probes hit the same side (speculative, Philox regenerated);
+// otherwise k_dots streams the other chain too.
 template <typename T>
 void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cudaStream_t s) {
   const int64_t n = op->n;
@@ -419,11 +491,19 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   const int64_t off = op->c.t - 1;
   Chain& F = (side == HD_RIGHT) ? op->R : op->L;
   Chain& O = (side == HD_RIGHT) ? op->L : op->R;
+  const int ochain = (side == HD_RIGHT) ? 1 : 0;
   const bool append_fold = !(op->cfg.skip_reflector && first);
+  const int64_t inj_before = op->c.inj_pos;
   Src<T> g = draw_src<T>(op, n);
   g.mask_begin = off;
+  const bool key_ok = (g.kind == kSrcInjected) ? (op->c.spec_inj == inj_before) : (op->c.spec_probe == g.probe);
+  const bool use_spec = op->c.spec_chain == ochain && key_ok && op->c.spec_count == (int)O.pan.count && O.pend < 0;
+  const bool reduce_spec = op->c.spec_chain >= 0 && use_spec;
+  const int spec_nblk = op->c.spec_nblk, spec_slot0 = op->c.spec_slot0, spec_count = op->c.spec_count;
+  op->c.spec_chain = -1;
 
-  // K1: a = P_F^T x, P_O^T g[off:], pending Gram columns, ||x||^2, ||g_tail||^2
+  // K1: a = P_F^T x (+ pending Gram), g[off:] -> new column of O, ||g_tail||^2,
+  // and (no speculation) P_O^T g[off:] (+ pending Gram of O)
   DotArgs<T> da;
   da.njobs = 2;
   da.n = n;
@@ -436,15 +516,15 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   da.job[0].check_finite = 1;
   da.job[1].P = static_cast<const T*>(O.pan.P);
   da.job[1].K = O.pan.K;
-  da.job[1].ncols = (int)O.pan.count;
-  da.job[1].pend = O.pend;
+  da.job[1].ncols = use_spec ? 0 : (int)O.pan.count;
+  da.job[1].pend = use_spec ? -1 : O.pend;
   da.job[1].rhs = g;
   da.job[1].wcol = static_cast<T*>(O.pan.P);
   da.job[1].wK = O.pan.K;
   da.job[1].wj = O.pan.count;
   da.job[1].pivot_out = op->scal + kScPivotG;
   da.job[1].pivot_row = off;
-  const double b1 = bytes_of(op, (double)n * (F.pan.count + O.pan.count + (F.pend >= 0) + (O.pend >= 0) + 2)) +
+  const double b1 = bytes_of(op, (double)n * (F.pan.count + da.job[1].ncols + (F.pend >= 0) + (da.job[1].pend >= 0) + 2)) +
                     (g.kind == kSrcInjected ? 8.0 * n : 0.0);
   const int grid = launch_dots<T>(op, s, da, b1);
 
@@ -462,7 +542,7 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   sa.kA = (int)F.pan.count;
   sa.kB = (int)O.pan.count;
   sa.pendA = F.pend;
-  sa.pendB = O.pend;
+  sa.pendB = use_spec ? -1 : O.pend;
   sa.slotA_dot = da.job[0].slot_dot;
   sa.slotA_pend = da.job[0].slot_pend;
   sa.slotA_ss = da.job[0].slot_sumsq;
@@ -480,6 +560,18 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   sa.csp = op->csp;
   sa.coefS = op->coefS;
   sa.is_haar = 1;
+  if (use_spec) {
+    sa.mix_dots = op->specbuf;
+    if (reduce_spec) {
+      sa.spec_parts = op->partsO;
+      sa.spec_nblk = spec_nblk;
+      sa.spec_slot0 = spec_slot0;
+      sa.spec_count = spec_count;
+      sa.spec_dst = op->specbuf;
+    }
+  } else {
+    sa.mix_dots = op->red + da.job[1].slot_dot;
+  }
   {
     LaunchScope ls(op, s, "small_dots", 0.0);
     k_small_dots<T><<<1, kSmallThreads, 0, s>>>(sa);
@@ -489,35 +581,33 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   O.pend = -1;
   O.pan.count += 1;  // mix reflector appended (haar.hpp:63), Gram known
 
-  // K2: p = D_F (x - P_F beta), new fold column
-  FoldArgs<T> fa;
+  // K2: p = D_F (x - P_F beta), new fold column, ||p[off:]||^2
+  ApplyArgs<T> fa;
   fa.P = static_cast<const T*>(F.pan.P);
   fa.K = F.pan.K;
   fa.ncols = (int)F.pan.count;
   fa.beta = op->beta1;
-  fa.x = xsrc;
+  fa.n = n;
+  fa.ntiles = ntiles;
   fa.D = F.dev.Drow;
   fa.Dtail = F.dev.Dtail;
   fa.Dlen = F.dev.Dlen;
+  fa.x = xsrc;
   fa.Pw = static_cast<T*>(F.pan.P);
   fa.newj = F.pan.count;
   fa.off = off;
   fa.escale = op->scal + kScEscale;
   fa.head = op->head;
-  fa.partials = op->partials2;
-  fa.n = n;
-  fa.status = op->status;
-  {
-    LaunchScope ls(op, s, "fold", bytes_of(op, (double)n * (F.pan.count + 2)));
-    k_fold<T><<<(unsigned)ntiles, kUpdThreads, sizeof(double) * std::max<int64_t>(F.pan.count, 1), s>>>(fa);
-  }
-  check_launch("k_fold");
+  const int gridF = launch_apply<T, kApplyFold>(op, s, fa, true, bytes_of(op, (double)n * (F.pan.count + 2)), "fold");
 
-  sa.partials = op->partials2;
-  sa.nblk = (int)ntiles;
+  sa.partials = op->partsF;
+  sa.nblk = gridF;
+  sa.fold_slot_ss = fa.slot_ss;
+  sa.fold_slot_spec = -1;
   sa.kA = (int)F.pan.count;
   sa.kB = (int)O.pan.count;
   sa.append = append_fold ? 1 : 0;
+  sa.spec_parts = nullptr;
   {
     LaunchScope ls(op, s, "small_fold", 0.0);
     k_small_fold<T><<<1, kSmallThreads, 0, s>>>(sa);
@@ -528,27 +618,48 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
     F.pan.count += 1;
   }
 
-  // K3: y = D_O z - P_O beta (+ dynamics epilogue)
-  OtherArgs<T> oa;
+  // K3: y = D_O z - P_O beta (+ dynamics), and the speculative Gram dots of
+  // P_O with the next probe's draw (rows >= off + 1)
+  ApplyArgs<T> oa;
   oa.P = static_cast<const T*>(O.pan.P);
   oa.K = O.pan.K;
   oa.ncols = (int)O.pan.count;
   oa.beta = op->beta1;
-  oa.z = op->zbuf;
-  oa.zlen = off + 1;
+  oa.n = n;
+  oa.ntiles = ntiles;
   oa.D = O.dev.Drow;
   oa.Dtail = O.dev.Dtail;
   oa.Dlen = O.dev.Dlen;
-  oa.n = n;
-  oa.status = op->status;
+  oa.z = op->zbuf;
+  oa.zlen = off + 1;
   oa.epi = epi;
+  const bool next_ok = (op->c.t < op->n) &&
+                       (op->cfg.draw_mode == HD_DRAWS_PHILOX || op->inj_size - op->c.inj_pos >= n);
+  if (next_ok) {
+    if (op->cfg.draw_mode == HD_DRAWS_INJECTED) {
+      oa.spec.kind = kSrcInjected;
+      oa.spec.inj = op->inj + op->c.inj_pos;
+    } else {
+      oa.spec.kind = kSrcPhilox;
+      oa.spec.seed = op->cfg.seed;
+      oa.spec.stream = (uint32_t)op->cfg.stream;
+      oa.spec.probe = op->c.probe_index;
+    }
+    oa.spec.mask_begin = off + 1;
+  }
   double eb = (double)n * (O.pan.count + 1);
   if (epi.kind == kEpiTanhMix) eb += (double)n * ((epi.xprev ? 1 : 0) + (epi.y ? 1 : 0));
-  {
-    LaunchScope ls(op, s, "other", bytes_of(op, eb));
-    k_other<T><<<(unsigned)ntiles, kUpdThreads, sizeof(double) * std::max<int64_t>(O.pan.count, 1), s>>>(oa);
+  const int gridO = launch_apply<T, kApplyOther>(op, s, oa, false, bytes_of(op, eb), "other");
+  op->last_other_grid = gridO;
+  op->last_other_slot_ss = oa.slot_ss;
+  if (next_ok) {
+    op->c.spec_chain = ochain;
+    op->c.spec_probe = op->c.probe_index;
+    op->c.spec_inj = (op->cfg.draw_mode == HD_DRAWS_INJECTED) ? op->c.inj_pos : -1;
+    op->c.spec_count = (int)O.pan.count;
+    op->c.spec_nblk = gridO;
+    op->c.spec_slot0 = oa.slot_spec;
   }
-  check_launch("k_other");
 }
 
 // ------------------------------------------------------------- Ginibre
@@ -633,30 +744,27 @@ void enqueue_ginibre(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi,
   F.pend = -1;
 
   // K2: p = D_F (x - P_F beta), new fold column, head p[0..off]
-  FoldArgs<T> fa;
+  ApplyArgs<T> fa;
   fa.P = static_cast<const T*>(F.pan.P);
   fa.K = F.pan.K;
   fa.ncols = (int)F.pan.count;
   fa.beta = op->beta1;
-  fa.x = xsrc;
+  fa.n = nin;
+  fa.ntiles = tin;
   fa.D = F.dev.Drow;
   fa.Dtail = F.dev.Dtail;
   fa.Dlen = F.dev.Dlen;
+  fa.x = xsrc;
   fa.Pw = static_cast<T*>(F.pan.P);
   fa.newj = F.pan.count;
   fa.off = off;
   fa.escale = op->scal + kScEscale;
   fa.head = op->head;
-  fa.partials = op->partials2;
-  fa.n = nin;
-  fa.status = op->status;
-  {
-    LaunchScope ls(op, s, "fold", bytes_of(op, (double)nin * (F.pan.count + 2)));
-    k_fold<T><<<(unsigned)tin, kUpdThreads, sizeof(double) * std::max<int64_t>(F.pan.count, 1), s>>>(fa);
-  }
-  check_launch("k_fold");
-  sa.partials = op->partials2;
-  sa.nblk = (int)tin;
+  const int gridF = launch_apply<T, kApplyFold>(op, s, fa, true, bytes_of(op, (double)nin * (F.pan.count + 2)), "fold");
+  sa.partials = op->partsF;
+  sa.nblk = gridF;
+  sa.fold_slot_ss = fa.slot_ss;
+  sa.fold_slot_spec = -1;
   sa.append = append_fold ? 1 : 0;
   {
     LaunchScope ls(op, s, "small_fold", 0.0);
@@ -960,10 +1068,16 @@ void enqueue_run(hd_op* op, const hd_run_args& a, int64_t dim_of_x1, cudaStream_
       epi.partials = op->partials2;
       enqueue_probe<T>(op, eff_side, vec_src<T>(x_cur, x_scale), epi, s);
       if (a.update == HD_UPDATE_NORMALIZE) {
-        const int64_t nblk = ((eff_side == HD_RIGHT) ? op->rows_pad_m : op->rows_pad_n) / kTile;
+        // ||y||^2 partials: k_apply(OTHER) slot (Haar) or per-tile (Ginibre/GOE)
+        const double* parts = op->partials2;
+        int64_t nblk = ((eff_side == HD_RIGHT) ? op->rows_pad_m : op->rows_pad_n) / kTile;
+        if (op->ens == HD_HAAR) {
+          parts = op->partsO + (size_t)op->last_other_slot_ss * op->last_other_grid;
+          nblk = op->last_other_grid;
+        }
         {
           LaunchScope ls(op, s, "small_norm", 0.0);
-          k_small_norm<<<1, kSmallThreads, 0, s>>>(op->partials2, (int)nblk, op->scal, op->status, epi.step);
+          k_small_norm<<<1, kSmallThreads, 0, s>>>(parts, (int)nblk, op->scal, op->status, epi.step);
         }
         check_launch("k_small_norm");
         // the next probe reads y * inv lazily; keep a private copy of inv
@@ -1280,7 +1394,7 @@ int hd_create(const hd_config* cfg, hd_op** out) {
   for (auto& b : op->ybuf) b = dmalloc<unsigned char>((size_t)rp * op->esz);
   op->gtmp = dmalloc<unsigned char>((size_t)rp * op->esz);
   op->partials2 = dmalloc<double>(rp / kTile + 8);
-  ensure_red(op.get(), 4 * K + 16, (size_t)op->nsm * 4);
+  ensure_capacity(op.get(), 0, 0);
   hard_reset(op.get());
   *out = op.release();
   return HD_OK;
@@ -1297,7 +1411,12 @@ int hd_destroy(hd_op* op) {
   free_chain(op->L);
   cudaFree(op->U.P);
   cudaFree(op->V.P);
-  for (double* p : {op->partials, op->partials2, op->red, op->scal, op->beta1, op->beta3, op->tmp, op->tmp2,
+  for (FlushBufs* fb : {&op->fbD, &op->fbF, &op->fbO}) {
+    cudaFree(fb->partials);
+    cudaFree(fb->scratch);
+    cudaFree(fb->counters);
+  }
+  for (double* p : {op->partials2, op->specbuf, op->red, op->scal, op->beta1, op->beta3, op->tmp, op->tmp2,
                     op->coefS, op->head, op->zbuf, op->csp, op->inj})
     cudaFree(p);
   cudaFree(op->status);
