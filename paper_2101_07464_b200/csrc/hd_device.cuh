@@ -247,6 +247,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Programmatic dependent launch: every kernel of the probe
+// sequence waits for its predecessor's completion before reading anything
+// the predecessor writes, and only then lets its own successor launch; so
+// the code before pdl_wait() may read data written two or more launches
+// back (the streaming kernels prefetch their panel chunks there).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

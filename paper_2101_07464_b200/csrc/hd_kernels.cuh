@@ -143,6 +143,7 @@ struct DotArgs {
   Flush out;
   int nslots = 0;
   int* status = nullptr;
+  int prefetch = 0;  // host-asserted: the previous launch writes no panel read here
 };
 
 // Shared-memory carve-up of the streaming kernels (per warp: ring + slots).
@@ -170,10 +171,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_dots(const __grid_constan
     mbar_fence_init();
   }
   __syncwarp();
-  const bool skip = aborted(a.status);
   const int64_t W = (int64_t)gridDim.x * nw;
   const int64_t gw = (int64_t)blockIdx.x * nw + w;
-  const int64_t t0 = gw * a.ntiles / W, t1 = skip ? t0 : (gw + 1) * a.ntiles / W;
+  const int64_t t0 = gw * a.ntiles / W;
+  int64_t t1 = (gw + 1) * a.ntiles / W;
   const int nch0 = (a.job[0].ncols + kCW - 1) / kCW;
   const int nch1 = (a.njobs > 1) ? (a.job[1].ncols + kCW - 1) / kCW : 0;
   const uint32_t nst = (uint32_t)((t1 - t0) * (nch0 + nch1));
@@ -188,8 +189,17 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_dots(const __grid_constan
     bulk_g2s(ring + (size_t)s * kCW * kTile * sizeof(T),
              J.P + (size_t)p.tile * (size_t)(J.K << kTileShift) + (size_t)p.chunk * kCW * kTile, bytes, full + s);
   };
-  if (lane == 0)
+  // panel chunks written two or more launches back: prefetch, then wait
+  if (a.prefetch && lane == 0)
     for (uint32_t it = 0; it < (uint32_t)kRing && it < nst; ++it) issue(it);
+  pdl_wait();
+  pdl_launch();
+  if (!a.prefetch && lane == 0)
+    for (uint32_t it = 0; it < (uint32_t)kRing && it < nst; ++it) issue(it);
+  if (aborted(a.status)) {  // drain the prefetched stages, then do nothing
+    for (uint32_t it = 0; it < (uint32_t)kRing && it < nst; ++it) mbar_wait(full + it % kRing, 0);
+    t1 = t0;
+  }
 
   double ss0 = 0.0, ss1 = 0.0;
   bool bad = false;
@@ -407,6 +417,7 @@ struct ApplyArgs {
   Flush out;
   int nslots = 0;
   int* status = nullptr;
+  int prefetch = 0;  // host-asserted: the previous launch writes no panel read here
 };
 
 template <typename T, int MODE>
@@ -427,12 +438,11 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
     for (int s = 0; s < kRing; ++s) mbar_init(full + s, 1);
     mbar_fence_init();
   }
-  __syncthreads();
-  const bool skip = aborted(a.status);
   const bool spec = (a.spec.kind != kSrcNone);
   const int64_t W = (int64_t)gridDim.x * nw;
   const int64_t gw = (int64_t)blockIdx.x * nw + w;
-  const int64_t t0 = gw * a.ntiles / W, t1 = skip ? t0 : (gw + 1) * a.ntiles / W;
+  const int64_t t0 = gw * a.ntiles / W;
+  int64_t t1 = (gw + 1) * a.ntiles / W;
   const int nch = (a.ncols + kCW - 1) / kCW;
   const uint32_t nst = (uint32_t)((t1 - t0) * nch);
   auto issue = [&](uint32_t it) {
@@ -446,8 +456,19 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
     bulk_g2s(ring + (size_t)s * kCW * kTile * sizeof(T),
              a.P + (size_t)tile * (size_t)(a.K << kTileShift) + (size_t)c * kCW * kTile, bytes, full + s);
   };
-  if (lane == 0)
+  __syncwarp();
+  if (a.prefetch && lane == 0)
     for (uint32_t it = 0; it < (uint32_t)kRing && it < nst; ++it) issue(it);
+  pdl_wait();
+  pdl_launch();
+  if (!a.prefetch && lane == 0)
+    for (uint32_t it = 0; it < (uint32_t)kRing && it < nst; ++it) issue(it);
+  for (int j = threadIdx.x; j < a.ncols; j += blockDim.x) beta_s[j] = a.beta[j];
+  __syncthreads();
+  if (aborted(a.status)) {
+    for (uint32_t it = 0; it < (uint32_t)kRing && it < nst; ++it) mbar_wait(full + it % kRing, 0);
+    t1 = t0;
+  }
 
   double ss = 0.0;
   bool bad = false;
@@ -586,6 +607,8 @@ template <typename T>
 __global__ void __launch_bounds__(kUpdThreads) k_ginout(const __grid_constant__ GinArgs<T> a) {
   extern __shared__ double beta_s[];  // [3][K]
   __shared__ double red_s[32];
+  pdl_wait();
+  pdl_launch();
   if (aborted(a.status)) return;
   double* b1 = beta_s;
   double* b3 = beta_s + a.K;
@@ -620,133 +643,6 @@ __global__ void __launch_bounds__(kUpdThreads) k_ginout(const __grid_constant__ 
   epilogue(a.epi, a.status, i, a.n, make_double2(y0, y1), red_s);
 }
 
-// ======================================================= small kernels
-constexpr int kSmallThreads = 512;
-
-// Deterministic sum over blocks: red[s] = sum_b partials[b][s].
-__device__ void sm_reduce(const double* partials, int nblk, int nslots, double* red) {
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int s = w; s < nslots; s += kSmallThreads / 32) {
-    double v = 0.0;
-    const double* ps = partials + (size_t)s * nblk;
-    for (int b = lane; b < nblk; b += 32) v += ps[b];
-    v = warp_sum(v);
-    if (lane == 0) red[s] = v;
-  }
-  __syncthreads();
-}
-
-// T_new[:k, k] = -c_k T[:k, :k] g  (g = G[:k, k]); warp per row, lanes
-// split the reduction so every load is independent (no serial chains).
-__device__ void sm_T_column(const ChainDev& ch, int k, double ck) {
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double* g = ch.G + (int64_t)k * ch.K;
-  for (int i = w; i < k; i += kSmallThreads / 32) {
-    double v = 0.0;
-    for (int l = i + lane; l < k; l += 32) v += ch.Tm[i + (int64_t)l * ch.K] * g[l];
-    v = warp_sum(v);
-    if (lane == 0) ch.Tm[i + (int64_t)k * ch.K] = -ck * v;
-  }
-  if (threadIdx.x == 0) ch.Tm[k + (int64_t)k * ch.K] = ck;
-  __syncthreads();
-}
-
-// Gram column + T column of a pending reflector (Schreiber-Van Loan):
-// T_new[:k, k] = -c_k T[:k, :k] G[:k, k], T_new[k, k] = c_k.
-__device__ void sm_finalize_pending(const ChainDev& ch, int pend, const double* rdots) {
-  const int64_t K = ch.K;
-  const double sp = ch.sig[pend];
-  for (int j = threadIdx.x; j <= pend; j += kSmallThreads) ch.G[j + pend * K] = ch.sig[j] * sp * rdots[j];
-  __syncthreads();
-  sm_T_column(ch, pend, ch.c[pend]);
-}
-
-// out = T^T a (k x k upper T): warp per output column.
-__device__ void sm_Tt(const ChainDev& ch, int k, const double* a, double* out) {
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int j = w; j < k; j += kSmallThreads / 32) {
-    double v = 0.0;
-    for (int i = lane; i <= j; i += 32) v += ch.Tm[i + (int64_t)j * ch.K] * a[i];
-    v = warp_sum(v);
-    if (lane == 0) out[j] = v;
-  }
-  __syncthreads();
-}
-
-// out = T a: warp per output row, lanes split the row.
-__device__ void sm_T(const ChainDev& ch, int k, const double* a, double* out) {
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = w; i < k; i += kSmallThreads / 32) {
-    double v = 0.0;
-    for (int j = i + lane; j < k; j += 32) v += ch.Tm[i + (int64_t)j * ch.K] * a[j];
-    v = warp_sum(v);
-    if (lane == 0) out[i] = v;
-  }
-  __syncthreads();
-}
-
-// out_j = sig_j * sum_{i < len} P[i, j] D(i) v[i]  (sparse-input corner).
-template <typename T>
-__device__ void sm_corner(const ChainDev& ch, const T* P, int k, const double* v, int64_t len, double* out) {
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int j = w; j < k; j += kSmallThreads / 32) {
-    double acc = 0.0;
-    for (int64_t i = lane; i < len; i += 32) acc += (double)P[paddr(i, j, ch.K)] * dval(ch.Drow, ch.Dtail, ch.Dlen, i) * v[i];
-    acc = warp_sum(acc);
-    if (lane == 0) out[j] = ch.sig[j] * acc;
-  }
-  __syncthreads();
-}
-
-// make_reflector (reflect.hpp:120-176) on the device, for a column whose
-// tail has already been streamed into the panel: pivot fix-up, scale,
-// coefficient, leading factor and the D update (for i >= off: D *= s).
-// Returns the sign used (0 for the negative-control rule's zeroing case).
-template <typename T>
-__device__ double sm_make_reflector(const ChainDev& ch, T* P, int j, int64_t off, double nrm, double pivot,
-                                    int rule, double colscale, double unscale, bool append, double* sign_out) {
-  __shared__ double s_sign;
-  if (threadIdx.x == 0) {
-    double sign;
-    if (rule == 0) sign = (pivot >= 0.0) ? 1.0 : -1.0;
-    else if (rule == 1) sign = (pivot > 0.0) ? 1.0 : -1.0;
-    else sign = (pivot >= 0.0) ? 1.0 : 0.0;
-    if (nrm == 0.0) sign = 1.0;
-    s_sign = sign;
-    if (append) {
-      if (nrm == 0.0) {  // identity reflector: zero column, c = 0, s = 1
-        ch.sig[j] = 0.0;
-        ch.c[j] = 0.0;
-        ch.s[j] = 1.0;
-      } else {
-        P[paddr(off, j, ch.K)] = (T)((pivot + sign * nrm) * colscale);
-        const double r = pivot / nrm;
-        ch.sig[j] = unscale / nrm;
-        ch.c[j] = 2.0 / (1.0 + 2.0 * sign * r + sign * sign);
-        ch.s[j] = -sign;
-      }
-    }
-  }
-  __syncthreads();
-  const double sign = s_sign;
-  if (append && nrm != 0.0) {
-    const double s = -sign;
-    for (int64_t i = off + threadIdx.x; i < ch.Dlen; i += kSmallThreads) ch.Drow[i] *= s;
-    if (threadIdx.x == 0) *ch.Dtail *= s;
-  }
-  if (sign_out) *sign_out = sign;
-  __syncthreads();
-  return sign;
-}
-
-// Append a column whose Gram column is known now (Haar mix reflector):
-// G[:k, k] from the streamed dots, then the T column.
-__device__ void sm_append_known_gram(const ChainDev& ch, int k, const double* G_col /*[k+1]*/) {
-  for (int j = threadIdx.x; j <= k; j += kSmallThreads) ch.G[j + (int64_t)k * ch.K] = G_col[j];
-  __syncthreads();
-  sm_T_column(ch, k, ch.c[k]);
-}
-
 // Scratch words shared between the small kernels of one probe.
 enum ScalarSlot {
   kScEscale = 0,   // 2^-e (fold column scale)
@@ -759,11 +655,19 @@ enum ScalarSlot {
   kScWords = 16,
 };
 
+// ======================================================= small kernels
+// One CTA of 1024 threads per stage. All small state a stage needs is
+// staged in shared memory in one global round (thread-per-slot reduction of
+// the group partials, sig/c, pivot rows, heads); the two chains touched by a
+// stage are then handled by two independent halves of the CTA (named
+// barriers 1 and 2), so the critical path is ~3 dependent L2 round trips
+// (DESIGN.md §4.3). T stays in global memory (k x k, up to 512^2).
+constexpr int kSmallThreads = 1024;
+constexpr int kHalf = kSmallThreads / 2;
+
 struct SmallArgs {
-  const double* partials = nullptr;
+  const double* partials = nullptr;  // [slot][nblk] group partials
   int nblk = 0;
-  int nslots = 0;
-  double* red = nullptr;
   double* scal = nullptr;
   int* status = nullptr;
   ChainDev chA, chB;   // fold chain / other chain
@@ -778,8 +682,6 @@ struct SmallArgs {
   int append = 1;      // fold / mix appended (skip_reflector fault)
   double* beta1 = nullptr;
   double* beta3 = nullptr;
-  double* tmp = nullptr;   // [K] scratch
-  double* tmp2 = nullptr;  // [K] scratch
   double* head = nullptr;  // p[0..off]
   double* zbuf = nullptr;
   double* csp = nullptr;
@@ -787,149 +689,370 @@ struct SmallArgs {
   double* coefS = nullptr;
   int nS = 0;
   int is_haar = 0;
-  // Haar mix Gram dots P_B^T g[off:]: from k_dots (red + slotB_dot) or from
-  // the speculative pass of the previous probe (spec buffer)
-  const double* mix_dots = nullptr;
-  // reduce a previous k_apply(OTHER)'s speculative slots into spec_dst
-  const double* spec_parts = nullptr;
+  int mix_from_spec = 0;   // Haar mix Gram dots from the speculative pass
+  const double* spec_parts = nullptr;  // [slot][spec_nblk] of the previous k_apply(OTHER)
   int spec_nblk = 0, spec_slot0 = 0, spec_count = 0;
-  double* spec_dst = nullptr;
-  // k_small_fold: ||p[off:]||^2 slot and speculative slots of k_apply(FOLD)
   int fold_slot_ss = 0;
-  int fold_slot_spec = -1;
-  double* fold_spec_dst = nullptr;
 };
 
-// dst[s] = sum_b parts[(slot0 + s) * nblk + b] for s < count (fixed order).
-__device__ void sm_reduce_slots(const double* parts, int nblk, int slot0, int count, double* dst) {
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int s = w; s < count; s += kSmallThreads / 32) {
+// dst[s] = sum_b parts[(slot0 + s) * nblk + b], thread per slot (fixed order).
+__device__ __forceinline__ void st_reduce(const double* parts, int nblk, int slot0, int count, double* dst, int tid,
+                                          int nthr) {
+  for (int s = tid; s < count; s += nthr) {
     const double* ps = parts + (size_t)(slot0 + s) * nblk;
     double v = 0.0;
-    for (int b = lane; b < nblk; b += 32) v += ps[b];
-    v = warp_sum(v);
-    if (lane == 0) dst[s] = v;
+    for (int b = 0; b < nblk; ++b) v += ps[b];
+    dst[s] = v;
   }
-  __syncthreads();
 }
 
-// After k_dots of a probe (Haar and Ginibre "fold" side): finalise pending
-// columns, the Haar mix reflector (chain B), the forward coefficients
-// beta1 = sig (T^T (sig a)) for k_fold, the power-of-two column scale, and
-// (Ginibre) the opposite-side sparse coefficients c.
+// T_new[:k, k] = -c T[:k, :k] g (g in shared memory), T_new[k, k] = c; the
+// new column is written to global memory and to tcol (shared). Warps
+// [w0, w0 + nw) of the CTA, warp per row.
+__device__ __forceinline__ void st_T_column(const ChainDev& ch, int k, double c, const double* g, double* tcol, int w0,
+                                            int nw) {
+  const int w = (threadIdx.x >> 5) - w0, lane = threadIdx.x & 31;
+  for (int i = w; i < k; i += nw) {
+    double v = 0.0;
+    for (int l = i + lane; l < k; l += 32) v += ch.Tm[i + (int64_t)l * ch.K] * g[l];
+    v = warp_sum(v);
+    if (lane == 0) {
+      tcol[i] = -c * v;
+      ch.Tm[i + (int64_t)k * ch.K] = -c * v;
+    }
+  }
+  if (threadIdx.x == w0 * 32) {
+    tcol[k] = c;
+    ch.Tm[k + (int64_t)k * ch.K] = c;
+  }
+}
+
+// out[j] = sum_{i <= j} T[i, j] u[i] for j < k (column p, if >= 0, comes
+// from tcol in shared memory). Warp per column: coalesced.
+__device__ __forceinline__ void st_Tt(const ChainDev& ch, int k, const double* u, double* out, int p,
+                                      const double* tcol, int w0, int nw) {
+  const int w = (threadIdx.x >> 5) - w0, lane = threadIdx.x & 31;
+  for (int j = w; j < k; j += nw) {
+    const double* col = (j == p) ? tcol : ch.Tm + (int64_t)j * ch.K;
+    double v = 0.0;
+    for (int i = lane; i <= j; i += 32) v += col[i] * u[i];
+    v = warp_sum(v);
+    if (lane == 0) out[j] = v;
+  }
+}
+
+// out[i] = sum_{j >= i} T[i, j] u[j] for i < k (column p from tcol).
+__device__ __forceinline__ void st_T(const ChainDev& ch, int k, const double* u, double* out, int p,
+                                     const double* tcol, int w0, int nw) {
+  const int w = (threadIdx.x >> 5) - w0, lane = threadIdx.x & 31;
+  for (int i = w; i < k; i += nw) {
+    double v = 0.0;
+    for (int j = i + lane; j < k; j += 32) v += ((j == p) ? tcol[i] : ch.Tm[i + (int64_t)j * ch.K]) * u[j];
+    v = warp_sum(v);
+    if (lane == 0) out[i] = v;
+  }
+}
+
+// make_reflector (reflect.hpp:120-176) scalars for a column streamed into
+// the panel: pivot fix-up, scale, coefficient, leading factor; returns the
+// sign (0 under the zeroing negative control). Single thread.
+template <typename T>
+__device__ __forceinline__ double st_reflector(const ChainDev& ch, T* P, int j, int64_t off, double nrm, double pivot,
+                                               int rule, double colscale, double unscale, bool append) {
+  double sign;
+  if (rule == 0) sign = (pivot >= 0.0) ? 1.0 : -1.0;
+  else if (rule == 1) sign = (pivot > 0.0) ? 1.0 : -1.0;
+  else sign = (pivot >= 0.0) ? 1.0 : 0.0;
+  if (nrm == 0.0) sign = 1.0;
+  if (append) {
+    if (nrm == 0.0) {  // identity reflector: zero column, c = 0, s = 1
+      ch.sig[j] = 0.0;
+      ch.c[j] = 0.0;
+      ch.s[j] = 1.0;
+    } else {
+      P[paddr(off, j, ch.K)] = (T)((pivot + sign * nrm) * colscale);
+      const double r = pivot / nrm;
+      ch.sig[j] = unscale / nrm;
+      ch.c[j] = 2.0 / (1.0 + 2.0 * sign * r + sign * sign);
+      ch.s[j] = -sign;
+    }
+  }
+  return sign;
+}
+
+// D update for a member with offset off and leading factor s: D[i] *= s for
+// i >= off (threads [t0, t0 + nthr)).
+__device__ __forceinline__ void st_D_update(const ChainDev& ch, int64_t off, double s, int t, int nthr) {
+  for (int64_t i = off + t; i < ch.Dlen; i += nthr) ch.Drow[i] *= s;
+  if (t == 0) *ch.Dtail *= s;
+}
+
+// Shared-memory layout of the small kernels: 12 vectors of length kv.
+struct SmallSmem {
+  double *v0, *v1, *v2, *v3, *v4, *v5, *v6, *v7, *v8, *v9, *v10, *v11;
+  double* sc;  // scalars [16]
+};
+
+__device__ __forceinline__ SmallSmem small_smem(double* base, int kv) {
+  SmallSmem m;
+  double* p = base;
+  double** v[12] = {&m.v0, &m.v1, &m.v2, &m.v3, &m.v4, &m.v5, &m.v6, &m.v7, &m.v8, &m.v9, &m.v10, &m.v11};
+  for (int i = 0; i < 12; ++i) {
+    *v[i] = p;
+    p += kv;
+  }
+  m.sc = p;
+  return m;
+}
+
+// After k_dots of a probe: finalise chain A's pending column and its forward
+// coefficients beta1 = sig (T_A^T (sig a)) (half 1), the Haar mix reflector
+// H(g, off) appended to chain B or (Ginibre) the opposite-side sparse
+// coefficients (half 2), and the power-of-two fold-column scale.
 template <typename T>
 __global__ void __launch_bounds__(kSmallThreads) k_small_dots(const __grid_constant__ SmallArgs a) {
+  extern __shared__ double ssm[];
+  pdl_wait();
+  pdl_launch();
   if (aborted(a.status)) return;
-  if (a.spec_parts) sm_reduce_slots(a.spec_parts, a.spec_nblk, a.spec_slot0, a.spec_count, a.spec_dst);
-  sm_reduce(a.partials, a.nblk, a.nslots, a.red);
-  if (threadIdx.x == 0 && *(volatile int*)(a.status + kStBadInput)) *(volatile int*)(a.status + kStAbort) = 1;
-  __syncthreads();
-  if (aborted(a.status)) return;
-  if (a.pendA >= 0) sm_finalize_pending(a.chA, a.pendA, a.red + a.slotA_pend);
-  if (a.pendB >= 0) sm_finalize_pending(a.chB, a.pendB, a.red + a.slotB_pend);
-  // forward coefficients for the fold chain
-  for (int j = threadIdx.x; j < a.kA; j += kSmallThreads) a.tmp[j] = a.chA.sig[j] * a.red[a.slotA_dot + j];
-  __syncthreads();
-  sm_Tt(a.chA, a.kA, a.tmp, a.tmp2);
-  for (int j = threadIdx.x; j < a.kA; j += kSmallThreads) a.beta1[j] = a.chA.sig[j] * a.tmp2[j];
-  if (threadIdx.x == 0) {
-    const double xn = sqrt(a.red[a.slotA_ss]);
-    int e = 0;
-    if (xn > 0.0 && isfinite(xn)) frexp(xn, &e);
-    a.scal[kScEscale] = ldexp(1.0, -e);
-    a.scal[kScIscale] = ldexp(1.0, e);
+  const int kv = max(a.kA, a.kB) + 2;
+  const SmallSmem m = small_smem(ssm, kv);
+  double* aA = m.v0;     // red A dot
+  double* pA = m.v1;     // red A pend
+  double* sgA = m.v2;    // sig A
+  double* gA = m.v3;     // G col A / scratch
+  double* tA = m.v4;     // new T col A
+  double* uA = m.v5;     // sig * a
+  double* aB = m.v6;     // mix dots (spec or red) / csp
+  double* pB = m.v7;     // red B pend
+  double* sgB = m.v8;    // sig B
+  double* rowB = m.v9;   // P_B[off, :]
+  double* gB = m.v10;    // G col B
+  double* tB = m.v11;    // new T col B
+  const int tid = threadIdx.x;
+  // ---- phase 1: one global round
+  if (a.kA > 0) st_reduce(a.partials, a.nblk, a.slotA_dot, a.kA, aA, tid, kSmallThreads);
+  if (a.pendA >= 0) st_reduce(a.partials, a.nblk, a.slotA_pend, a.pendA + 1, pA, tid, kSmallThreads);
+  if (a.is_haar && a.mix_from_spec) {
+    if (a.kB > 0) st_reduce(a.spec_parts, a.spec_nblk, a.spec_slot0, a.kB, aB, tid, kSmallThreads);
+  } else if (a.kB > 0) {
+    st_reduce(a.partials, a.nblk, a.slotB_dot, a.kB, aB, tid, kSmallThreads);
   }
+  if (a.pendB >= 0) st_reduce(a.partials, a.nblk, a.slotB_pend, a.pendB + 1, pB, tid, kSmallThreads);
+  for (int j = tid; j < a.kA; j += kSmallThreads) sgA[j] = a.chA.sig[j];
   if (a.is_haar) {
-    // mix reflector H(g, off) appended to chain B at column kB
-    const double nrm = sqrt(a.red[a.slotB_ss]);
-    const double piv = a.scal[kScPivotG];
-    double sign;
-    sm_make_reflector<T>(a.chB, (T*)a.PB, a.kB, a.off, nrm, piv, a.rule, 1.0, 1.0, true, &sign);
-    // Gram column: G[j, kB] = sig_j (P[:,j].g_tail / nrm + sign P[off, j])
     const T* PB = (const T*)a.PB;
-    for (int j = threadIdx.x; j < a.kB; j += kSmallThreads) {
-      a.tmp[j] = (nrm == 0.0) ? 0.0
-                              : a.chB.sig[j] * (a.mix_dots[j] / nrm + sign * (double)PB[paddr(a.off, j, a.chB.K)]);
+    for (int j = tid; j < a.kB; j += kSmallThreads) {
+      sgB[j] = a.chB.sig[j];
+      rowB[j] = (double)PB[paddr(a.off, j, a.chB.K)];
     }
-    if (threadIdx.x == 0) a.tmp[a.kB] = (nrm == 0.0) ? 0.0 : 2.0 / a.chB.c[a.kB];
-    __syncthreads();
-    sm_append_known_gram(a.chB, a.kB, a.tmp);
+  }
+  if (tid == 0) {
+    st_reduce(a.partials, a.nblk, a.slotA_ss, 1, m.sc + 0, 0, 1);
+    if (a.slotB_ss >= 0) st_reduce(a.partials, a.nblk, a.slotB_ss, 1, m.sc + 1, 0, 1);
+    m.sc[2] = (a.pendA >= 0) ? a.chA.c[a.pendA] : 0.0;
+    m.sc[3] = (a.pendB >= 0) ? a.chB.c[a.pendB] : 0.0;
+    m.sc[4] = a.scal[kScPivotG];
+    if (*(volatile int*)(a.status + kStBadInput)) *(volatile int*)(a.status + kStAbort) = 1;
+  }
+  __syncthreads();
+  if (aborted(a.status)) return;
+  if (tid < kHalf) {
+    // ---- half 1: chain A
+    const int p = a.pendA;
+    if (p >= 0) {
+      for (int j = tid; j <= p; j += kHalf) {
+        gA[j] = sgA[j] * sgA[p] * pA[j];
+        a.chA.G[j + (int64_t)p * a.chA.K] = gA[j];
+      }
+      named_sync(1, kHalf);
+      st_T_column(a.chA, p, m.sc[2], gA, tA, 0, kHalf / 32);
+    }
+    for (int j = tid; j < a.kA; j += kHalf) uA[j] = sgA[j] * aA[j];
+    named_sync(1, kHalf);
+    st_Tt(a.chA, a.kA, uA, gA, p, tA, 0, kHalf / 32);
+    named_sync(1, kHalf);
+    for (int j = tid; j < a.kA; j += kHalf) a.beta1[j] = sgA[j] * gA[j];
+    if (tid == 0) {
+      const double xn = sqrt(m.sc[0]);
+      int e = 0;
+      if (xn > 0.0 && isfinite(xn)) frexp(xn, &e);
+      a.scal[kScEscale] = ldexp(1.0, -e);
+      a.scal[kScIscale] = ldexp(1.0, e);
+    }
   } else {
-    // Ginibre: opposite-side coefficients <v_i, x> (or <u_i, x>), rows < nB
-    for (int q = threadIdx.x; q < a.kB; q += kSmallThreads) a.csp[q] = a.red[a.slotB_dot + q];
+    // ---- half 2: chain B
+    const int t2 = tid - kHalf;
+    if (a.is_haar) {
+      int kB = a.kB;
+      const int p = a.pendB;
+      if (p >= 0) {  // fallback path only (same-side speculation unavailable)
+        for (int j = t2; j <= p; j += kHalf) {
+          gB[j] = a.chB.sig[j] * a.chB.sig[p] * pB[j];
+          a.chB.G[j + (int64_t)p * a.chB.K] = gB[j];
+        }
+        named_sync(2, kHalf);
+        st_T_column(a.chB, p, m.sc[3], gB, tB, kHalf / 32, kHalf / 32);
+        named_sync(2, kHalf);
+      }
+      // mix reflector H(g, off) -> column kB of chain B
+      const double nrm = sqrt(m.sc[1]);
+      const double piv = m.sc[4];
+      if (t2 == 0) {
+        const double sign = st_reflector<T>(a.chB, (T*)a.PB, kB, a.off, nrm, piv, a.rule, 1.0, 1.0, true);
+        m.sc[5] = sign;
+        m.sc[6] = (nrm == 0.0) ? 0.0 : a.chB.c[kB];
+      }
+      named_sync(2, kHalf);
+      const double sign = m.sc[5], cB = m.sc[6];
+      for (int j = t2; j < kB; j += kHalf) {
+        gB[j] = (nrm == 0.0) ? 0.0 : sgB[j] * (aB[j] / nrm + sign * rowB[j]);
+        a.chB.G[j + (int64_t)kB * a.chB.K] = gB[j];
+      }
+      if (t2 == 0) a.chB.G[kB + (int64_t)kB * a.chB.K] = (nrm == 0.0) ? 0.0 : 2.0 / cB;
+      if (nrm != 0.0) st_D_update(a.chB, a.off, -sign, t2, kHalf);
+      named_sync(2, kHalf);
+      st_T_column(a.chB, kB, cB, gB, tB, kHalf / 32, kHalf / 32);
+    } else {
+      // Ginibre: opposite-side coefficients <v_i, x> (or <u_i, x>), rows < kB
+      for (int q = t2; q < a.kB; q += kHalf) a.csp[q] = aB[q];
+    }
   }
 }
 
-// After k_fold: finalise the fold reflector H(p, off) (appended unless the
-// skip fault fires), then either (Haar) the sparse reverse application of
-// chain B to z = H p, or (Ginibre) the coefficient of the current probe.
+// After k_apply(FOLD): finalise the fold reflector H(p, off) (appended
+// unless the skip fault fires), then (Haar) beta = sig (T_B (W_B^T D_B z))
+// for the sparse folded iterate z = H p, or (Ginibre) the current coefficient.
 template <typename T>
 __global__ void __launch_bounds__(kSmallThreads) k_small_fold(const __grid_constant__ SmallArgs a) {
+  extern __shared__ double ssm[];
+  pdl_wait();
+  pdl_launch();
   if (aborted(a.status)) return;
-  __shared__ double s_nrm;
-  // deterministic sum of the per-block ||p[off:]||^2 partials
-  {
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __shared__ double ws[kSmallThreads / 32];
+  const int kv = max(a.kA, a.kB) + 2;
+  const SmallSmem m = small_smem(ssm, kv);
+  double* az = m.v0;    // corner partial sig_j sum_{i<off} P_B[i,j] D_B(i) p_i
+  double* rowB = m.v1;  // P_B[off, :]
+  double* tmp = m.v2;
+  double* sgB = m.v3;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const T* PB = (const T*)a.PB;
+  // ---- phase 1
+  if (a.is_haar) {
+    for (int j = w; j < a.kB; j += kSmallThreads / 32) {
+      double v = 0.0;
+      for (int64_t i = lane; i < a.off; i += 32)
+        v += (double)PB[paddr(i, j, a.chB.K)] * dval(a.chB.Drow, a.chB.Dtail, a.chB.Dlen, i) * a.head[i];
+      v = warp_sum(v);
+      if (lane == 0) {
+        az[j] = v;
+        rowB[j] = (double)PB[paddr(a.off, j, a.chB.K)];
+        sgB[j] = a.chB.sig[j];
+      }
+    }
+    for (int64_t i = tid; i < a.off; i += kSmallThreads) a.zbuf[i] = a.head[i];
+  }
+  if (w == 0) {
     const double* ps = a.partials + (size_t)a.fold_slot_ss * a.nblk;
     double v = 0.0;
-    for (int b = threadIdx.x; b < a.nblk; b += kSmallThreads) v += ps[b];
+    for (int b = lane; b < a.nblk; b += 32) v += ps[b];
     v = warp_sum(v);
-    if (lane == 0) ws[w] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int u = 0; u < kSmallThreads / 32; ++u) t += ws[u];
-      s_nrm = sqrt(t);
+    if (lane == 0) {
+      m.sc[0] = sqrt(v);
+      m.sc[1] = a.head[a.off];
+      m.sc[2] = (a.is_haar && a.off < a.chB.Dlen) ? a.chB.Drow[a.off] : *a.chB.Dtail;
     }
-    __syncthreads();
   }
-  if (a.fold_slot_spec >= 0) sm_reduce_slots(a.partials, a.nblk, a.fold_slot_spec, a.kA + 1, a.fold_spec_dst);
-  const double nrm = s_nrm;
-  const double piv = a.head[a.off];
-  double sign;
-  sm_make_reflector<T>(a.chA, (T*)a.PA, a.kA, a.off, nrm, piv, a.rule, a.scal[kScEscale], a.scal[kScIscale],
-                       a.append != 0, &sign);
-  // (H p)[off]: +||p[off:]|| (0 under the zeroing negative control)
-  const double zoff = (nrm == 0.0) ? piv : (sign == 0.0 ? 0.0 : nrm);
-  if (threadIdx.x == 0) {
+  __syncthreads();
+  const double nrm = m.sc[0], piv = m.sc[1];
+  if (tid == 0) {
+    const double sign = st_reflector<T>(a.chA, (T*)a.PA, a.kA, a.off, nrm, piv, a.rule, a.scal[kScEscale],
+                                        a.scal[kScIscale], a.append != 0);
+    // (H p)[off]: +||p[off:]|| (0 under the zeroing negative control)
+    const double zoff = (nrm == 0.0) ? piv : (sign == 0.0 ? 0.0 : nrm);
+    m.sc[3] = sign;
+    m.sc[4] = zoff;
     a.scal[kScNrm] = nrm;
     a.scal[kScCoefCur] = a.append ? zoff : piv;
     a.scal[kScSign] = sign;
+    if (a.is_haar) a.zbuf[a.off] = zoff;
   }
+  __syncthreads();
+  if (a.append && nrm != 0.0) st_D_update(a.chA, a.off, -m.sc[3], tid, kSmallThreads);
   if (a.is_haar) {
-    for (int64_t i = threadIdx.x; i <= a.off; i += kSmallThreads) a.zbuf[i] = (i < a.off) ? a.head[i] : zoff;
+    const double zoff = m.sc[4], doff = m.sc[2];
+    for (int j = tid; j < a.kB; j += kSmallThreads) tmp[j] = sgB[j] * (az[j] + rowB[j] * doff * zoff);
     __syncthreads();
-    // beta = sig (T_B (W_B^T (D_B z)))
-    sm_corner<T>(a.chB, (const T*)a.PB, a.kB, a.zbuf, a.off + 1, a.tmp);
-    sm_T(a.chB, a.kB, a.tmp, a.tmp2);
-    for (int j = threadIdx.x; j < a.kB; j += kSmallThreads) a.beta1[j] = a.chB.sig[j] * a.tmp2[j];
+    st_T(a.chB, a.kB, tmp, az, -1, nullptr, 0, kSmallThreads / 32);
+    __syncthreads();
+    for (int j = tid; j < a.kB; j += kSmallThreads) a.beta1[j] = sgB[j] * az[j];
   }
 }
 
 // Ginibre, after k_dots over the opposite chain with v = D g_m: pending
-// column, beta1 = sig (T (sig a_g)) for the new basis vector, beta3 for the
-// sparse part L-rev-adj(c), and the coefficients of the same-side store.
+// column, beta1 = sig (T (sig a_g)) for the new basis vector (half 1), beta3
+// for the sparse part L-rev-adj(c) (half 2), same-side store coefficients.
 template <typename T>
 __global__ void __launch_bounds__(kSmallThreads) k_small_gin(const __grid_constant__ SmallArgs a) {
+  extern __shared__ double ssm[];
+  pdl_wait();
+  pdl_launch();
   if (aborted(a.status)) return;
-  sm_reduce(a.partials, a.nblk, a.nslots, a.red);
-  if (a.pendB >= 0) sm_finalize_pending(a.chB, a.pendB, a.red + a.slotB_pend);
-  for (int j = threadIdx.x; j < a.kB; j += kSmallThreads) a.tmp[j] = a.chB.sig[j] * a.red[a.slotB_dot + j];
+  const int kv = a.kB + 2;
+  const SmallSmem m = small_smem(ssm, kv);
+  double* ag = m.v0;
+  double* pB = m.v1;
+  double* sg = m.v2;
+  double* gB = m.v3;
+  double* tB = m.v4;
+  double* u1 = m.v5;
+  double* o1 = m.v6;
+  double* ac = m.v7;
+  double* o3 = m.v8;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const T* PB = (const T*)a.PB;
+  if (a.kB > 0) st_reduce(a.partials, a.nblk, a.slotB_dot, a.kB, ag, tid, kSmallThreads);
+  if (a.pendB >= 0) st_reduce(a.partials, a.nblk, a.slotB_pend, a.pendB + 1, pB, tid, kSmallThreads);
+  for (int j = tid; j < a.kB; j += kSmallThreads) sg[j] = a.chB.sig[j];
+  // corner W_B^T (D_B c) over rows < csplen (does not involve the pending T)
+  for (int j = w; j < a.kB; j += kSmallThreads / 32) {
+    double v = 0.0;
+    for (int64_t i = lane; i < a.csplen; i += 32)
+      v += (double)PB[paddr(i, j, a.chB.K)] * dval(a.chB.Drow, a.chB.Dtail, a.chB.Dlen, i) * a.csp[i];
+    v = warp_sum(v);
+    if (lane == 0) ac[j] = v;
+  }
+  for (int q = tid; q < a.nS; q += kSmallThreads) a.coefS[q] = a.head[q];
+  if (tid == 0) m.sc[0] = (a.pendB >= 0) ? a.chB.c[a.pendB] : 0.0;
   __syncthreads();
-  sm_T(a.chB, a.kB, a.tmp, a.tmp2);
-  for (int j = threadIdx.x; j < a.kB; j += kSmallThreads) a.beta1[j] = a.chB.sig[j] * a.tmp2[j];
+  const int p = a.pendB;
+  if (p >= 0) {
+    for (int j = tid; j <= p; j += kSmallThreads) {
+      gB[j] = sg[j] * sg[p] * pB[j];
+      a.chB.G[j + (int64_t)p * a.chB.K] = gB[j];
+    }
+    __syncthreads();
+    st_T_column(a.chB, p, m.sc[0], gB, tB, 0, kSmallThreads / 32);
+  }
+  for (int j = tid; j < a.kB; j += kSmallThreads) {
+    u1[j] = sg[j] * ag[j];
+    ac[j] = sg[j] * ac[j];
+  }
   __syncthreads();
-  sm_corner<T>(a.chB, (const T*)a.PB, a.kB, a.csp, a.csplen, a.tmp);
-  sm_T(a.chB, a.kB, a.tmp, a.tmp2);
-  for (int j = threadIdx.x; j < a.kB; j += kSmallThreads) a.beta3[j] = a.chB.sig[j] * a.tmp2[j];
-  // same-side store coefficients: column q <-> head p[q]
-  for (int q = threadIdx.x; q < a.nS; q += kSmallThreads) a.coefS[q] = a.head[q];
+  if (tid < kHalf) st_T(a.chB, a.kB, u1, o1, p, tB, 0, kHalf / 32);
+  else st_T(a.chB, a.kB, ac, o3, p, tB, kHalf / 32, kHalf / 32);
+  __syncthreads();
+  for (int j = tid; j < a.kB; j += kSmallThreads) {
+    a.beta1[j] = sg[j] * o1[j];
+    a.beta3[j] = sg[j] * o3[j];
+  }
 }
 
 // Normalize dynamics: inv = ||y|| > 0 ? 1/||y|| : 1 (bench.cpp:25-28).
 __global__ void __launch_bounds__(kSmallThreads) k_small_norm(const double* partials, int nblk, double* scal,
                                                               int* status, int step) {
+  pdl_wait();
+  pdl_launch();
   if (aborted(status)) return;
   __shared__ double ws[kSmallThreads / 32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -954,17 +1077,23 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_norm(const double* part
 // x = scale * y (materialise a lazily normalised iterate).
 template <typename T>
 __global__ void k_scale_copy(const T* y, const double* scale, T* x, int64_t n) {
+  pdl_wait();
+  pdl_launch();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) x[i] = (T)(*scale * (double)y[i]);
 }
 
 __global__ void k_reset_chain(ChainDev ch) {
+  pdl_wait();
+  pdl_launch();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ch.Dlen; i += (int64_t)gridDim.x * blockDim.x)
     ch.Drow[i] = 1.0;
   if (blockIdx.x == 0 && threadIdx.x == 0) *ch.Dtail = 1.0;
 }
 
 __global__ void k_reset_status(int* status) {
+  pdl_wait();
+  pdl_launch();
   if (threadIdx.x == 0) {
     status[kStAbort] = 0;
     status[kStBadStep] = INT_MAX;

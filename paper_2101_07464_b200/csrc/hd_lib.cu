@@ -14,6 +14,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -140,6 +141,7 @@ struct hd_op {
   std::map<long, int> dots_bps;  // smem bytes -> co-resident clusters
   std::map<long, int> apply_bps;
   int last_other_grid = 0, last_other_slot_ss = 0;  // normalize partials of k_apply(OTHER)
+  bool pdl = true;  // programmatic dependent launch (HD_NO_PDL=1 disables)
   // graph cache (hd_run from a fresh state)
   cudaGraphExec_t graph = nullptr;
   std::string graph_key;
@@ -375,6 +377,25 @@ void check_launch(const char* what) {
 // Persistent launch of a streaming kernel: grid = SMs x co-resident CTAs
 // (at most one warp-tile per warp); partial sums leave through Flush in
 // groups of kGroup CTAs. Returns the number of partial rows (groups).
+// Every kernel of the probe sequence is launched with programmatic stream
+// serialization (PDL); the kernels order themselves with
+// griddepcontrol.wait / launch_dependents.
+template <typename... KArgs, typename... Args>
+void launch_k(hd_op* op, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = op->pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  ck(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
+}
+
 // Persistent launch of a per-warp TMA streaming kernel: up to kMaxWarps
 // warps per CTA (as many as the per-warp ring + slot rows fit in the opt-in
 // shared memory), one CTA per SM; partial sums leave through Flush in groups
@@ -393,7 +414,7 @@ int launch_tma(hd_op* op, cudaStream_t s, void (*kernel)(Args), Args& args, size
   args.out.partials = fb.partials;
   args.out.scratch = fb.scratch;
   args.out.counters = fb.counters;
-  kernel<<<grid, nw * 32, smem, s>>>(args);
+  launch_k(op, kernel, dim3(grid), dim3(nw * 32), smem, s, args);
   return (int)ceil_div(grid, kGroup);
 }
 
@@ -442,6 +463,11 @@ int launch_apply(hd_op* op, cudaStream_t s, ApplyArgs<T>& a, bool fold_buffer, d
   }
   check_launch("k_apply");
   return grid;
+}
+
+size_t small_smem_bytes(const SmallArgs& a) {
+  const size_t kv = (size_t)std::max(a.kA, a.kB) + 2;
+  return sizeof(double) * (12 * kv + 16);
 }
 
 template <typename T>
@@ -524,6 +550,8 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   da.job[1].wj = O.pan.count;
   da.job[1].pivot_out = op->scal + kScPivotG;
   da.job[1].pivot_row = off;
+  // predecessor = previous probe's k_apply(OTHER) (writes y / x_{t+1} only)
+  da.prefetch = 1;
   const double b1 = bytes_of(op, (double)n * (F.pan.count + da.job[1].ncols + (F.pend >= 0) + (da.job[1].pend >= 0) + 2)) +
                     (g.kind == kSrcInjected ? 8.0 * n : 0.0);
   const int grid = launch_dots<T>(op, s, da, b1);
@@ -531,8 +559,6 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   SmallArgs sa;
   sa.partials = op->partials;
   sa.nblk = grid;
-  sa.nslots = da.nslots;
-  sa.red = op->red;
   sa.scal = op->scal;
   sa.status = op->status;
   sa.chA = F.dev;
@@ -553,28 +579,21 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   sa.rule = op->cfg.sign_rule;
   sa.beta1 = op->beta1;
   sa.beta3 = op->beta3;
-  sa.tmp = op->tmp;
-  sa.tmp2 = op->tmp2;
   sa.head = op->head;
   sa.zbuf = op->zbuf;
   sa.csp = op->csp;
   sa.coefS = op->coefS;
   sa.is_haar = 1;
+  sa.mix_from_spec = use_spec ? 1 : 0;
   if (use_spec) {
-    sa.mix_dots = op->specbuf;
-    if (reduce_spec) {
-      sa.spec_parts = op->partsO;
-      sa.spec_nblk = spec_nblk;
-      sa.spec_slot0 = spec_slot0;
-      sa.spec_count = spec_count;
-      sa.spec_dst = op->specbuf;
-    }
-  } else {
-    sa.mix_dots = op->red + da.job[1].slot_dot;
+    sa.spec_parts = op->partsO;
+    sa.spec_nblk = spec_nblk;
+    sa.spec_slot0 = spec_slot0;
+    sa.spec_count = spec_count;
   }
   {
     LaunchScope ls(op, s, "small_dots", 0.0);
-    k_small_dots<T><<<1, kSmallThreads, 0, s>>>(sa);
+    launch_k(op, k_small_dots<T>, dim3(1), dim3(kSmallThreads), small_smem_bytes(sa), s, sa);
   }
   check_launch("k_small_dots");
   F.pend = -1;
@@ -598,19 +617,19 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   fa.off = off;
   fa.escale = op->scal + kScEscale;
   fa.head = op->head;
+  fa.prefetch = 1;  // predecessor k_small_dots writes chain O's pivot, not P_F
   const int gridF = launch_apply<T, kApplyFold>(op, s, fa, true, bytes_of(op, (double)n * (F.pan.count + 2)), "fold");
 
   sa.partials = op->partsF;
   sa.nblk = gridF;
   sa.fold_slot_ss = fa.slot_ss;
-  sa.fold_slot_spec = -1;
   sa.kA = (int)F.pan.count;
   sa.kB = (int)O.pan.count;
   sa.append = append_fold ? 1 : 0;
   sa.spec_parts = nullptr;
   {
     LaunchScope ls(op, s, "small_fold", 0.0);
-    k_small_fold<T><<<1, kSmallThreads, 0, s>>>(sa);
+    launch_k(op, k_small_fold<T>, dim3(1), dim3(kSmallThreads), small_smem_bytes(sa), s, sa);
   }
   check_launch("k_small_fold");
   if (append_fold) {
@@ -633,6 +652,7 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   oa.z = op->zbuf;
   oa.zlen = off + 1;
   oa.epi = epi;
+  oa.prefetch = 1;  // predecessor k_small_fold writes chain F's pivot, not P_O
   const bool next_ok = (op->c.t < op->n) &&
                        (op->cfg.draw_mode == HD_DRAWS_PHILOX || op->inj_size - op->c.inj_pos >= n);
   if (next_ok) {
@@ -709,8 +729,6 @@ void enqueue_ginibre(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi,
   SmallArgs sa;
   sa.partials = op->partials;
   sa.nblk = grid;
-  sa.nslots = da.nslots;
-  sa.red = op->red;
   sa.scal = op->scal;
   sa.status = op->status;
   sa.chA = F.dev;
@@ -725,12 +743,11 @@ void enqueue_ginibre(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi,
   sa.slotA_pend = da.job[0].slot_pend;
   sa.slotA_ss = da.job[0].slot_sumsq;
   sa.slotB_dot = da.job[1].slot_dot;
+  sa.slotB_ss = -1;
   sa.off = off;
   sa.rule = op->cfg.sign_rule;
   sa.beta1 = op->beta1;
   sa.beta3 = op->beta3;
-  sa.tmp = op->tmp;
-  sa.tmp2 = op->tmp2;
   sa.head = op->head;
   sa.zbuf = op->zbuf;
   sa.csp = op->csp;
@@ -738,7 +755,7 @@ void enqueue_ginibre(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi,
   sa.is_haar = 0;
   {
     LaunchScope ls(op, s, "small_dots", 0.0);
-    k_small_dots<T><<<1, kSmallThreads, 0, s>>>(sa);
+    launch_k(op, k_small_dots<T>, dim3(1), dim3(kSmallThreads), small_smem_bytes(sa), s, sa);
   }
   check_launch("k_small_dots");
   F.pend = -1;
@@ -764,11 +781,10 @@ void enqueue_ginibre(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi,
   sa.partials = op->partsF;
   sa.nblk = gridF;
   sa.fold_slot_ss = fa.slot_ss;
-  sa.fold_slot_spec = -1;
   sa.append = append_fold ? 1 : 0;
   {
     LaunchScope ls(op, s, "small_fold", 0.0);
-    k_small_fold<T><<<1, kSmallThreads, 0, s>>>(sa);
+    launch_k(op, k_small_fold<T>, dim3(1), dim3(kSmallThreads), small_smem_bytes(sa), s, sa);
   }
   check_launch("k_small_fold");
   if (append_fold) {
@@ -793,7 +809,6 @@ void enqueue_ginibre(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi,
   SmallArgs sg = sa;
   sg.partials = op->partials;
   sg.nblk = grid;
-  sg.nslots = db.nslots;
   sg.chB = O.dev;
   sg.PB = O.pan.P;
   sg.kB = (int)O.pan.count;
@@ -804,7 +819,7 @@ void enqueue_ginibre(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi,
   sg.nS = (int)S.count;
   {
     LaunchScope ls(op, s, "small_gin", 0.0);
-    k_small_gin<T><<<1, kSmallThreads, 0, s>>>(sg);
+    launch_k(op, k_small_gin<T>, dim3(1), dim3(kSmallThreads), small_smem_bytes(sg), s, sg);
   }
   check_launch("k_small_gin");
   O.pend = -1;
@@ -838,7 +853,7 @@ void enqueue_ginibre(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi,
   {
     LaunchScope ls(op, s, "ginout", bytes_of(op, eb));
     const size_t smem = sizeof(double) * (2 * O.pan.K + std::max<int64_t>(S.K, 1));
-    k_ginout<T><<<(unsigned)tout, kUpdThreads, smem, s>>>(ga);
+    launch_k(op, k_ginout<T>, dim3((unsigned)tout), dim3(kUpdThreads), smem, s, ga);
   }
   check_launch("k_ginout");
   S.count += 1;
@@ -906,13 +921,13 @@ Counters take_snapshot(const hd_op* op) {
 void reset_device_state(hd_op* op, cudaStream_t s) {
   {
     LaunchScope ls(op, s, "reset", 0.0);
-    k_reset_status<<<1, 32, 0, s>>>(op->status);
+    launch_k(op, k_reset_status, dim3(1), dim3(32), 0, s, op->status);
   }
   for (Chain* ch : {&op->R, &op->L}) {
     if (!ch->pan.P) continue;
     LaunchScope ls(op, s, "reset", 0.0);
-    k_reset_chain<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ch->dev.Dlen, 256), 1024)), 256, 0, s>>>(
-        ch->dev);
+    launch_k(op, k_reset_chain, dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ch->dev.Dlen, 256), 1024))),
+             dim3(256), 0, s, ch->dev);
   }
   check_launch("reset");
 }
@@ -932,7 +947,7 @@ void read_status(hd_op* op, int st[kStWords]) {
 }
 
 void clear_status(hd_op* op, cudaStream_t s) {
-  k_reset_status<<<1, 32, 0, s>>>(op->status);
+  launch_k(op, k_reset_status, dim3(1), dim3(32), 0, s, op->status);
   check_launch("reset status");
 }
 
@@ -1077,7 +1092,8 @@ void enqueue_run(hd_op* op, const hd_run_args& a, int64_t dim_of_x1, cudaStream_
         }
         {
           LaunchScope ls(op, s, "small_norm", 0.0);
-          k_small_norm<<<1, kSmallThreads, 0, s>>>(parts, (int)nblk, op->scal, op->status, epi.step);
+          launch_k(op, k_small_norm, dim3(1), dim3(kSmallThreads), 0, s, parts, (int)nblk, op->scal, op->status,
+                   epi.step);
         }
         check_launch("k_small_norm");
         // the next probe reads y * inv lazily; keep a private copy of inv
@@ -1367,6 +1383,7 @@ int hd_create(const hd_config* cfg, hd_op** out) {
   op->rows_pad_m = ceil_div(m, kTile) * kTile;
   op->rows_pad_n = ceil_div(n, kTile) * kTile;
   op->budget = (c.ensemble == HD_HAAR) ? n : std::min(m, n);
+  if (const char* e = std::getenv("HD_NO_PDL")) op->pdl = !(e[0] == '1');
   ck(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking), "stream");
   ck(cudaDeviceGetAttribute(&op->nsm, cudaDevAttrMultiProcessorCount, c.device), "attr");
   const int64_t per_outer = (c.ensemble == HD_GOE) ? 2 : 1;
