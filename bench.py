@@ -42,6 +42,29 @@ def alg_bytes_haar(n: int, T: int, s: int = 8) -> float:
     return float(s) * n * (3.0 * T * (T + 1) / 2.0 + 2.0 * T)
 
 
+def rank_seed(base: int, rank: int) -> int:
+    """One independent trial per rank (trial sharding)."""
+    return base + 1000 * rank
+
+
+def shard_trials(total: int, world: int, rank: int):
+    """Contiguous trial range of `rank` (batched-trial configs)."""
+    return (total * rank // world, total * (rank + 1) // world)
+
+
+def max_over_ranks(x: float, dist, device) -> float:
+    import torch
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_value(world: int, n: int, T: int, steps: int, ms: float) -> float:
+    """Aggregate element-updates/s over all ranks, timed by the slowest rank."""
+    return world * elem_updates(n, T) * steps / (ms / 1e3)
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -205,7 +228,7 @@ def main():
     from paper_2101_07464_b200 import lazymat
 
     n, T = args.n, args.T
-    seed = args.seed + 1000 * rank  # one independent trial per rank
+    seed = rank_seed(args.seed, rank)
     op = lazymat.HaarOperator(n, seed=seed, capacity=T, device=local)
     gen = torch.Generator(device=dev).manual_seed(seed)
     x1 = torch.randn(n, dtype=torch.float64, device=dev, generator=gen)
@@ -235,12 +258,10 @@ def main():
     launches = (op.launch_count() - l0) // args.steps
     ms = ev0.elapsed_time(ev1)
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms, dist, dev)
         dist.barrier()
     ms_step = ms / args.steps
-    value = world * elem_updates(n, T) * args.steps / (ms / 1e3)
+    value = whole_job_value(world, n, T, args.steps, ms)
     final_norm = float(out.norm())
 
     # e2e through the public API with host buffers (H2D x_1, x_0; D2H x_{T+1})
@@ -256,10 +277,8 @@ def main():
         outh = op.run(x1h, T, update="tanh_mix", sides="right", x0=x0h, use_graph=use_graph)
     e2e_s = time.perf_counter() - t0
     if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_val = world * elem_updates(n, T) * args.steps / e2e_s
+        e2e_s = max_over_ranks(e2e_s, dist, dev)
+    e2e_val = whole_job_value(world, n, T, args.steps, e2e_s * 1e3)
     assert np.isfinite(outh).all()
 
     # roofline: instrumented pass (CUDA events around every launch on the op's stream)
@@ -275,11 +294,15 @@ def main():
     achieved = (d["alg_bytes"] / d["launches"]) / (d["ms"] / d["launches"] / 1e3) / 1e9
     tot_ms = sum(v["ms"] for v in stats.values())
     tot_bytes = sum(v["alg_bytes"] for v in stats.values())
+    # DRAM bytes per launch of the dominant kernel: the committed ncu capture's
+    # DRAM/algorithmic ratio (probe t = 91) applied to this run's per-launch bytes
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(dom)
+            tr = json.load(open(tp)).get(dom)
+            if tr:
+                traffic = tr["ratio"] * d["alg_bytes"] / d["launches"]
         except Exception:
             traffic = None
 
