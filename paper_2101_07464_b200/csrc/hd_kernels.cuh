@@ -144,6 +144,7 @@ struct DotArgs {
   int nslots = 0;
   int* status = nullptr;
   int prefetch = 0;  // host-asserted: the previous launch writes no panel read here
+  unsigned long long* trace = nullptr;  // debug: latest CTA exit time -> trace[8]
 };
 
 // Shared-memory carve-up of the streaming kernels (per warp: ring + slots).
@@ -264,6 +265,11 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_dots(const __grid_constan
     accs[s] = v;  // row 0 (each slot owned by one thread here)
   }
   flush_row(accs, a.nslots, a.out);
+  if (a.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    atomicMax(a.trace + 8, t);
+  }
 }
 
 // ============================================================ GEMV-N core
@@ -693,28 +699,86 @@ struct SmallArgs {
   const double* spec_parts = nullptr;  // [slot][spec_nblk] of the previous k_apply(OTHER)
   int spec_nblk = 0, spec_slot0 = 0, spec_count = 0;
   int fold_slot_ss = 0;
+  int stageA = 0, stageB = 0;  // stage T_A / T_B in shared memory (host: fits the budget)
+  int nslots_in = 0;           // slot rows of `partials` staged by the stage
+  int stageC = 0;              // stage the sparse-input corner of P_B in shared memory
+  unsigned long long* trace = nullptr;  // debug: %globaltimer stamps per phase (HD_TRACE)
 };
 
-// dst[s] = sum_b parts[(slot0 + s) * nblk + b], thread per slot (fixed order).
-__device__ __forceinline__ void st_reduce(const double* parts, int nblk, int slot0, int count, double* dst, int tid,
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define HD_STAMP(a, k)                                   \
+  do {                                                   \
+    if ((a).trace && threadIdx.x == 0) (a).trace[k] = gtimer(); \
+  } while (0)
+// intra-kernel stamps in SM cycles (globaltimer is too coarse for sub-us)
+#define HD_CLK(a, k)                                               \
+  do {                                                             \
+    if ((a).trace && threadIdx.x == 0) (a).trace[k] = clock64();   \
+  } while (0)
+
+// dst[s] = sum_b parts[(slot0 + s) * nblk + b], thread per slot (fixed order;
+// four independent accumulators so the loads are all in flight together).
+__device__ __noinline__ void st_reduce(const double* parts, int nblk, int slot0, int count, double* dst, int tid,
                                           int nthr) {
+#pragma unroll 1
   for (int s = tid; s < count; s += nthr) {
     const double* ps = parts + (size_t)(slot0 + s) * nblk;
-    double v = 0.0;
-    for (int b = 0; b < nblk; ++b) v += ps[b];
-    dst[s] = v;
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    int b = 0;
+#pragma unroll 1
+    for (; b + 4 <= nblk; b += 4) {
+      v0 += ps[b];
+      v1 += ps[b + 1];
+      v2 += ps[b + 2];
+      v3 += ps[b + 3];
+    }
+#pragma unroll 1
+    for (; b < nblk; ++b) v0 += ps[b];
+    dst[s] = (v0 + v1) + (v2 + v3);
   }
+}
+
+// Async-stage `count` contiguous doubles (global -> shared).
+__device__ __noinline__ void st_stage(const double* src, int64_t count, double* dst, int t, int nthr) {
+#pragma unroll 1
+  for (int64_t e = t; e < count; e += nthr) cp_async8(dst + e, src + e);
+}
+
+// Read view of a compact-WY T (column-major, leading dimension ld): either
+// the chain's HBM copy or a shared-memory stage of its k x k corner.
+struct TView {
+  const double* p;
+  int64_t ld;
+  __device__ __forceinline__ double operator()(int i, int j) const { return p[i + (int64_t)j * ld]; }
+};
+
+// Stage T[:k, :k] into shared memory (ld = k | 1, conflict-free rows) with
+// one fully parallel coalesced sweep; threads [t0, t0 + nthr).
+__device__ __noinline__ TView st_stage_T(const ChainDev& ch, int k, double* dst, int t, int nthr) {
+  const int64_t ld = k | 1;
+  const int w = t >> 5, lane = t & 31, nw = nthr >> 5;  // warp per column, no integer division
+#pragma unroll 1
+  for (int j = w; j < k; j += nw)
+#pragma unroll 1
+    for (int i = lane; i < k; i += 32) cp_async8(dst + i + (int64_t)j * ld, ch.Tm + i + (int64_t)j * ch.K);
+  return TView{dst, ld};  // valid after cp_async_wait_all() + barrier
 }
 
 // T_new[:k, k] = -c T[:k, :k] g (g in shared memory), T_new[k, k] = c; the
 // new column is written to global memory and to tcol (shared). Warps
 // [w0, w0 + nw) of the CTA, warp per row.
-__device__ __forceinline__ void st_T_column(const ChainDev& ch, int k, double c, const double* g, double* tcol, int w0,
-                                            int nw) {
+__device__ __noinline__ void st_T_column(const ChainDev& ch, const TView& tv, int k, double c, const double* g,
+                                            double* tcol, int w0, int nw) {
   const int w = (threadIdx.x >> 5) - w0, lane = threadIdx.x & 31;
+#pragma unroll 1
   for (int i = w; i < k; i += nw) {
     double v = 0.0;
-    for (int l = i + lane; l < k; l += 32) v += ch.Tm[i + (int64_t)l * ch.K] * g[l];
+#pragma unroll 1
+    for (int l = i + lane; l < k; l += 32) v += tv(i, l) * g[l];
     v = warp_sum(v);
     if (lane == 0) {
       tcol[i] = -c * v;
@@ -728,13 +792,15 @@ __device__ __forceinline__ void st_T_column(const ChainDev& ch, int k, double c,
 }
 
 // out[j] = sum_{i <= j} T[i, j] u[i] for j < k (column p, if >= 0, comes
-// from tcol in shared memory). Warp per column: coalesced.
-__device__ __forceinline__ void st_Tt(const ChainDev& ch, int k, const double* u, double* out, int p,
+// from tcol in shared memory). Warp per column.
+__device__ __noinline__ void st_Tt(const TView& tv, int k, const double* u, double* out, int p,
                                       const double* tcol, int w0, int nw) {
   const int w = (threadIdx.x >> 5) - w0, lane = threadIdx.x & 31;
+#pragma unroll 1
   for (int j = w; j < k; j += nw) {
-    const double* col = (j == p) ? tcol : ch.Tm + (int64_t)j * ch.K;
     double v = 0.0;
+    const double* col = (j == p) ? tcol : tv.p + (int64_t)j * tv.ld;
+#pragma unroll 1
     for (int i = lane; i <= j; i += 32) v += col[i] * u[i];
     v = warp_sum(v);
     if (lane == 0) out[j] = v;
@@ -742,12 +808,14 @@ __device__ __forceinline__ void st_Tt(const ChainDev& ch, int k, const double* u
 }
 
 // out[i] = sum_{j >= i} T[i, j] u[j] for i < k (column p from tcol).
-__device__ __forceinline__ void st_T(const ChainDev& ch, int k, const double* u, double* out, int p,
+__device__ __noinline__ void st_T(const TView& tv, int k, const double* u, double* out, int p,
                                      const double* tcol, int w0, int nw) {
   const int w = (threadIdx.x >> 5) - w0, lane = threadIdx.x & 31;
+#pragma unroll 1
   for (int i = w; i < k; i += nw) {
     double v = 0.0;
-    for (int j = i + lane; j < k; j += 32) v += ((j == p) ? tcol[i] : ch.Tm[i + (int64_t)j * ch.K]) * u[j];
+#pragma unroll 1
+    for (int j = i + lane; j < k; j += 32) v += ((j == p) ? tcol[i] : tv(i, j)) * u[j];
     v = warp_sum(v);
     if (lane == 0) out[i] = v;
   }
@@ -757,7 +825,7 @@ __device__ __forceinline__ void st_T(const ChainDev& ch, int k, const double* u,
 // the panel: pivot fix-up, scale, coefficient, leading factor; returns the
 // sign (0 under the zeroing negative control). Single thread.
 template <typename T>
-__device__ __forceinline__ double st_reflector(const ChainDev& ch, T* P, int j, int64_t off, double nrm, double pivot,
+__device__ __noinline__ double st_reflector(const ChainDev& ch, T* P, int j, int64_t off, double nrm, double pivot,
                                                int rule, double colscale, double unscale, bool append) {
   double sign;
   if (rule == 0) sign = (pivot >= 0.0) ? 1.0 : -1.0;
@@ -782,9 +850,16 @@ __device__ __forceinline__ double st_reflector(const ChainDev& ch, T* P, int j, 
 
 // D update for a member with offset off and leading factor s: D[i] *= s for
 // i >= off (threads [t0, t0 + nthr)).
-__device__ __forceinline__ void st_D_update(const ChainDev& ch, int64_t off, double s, int t, int nthr) {
+__device__ __noinline__ void st_D_update(const ChainDev& ch, int64_t off, double s, int t, int nthr) {
   for (int64_t i = off + t; i < ch.Dlen; i += nthr) ch.Drow[i] *= s;
   if (t == 0) *ch.Dtail *= s;
+}
+
+// Vector length of the single-CTA stages' shared-memory layout (>= 32 so a
+// vector can also hold the <= 19 group partials of one slot).
+__host__ __device__ inline int small_kv(int kA, int kB) {
+  const int k = (kA > kB ? kA : kB) + 2;
+  return k < 32 ? 32 : k;
 }
 
 // Shared-memory layout of the small kernels: 12 vectors of length kv.
@@ -809,13 +884,14 @@ __device__ __forceinline__ SmallSmem small_smem(double* base, int kv) {
 // coefficients beta1 = sig (T_A^T (sig a)) (half 1), the Haar mix reflector
 // H(g, off) appended to chain B or (Ginibre) the opposite-side sparse
 // coefficients (half 2), and the power-of-two fold-column scale.
-template <typename T>
+template <typename T, bool HAAR>
 __global__ void __launch_bounds__(kSmallThreads) k_small_dots(const __grid_constant__ SmallArgs a) {
   extern __shared__ double ssm[];
+  HD_STAMP(a, 0);
   pdl_wait();
+  HD_STAMP(a, 1);
   pdl_launch();
-  if (aborted(a.status)) return;
-  const int kv = max(a.kA, a.kB) + 2;
+  const int kv = small_kv(a.kA, a.kB);
   const SmallSmem m = small_smem(ssm, kv);
   double* aA = m.v0;     // red A dot
   double* pA = m.v1;     // red A pend
@@ -829,50 +905,86 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_dots(const __grid_const
   double* rowB = m.v9;   // P_B[off, :]
   double* gB = m.v10;    // G col B
   double* tB = m.v11;    // new T col B
+  double* tsA = m.sc + 16;
+  double* tsB = tsA + (a.stageA ? (size_t)a.kA * (a.kA | 1) : 0);
+  double* ps = tsB + (a.stageB ? (size_t)a.kB * (a.kB | 1) : 0);  // [nslots_in][nblk]
+  double* ss = ps + (size_t)a.nslots_in * a.nblk;                  // spec rows [kB][spec_nblk]
+  T* rowT = reinterpret_cast<T*>(gB);                               // raw pivot row (converted below)
+  int* st = reinterpret_cast<int*>(m.sc + 12);                      // staged status words
   const int tid = threadIdx.x;
-  // ---- phase 1: one global round
-  if (a.kA > 0) st_reduce(a.partials, a.nblk, a.slotA_dot, a.kA, aA, tid, kSmallThreads);
-  if (a.pendA >= 0) st_reduce(a.partials, a.nblk, a.slotA_pend, a.pendA + 1, pA, tid, kSmallThreads);
-  if (a.is_haar && a.mix_from_spec) {
-    if (a.kB > 0) st_reduce(a.spec_parts, a.spec_nblk, a.spec_slot0, a.kB, aB, tid, kSmallThreads);
-  } else if (a.kB > 0) {
-    st_reduce(a.partials, a.nblk, a.slotB_dot, a.kB, aB, tid, kSmallThreads);
-  }
-  if (a.pendB >= 0) st_reduce(a.partials, a.nblk, a.slotB_pend, a.pendB + 1, pB, tid, kSmallThreads);
-  for (int j = tid; j < a.kA; j += kSmallThreads) sgA[j] = a.chA.sig[j];
-  if (a.is_haar) {
+  const bool spec = HAAR && a.mix_from_spec && a.kB > 0;
+  // ---- phase 1: every global load issued asynchronously (no register round
+  // trips: the panel row and scalars miss L2 right after a streaming pass)
+  HD_CLK(a, 5);
+  const TView tvA = a.stageA ? st_stage_T(a.chA, a.kA, tsA, tid, kSmallThreads) : TView{a.chA.Tm, a.chA.K};
+  const TView tvB = (HAAR && a.stageB) ? st_stage_T(a.chB, a.kB, tsB, tid, kSmallThreads) : TView{a.chB.Tm, a.chB.K};
+  HD_CLK(a, 6);
+  st_stage(a.partials, (int64_t)a.nslots_in * a.nblk, ps, tid, kSmallThreads);
+  if (spec) st_stage(a.spec_parts + (size_t)a.spec_slot0 * a.spec_nblk, (int64_t)a.kB * a.spec_nblk, ss, tid, kSmallThreads);
+  #pragma unroll 1
+  for (int j = tid; j < a.kA; j += kSmallThreads) cp_async8(sgA + j, a.chA.sig + j);
+  if (HAAR) {
     const T* PB = (const T*)a.PB;
+    #pragma unroll 1
     for (int j = tid; j < a.kB; j += kSmallThreads) {
-      sgB[j] = a.chB.sig[j];
-      rowB[j] = (double)PB[paddr(a.off, j, a.chB.K)];
+      cp_async8(sgB + j, a.chB.sig + j);
+      cp_async_elem(rowT + j, PB + paddr(a.off, j, a.chB.K));
     }
   }
   if (tid == 0) {
-    st_reduce(a.partials, a.nblk, a.slotA_ss, 1, m.sc + 0, 0, 1);
-    if (a.slotB_ss >= 0) st_reduce(a.partials, a.nblk, a.slotB_ss, 1, m.sc + 1, 0, 1);
-    m.sc[2] = (a.pendA >= 0) ? a.chA.c[a.pendA] : 0.0;
-    m.sc[3] = (a.pendB >= 0) ? a.chB.c[a.pendB] : 0.0;
-    m.sc[4] = a.scal[kScPivotG];
-    if (*(volatile int*)(a.status + kStBadInput)) *(volatile int*)(a.status + kStAbort) = 1;
+    if (a.pendA >= 0) cp_async8(m.sc + 2, a.chA.c + a.pendA);
+    if (a.pendB >= 0) cp_async8(m.sc + 3, a.chB.c + a.pendB);
+    cp_async8(m.sc + 4, a.scal + kScPivotG);
+    cp_async4(st + 0, a.status + kStAbort);
+    cp_async4(st + 1, a.status + kStBadInput);
+  }
+  HD_CLK(a, 7);
+  cp_async_wait_all();
+  HD_CLK(a, 9);
+  __syncthreads();
+  HD_CLK(a, 10);
+  if (st[0] != 0) return;
+  if (st[1] != 0) {  // non-finite probe input seen by k_dots: abort the probe
+    if (tid == 0) *(volatile int*)(a.status + kStAbort) = 1;
+    return;
+  }
+  if (a.pendA < 0 && tid == 0) m.sc[2] = 0.0;
+  if (a.pendB < 0 && tid == 0) m.sc[3] = 0.0;
+  if (HAAR)
+    #pragma unroll 1
+    for (int j = tid; j < a.kB; j += kSmallThreads) rowB[j] = (double)rowT[j];
+  if (a.kA > 0) st_reduce(ps, a.nblk, a.slotA_dot, a.kA, aA, tid, kSmallThreads);
+  if (a.pendA >= 0) st_reduce(ps, a.nblk, a.slotA_pend, a.pendA + 1, pA, tid, kSmallThreads);
+  if (spec) st_reduce(ss, a.spec_nblk, 0, a.kB, aB, tid, kSmallThreads);
+  else if (a.kB > 0) st_reduce(ps, a.nblk, a.slotB_dot, a.kB, aB, tid, kSmallThreads);
+  if (a.pendB >= 0) st_reduce(ps, a.nblk, a.slotB_pend, a.pendB + 1, pB, tid, kSmallThreads);
+  if (tid == 0) {
+    st_reduce(ps, a.nblk, a.slotA_ss, 1, m.sc + 0, 0, 1);
+    if (a.slotB_ss >= 0) st_reduce(ps, a.nblk, a.slotB_ss, 1, m.sc + 1, 0, 1);
   }
   __syncthreads();
-  if (aborted(a.status)) return;
+  HD_CLK(a, 11);
+  HD_STAMP(a, 2);
   if (tid < kHalf) {
     // ---- half 1: chain A
     const int p = a.pendA;
     if (p >= 0) {
+      #pragma unroll 1
       for (int j = tid; j <= p; j += kHalf) {
         gA[j] = sgA[j] * sgA[p] * pA[j];
         a.chA.G[j + (int64_t)p * a.chA.K] = gA[j];
       }
       named_sync(1, kHalf);
-      st_T_column(a.chA, p, m.sc[2], gA, tA, 0, kHalf / 32);
+      st_T_column(a.chA, tvA, p, m.sc[2], gA, tA, 0, kHalf / 32);
     }
+    #pragma unroll 1
     for (int j = tid; j < a.kA; j += kHalf) uA[j] = sgA[j] * aA[j];
     named_sync(1, kHalf);
-    st_Tt(a.chA, a.kA, uA, gA, p, tA, 0, kHalf / 32);
+    st_Tt(tvA, a.kA, uA, gA, p, tA, 0, kHalf / 32);
     named_sync(1, kHalf);
+    #pragma unroll 1
     for (int j = tid; j < a.kA; j += kHalf) a.beta1[j] = sgA[j] * gA[j];
+    HD_STAMP(a, 3);
     if (tid == 0) {
       const double xn = sqrt(m.sc[0]);
       int e = 0;
@@ -883,16 +995,21 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_dots(const __grid_const
   } else {
     // ---- half 2: chain B
     const int t2 = tid - kHalf;
-    if (a.is_haar) {
+    if (HAAR) {
       int kB = a.kB;
       const int p = a.pendB;
       if (p >= 0) {  // fallback path only (same-side speculation unavailable)
+        #pragma unroll 1
         for (int j = t2; j <= p; j += kHalf) {
           gB[j] = a.chB.sig[j] * a.chB.sig[p] * pB[j];
           a.chB.G[j + (int64_t)p * a.chB.K] = gB[j];
         }
         named_sync(2, kHalf);
-        st_T_column(a.chB, p, m.sc[3], gB, tB, kHalf / 32, kHalf / 32);
+        st_T_column(a.chB, tvB, p, m.sc[3], gB, tB, kHalf / 32, kHalf / 32);
+        named_sync(2, kHalf);
+        if (a.stageB)  // the staged copy must see the finished column p
+          #pragma unroll 1
+          for (int i = t2; i <= p; i += kHalf) tsB[i + (int64_t)p * tvB.ld] = tB[i];
         named_sync(2, kHalf);
       }
       // mix reflector H(g, off) -> column kB of chain B
@@ -905,6 +1022,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_dots(const __grid_const
       }
       named_sync(2, kHalf);
       const double sign = m.sc[5], cB = m.sc[6];
+      #pragma unroll 1
       for (int j = t2; j < kB; j += kHalf) {
         gB[j] = (nrm == 0.0) ? 0.0 : sgB[j] * (aB[j] / nrm + sign * rowB[j]);
         a.chB.G[j + (int64_t)kB * a.chB.K] = gB[j];
@@ -912,62 +1030,102 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_dots(const __grid_const
       if (t2 == 0) a.chB.G[kB + (int64_t)kB * a.chB.K] = (nrm == 0.0) ? 0.0 : 2.0 / cB;
       if (nrm != 0.0) st_D_update(a.chB, a.off, -sign, t2, kHalf);
       named_sync(2, kHalf);
-      st_T_column(a.chB, kB, cB, gB, tB, kHalf / 32, kHalf / 32);
+      st_T_column(a.chB, tvB, kB, cB, gB, tB, kHalf / 32, kHalf / 32);
     } else {
       // Ginibre: opposite-side coefficients <v_i, x> (or <u_i, x>), rows < kB
+      #pragma unroll 1
       for (int q = t2; q < a.kB; q += kHalf) a.csp[q] = aB[q];
     }
+  }
+  if (a.trace) {
+    __syncthreads();
+    HD_STAMP(a, 4);
   }
 }
 
 // After k_apply(FOLD): finalise the fold reflector H(p, off) (appended
 // unless the skip fault fires), then (Haar) beta = sig (T_B (W_B^T D_B z))
 // for the sparse folded iterate z = H p, or (Ginibre) the current coefficient.
-template <typename T>
+template <typename T, bool HAAR>
 __global__ void __launch_bounds__(kSmallThreads) k_small_fold(const __grid_constant__ SmallArgs a) {
   extern __shared__ double ssm[];
   pdl_wait();
   pdl_launch();
-  if (aborted(a.status)) return;
-  const int kv = max(a.kA, a.kB) + 2;
+  const int kv = small_kv(a.kA, a.kB);
   const SmallSmem m = small_smem(ssm, kv);
-  double* az = m.v0;    // corner partial sig_j sum_{i<off} P_B[i,j] D_B(i) p_i
+  double* az = m.v0;    // corner partial sum_{i<off} P_B[i,j] D_B(i) p_i
   double* rowB = m.v1;  // P_B[off, :]
   double* tmp = m.v2;
   double* sgB = m.v3;
+  double* psf = m.v4;   // ||p[off:]||^2 group partials (nblk <= kv)
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const T* PB = (const T*)a.PB;
-  // ---- phase 1
-  if (a.is_haar) {
+  const int64_t nr = a.off + 1;
+  double* tsB = m.sc + 16;
+  double* hs = tsB + (a.stageB ? (size_t)a.kB * (a.kB | 1) : 0);  // head p[0..off]
+  double* ds = hs + nr;                                               // D_B[0..off]
+  T* cs = reinterpret_cast<T*>(ds + nr);                              // corner [kB][nr]
+  // ---- phase 1: every global load issued asynchronously, one wait
+  const TView tvB = (HAAR && a.stageB) ? st_stage_T(a.chB, a.kB, tsB, tid, kSmallThreads)
+                                            : TView{a.chB.Tm, a.chB.K};
+  st_stage(a.partials + (size_t)a.fold_slot_ss * a.nblk, a.nblk, psf, tid, kSmallThreads);
+  st_stage(a.head, nr, hs, tid, kSmallThreads);
+  int* st = reinterpret_cast<int*>(m.sc + 12);
+  if (tid == 0) {
+    cp_async8(m.sc + 8, a.scal + kScEscale);
+    cp_async8(m.sc + 9, a.scal + kScIscale);
+    cp_async4(st, a.status + kStAbort);
+  }
+  if (HAAR) {
+    #pragma unroll 1
+    for (int64_t i = tid; i < nr; i += kSmallThreads) cp_async8(ds + i, i < a.chB.Dlen ? a.chB.Drow + i : a.chB.Dtail);
+    #pragma unroll 1
+    for (int j = tid; j < a.kB; j += kSmallThreads) cp_async8(sgB + j, a.chB.sig + j);
+    if (a.stageC)
+      #pragma unroll 1
+      for (int j = w; j < a.kB; j += kSmallThreads / 32)
+        #pragma unroll 1
+        for (int64_t i = lane; i < nr; i += 32) cp_async_elem(cs + j * nr + i, PB + paddr(i, j, a.chB.K));
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (st[0] != 0) return;
+  if (HAAR) {
+    #pragma unroll 1
     for (int j = w; j < a.kB; j += kSmallThreads / 32) {
       double v = 0.0;
-      for (int64_t i = lane; i < a.off; i += 32)
-        v += (double)PB[paddr(i, j, a.chB.K)] * dval(a.chB.Drow, a.chB.Dtail, a.chB.Dlen, i) * a.head[i];
+      if (a.stageC) {
+        #pragma unroll 1
+        for (int64_t i = lane; i < a.off; i += 32) v += (double)cs[j * nr + i] * ds[i] * hs[i];
+      } else {
+        #pragma unroll 1
+        for (int64_t i = lane; i < a.off; i += 32) v += (double)PB[paddr(i, j, a.chB.K)] * ds[i] * hs[i];
+      }
       v = warp_sum(v);
       if (lane == 0) {
         az[j] = v;
-        rowB[j] = (double)PB[paddr(a.off, j, a.chB.K)];
-        sgB[j] = a.chB.sig[j];
+        rowB[j] = a.stageC ? (double)cs[j * nr + a.off] : (double)PB[paddr(a.off, j, a.chB.K)];
       }
     }
-    for (int64_t i = tid; i < a.off; i += kSmallThreads) a.zbuf[i] = a.head[i];
+    #pragma unroll 1
+    for (int64_t i = tid; i < a.off; i += kSmallThreads) a.zbuf[i] = hs[i];
   }
   if (w == 0) {
-    const double* ps = a.partials + (size_t)a.fold_slot_ss * a.nblk;
     double v = 0.0;
-    for (int b = lane; b < a.nblk; b += 32) v += ps[b];
+    #pragma unroll 1
+    for (int b = lane; b < a.nblk; b += 32) v += psf[b];
     v = warp_sum(v);
     if (lane == 0) {
       m.sc[0] = sqrt(v);
-      m.sc[1] = a.head[a.off];
-      m.sc[2] = (a.is_haar && a.off < a.chB.Dlen) ? a.chB.Drow[a.off] : *a.chB.Dtail;
+      m.sc[1] = hs[a.off];
+      m.sc[2] = HAAR ? ds[a.off] : 0.0;
     }
   }
   __syncthreads();
   const double nrm = m.sc[0], piv = m.sc[1];
   if (tid == 0) {
-    const double sign = st_reflector<T>(a.chA, (T*)a.PA, a.kA, a.off, nrm, piv, a.rule, a.scal[kScEscale],
-                                        a.scal[kScIscale], a.append != 0);
+    const double sign = st_reflector<T>(a.chA, (T*)a.PA, a.kA, a.off, nrm, piv, a.rule, m.sc[8], m.sc[9],
+                                        a.append != 0);
     // (H p)[off]: +||p[off:]|| (0 under the zeroing negative control)
     const double zoff = (nrm == 0.0) ? piv : (sign == 0.0 ? 0.0 : nrm);
     m.sc[3] = sign;
@@ -975,16 +1133,18 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_fold(const __grid_const
     a.scal[kScNrm] = nrm;
     a.scal[kScCoefCur] = a.append ? zoff : piv;
     a.scal[kScSign] = sign;
-    if (a.is_haar) a.zbuf[a.off] = zoff;
+    if (HAAR) a.zbuf[a.off] = zoff;
   }
   __syncthreads();
   if (a.append && nrm != 0.0) st_D_update(a.chA, a.off, -m.sc[3], tid, kSmallThreads);
-  if (a.is_haar) {
+  if (HAAR) {
     const double zoff = m.sc[4], doff = m.sc[2];
+    #pragma unroll 1
     for (int j = tid; j < a.kB; j += kSmallThreads) tmp[j] = sgB[j] * (az[j] + rowB[j] * doff * zoff);
     __syncthreads();
-    st_T(a.chB, a.kB, tmp, az, -1, nullptr, 0, kSmallThreads / 32);
+    st_T(tvB, a.kB, tmp, az, -1, nullptr, 0, kSmallThreads / 32);
     __syncthreads();
+    #pragma unroll 1
     for (int j = tid; j < a.kB; j += kSmallThreads) a.beta1[j] = sgB[j] * az[j];
   }
 }
@@ -998,7 +1158,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_gin(const __grid_consta
   pdl_wait();
   pdl_launch();
   if (aborted(a.status)) return;
-  const int kv = a.kB + 2;
+  const int kv = small_kv(0, a.kB);
   const SmallSmem m = small_smem(ssm, kv);
   double* ag = m.v0;
   double* pB = m.v1;
@@ -1011,37 +1171,70 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_gin(const __grid_consta
   double* o3 = m.v8;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const T* PB = (const T*)a.PB;
-  if (a.kB > 0) st_reduce(a.partials, a.nblk, a.slotB_dot, a.kB, ag, tid, kSmallThreads);
-  if (a.pendB >= 0) st_reduce(a.partials, a.nblk, a.slotB_pend, a.pendB + 1, pB, tid, kSmallThreads);
-  for (int j = tid; j < a.kB; j += kSmallThreads) sg[j] = a.chB.sig[j];
+  const int64_t nr = a.csplen;
+  double* tsB = m.sc + 16;
+  double* ps = tsB + (a.stageB ? (size_t)a.kB * (a.kB | 1) : 0);  // [nslots_in][nblk]
+  double* cps = ps + (size_t)a.nslots_in * a.nblk;                  // D_B(i) c_i, i < nr
+  double* dsg = cps + nr;                                           // D_B rows (staging)
+  T* cs = reinterpret_cast<T*>(dsg + nr);                           // corner [kB][nr]
+  // ---- phase 1: every global load issued asynchronously, one wait
+  const TView tvB = a.stageB ? st_stage_T(a.chB, a.kB, tsB, tid, kSmallThreads) : TView{a.chB.Tm, a.chB.K};
+  st_stage(a.partials, (int64_t)a.nslots_in * a.nblk, ps, tid, kSmallThreads);
+  st_stage(a.csp, nr, cps, tid, kSmallThreads);
+  #pragma unroll 1
+  for (int64_t i = tid; i < nr; i += kSmallThreads) cp_async8(dsg + i, i < a.chB.Dlen ? a.chB.Drow + i : a.chB.Dtail);
+  #pragma unroll 1
+  for (int j = tid; j < a.kB; j += kSmallThreads) cp_async8(sg + j, a.chB.sig + j);
+  if (a.stageC)
+    #pragma unroll 1
+    for (int j = w; j < a.kB; j += kSmallThreads / 32)
+      #pragma unroll 1
+      for (int64_t i = lane; i < nr; i += 32) cp_async_elem(cs + j * nr + i, PB + paddr(i, j, a.chB.K));
+  #pragma unroll 1
+  for (int q = tid; q < a.nS; q += kSmallThreads) a.coefS[q] = a.head[q];
+  if (tid == 0) m.sc[0] = (a.pendB >= 0) ? a.chB.c[a.pendB] : 0.0;
+  cp_async_wait_all();
+  __syncthreads();
+  if (a.kB > 0) st_reduce(ps, a.nblk, a.slotB_dot, a.kB, ag, tid, kSmallThreads);
+  if (a.pendB >= 0) st_reduce(ps, a.nblk, a.slotB_pend, a.pendB + 1, pB, tid, kSmallThreads);
+  #pragma unroll 1
+  for (int64_t i = tid; i < nr; i += kSmallThreads) cps[i] *= dsg[i];
+  __syncthreads();
   // corner W_B^T (D_B c) over rows < csplen (does not involve the pending T)
+  #pragma unroll 1
   for (int j = w; j < a.kB; j += kSmallThreads / 32) {
     double v = 0.0;
-    for (int64_t i = lane; i < a.csplen; i += 32)
-      v += (double)PB[paddr(i, j, a.chB.K)] * dval(a.chB.Drow, a.chB.Dtail, a.chB.Dlen, i) * a.csp[i];
+    if (a.stageC) {
+      #pragma unroll 1
+      for (int64_t i = lane; i < nr; i += 32) v += (double)cs[j * nr + i] * cps[i];
+    } else {
+      #pragma unroll 1
+      for (int64_t i = lane; i < nr; i += 32) v += (double)PB[paddr(i, j, a.chB.K)] * cps[i];
+    }
     v = warp_sum(v);
     if (lane == 0) ac[j] = v;
   }
-  for (int q = tid; q < a.nS; q += kSmallThreads) a.coefS[q] = a.head[q];
-  if (tid == 0) m.sc[0] = (a.pendB >= 0) ? a.chB.c[a.pendB] : 0.0;
   __syncthreads();
   const int p = a.pendB;
   if (p >= 0) {
+    #pragma unroll 1
     for (int j = tid; j <= p; j += kSmallThreads) {
       gB[j] = sg[j] * sg[p] * pB[j];
       a.chB.G[j + (int64_t)p * a.chB.K] = gB[j];
     }
     __syncthreads();
-    st_T_column(a.chB, p, m.sc[0], gB, tB, 0, kSmallThreads / 32);
+    st_T_column(a.chB, tvB, p, m.sc[0], gB, tB, 0, kSmallThreads / 32);
   }
+  #pragma unroll 1
   for (int j = tid; j < a.kB; j += kSmallThreads) {
     u1[j] = sg[j] * ag[j];
     ac[j] = sg[j] * ac[j];
   }
   __syncthreads();
-  if (tid < kHalf) st_T(a.chB, a.kB, u1, o1, p, tB, 0, kHalf / 32);
-  else st_T(a.chB, a.kB, ac, o3, p, tB, kHalf / 32, kHalf / 32);
+  if (tid < kHalf) st_T(tvB, a.kB, u1, o1, p, tB, 0, kHalf / 32);
+  else st_T(tvB, a.kB, ac, o3, p, tB, kHalf / 32, kHalf / 32);
   __syncthreads();
+  #pragma unroll 1
   for (int j = tid; j < a.kB; j += kSmallThreads) {
     a.beta1[j] = sg[j] * o1[j];
     a.beta3[j] = sg[j] * o3[j];

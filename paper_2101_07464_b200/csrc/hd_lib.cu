@@ -142,6 +142,9 @@ struct hd_op {
   std::map<long, int> apply_bps;
   int last_other_grid = 0, last_other_slot_ss = 0;  // normalize partials of k_apply(OTHER)
   bool pdl = true;  // programmatic dependent launch (HD_NO_PDL=1 disables)
+  unsigned long long* trace = nullptr;  // HD_TRACE=1: phase stamps of k_small_dots
+  std::vector<double> trace_acc;        // accumulated phase durations (ns)
+  int64_t trace_n = 0;
   // graph cache (hd_run from a fresh state)
   cudaGraphExec_t graph = nullptr;
   std::string graph_key;
@@ -465,9 +468,54 @@ int launch_apply(hd_op* op, cudaStream_t s, ApplyArgs<T>& a, bool fold_buffer, d
   return grid;
 }
 
-size_t small_smem_bytes(const SmallArgs& a) {
-  const size_t kv = (size_t)std::max(a.kA, a.kB) + 2;
-  return sizeof(double) * (12 * kv + 16);
+// Shared memory of a single-CTA stage (k_small_dots = 0, k_small_fold = 1,
+// k_small_gin = 2); decides what is staged within the budget: the partial
+// rows, heads and sparse-input corner first, then the T corners (k x (k|1)).
+size_t small_smem_bytes(SmallArgs& a, int which, size_t esz) {
+  const size_t kv = (size_t)small_kv(a.kA, a.kB);
+  const size_t budget = 210 * 1024;
+  size_t bytes = sizeof(double) * (12 * kv + 16);
+  a.stageA = a.stageB = a.stageC = 0;
+  bool needA = false, needB = false;
+  size_t nr = 0;
+  if (which == 0) {
+    bytes += sizeof(double) * (size_t)a.nslots_in * a.nblk;
+    if (a.is_haar && a.mix_from_spec) bytes += sizeof(double) * (size_t)a.kB * a.spec_nblk;
+    needA = true;
+    needB = a.is_haar != 0;
+  } else if (which == 1) {
+    nr = (size_t)a.off + 1;
+    bytes += sizeof(double) * 2 * nr;
+    needB = a.is_haar != 0;
+  } else {
+    nr = (size_t)a.csplen;
+    bytes += sizeof(double) * ((size_t)a.nslots_in * a.nblk + 2 * nr);
+    needB = true;
+  }
+  if (nr > 0 && (which == 2 || a.is_haar)) {
+    const size_t c = esz * (size_t)a.kB * nr + 16;
+    if (bytes + c <= budget) {
+      a.stageC = 1;
+      bytes += c;
+    }
+  }
+  const size_t tA = sizeof(double) * (size_t)a.kA * (size_t)(a.kA | 1);
+  const size_t tB = sizeof(double) * (size_t)a.kB * (size_t)(a.kB | 1);
+  if (needA && a.kA > 0 && bytes + tA <= budget) {
+    a.stageA = 1;
+    bytes += tA;
+  }
+  if (needB && a.kB > 0 && bytes + tB <= budget) {
+    a.stageB = 1;
+    bytes += tB;
+  }
+  if (bytes > 227 * 1024) throw HdError(HD_ERR_RESOURCE_CAP, "hd: single-CTA stage exceeds shared memory");
+  return bytes;
+}
+
+template <typename K>
+void allow_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) ck(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes), "smem");
 }
 
 template <typename T>
@@ -550,6 +598,7 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   da.job[1].wj = O.pan.count;
   da.job[1].pivot_out = op->scal + kScPivotG;
   da.job[1].pivot_row = off;
+  da.trace = op->trace;
   // predecessor = previous probe's k_apply(OTHER) (writes y / x_{t+1} only)
   da.prefetch = 1;
   const double b1 = bytes_of(op, (double)n * (F.pan.count + da.job[1].ncols + (F.pend >= 0) + (da.job[1].pend >= 0) + 2)) +
@@ -584,6 +633,7 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   sa.csp = op->csp;
   sa.coefS = op->coefS;
   sa.is_haar = 1;
+  sa.trace = op->trace;
   sa.mix_from_spec = use_spec ? 1 : 0;
   if (use_spec) {
     sa.spec_parts = op->partsO;
@@ -593,7 +643,10 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   }
   {
     LaunchScope ls(op, s, "small_dots", 0.0);
-    launch_k(op, k_small_dots<T>, dim3(1), dim3(kSmallThreads), small_smem_bytes(sa), s, sa);
+    sa.nslots_in = da.nslots;
+    const size_t sm = small_smem_bytes(sa, 0, op->esz);
+    allow_smem(k_small_dots<T, true>, sm);
+    launch_k(op, k_small_dots<T, true>, dim3(1), dim3(kSmallThreads), sm, s, sa);
   }
   check_launch("k_small_dots");
   F.pend = -1;
@@ -629,7 +682,9 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   sa.spec_parts = nullptr;
   {
     LaunchScope ls(op, s, "small_fold", 0.0);
-    launch_k(op, k_small_fold<T>, dim3(1), dim3(kSmallThreads), small_smem_bytes(sa), s, sa);
+    const size_t sm = small_smem_bytes(sa, 1, op->esz);
+    allow_smem(k_small_fold<T, true>, sm);
+    launch_k(op, k_small_fold<T, true>, dim3(1), dim3(kSmallThreads), sm, s, sa);
   }
   check_launch("k_small_fold");
   if (append_fold) {
@@ -755,7 +810,10 @@ void enqueue_ginibre(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi,
   sa.is_haar = 0;
   {
     LaunchScope ls(op, s, "small_dots", 0.0);
-    launch_k(op, k_small_dots<T>, dim3(1), dim3(kSmallThreads), small_smem_bytes(sa), s, sa);
+    sa.nslots_in = da.nslots;
+    const size_t sm = small_smem_bytes(sa, 0, op->esz);
+    allow_smem(k_small_dots<T, false>, sm);
+    launch_k(op, k_small_dots<T, false>, dim3(1), dim3(kSmallThreads), sm, s, sa);
   }
   check_launch("k_small_dots");
   F.pend = -1;
@@ -784,7 +842,9 @@ void enqueue_ginibre(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi,
   sa.append = append_fold ? 1 : 0;
   {
     LaunchScope ls(op, s, "small_fold", 0.0);
-    launch_k(op, k_small_fold<T>, dim3(1), dim3(kSmallThreads), small_smem_bytes(sa), s, sa);
+    const size_t sm = small_smem_bytes(sa, 1, op->esz);
+    allow_smem(k_small_fold<T, false>, sm);
+    launch_k(op, k_small_fold<T, false>, dim3(1), dim3(kSmallThreads), sm, s, sa);
   }
   check_launch("k_small_fold");
   if (append_fold) {
@@ -819,7 +879,10 @@ void enqueue_ginibre(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi,
   sg.nS = (int)S.count;
   {
     LaunchScope ls(op, s, "small_gin", 0.0);
-    launch_k(op, k_small_gin<T>, dim3(1), dim3(kSmallThreads), small_smem_bytes(sg), s, sg);
+    sg.nslots_in = db.nslots;
+    const size_t sm = small_smem_bytes(sg, 2, op->esz);
+    allow_smem(k_small_gin<T>, sm);
+    launch_k(op, k_small_gin<T>, dim3(1), dim3(kSmallThreads), sm, s, sg);
   }
   check_launch("k_small_gin");
   O.pend = -1;
@@ -1013,6 +1076,20 @@ void do_probe(hd_op* op, const void* x, int64_t x_len, void* y, int64_t y_len, i
                        s),
        "copy y");
   ck(cudaStreamSynchronize(s), "probe sync");
+  if (op->trace) {
+    unsigned long long h[16];
+    ck(cudaMemcpy(h, op->trace, sizeof h, cudaMemcpyDeviceToHost), "trace");
+    // [0] dots exit -> small start, [1] start -> after wait, [2] wait -> phase 1,
+    // [3] phase 1 -> beta, [4] beta -> end
+    const double cyc = 1.965;  // SM cycles per ns at max clock (stamps 5..11 are clock64)
+    const double d[8] = {(double)h[0] - (double)h[8], (double)h[1] - (double)h[0], (double)h[2] - (double)h[1],
+                         ((double)h[6] - (double)h[5]) / cyc, ((double)h[7] - (double)h[6]) / cyc,
+                         ((double)h[9] - (double)h[7]) / cyc, ((double)h[10] - (double)h[9]) / cyc,
+                         ((double)h[11] - (double)h[10]) / cyc};
+    for (int i = 0; i < 8; ++i) op->trace_acc[i] += d[i];
+    op->trace_n++;
+    ck(cudaMemset(op->trace, 0, sizeof h), "trace reset");
+  }
   int st[kStWords];
   read_status(op, st);
   if (st[kStBadInput]) {
@@ -1384,6 +1461,12 @@ int hd_create(const hd_config* cfg, hd_op** out) {
   op->rows_pad_n = ceil_div(n, kTile) * kTile;
   op->budget = (c.ensemble == HD_HAAR) ? n : std::min(m, n);
   if (const char* e = std::getenv("HD_NO_PDL")) op->pdl = !(e[0] == '1');
+  if (const char* e = std::getenv("HD_TRACE")) {
+    if (e[0] == '1') {
+      op->trace = dmalloc<unsigned long long>(16);
+      op->trace_acc.assign(16, 0.0);
+    }
+  }
   ck(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking), "stream");
   ck(cudaDeviceGetAttribute(&op->nsm, cudaDevAttrMultiProcessorCount, c.device), "attr");
   const int64_t per_outer = (c.ensemble == HD_GOE) ? 2 : 1;
@@ -1421,6 +1504,13 @@ int hd_create(const hd_config* cfg, hd_op** out) {
 int hd_destroy(hd_op* op) {
   HD_TRY
   if (!op) return HD_OK;
+  if (op->trace && op->trace_n > 0) {
+    std::fprintf(stderr, "HD_TRACE k_small_dots over %lld probes (us):", (long long)op->trace_n);
+    const char* nm[8] = {"dots_end->start", "start->wait", "wait->phase1end(gt)", "stageT_issue(clk)",
+                         "rest_issue(clk)", "cp_async_wait(clk)", "sync(clk)", "reduce(clk)"};
+    for (int i = 0; i < 8; ++i) std::fprintf(stderr, " %s %.2f", nm[i], op->trace_acc[i] / op->trace_n / 1e3);
+    std::fprintf(stderr, "\n");
+  }
   cudaSetDevice(op->cfg.device);
   cudaStreamSynchronize(op->stream);
   if (op->graph) cudaGraphExecDestroy(op->graph);
