@@ -145,6 +145,15 @@ int hd_run_callback(hd_op* op, int64_t iterations, int32_t depth, const void* co
                     hd_side_fn side_of, hd_update_fn update, void* user, void* final_out_dev);
 
 /* ---------------------------------------------------------------------------
+ * Standalone reflector: make_reflector(p, offset, zero_tol, sign_rule) built
+ * on the device and applied to `count` vectors x (each n long, contiguous)
+ * into y (reflect.hpp:70-83,120-176; bindings module.cpp:48-66). Real
+ * reflectors are self-adjoint. info (host, optional) receives c, s and the
+ * identity flag. Validation messages follow reflect.hpp:124-127. */
+int hd_reflector_apply(const double* p, int64_t n, int64_t offset, double zero_tol, int32_t sign_rule,
+                       const double* x, double* y, int64_t count, int32_t on_device, double* info);
+
+/* ---------------------------------------------------------------------------
  * Instrumentation: per-kernel-kind launch counts, device time (CUDA events
  * on the handle's stream) and algorithmic bytes. Off by default. */
 typedef struct hd_kernel_stats {

@@ -1276,6 +1276,88 @@ __global__ void k_scale_copy(const T* y, const double* scale, T* x, int64_t n) {
   if (i < n) x[i] = (T)(*scale * (double)y[i]);
 }
 
+// ---------------------------------------------------- standalone reflector
+// make_reflector(p, offset, zero_tol, rule) + Reflector::apply on `count`
+// vectors (reflect.hpp:70-83,120-176; bindings module.cpp:48-66). One CTA;
+// norms are scaled by the largest magnitude (the stableNorm branch of
+// reflect.hpp:132-136), so inputs at 1e-300 .. 1e290 stay finite.
+constexpr int kReflThreads = 1024;
+
+__device__ double block_max(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int u = 0; u < kReflThreads / 32; ++u) t = fmax(t, sh[u]);
+  __syncthreads();
+  return t;
+}
+
+__device__ double scaled_norm(const double* x, int64_t n, double* sh) {
+  double mx = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += kReflThreads) mx = fmax(mx, fabs(x[i]));
+  const double scale = block_max(mx, sh);
+  if (scale == 0.0 || !isfinite(scale)) return scale;
+  double ss = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += kReflThreads) {
+    const double v = x[i] / scale;
+    ss += v * v;
+  }
+  return scale * sqrt(block_sum<kReflThreads>(ss, sh));
+}
+
+__global__ void __launch_bounds__(kReflThreads) k_reflector(const double* p, int64_t n, int64_t off, double zero_tol,
+                                                            int rule, const double* x, double* y, int64_t count,
+                                                            double* info) {
+  __shared__ double sh[32];
+  const int64_t len = n - off;
+  const double* tail = p + off;
+  const double nrm = scaled_norm(tail, len, sh);
+  bool ident = (nrm == 0.0);
+  if (!ident && zero_tol > 0.0) ident = nrm <= zero_tol * scaled_norm(p, n, sh);
+  const double v1 = tail[0];
+  double sign = 1.0;
+  if (rule == 0) sign = (v1 >= 0.0) ? 1.0 : -1.0;
+  else if (rule == 1) sign = (v1 > 0.0) ? 1.0 : -1.0;
+  else sign = (v1 >= 0.0) ? 1.0 : 0.0;
+  double c = 0.0, s = 1.0;
+  if (!ident) {
+    double a2 = 0.0;
+    for (int64_t i = threadIdx.x; i < len; i += kReflThreads) {
+      const double ai = tail[i] / nrm + (i == 0 ? sign : 0.0);
+      a2 += ai * ai;
+    }
+    a2 = block_sum<kReflThreads>(a2, sh);
+    c = 2.0 / a2;
+    s = -sign;
+  }
+  if (threadIdx.x == 0 && info) {
+    info[0] = c;
+    info[1] = s;
+    info[2] = ident ? 1.0 : 0.0;
+  }
+  for (int64_t v = 0; v < count; ++v) {
+    const double* xv = x + v * n;
+    double* yv = y + v * n;
+    for (int64_t i = threadIdx.x; i < off; i += kReflThreads) yv[i] = xv[i];
+    if (ident) {
+      for (int64_t i = threadIdx.x; i < len; i += kReflThreads) yv[off + i] = xv[off + i];
+      continue;
+    }
+    double proj = 0.0;
+    for (int64_t i = threadIdx.x; i < len; i += kReflThreads)
+      proj += (tail[i] / nrm + (i == 0 ? sign : 0.0)) * xv[off + i];
+    proj = block_sum<kReflThreads>(proj, sh);
+    const double cp = c * proj;
+    for (int64_t i = threadIdx.x; i < len; i += kReflThreads) {
+      const double ai = tail[i] / nrm + (i == 0 ? sign : 0.0);
+      yv[off + i] = (xv[off + i] - cp * ai) * s;
+    }
+  }
+}
+
 __global__ void k_reset_chain(ChainDev ch) {
   pdl_wait();
   pdl_launch();

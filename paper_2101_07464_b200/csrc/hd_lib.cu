@@ -1659,6 +1659,46 @@ int hd_run_callback(hd_op* op, int64_t iterations, int32_t depth, const void* co
   HD_CATCH
 }
 
+int hd_reflector_apply(const double* p, int64_t n, int64_t offset, double zero_tol, int32_t sign_rule,
+                       const double* x, double* y, int64_t count, int32_t on_device, double* info) {
+  HD_TRY
+  // validation order of make_reflector (reflect.hpp:124-127)
+  require(p != nullptr && n >= 1, "make_reflector: empty vector");
+  require(offset >= 0 && offset < n, "make_reflector: offset out of range");
+  require(sign_rule >= 0 && sign_rule <= 2, "make_reflector: unknown sign rule");
+  require(count >= 0 && (count == 0 || (x && y)), "Reflector::apply: dimension mismatch");
+  const size_t pb = sizeof(double) * (size_t)n, xb = pb * (size_t)count;
+  std::vector<double> hp;
+  if (!on_device) {
+    require(host_all_finite(p, n, false), "make_reflector: non-finite entries");
+  } else {
+    hp.resize((size_t)n);
+    ck(cudaMemcpy(hp.data(), p, pb, cudaMemcpyDeviceToHost), "copy p");
+    require(host_all_finite(hp.data(), n, false), "make_reflector: non-finite entries");
+  }
+  double *dp = nullptr, *dx = nullptr, *dy = nullptr, *di = nullptr;
+  ck(cudaMalloc(&dp, pb), "alloc");
+  ck(cudaMalloc(&di, 4 * sizeof(double)), "alloc");
+  if (count > 0) {
+    ck(cudaMalloc(&dx, xb), "alloc");
+    ck(cudaMalloc(&dy, xb), "alloc");
+  }
+  const cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  ck(cudaMemcpy(dp, p, pb, k), "copy p");
+  if (count > 0) ck(cudaMemcpy(dx, x, xb, k), "copy x");
+  k_reflector<<<1, kReflThreads>>>(dp, n, offset, zero_tol, sign_rule, dx, dy, count, di);
+  const cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess && count > 0) ck(cudaMemcpy(y, dy, xb, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost), "copy y");
+  if (e == cudaSuccess && info) ck(cudaMemcpy(info, di, 3 * sizeof(double), cudaMemcpyDeviceToHost), "copy info");
+  cudaFree(dp);
+  cudaFree(di);
+  cudaFree(dx);
+  cudaFree(dy);
+  ck(e, "k_reflector");
+  return HD_OK;
+  HD_CATCH
+}
+
 int hd_set_profiling(hd_op* op, int32_t enabled) {
   HD_TRY
   require(op, "hd_set_profiling: null argument");

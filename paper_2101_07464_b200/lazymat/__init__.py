@@ -18,6 +18,8 @@ through the C-ABI of libhd_b200.so; there is no CPU fallback.
 
 Out of scope this round: sample_dense_haar,
 ista_curves, spectral_summary, two_sample_ks raise NotImplementedError.
+make_reflector / Reflector (module.cpp:48-66) build and apply the reflector
+on the device through hd_reflector_apply.
 """
 from __future__ import annotations
 
@@ -29,8 +31,9 @@ from .. import _native as N
 from .._native import BudgetExhausted, ResourceCapExceeded
 
 __all__ = [
-    "BudgetExhausted", "GinibreOperator", "HaarOperator", "GOEOperator", "ResourceCapExceeded",
-    "derive_seed", "ista_curves", "make_reflector", "sample_dense_haar", "spectral_summary", "two_sample_ks",
+    "BudgetExhausted", "GinibreOperator", "HaarOperator", "GOEOperator", "Reflector", "ResourceCapExceeded",
+    "SubsampledHaarOperator", "USVOperator", "derive_seed", "ista_curves", "make_reflector", "sample_dense_haar",
+    "spectral_summary", "two_sample_ks",
 ]
 
 __version__ = "0.1.0"
@@ -273,9 +276,149 @@ class GOEOperator(_Operator):
         super().__init__(n, n, sigma, seed, **kw)
 
 
+class Reflector:
+    """Generalised Householder reflector H_k(p) (reflect.hpp:47-104), built and
+    applied on the device; exposes dim / offset / is_identity / apply like the
+    reference binding (module.cpp:48-57)."""
+
+    def __init__(self, p: np.ndarray, offset: int, info):
+        self._p = p
+        self._offset = int(offset)
+        self._c, self._s, ident = info
+        self._identity = bool(ident)
+
+    @property
+    def dim(self) -> int:
+        return int(self._p.size)
+
+    @property
+    def offset(self) -> int:
+        return self._offset
+
+    @property
+    def is_identity(self) -> bool:
+        return self._identity
+
+    def apply(self, x, adjoint: bool = False):
+        # real reflectors are self-adjoint (reflect.hpp:80)
+        xa = np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(-1))
+        if xa.size != self.dim:
+            raise ValueError("Reflector::apply: dimension mismatch")
+        y = np.empty_like(xa)
+        N.check(N.lib().hd_reflector_apply(self._p.ctypes.data_as(C.c_void_p), self.dim, self._offset, 0.0, 0,
+                                           xa.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.c_void_p), 1, 0, None))
+        return y
+
+
 def make_reflector(p, offset: int = 0):
-    raise NotImplementedError("make_reflector: standalone reflector utility is served inside the operators "
-                              "this round (SURVEY.md §8a a5); see DESIGN.md")
+    """Orthogonal reflector sending p[offset:] to +||p[offset:]|| e_1 and fixing
+    the first `offset` coordinates (reflect.hpp:120-176, module.cpp:59-66)."""
+    pa = np.ascontiguousarray(np.asarray(p, dtype=np.float64).reshape(-1)).copy()
+    info = (C.c_double * 3)()
+    N.check(N.lib().hd_reflector_apply(pa.ctypes.data_as(C.c_void_p), pa.size, int(offset), 0.0, 0, None, None, 0, 0,
+                                       info))
+    return Reflector(pa, offset, (info[0], info[1], info[2]))
+
+
+def _xp_zeros(like, n):
+    if _is_torch_cuda(like):
+        import torch
+
+        return torch.zeros(n, dtype=like.dtype, device=like.device)
+    return np.zeros(n, dtype=np.asarray(like).dtype)
+
+
+class USVOperator:
+    """Q = U S V over two square lazy factors and a fixed rectangular diagonal
+    (ensembles.hpp:133-180); one probe of each device factor per probe."""
+
+    def __init__(self, u, v, singular_values):
+        if u is None or v is None:
+            raise ValueError("USVOperator: null factor")
+        if u.rows != u.cols or v.rows != v.cols:
+            raise ValueError("USVOperator: factors must be square")
+        sv = np.asarray(singular_values, dtype=np.float64).reshape(-1)
+        if sv.size != min(u.rows, v.cols):
+            raise ValueError("USVOperator: need min(rows, cols) singular values")
+        self.u, self.v, self._sv = u, v, sv
+
+    @property
+    def rows(self):
+        return self.u.rows
+
+    @property
+    def cols(self):
+        return self.v.cols
+
+    @property
+    def remaining_probes(self):
+        return min(self.u.remaining_probes, self.v.remaining_probes)
+
+    @property
+    def singular_values(self):
+        return self._sv.copy()
+
+    def probe(self, x, side: str = "right"):
+        s_ = _side(side)
+        want = self.cols if s_ == N.HD_RIGHT else self.rows
+        if (x.numel() if _is_torch_cuda(x) else np.asarray(x).size) != want:
+            raise ValueError("probe: input dimension mismatch")
+        if self.remaining_probes == 0:
+            raise BudgetExhausted("USVOperator: factor budget spent")
+        k = self._sv.size
+        if s_ == N.HD_RIGHT:
+            t = self.v.probe(x, "right")
+            s = _xp_zeros(t, self.rows)
+            s[:k] = self._sv_like(t)[:k] * t[:k]
+            return self.u.probe(s, "right")
+        t = self.u.probe(x, "left")
+        s = _xp_zeros(t, self.cols)
+        s[:k] = self._sv_like(t)[:k] * t[:k]
+        return self.v.probe(s, "left")
+
+    def _sv_like(self, t):
+        if _is_torch_cuda(t):
+            import torch
+
+            return torch.as_tensor(self._sv, dtype=t.dtype, device=t.device)
+        return self._sv.astype(t.dtype)
+
+
+class SubsampledHaarOperator:
+    """A = [I 0] Q: the first `rows` coordinates of a square lazy operator
+    (ensembles.hpp:182-215)."""
+
+    def __init__(self, q, rows: int):
+        if q is None:
+            raise ValueError("SubsampledHaarOperator: null inner operator")
+        if q.rows != q.cols:
+            raise ValueError("SubsampledHaarOperator: inner operator must be square")
+        if not (1 <= rows <= q.rows):
+            raise ValueError("SubsampledHaarOperator: need 1 <= rows <= inner dim")
+        self.q, self._rows = q, int(rows)
+
+    @property
+    def rows(self):
+        return self._rows
+
+    @property
+    def cols(self):
+        return self.q.cols
+
+    @property
+    def remaining_probes(self):
+        return self.q.remaining_probes
+
+    def probe(self, x, side: str = "right"):
+        s_ = _side(side)
+        want = self.cols if s_ == N.HD_RIGHT else self.rows
+        if (x.numel() if _is_torch_cuda(x) else np.asarray(x).size) != want:
+            raise ValueError("probe: input dimension mismatch")
+        if s_ == N.HD_RIGHT:
+            return self.q.probe(x, "right")[: self._rows]
+        padded = _xp_zeros(x, self.cols)
+        padded[: self._rows] = x
+        return self.q.probe(padded, "left")
 
 
 def sample_dense_haar(n: int, seed: int = 1):
