@@ -133,6 +133,18 @@ typedef struct hd_run_args {
  * ("run_dynamics: non-finite iterate at step N") follow dynamics.hpp:44-67. */
 int hd_run(hd_op* op, const hd_run_args* args);
 
+/* Asynchronous run: enqueue the whole T-step run (CUDA-graph replay when
+ * use_graph) on the handle's / given stream and return; hd_wait completes it
+ * (status words, error reporting as hd_run, host copies). Device final_out is
+ * written in stream order. Many handles on their own streams run
+ * concurrently (batched independent trials, BASELINE config 3). */
+int hd_run_async(hd_op* op, const hd_run_args* args);
+int hd_wait(hd_op* op);
+
+/* Fresh operator state with a new RandomSource seed (Philox key), without a
+ * host synchronisation: one captured run graph serves every trial seed. */
+int hd_reseed(hd_op* op, uint64_t seed);
+
 /* User update map on device memory: called once per step after the probe
  * with y_t and the history window newest first (device pointers of the op's
  * dtype, each dim elements); must write x_{t+1} into `next` on `stream`.

@@ -32,6 +32,7 @@ EXPORTS = (
     "hd_create", "hd_destroy", "hd_shape", "hd_remaining", "hd_counts", "hd_chain_sizes", "hd_probe",
     "hd_push_draws", "hd_reset", "hd_run", "hd_run_callback", "hd_set_profiling", "hd_get_stats",
     "hd_reset_stats", "hd_launch_count", "hd_last_error", "hd_version", "hd_reflector_apply",
+    "hd_run_async", "hd_wait", "hd_reseed",
 )
 
 
@@ -100,6 +101,9 @@ def lib():
         L.hd_reset_stats.argtypes = [vp]
         L.hd_launch_count.argtypes = [vp, C.POINTER(i64)]
         L.hd_reflector_apply.argtypes = [vp, i64, i64, C.c_double, i32, vp, vp, i64, i32, vp]
+        L.hd_run_async.argtypes = [vp, C.POINTER(hd_run_args)]
+        L.hd_wait.argtypes = [vp]
+        L.hd_reseed.argtypes = [vp, C.c_uint64]
         for name in EXPORTS:
             if name not in ("hd_last_error", "hd_version"):
                 getattr(L, name).restype = C.c_int

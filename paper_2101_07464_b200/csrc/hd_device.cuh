@@ -74,7 +74,7 @@ struct Src {
   int kind = kSrcNone;
   const T* x = nullptr;
   const double* xscale = nullptr;  // device scalar or null
-  uint64_t seed = 0;
+  const unsigned long long* seedp = nullptr;  // device word: one graph serves every reseed
   uint32_t stream = 0;
   uint32_t probe = 0;
   const double* inj = nullptr;  // this probe's injected draws (length n)
@@ -112,7 +112,7 @@ __device__ __forceinline__ double2 src_pair(const Src<T>& s, int64_t i, int64_t 
     }
   } else if (s.kind == kSrcPhilox) {
     if (i < n) {
-      v = philox_normal_pair(s.seed, s.stream, s.probe, (uint64_t)(i >> 1));
+      v = philox_normal_pair(*s.seedp, s.stream, s.probe, (uint64_t)(i >> 1));
       if constexpr (sizeof(T) == 4) {  // fp32 path consumes fp32-rounded draws
         v.x = (double)(float)v.x;
         v.y = (double)(float)v.y;

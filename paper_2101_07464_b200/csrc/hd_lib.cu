@@ -142,6 +142,14 @@ struct hd_op {
   std::map<long, int> apply_bps;
   int last_other_grid = 0, last_other_slot_ss = 0;  // normalize partials of k_apply(OTHER)
   bool pdl = true;  // programmatic dependent launch (HD_NO_PDL=1 disables)
+  unsigned long long* seed_dev = nullptr;  // Philox key (device word, hd_reseed)
+  // hd_run_async bookkeeping, completed by hd_wait
+  bool run_pending = false;
+  hd_run_args pend_args{};
+  std::vector<Counters> pend_snaps;
+  int64_t pend_fdim = 0, pend_dim1 = 0;
+  void* pend_traj_dev = nullptr;
+  cudaStream_t pend_stream = nullptr;
   unsigned long long* trace = nullptr;  // HD_TRACE=1: phase stamps of k_small_dots
   std::vector<double> trace_acc;        // accumulated phase durations (ns)
   int64_t trace_n = 0;
@@ -198,6 +206,8 @@ void alloc_store(hd_op* op, Panel& p, int64_t rows_pad, int64_t K) {
   p.P = dmalloc<unsigned char>((size_t)rows_pad * K * op->esz);
   ck(cudaMemsetAsync(p.P, 0, (size_t)rows_pad * K * op->esz, op->stream), "memset store");
 }
+
+__global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
 
 __global__ void k_fill(double* p, int64_t n, const double* v) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -539,7 +549,7 @@ Src<T> draw_src(hd_op* op, int64_t len) {
     op->c.inj_pos += len;
   } else {
     s.kind = kSrcPhilox;
-    s.seed = op->cfg.seed;
+    s.seedp = op->seed_dev;
     s.stream = (uint32_t)op->cfg.stream;
     s.probe = op->c.probe_index;
   }
@@ -716,7 +726,7 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
       oa.spec.inj = op->inj + op->c.inj_pos;
     } else {
       oa.spec.kind = kSrcPhilox;
-      oa.spec.seed = op->cfg.seed;
+      oa.spec.seedp = op->seed_dev;
       oa.spec.stream = (uint32_t)op->cfg.stream;
       oa.spec.probe = op->c.probe_index;
     }
@@ -1224,8 +1234,9 @@ const void* final_location(hd_op* op, const hd_run_args& a) {
 }
 
 template <typename T>
-void do_run(hd_op* op, const hd_run_args& a) {
+void do_run_enqueue(hd_op* op, const hd_run_args& a) {
   cudaStream_t s = a.stream ? static_cast<cudaStream_t>(a.stream) : op->stream;
+  require(!op->run_pending, "hd_run: the previous hd_run_async was not waited for");
   require(a.iterations >= 0, "run_dynamics: negative iteration count");
   require(a.update >= 0 && a.update <= 2, "run_dynamics: unknown update map");
   require(a.side_rule >= 0 && a.side_rule <= 2, "run_dynamics: unknown side schedule");
@@ -1308,37 +1319,68 @@ void do_run(hd_op* op, const hd_run_args& a) {
     if (traj_dev && !a.on_device) cudaFree(traj_dev);
     throw;
   }
-  ck(cudaStreamSynchronize(s), "run sync");
-  int st[kStWords];
-  read_status(op, st);
-  if (st[kStBadInput]) {
-    restore(op, snap0);
-    if (traj_dev && !a.on_device) cudaFree(traj_dev);
-    throw HdError(HD_ERR_INVALID_ARGUMENT, "probe: non-finite input");
-  }
-  if (st[kStBadStep] != INT_MAX) {
-    const int64_t bad = st[kStBadStep];
-    restore(op, snaps[(size_t)std::min<int64_t>(bad, (int64_t)snaps.size() - 1)]);
-    if (traj_dev && !a.on_device) cudaFree(traj_dev);
-    throw HdError(HD_ERR_RUNTIME, "run_dynamics: non-finite iterate at step " + std::to_string(bad));
-  }
   const void* fin = final_location<T>(op, a);
-  // dimension of x_{T+1}
-  int64_t fdim = dim1;
+  int64_t fdim = dim1;  // dimension of x_{T+1}
   if (a.iterations > 0) {
     const int sideT = side_for(a.side_rule, a.iterations);
     const int effT = (op->ens == HD_GOE) ? HD_RIGHT : sideT;
     fdim = (effT == HD_RIGHT) ? op->m : op->n;
   }
-  if (a.final_out)
-    ck(cudaMemcpyAsync(a.final_out, fin, (size_t)fdim * op->esz, a.on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                       s),
-       "copy final");
-  if (a.traj && !a.on_device) {
-    ck(cudaMemcpyAsync(a.traj, traj_dev, xbytes * (size_t)(a.iterations + 1), cudaMemcpyDeviceToHost, s), "copy traj");
+  if (a.final_out && a.on_device)
+    ck(cudaMemcpyAsync(a.final_out, fin, (size_t)fdim * op->esz, cudaMemcpyDeviceToDevice, s), "copy final");
+  op->run_pending = true;
+  op->pend_args = a;
+  op->pend_snaps = std::move(snaps);
+  op->pend_fdim = fdim;
+  op->pend_dim1 = dim1;
+  op->pend_traj_dev = traj_dev;
+  op->pend_stream = s;
+}
+
+// Completion of a run: status words, error restore (dynamics.hpp:64-67),
+// host copies of x_{T+1} / the trajectory.
+template <typename T>
+void do_run_complete(hd_op* op) {
+  require(op->run_pending, "hd_wait: no run in flight");
+  op->run_pending = false;
+  const hd_run_args a = op->pend_args;
+  cudaStream_t s = op->pend_stream;
+  void* traj_dev = op->pend_traj_dev;
+  auto free_traj = [&] {
+    if (traj_dev && !a.on_device) cudaFree(traj_dev);
+  };
+  const cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    free_traj();
+    ck(e, "run sync");
   }
-  ck(cudaStreamSynchronize(s), "run sync");
-  if (traj_dev && !a.on_device) cudaFree(traj_dev);
+  int st[kStWords];
+  read_status(op, st);
+  if (st[kStBadInput]) {
+    restore(op, op->pend_snaps.front());
+    free_traj();
+    throw HdError(HD_ERR_INVALID_ARGUMENT, "probe: non-finite input");
+  }
+  if (st[kStBadStep] != INT_MAX) {
+    const int64_t bad = st[kStBadStep];
+    restore(op, op->pend_snaps[(size_t)std::min<int64_t>(bad, (int64_t)op->pend_snaps.size() - 1)]);
+    free_traj();
+    throw HdError(HD_ERR_RUNTIME, "run_dynamics: non-finite iterate at step " + std::to_string(bad));
+  }
+  if (a.final_out && !a.on_device)
+    ck(cudaMemcpy(a.final_out, final_location<T>(op, a), (size_t)op->pend_fdim * op->esz, cudaMemcpyDeviceToHost),
+       "copy final");
+  if (a.traj && !a.on_device)
+    ck(cudaMemcpy(a.traj, traj_dev, (size_t)op->pend_dim1 * op->esz * (size_t)(a.iterations + 1),
+                  cudaMemcpyDeviceToHost),
+       "copy traj");
+  free_traj();
+}
+
+template <typename T>
+void do_run(hd_op* op, const hd_run_args& a) {
+  do_run_enqueue<T>(op, a);
+  do_run_complete<T>(op);
 }
 
 // ------------------------------------------------- user callback dynamics
@@ -1488,6 +1530,9 @@ int hd_create(const hd_config* cfg, hd_op** out) {
   op->scal = dmalloc<double>(kScWords);
   ck(cudaMemsetAsync(op->scal, 0, sizeof(double) * kScWords, op->stream), "memset");
   op->status = dmalloc<int>(kStWords);
+  op->seed_dev = dmalloc<unsigned long long>(1);
+  k_set_u64<<<1, 1, 0, op->stream>>>(op->seed_dev, (unsigned long long)c.seed);
+  ck(cudaGetLastError(), "seed");
   const int64_t rp = std::max(op->rows_pad_m, op->rows_pad_n);
   op->io_len = rp;
   op->xbuf = dmalloc<unsigned char>((size_t)rp * op->esz);
@@ -1527,6 +1572,7 @@ int hd_destroy(hd_op* op) {
                     op->coefS, op->head, op->zbuf, op->csp, op->inj})
     cudaFree(p);
   cudaFree(op->status);
+  cudaFree(op->seed_dev);
   cudaFree(op->xbuf);
   for (auto b : op->ybuf) cudaFree(b);
   cudaFree(op->gtmp);
@@ -1642,6 +1688,49 @@ int hd_run(hd_op* op, const hd_run_args* args) {
     do_run<float>(op, *args);
   else
     do_run<double>(op, *args);
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_run_async(hd_op* op, const hd_run_args* args) {
+  HD_TRY
+  require(op && args, "hd_run_async: null argument");
+  cudaSetDevice(op->cfg.device);
+  if (op->f32)
+    do_run_enqueue<float>(op, *args);
+  else
+    do_run_enqueue<double>(op, *args);
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_wait(hd_op* op) {
+  HD_TRY
+  require(op, "hd_wait: null argument");
+  cudaSetDevice(op->cfg.device);
+  if (op->f32)
+    do_run_complete<float>(op);
+  else
+    do_run_complete<double>(op);
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_reseed(hd_op* op, uint64_t seed) {
+  HD_TRY
+  require(op, "hd_reseed: null argument");
+  require(!op->run_pending, "hd_reseed: a run is in flight (hd_wait first)");
+  require(op->cfg.draw_mode == HD_DRAWS_PHILOX, "hd_reseed: only for HD_DRAWS_PHILOX operators");
+  cudaSetDevice(op->cfg.device);
+  // fresh state without a host sync: counters on the host, device words and
+  // D tables by kernels on the handle's stream (graph replays reset too)
+  op->cfg.seed = seed;
+  op->c = Counters{};
+  op->R.pan.count = op->L.pan.count = op->U.count = op->V.count = 0;
+  op->R.pend = op->L.pend = -1;
+  k_set_u64<<<1, 1, 0, op->stream>>>(op->seed_dev, (unsigned long long)seed);
+  ck(cudaGetLastError(), "seed");
+  reset_device_state(op, op->stream);
   return HD_OK;
   HD_CATCH
 }

@@ -32,7 +32,8 @@ from .._native import BudgetExhausted, ResourceCapExceeded
 
 __all__ = [
     "BudgetExhausted", "GinibreOperator", "HaarOperator", "GOEOperator", "Reflector", "ResourceCapExceeded",
-    "SubsampledHaarOperator", "USVOperator", "derive_seed", "ista_curves", "make_reflector", "sample_dense_haar",
+    "SubsampledHaarOperator", "USVOperator", "derive_seed", "ista_curves", "make_reflector", "run_trials",
+    "sample_dense_haar",
     "spectral_summary", "two_sample_ks",
 ]
 
@@ -204,6 +205,35 @@ class _Operator:
         N.check(N.lib().hd_run(self._h, C.byref(a)))
         return traj if keep_trajectory else fin
 
+    # ---- asynchronous runs (many handles on their own streams: batched trials)
+    def reseed(self, seed: int) -> None:
+        """Fresh state with a new seed (Philox key) without host sync."""
+        N.check(N.lib().hd_reseed(self._h, int(seed) & _MASK))
+
+    def run_async(self, x1, iterations: int, out, update: str = "normalize", sides: str = "alternate", x0=None,
+                  use_graph: bool = True) -> None:
+        """Enqueue a whole run on the operator's own stream; `x1` / `x0` / `out`
+        are CUDA tensors of the operator's dtype that must stay alive until
+        wait(). Producers of x1 must be complete (e.g. synchronise first)."""
+        a = N.hd_run_args()
+        a.update = N.UPDATES[update]
+        a.side_rule = N.SIDE_RULES[sides]
+        a.iterations = int(iterations)
+        a.use_graph = int(bool(use_graph))
+        a.x1 = x1.data_ptr()
+        if x0 is not None:
+            a.x0 = x0.data_ptr()
+        a.on_device = 1
+        a.final_out = out.data_ptr()
+        self._inflight = (x1, x0, out)
+        N.check(N.lib().hd_run_async(self._h, C.byref(a)))
+
+    def wait(self) -> None:
+        try:
+            N.check(N.lib().hd_wait(self._h))
+        finally:
+            self._inflight = None
+
     def _final_dim(self, iterations: int, sides: str, dim1: int) -> int:
         if iterations == 0:
             return dim1
@@ -308,6 +338,57 @@ class Reflector:
         N.check(N.lib().hd_reflector_apply(self._p.ctypes.data_as(C.c_void_p), self.dim, self._offset, 0.0, 0,
                                            xa.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.c_void_p), 1, 0, None))
         return y
+
+
+def run_trials(ensemble: str, trials: int, n: int, T: int, *, m: int = None, sigma: float = None, seed: int = 1,
+               dtype: str = "f64", update: str = "normalize", sides: str = "alternate", concurrency: int = 16,
+               x1=None, first_trial: int = 0, device: int = 0, return_ops: bool = False):
+    """Independent HD trials (BASELINE config 3: trial b uses seed + b). Keeps
+    `concurrency` device operators in flight, each on its own CUDA stream
+    replaying one captured run graph (reseeded per trial), so the latency of
+    one trial's probe sequence overlaps the HBM streaming of the others.
+    Returns x_{T+1} of every trial as a (trials, dim) CUDA tensor.
+    x1: optional (trials, dim) CUDA tensor; default N(0, I) per trial."""
+    import torch
+
+    m = n if m is None else m
+    if sigma is None:
+        sigma = 1.0 / float(n) ** 0.5
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    dev = torch.device("cuda", device)
+    make = {
+        "ginibre": lambda: GinibreOperator(m, n, sigma, seed, dtype=dtype, capacity=T, device=device),
+        "haar": lambda: HaarOperator(n, seed, dtype=dtype, capacity=T, device=device),
+        "goe": lambda: GOEOperator(n, seed, sigma=sigma, dtype=dtype, capacity=T, device=device),
+    }[ensemble]
+    ops = [make() for _ in range(max(1, min(concurrency, trials)))]
+    dim1 = n if (ensemble != "ginibre" or sides != "left") else m
+    fdim = ops[0]._final_dim(T, sides, dim1)
+    if x1 is None:
+        x1 = torch.empty((trials, dim1), dtype=tdt, device=dev)
+        for b in range(trials):
+            g = torch.Generator(device=dev).manual_seed(seed + first_trial + b)
+            x1[b] = torch.randn(dim1, dtype=tdt, device=dev, generator=g)
+    out = torch.empty((trials, fdim), dtype=tdt, device=dev)
+    torch.cuda.synchronize(dev)
+    nxt = 0
+    busy = []
+    for op in ops:
+        if nxt >= trials:
+            break
+        op.reseed(seed + first_trial + nxt)
+        op.run_async(x1[nxt], T, out[nxt], update=update, sides=sides)
+        busy.append(op)
+        nxt += 1
+    while busy:
+        op = busy.pop(0)
+        op.wait()
+        if nxt < trials:
+            op.reseed(seed + first_trial + nxt)
+            op.run_async(x1[nxt], T, out[nxt], update=update, sides=sides)
+            busy.append(op)
+            nxt += 1
+    return (out, ops) if return_ops else out
 
 
 def make_reflector(p, offset: int = 0):
