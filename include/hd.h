@@ -88,8 +88,10 @@ int hd_chain_sizes(const hd_op* op, int64_t* right_chain, int64_t* left_chain);
  * Q^T x (left). x/y are host pointers (on_device = 0) or device pointers of
  * the operator's dtype (on_device = 1). Validation order follows
  * check_probe_input then the budget check (operators.hpp:44-48,
- * ginibre.hpp:59-62). Synchronous: returns after y is written. `stream` is a
- * cudaStream_t or NULL for the handle's own stream. */
+ * ginibre.hpp:59-62). Synchronous: returns after y is written. `stream` is
+ * the caller's cudaStream_t (NULL = the legacy default stream): the probe
+ * runs on the handle's own stream, ordered after all work already enqueued
+ * on `stream`, so a device x produced there is complete before it is read. */
 int hd_probe(hd_op* op, const void* x, int64_t x_len, void* y, int64_t y_len, int32_t side, int32_t on_device,
              void* stream);
 
@@ -126,7 +128,8 @@ typedef struct hd_run_args {
   int32_t use_graph;   /* capture the T-step launch sequence in a CUDA graph */
   void* traj;          /* optional (T+1) x dim iterates x_1..x_{T+1}         */
   void* final_out;     /* optional x_{T+1}                                   */
-  void* stream;        /* cudaStream_t or NULL                               */
+  void* stream;        /* caller's cudaStream_t (NULL = legacy default); the
+                          run is ordered after work already enqueued on it  */
 } hd_run_args;
 
 /* run_dynamics(op, spec): validation messages and the non-finite abort
@@ -134,10 +137,10 @@ typedef struct hd_run_args {
 int hd_run(hd_op* op, const hd_run_args* args);
 
 /* Asynchronous run: enqueue the whole T-step run (CUDA-graph replay when
- * use_graph) on the handle's / given stream and return; hd_wait completes it
- * (status words, error reporting as hd_run, host copies). Device final_out is
- * written in stream order. Many handles on their own streams run
- * concurrently (batched independent trials, BASELINE config 3). */
+ * use_graph) on the handle's own stream, ordered after `args->stream`, and
+ * return; hd_wait completes it (status words, error reporting as hd_run, host
+ * copies). Device outputs are valid once hd_wait returns. Many handles run
+ * concurrently on their own streams (batched independent trials, config 3). */
 int hd_run_async(hd_op* op, const hd_run_args* args);
 int hd_wait(hd_op* op);
 

@@ -670,4 +670,77 @@ int or_bench_workload(int ensemble, std::int64_t m, std::int64_t n, double sigma
   OR_CATCH
 }
 
+// ---------------------------------------------------------------------------
+// BASELINE configs 4 and 5 dynamics (not in the reference, SPEC.md:439 lists
+// AMP as a non-goal; defined here and in paper_2101_07464_b200/lazymat):
+//
+// AMP for sparse regression on A = Ginibre m x n (entries N(0, sigma^2)),
+// delta = m / n, y = A beta + w (one right probe, experiments.cpp:80-82):
+//   x^0 = 0, z^0 = y; for t = 0 .. T-1:
+//     r   = x^t + A^T z^t                       (left probe)
+//     th  = alpha * ||z^t|| / sqrt(m)           (tau_t = ||z^t|| / sqrt(m))
+//     x^{t+1} = soft(r, th)                     (experiments.cpp:31-39)
+//     b   = (#{i : x^{t+1}_i != 0} / n) / delta (Onsager coefficient)
+//     z^{t+1} = y - A x^{t+1} + b z^t           (right probe)
+//   mse_t = ||x^{t+1} - beta||^2 / n.
+int or_amp(void* p, const double* beta, const double* w, std::int64_t T, double alpha, double* x_out,
+           double* mse_out) {
+  OR_TRY
+  auto* b = static_cast<OpBox*>(p);
+  ProbeOperator& A = *b->op;
+  const Index m = A.rows(), n = A.cols();
+  const double delta = double(m) / double(n);
+  Vec bv(beta, beta + n);
+  Vec y = A.probe(bv, Side::right);
+  for (Index i = 0; i < m; ++i) y[static_cast<size_t>(i)] += w[i];
+  Vec x(static_cast<size_t>(n), 0.0), z = y;
+  for (Index t = 0; t < T; ++t) {
+    const Vec atz = A.probe(z, Side::left);
+    const double th = alpha * norm(z) / std::sqrt(double(m));
+    Index nnz = 0;
+    for (Index i = 0; i < n; ++i) {
+      const double r = x[static_cast<size_t>(i)] + atz[static_cast<size_t>(i)];
+      const double mag = std::abs(r) - th;
+      x[static_cast<size_t>(i)] = (mag > 0.0) ? (r > 0.0 ? mag : -mag) : 0.0;
+      nnz += (mag > 0.0) ? 1 : 0;
+    }
+    const double onsager = (double(nnz) / double(n)) / delta;
+    const Vec ax = A.probe(x, Side::right);
+    for (Index i = 0; i < m; ++i)
+      z[static_cast<size_t>(i)] = y[static_cast<size_t>(i)] - ax[static_cast<size_t>(i)] + onsager * z[static_cast<size_t>(i)];
+    double e = 0.0;
+    for (Index i = 0; i < n; ++i) {
+      const double d = x[static_cast<size_t>(i)] - beta[i];
+      e += d * d;
+    }
+    if (mse_out) mse_out[t] = e / double(n);
+  }
+  std::memcpy(x_out, x.data(), x.size() * sizeof(double));
+  return 0;
+  OR_CATCH
+}
+
+// Spiked-GOE power method (BASELINE config 5): G = GOE probe operator,
+// x_{t+1} = (G x_t + theta <u, x_t> u) / ||.||, u a unit vector.
+int or_spiked_power(void* p, const double* u, const double* x1, std::int64_t T, double theta, double* x_out,
+                    double* overlap_out) {
+  OR_TRY
+  auto* b = static_cast<OpBox*>(p);
+  ProbeOperator& G = *b->op;
+  const Index n = G.cols();
+  Vec x(x1, x1 + n);
+  for (Index t = 0; t < T; ++t) {
+    Vec gx = G.probe(x, Side::right);
+    const double ux = dot(u, x.data(), n);
+    for (Index i = 0; i < n; ++i) gx[static_cast<size_t>(i)] += theta * ux * u[i];
+    const double nr = norm(gx);
+    const double inv = nr > 0 ? 1.0 / nr : 1.0;
+    for (Index i = 0; i < n; ++i) x[static_cast<size_t>(i)] = inv * gx[static_cast<size_t>(i)];
+    if (overlap_out) overlap_out[t] = dot(u, x.data(), n);
+  }
+  std::memcpy(x_out, x.data(), x.size() * sizeof(double));
+  return 0;
+  OR_CATCH
+}
+
 }  // extern "C"

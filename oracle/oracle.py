@@ -73,6 +73,8 @@ def lib():
         L.or_op_probe.argtypes = [C.c_void_p, _dp, C.c_int64, C.c_int, _dp, C.c_int64]
         L.or_run_builtin.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int64, _dp, C.c_void_p,
                                      C.c_int64, C.c_int, _dp]
+        L.or_amp.argtypes = [C.c_void_p, _dp, _dp, C.c_int64, C.c_double, _dp, _dp]
+        L.or_spiked_power.argtypes = [C.c_void_p, _dp, _dp, C.c_int64, C.c_double, _dp, _dp]
         L.or_bench_workload.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_double, C.c_int, C.c_int,
                                         C.c_int64, C.c_uint64, C.c_int, C.c_int,
                                         C.POINTER(C.c_double), C.POINTER(C.c_double)]
@@ -196,6 +198,24 @@ class Operator:
         y = np.empty(out_len, dtype=np.float64)
         _check(lib().or_op_probe(self._h, x, x.size, SIDES[side], y, out_len))
         return y
+
+    def amp(self, beta, w, T: int, alpha: float = 1.5):
+        """AMP for sparse regression (BASELINE config 4, defined in or_amp)."""
+        beta = np.ascontiguousarray(beta, dtype=np.float64)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        x = np.empty(self.cols, dtype=np.float64)
+        mse = np.empty(max(T, 1), dtype=np.float64)
+        _check(lib().or_amp(self._h, beta, w, T, alpha, x, mse))
+        return x, mse[:T]
+
+    def spiked_power(self, u, x1, T: int, theta: float = 2.0):
+        """Spiked-GOE power method (BASELINE config 5, or_spiked_power)."""
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        x1 = np.ascontiguousarray(x1, dtype=np.float64)
+        x = np.empty(self.cols, dtype=np.float64)
+        ov = np.empty(max(T, 1), dtype=np.float64)
+        _check(lib().or_spiked_power(self._h, u, x1, T, theta, x, ov))
+        return x, ov[:T]
 
     def run(self, kind: str, side_rule: str, T: int, x1, x0=None, keep: bool = True) -> np.ndarray:
         x1 = np.ascontiguousarray(x1, dtype=np.float64)

@@ -46,11 +46,22 @@ void ck(cudaError_t e, const char* what) {
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// HD_POISON=1 (debug): fill every fresh allocation with 0xFF bytes (NaN for
+// doubles, -1 for ints) so a read-before-write shows up in the parity tests.
+bool poison_allocs() {
+  const char* e = std::getenv("HD_POISON");
+  return e && e[0] == '1';
+}
+
 template <typename P>
 P* dmalloc(size_t count) {
   void* p = nullptr;
   if (count == 0) count = 1;
   ck(cudaMalloc(&p, count * sizeof(P)), "cudaMalloc");
+  if (poison_allocs()) {
+    ck(cudaMemset(p, 0xFF, count * sizeof(P)), "poison");
+    ck(cudaDeviceSynchronize(), "poison sync");
+  }
   return static_cast<P*>(p);
 }
 
@@ -136,7 +147,8 @@ struct hd_op {
   int64_t io_len = 0;
   double* inj = nullptr;
   int64_t inj_cap = 0, inj_size = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;  // every kernel of the handle runs here
+  cudaEvent_t ev_fork = nullptr;  // orders `stream` after the caller's stream
   int nsm = 148;
   std::map<long, int> dots_bps;  // smem bytes -> co-resident clusters
   std::map<long, int> apply_bps;
@@ -329,6 +341,17 @@ void ensure_capacity(hd_op* op, int64_t nr, int64_t nl) {
   op->partsF = op->fbF.partials;
   op->partsO = op->fbO.partials;
   ensure_red(op, slots);
+}
+
+// The handle's stream is non-blocking, so nothing orders it after the
+// caller's stream implicitly (not even the legacy NULL stream). Every entry
+// point that reads caller data first makes op->stream wait for the work
+// already enqueued on the caller's stream. No join is needed: every entry
+// point returns after a host sync of op->stream (hd_wait for async runs).
+void fork_from(hd_op* op, cudaStream_t caller) {
+  if (caller == op->stream) return;
+  ck(cudaEventRecord(op->ev_fork, caller), "fork record");
+  ck(cudaStreamWaitEvent(op->stream, op->ev_fork, 0), "fork wait");
 }
 
 // ========================================================= instrumentation
@@ -582,7 +605,6 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   g.mask_begin = off;
   const bool key_ok = (g.kind == kSrcInjected) ? (op->c.spec_inj == inj_before) : (op->c.spec_probe == g.probe);
   const bool use_spec = op->c.spec_chain == ochain && key_ok && op->c.spec_count == (int)O.pan.count && O.pend < 0;
-  const bool reduce_spec = op->c.spec_chain >= 0 && use_spec;
   const int spec_nblk = op->c.spec_nblk, spec_slot0 = op->c.spec_slot0, spec_count = op->c.spec_count;
   op->c.spec_chain = -1;
 
@@ -1235,7 +1257,7 @@ const void* final_location(hd_op* op, const hd_run_args& a) {
 
 template <typename T>
 void do_run_enqueue(hd_op* op, const hd_run_args& a) {
-  cudaStream_t s = a.stream ? static_cast<cudaStream_t>(a.stream) : op->stream;
+  cudaStream_t s = op->stream;
   require(!op->run_pending, "hd_run: the previous hd_run_async was not waited for");
   require(a.iterations >= 0, "run_dynamics: negative iteration count");
   require(a.update >= 0 && a.update <= 2, "run_dynamics: unknown update map");
@@ -1258,6 +1280,7 @@ void do_run_enqueue(hd_op* op, const hd_run_args& a) {
     }
     ensure_capacity(op, nr, nl);
   }
+  fork_from(op, static_cast<cudaStream_t>(a.stream));
   const Counters snap0 = take_snapshot(op);
   const bool fresh = (op->c.r == 0 && op->c.l == 0 && op->c.t == 0 && op->R.pan.count == 0 && op->L.pan.count == 0);
   const size_t xbytes = (size_t)dim1 * op->esz;
@@ -1274,7 +1297,7 @@ void do_run_enqueue(hd_op* op, const hd_run_args& a) {
     if (a.on_device) {
       traj_dev = a.traj;
     } else {
-      ck(cudaMalloc(&traj_dev, xbytes * (size_t)(a.iterations + 1)), "traj alloc");
+      traj_dev = dmalloc<unsigned char>(xbytes * (size_t)(a.iterations + 1));
     }
     ck(cudaMemcpyAsync(traj_dev, a.x1, xbytes, k, s), "traj x1");
   }
@@ -1398,11 +1421,11 @@ void do_run_callback(hd_op* op, int64_t T_, int32_t depth, const void* const* in
   const int64_t dim = std::max(op->m, op->n);
   const size_t bytes = (size_t)dim * op->esz;
   std::vector<void*> hist(depth + 1);
-  for (auto& h : hist) ck(cudaMalloc(&h, std::max<size_t>(bytes, 16)), "hist alloc");
+  for (auto& h : hist) h = dmalloc<unsigned char>(std::max<size_t>(bytes, 16));
   void* ybuf = nullptr;
   void* nbuf = nullptr;
-  ck(cudaMalloc(&ybuf, std::max<size_t>(bytes, 16)), "alloc");
-  ck(cudaMalloc(&nbuf, std::max<size_t>(bytes, 16)), "alloc");
+  ybuf = dmalloc<unsigned char>(std::max<size_t>(bytes, 16));
+  nbuf = dmalloc<unsigned char>(std::max<size_t>(bytes, 16));
   auto cleanup = [&] {
     for (auto h : hist) cudaFree(h);
     cudaFree(ybuf);
@@ -1510,6 +1533,7 @@ int hd_create(const hd_config* cfg, hd_op** out) {
     }
   }
   ck(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking), "stream");
+  ck(cudaEventCreateWithFlags(&op->ev_fork, cudaEventDisableTiming), "event");
   ck(cudaDeviceGetAttribute(&op->nsm, cudaDevAttrMultiProcessorCount, c.device), "attr");
   const int64_t per_outer = (c.ensemble == HD_GOE) ? 2 : 1;
   int64_t K;
@@ -1581,6 +1605,7 @@ int hd_destroy(hd_op* op) {
     cudaEventDestroy(e.b);
   }
   for (auto e : op->evpool) cudaEventDestroy(e);
+  if (op->ev_fork) cudaEventDestroy(op->ev_fork);
   cudaStreamDestroy(op->stream);
   delete op;
   return HD_OK;
@@ -1632,11 +1657,11 @@ int hd_probe(hd_op* op, const void* x, int64_t x_len, void* y, int64_t y_len, in
   HD_TRY
   require(op && x && y, "hd_probe: null argument");
   cudaSetDevice(op->cfg.device);
-  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : op->stream;
+  fork_from(op, static_cast<cudaStream_t>(stream));
   if (op->f32)
-    do_probe<float>(op, x, x_len, y, y_len, side, on_device, s);
+    do_probe<float>(op, x, x_len, y, y_len, side, on_device, op->stream);
   else
-    do_probe<double>(op, x, x_len, y, y_len, side, on_device, s);
+    do_probe<double>(op, x, x_len, y, y_len, side, on_device, op->stream);
   return HD_OK;
   HD_CATCH
 }

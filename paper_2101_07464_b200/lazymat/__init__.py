@@ -32,7 +32,7 @@ from .._native import BudgetExhausted, ResourceCapExceeded
 
 __all__ = [
     "BudgetExhausted", "GinibreOperator", "HaarOperator", "GOEOperator", "Reflector", "ResourceCapExceeded",
-    "SubsampledHaarOperator", "USVOperator", "derive_seed", "ista_curves", "make_reflector", "run_trials",
+    "SubsampledHaarOperator", "USVOperator", "derive_seed", "ista_curves", "make_reflector", "run_trials", "amp_sparse_regression", "spiked_power",
     "sample_dense_haar",
     "spectral_summary", "two_sample_ks",
 ]
@@ -212,9 +212,11 @@ class _Operator:
 
     def run_async(self, x1, iterations: int, out, update: str = "normalize", sides: str = "alternate", x0=None,
                   use_graph: bool = True) -> None:
-        """Enqueue a whole run on the operator's own stream; `x1` / `x0` / `out`
-        are CUDA tensors of the operator's dtype that must stay alive until
-        wait(). Producers of x1 must be complete (e.g. synchronise first)."""
+        """Enqueue a whole run on the operator's own stream, ordered after the
+        work already queued on torch's current stream; `x1` / `x0` / `out` are
+        CUDA tensors of the operator's dtype that must stay alive until wait()."""
+        import torch
+
         a = N.hd_run_args()
         a.update = N.UPDATES[update]
         a.side_rule = N.SIDE_RULES[sides]
@@ -225,6 +227,7 @@ class _Operator:
             a.x0 = x0.data_ptr()
         a.on_device = 1
         a.final_out = out.data_ptr()
+        a.stream = torch.cuda.current_stream(x1.device).cuda_stream
         self._inflight = (x1, x0, out)
         N.check(N.lib().hd_run_async(self._h, C.byref(a)))
 
@@ -389,6 +392,52 @@ def run_trials(ensemble: str, trials: int, n: int, T: int, *, m: int = None, sig
             busy.append(op)
             nxt += 1
     return (out, ops) if return_ops else out
+
+
+def amp_sparse_regression(op, beta, w, T: int, alpha: float = 1.5):
+    """AMP for sparse regression on a device Ginibre design A (BASELINE config 4;
+    not in the reference — the same recurrence is or_amp in the test oracle):
+    y = A beta + w (one right probe, experiments.cpp:80-82), x^0 = 0, z^0 = y,
+      x^{t+1} = soft(x^t + A^T z^t, alpha ||z^t|| / sqrt(m))   (soft: experiments.cpp:31-39)
+      z^{t+1} = y - A x^{t+1} + (nnz(x^{t+1}) / n / delta) z^t,  delta = m / n.
+    Probes alternate Q^T, Q on the device; the update runs on device tensors.
+    Returns (x^T, mse curve ||x^t - beta||^2 / n as a device tensor)."""
+    import torch
+
+    m, n = op.rows, op.cols
+    delta = m / n
+    beta = torch.as_tensor(beta, dtype=torch.float64, device="cuda")
+    w = torch.as_tensor(w, dtype=torch.float64, device="cuda")
+    y = op.probe(beta, "right") + w
+    x = torch.zeros(n, dtype=torch.float64, device="cuda")
+    z = y.clone()
+    mse = torch.empty(T, dtype=torch.float64, device="cuda")
+    for t in range(T):
+        r = x + op.probe(z, "left")
+        th = alpha * torch.linalg.vector_norm(z) / (m ** 0.5)
+        x = torch.sign(r) * torch.clamp(r.abs() - th, min=0.0)
+        ons = torch.count_nonzero(x).to(torch.float64) / n / delta
+        z = y - op.probe(x, "right") + ons * z
+        mse[t] = torch.sum((x - beta) ** 2) / n
+    return x, mse
+
+
+def spiked_power(op, u, x1, T: int, theta: float = 2.0):
+    """Power method on Q + theta u u^T with Q a device GOE operator (BASELINE
+    config 5): x_{t+1} = (Q x_t + theta <u, x_t> u) / ||.||. Returns (x_T,
+    overlaps <u, x_t> as a device tensor)."""
+    import torch
+
+    u = torch.as_tensor(u, dtype=torch.float64, device="cuda")
+    x = torch.as_tensor(x1, dtype=torch.float64, device="cuda").clone()
+    ov = torch.empty(T, dtype=torch.float64, device="cuda")
+    for t in range(T):
+        gx = op.probe(x, "right")
+        gx = gx + theta * torch.dot(u, x) * u
+        nr = torch.linalg.vector_norm(gx)
+        x = gx * torch.where(nr > 0, 1.0 / nr, torch.ones_like(nr))
+        ov[t] = torch.dot(u, x)
+    return x, ov
 
 
 def make_reflector(p, offset: int = 0):

@@ -378,3 +378,39 @@ def test_large_haar_isometry(lm):
     # inner products between same-side probes are preserved
     (x1, y1), (x2, y2) = xs[1], xs[2]
     assert abs(float(y1 @ y2) - float(x1 @ x2)) <= 1e-10 * float(x1.norm() * x2.norm())
+
+
+# ------------------------------------- BASELINE configs 4 and 5 dynamics
+def test_amp_sparse_regression_parity(orc, lm):
+    # config 4 shape at reduced n: m = 2n, entries N(0, 1/m), beta ~ Bernoulli(0.1) N(0,1), w ~ N(0, 0.01)
+    n, T, seed = 1500, 12, 21
+    m = 2 * n
+    rng = np.random.default_rng(0)
+    beta = (rng.random(n) < 0.1) * rng.standard_normal(n)
+    w = 0.1 * rng.standard_normal(m)
+    ref = orc.Operator("ginibre", m=m, n=n, sigma=m ** -0.5, seed=seed)
+    xr, mser = ref.amp(beta, w, T)
+    op = lm.GinibreOperator(m, n, m ** -0.5, seed, draws="injected", capacity=2 * T + 1)
+    op.push_draws(orc.draws_for(seed, [m] + [n, m] * T))
+    x, mse = op_amp = lm.amp_sparse_regression(op, beta, w, T)
+    x, mse = x.cpu().numpy(), mse.cpu().numpy()
+    assert rel(x, xr) < TOL64
+    assert np.max(np.abs(mse - mser) / mser) < 1e-9
+    assert mse[-1] < 0.5 * mse[0]  # AMP converges
+
+
+def test_spiked_goe_power_parity(orc, lm):
+    # config 5 shape at reduced n: GOE inner sigma = 1/sqrt(n), theta = 2
+    n, T, seed = 900, 20, 31
+    u = orc.RandomSource(seed, 1).normal_vector(n)
+    u /= np.linalg.norm(u)
+    x1 = orc.RandomSource(seed, 2).normal_vector(n)
+    x1 /= np.linalg.norm(x1)
+    ref = orc.Operator("goe", n=n, sigma=n ** -0.5, seed=seed)
+    xr, ovr = ref.spiked_power(u, x1, T)
+    op = lm.GOEOperator(n, seed, sigma=n ** -0.5, draws="injected", capacity=T)
+    op.push_draws(orc.draws_for(seed, [n] * (2 * T)))
+    x, ov = lm.spiked_power(op, u, x1, T)
+    assert rel(x.cpu().numpy(), xr) < TOL64
+    assert np.max(np.abs(ov.cpu().numpy() - ovr)) < 1e-9
+    assert abs(ovr[-1]) > 0.5  # theta = 2 > 1: the spike is detected

@@ -10,7 +10,7 @@ res = {}
 for dtype, B in (("f64", int(os.environ.get("C3_B64", 1024))), ("f32", int(os.environ.get("C3_B32", 1024)))):
     tdt = torch.float64 if dtype == "f64" else torch.float32
     x1 = torch.randn((B, n), dtype=tdt, device="cuda", generator=torch.Generator("cuda").manual_seed(1))
-    for conc in (16, 32):
+    for conc in [int(c) for c in os.environ.get("C3_CONC", "16").split(",")]:
         lazymat.run_trials("ginibre", min(B, 2 * conc), n, T, seed=1, dtype=dtype, concurrency=conc,
                            x1=x1[: min(B, 2 * conc)])  # warm: capture graphs
         torch.cuda.synchronize()
