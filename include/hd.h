@@ -41,10 +41,14 @@ typedef enum hd_status {
 typedef enum hd_ensemble { HD_GINIBRE = 0, HD_HAAR = 1, HD_GOE = 2 } hd_ensemble;
 typedef enum hd_side { HD_RIGHT = 0, HD_LEFT = 1 } hd_side; /* types.hpp:26 */
 typedef enum hd_dtype { HD_F64 = 0, HD_F32 = 1 } hd_dtype;
-/* Gaussian draws: device Philox4x32-10 keyed by (seed, stream) with counter
- * (row, probe) — production; or the caller injects them in probe order
- * (parity mode: e.g. the reference RandomSource(seed).normals(len) stream). */
-typedef enum hd_draw_mode { HD_DRAWS_PHILOX = 0, HD_DRAWS_INJECTED = 1 } hd_draw_mode;
+/* Gaussian draws:
+ *  PHILOX    device Philox4x32-10 keyed by (seed, stream), counter (row, probe):
+ *            production, generated inside the streaming kernels;
+ *  INJECTED  the caller pushes them in probe order (hd_push_draws);
+ *  REFERENCE the reference's own RandomSource(seed, stream) stream
+ *            (xoshiro256++ + ziggurat, random.cpp:78-176), generated on the
+ *            host and queued: the same seed gives the reference's matrix. */
+typedef enum hd_draw_mode { HD_DRAWS_PHILOX = 0, HD_DRAWS_INJECTED = 1, HD_DRAWS_REFERENCE = 2 } hd_draw_mode;
 /* reflect.hpp:33 SignRule; FaultFlags operators.hpp:16-22 */
 typedef enum hd_sign_rule {
   HD_SIGN_STABLE = 0,
@@ -185,6 +189,19 @@ int hd_reset_stats(hd_op* op);
 int hd_launch_count(const hd_op* op, int64_t* count);
 
 const char* hd_last_error(void);
+
+/* ---------------------------------------------------------------------------
+ * The reference's RandomSource (random.hpp:55-112) on the host, for callers
+ * that draw their data the way the reference does (experiments.cpp:124-125:
+ * matrix stream 0, data stream 1). normal_vector fills `out` (len >= 1). */
+typedef struct hd_rs hd_rs;
+int hd_rs_create(uint64_t seed, uint64_t stream, hd_rs** out);
+void hd_rs_destroy(hd_rs* rs);
+uint64_t hd_rs_next_u64(hd_rs* rs);
+double hd_rs_uniform(hd_rs* rs);
+double hd_rs_normal(hd_rs* rs);
+int hd_rs_normal_vector(hd_rs* rs, int64_t len, double* out);
+uint64_t hd_derive_seed(uint64_t base, uint64_t index); /* random.cpp:73-76 */
 const char* hd_version(void);
 
 #ifdef __cplusplus

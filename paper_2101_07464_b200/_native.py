@@ -22,7 +22,8 @@ HD_ERR_NCCL = 6
 HD_GINIBRE, HD_HAAR, HD_GOE = 0, 1, 2
 HD_RIGHT, HD_LEFT = 0, 1
 HD_F64, HD_F32 = 0, 1
-HD_DRAWS_PHILOX, HD_DRAWS_INJECTED = 0, 1
+HD_DRAWS_PHILOX, HD_DRAWS_INJECTED, HD_DRAWS_REFERENCE = 0, 1, 2
+DRAW_MODES = {"philox": HD_DRAWS_PHILOX, "injected": HD_DRAWS_INJECTED, "reference": HD_DRAWS_REFERENCE}
 SIGN_RULES = {"stable": 0, "negative_at_zero": 1, "zero_when_negative": 2}
 UPDATES = {"identity": 0, "normalize": 1, "tanh_mix": 2}
 SIDE_RULES = {"alternate": 0, "right": 1, "left": 2}
@@ -32,8 +33,11 @@ EXPORTS = (
     "hd_create", "hd_destroy", "hd_shape", "hd_remaining", "hd_counts", "hd_chain_sizes", "hd_probe",
     "hd_push_draws", "hd_reset", "hd_run", "hd_run_callback", "hd_set_profiling", "hd_get_stats",
     "hd_reset_stats", "hd_launch_count", "hd_last_error", "hd_version", "hd_reflector_apply",
-    "hd_run_async", "hd_wait", "hd_reseed",
+    "hd_run_async", "hd_wait", "hd_reseed", "hd_rs_create", "hd_rs_destroy", "hd_rs_next_u64", "hd_rs_uniform",
+    "hd_rs_normal", "hd_rs_normal_vector", "hd_derive_seed",
 )
+_NON_STATUS = ("hd_last_error", "hd_version", "hd_rs_destroy", "hd_rs_next_u64", "hd_rs_uniform", "hd_rs_normal",
+               "hd_derive_seed")
 
 
 class hd_config(C.Structure):
@@ -104,8 +108,20 @@ def lib():
         L.hd_run_async.argtypes = [vp, C.POINTER(hd_run_args)]
         L.hd_wait.argtypes = [vp]
         L.hd_reseed.argtypes = [vp, C.c_uint64]
+        L.hd_rs_create.argtypes = [C.c_uint64, C.c_uint64, C.POINTER(vp)]
+        L.hd_rs_destroy.argtypes = [vp]
+        L.hd_rs_destroy.restype = None
+        L.hd_rs_next_u64.argtypes = [vp]
+        L.hd_rs_next_u64.restype = C.c_uint64
+        L.hd_rs_uniform.argtypes = [vp]
+        L.hd_rs_uniform.restype = C.c_double
+        L.hd_rs_normal.argtypes = [vp]
+        L.hd_rs_normal.restype = C.c_double
+        L.hd_rs_normal_vector.argtypes = [vp, i64, vp]
+        L.hd_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
+        L.hd_derive_seed.restype = C.c_uint64
         for name in EXPORTS:
-            if name not in ("hd_last_error", "hd_version"):
+            if name not in _NON_STATUS:
                 getattr(L, name).restype = C.c_int
         _lib = L
     return _lib

@@ -10,6 +10,8 @@
 //   check_probe_input        include/lazymat/operators.hpp:44-48
 #include <cuda_runtime.h>
 
+#include "hd_refrng.hpp"
+
 #include <algorithm>
 #include <climits>
 #include <cmath>
@@ -145,8 +147,13 @@ struct hd_op {
   void* ybuf[3] = {nullptr, nullptr, nullptr};
   void* gtmp = nullptr;   // GOE right-probe partial output
   int64_t io_len = 0;
+  // queued draws (HD_DRAWS_INJECTED / HD_DRAWS_REFERENCE): inj[i] is draw
+  // number inj_base + i of the operator's flat Gaussian stream; c.inj_pos is
+  // the next one a probe consumes
   double* inj = nullptr;
-  int64_t inj_cap = 0, inj_size = 0;
+  int64_t inj_cap = 0, inj_size = 0, inj_base = 0;
+  std::unique_ptr<hd::refrng::Source> ref;  // HD_DRAWS_REFERENCE generator
+  std::vector<double> ref_host;             // staging for generated draws
   cudaStream_t stream = nullptr;  // every kernel of the handle runs here
   cudaEvent_t ev_fork = nullptr;  // orders `stream` after the caller's stream
   int nsm = 148;
@@ -560,15 +567,63 @@ Src<T> vec_src(const void* x, const double* xscale) {
   return s;
 }
 
+int64_t inj_avail(const hd_op* op) { return op->inj_base + op->inj_size - op->c.inj_pos; }
+const double* inj_at(const hd_op* op, int64_t pos) { return op->inj + (pos - op->inj_base); }
+
+// Append `len` draws (host or device pointer) to the queue.
+void inj_append(hd_op* op, const double* g, int64_t len, bool on_device) {
+  if (op->inj_size + len > op->inj_cap) {
+    const int64_t ncap = std::max<int64_t>(op->inj_cap * 2, op->inj_size + len);
+    double* np = dmalloc<double>(ncap);
+    if (op->inj_size > 0)
+      ck(cudaMemcpyAsync(np, op->inj, sizeof(double) * op->inj_size, cudaMemcpyDeviceToDevice, op->stream), "grow");
+    ck(cudaStreamSynchronize(op->stream), "sync");
+    cudaFree(op->inj);
+    op->inj = np;
+    op->inj_cap = ncap;
+  }
+  ck(cudaMemcpyAsync(op->inj + op->inj_size, g, sizeof(double) * len,
+                     on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, op->stream),
+     "push");
+  ck(cudaStreamSynchronize(op->stream), "sync");
+  op->inj_size += len;
+}
+
+// HD_DRAWS_REFERENCE: make at least `count` unconsumed draws of the
+// reference stream RandomSource(seed, stream) available. Consumed draws are
+// dropped first (no probe can rewind below c.inj_pos: every snapshot is
+// taken after this call), so the queue holds at most one run's draws.
+void ref_ensure(hd_op* op, int64_t count) {
+  if (op->cfg.draw_mode != HD_DRAWS_REFERENCE) return;
+  const int64_t avail = inj_avail(op);
+  if (avail >= count) return;
+  const int64_t drop = op->c.inj_pos - op->inj_base;
+  if (drop > 0) {
+    if (avail > 0) {
+      double* np = dmalloc<double>(std::max<int64_t>(op->inj_cap, 1));
+      ck(cudaMemcpyAsync(np, op->inj + drop, sizeof(double) * avail, cudaMemcpyDeviceToDevice, op->stream), "compact");
+      ck(cudaStreamSynchronize(op->stream), "sync");
+      cudaFree(op->inj);
+      op->inj = np;
+    }
+    op->inj_size = avail;
+    op->inj_base = op->c.inj_pos;
+  }
+  const int64_t need = count - avail;
+  op->ref_host.resize((size_t)need);
+  op->ref->normal_fill(op->ref_host.data(), need);
+  inj_append(op, op->ref_host.data(), need, false);
+}
+
 // The fresh draw of the current inner probe (ginibre.hpp:67/86, haar.hpp:48).
 template <typename T>
 Src<T> draw_src(hd_op* op, int64_t len) {
   Src<T> s;
-  if (op->cfg.draw_mode == HD_DRAWS_INJECTED) {
-    if (op->inj_size - op->c.inj_pos < len)
+  if (op->cfg.draw_mode != HD_DRAWS_PHILOX) {
+    if (inj_avail(op) < len)
       throw HdError(HD_ERR_INVALID_ARGUMENT, "hd: injected draws exhausted (push one vector per probe)");
     s.kind = kSrcInjected;
-    s.inj = op->inj + op->c.inj_pos;
+    s.inj = inj_at(op, op->c.inj_pos);
     op->c.inj_pos += len;
   } else {
     s.kind = kSrcPhilox;
@@ -741,11 +796,11 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   oa.epi = epi;
   oa.prefetch = 1;  // predecessor k_small_fold writes chain F's pivot, not P_O
   const bool next_ok = (op->c.t < op->n) &&
-                       (op->cfg.draw_mode == HD_DRAWS_PHILOX || op->inj_size - op->c.inj_pos >= n);
+                       (op->cfg.draw_mode == HD_DRAWS_PHILOX || inj_avail(op) >= n);
   if (next_ok) {
-    if (op->cfg.draw_mode == HD_DRAWS_INJECTED) {
+    if (op->cfg.draw_mode != HD_DRAWS_PHILOX) {
       oa.spec.kind = kSrcInjected;
-      oa.spec.inj = op->inj + op->c.inj_pos;
+      oa.spec.inj = inj_at(op, op->c.inj_pos);
     } else {
       oa.spec.kind = kSrcPhilox;
       oa.spec.seedp = op->seed_dev;
@@ -762,7 +817,7 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   if (next_ok) {
     op->c.spec_chain = ochain;
     op->c.spec_probe = op->c.probe_index;
-    op->c.spec_inj = (op->cfg.draw_mode == HD_DRAWS_INJECTED) ? op->c.inj_pos : -1;
+    op->c.spec_inj = (op->cfg.draw_mode != HD_DRAWS_PHILOX) ? op->c.inj_pos : -1;
     op->c.spec_count = (int)O.pan.count;
     op->c.spec_nblk = gridO;
     op->c.spec_slot0 = oa.slot_spec;
@@ -1032,6 +1087,9 @@ void hard_reset(hd_op* op) {
   op->R.pan.count = op->L.pan.count = op->U.count = op->V.count = 0;
   op->R.pend = op->L.pend = -1;
   op->inj_size = 0;
+  op->inj_base = 0;
+  if (op->cfg.draw_mode == HD_DRAWS_REFERENCE)
+    op->ref = std::make_unique<hd::refrng::Source>(op->cfg.seed, op->cfg.stream);
   reset_device_state(op, op->stream);
   ck(cudaStreamSynchronize(op->stream), "sync");
 }
@@ -1082,6 +1140,13 @@ void do_probe(hd_op* op, const void* x, int64_t x_len, void* y, int64_t y_len, i
   }
   if (op->ens == HD_GOE) ensure_capacity(op, 1, 1);
   else ensure_capacity(op, eff_side == HD_RIGHT ? 1 : 0, eff_side == HD_LEFT ? 1 : 0);
+  if (op->cfg.draw_mode == HD_DRAWS_REFERENCE) {
+    // this probe's draws (GOE: inner right then inner left); Haar also queues
+    // the next probe's draw so its Gram dots can be computed speculatively
+    int64_t need = (op->ens == HD_GOE) ? 2 * op->n : (op->ens == HD_HAAR) ? op->n : (eff_side == HD_RIGHT ? rows : cols);
+    if (op->ens == HD_HAAR && remaining(op) >= 2) need += op->n;
+    ref_ensure(op, need);
+  }
   const Counters snap = take_snapshot(op);
   // stage input (16 B aligned for vector loads)
   const void* xin = x;
@@ -1279,6 +1344,8 @@ void do_run_enqueue(hd_op* op, const hd_run_args& a) {
       else ++nl;
     }
     ensure_capacity(op, nr, nl);
+    if (op->cfg.draw_mode == HD_DRAWS_REFERENCE)  // draws of every inner probe of the run
+      ref_ensure(op, (op->ens == HD_HAAR) ? (nr + nl) * op->n : nr * op->m + nl * op->n);
   }
   fork_from(op, static_cast<cudaStream_t>(a.stream));
   const Counters snap0 = take_snapshot(op);
@@ -1498,7 +1565,8 @@ int hd_create(const hd_config* cfg, hd_op** out) {
   require(cfg != nullptr && out != nullptr, "hd_create: null argument");
   const hd_config& c = *cfg;
   require(c.dtype == HD_F64 || c.dtype == HD_F32, "hd_create: dtype must be HD_F64 or HD_F32");
-  require(c.draw_mode == HD_DRAWS_PHILOX || c.draw_mode == HD_DRAWS_INJECTED, "hd_create: unknown draw mode");
+  require(c.draw_mode == HD_DRAWS_PHILOX || c.draw_mode == HD_DRAWS_INJECTED || c.draw_mode == HD_DRAWS_REFERENCE,
+          "hd_create: unknown draw mode");
   require(c.sign_rule >= 0 && c.sign_rule <= 2, "hd_create: unknown sign rule");
   int64_t m = c.m, n = c.n;
   if (c.ensemble == HD_GINIBRE) {
@@ -1673,25 +1741,7 @@ int hd_push_draws(hd_op* op, const double* g, int64_t len, int32_t on_device) {
   require(len >= 1, "normal_vector: len must be >= 1");
   cudaSetDevice(op->cfg.device);
   // compact consumed prefix, then grow
-  if (op->c.inj_pos > 0 && op->c.r == 0 && op->c.l == 0 && op->c.t == 0) {
-    // nothing consumed by live probes can be referenced any more only when
-    // the queue was reset; keep it simple: never compact live queues
-  }
-  if (op->inj_size + len > op->inj_cap) {
-    const int64_t ncap = std::max<int64_t>(op->inj_cap * 2, op->inj_size + len);
-    double* np = dmalloc<double>(ncap);
-    if (op->inj_size > 0)
-      ck(cudaMemcpyAsync(np, op->inj, sizeof(double) * op->inj_size, cudaMemcpyDeviceToDevice, op->stream), "grow");
-    ck(cudaStreamSynchronize(op->stream), "sync");
-    cudaFree(op->inj);
-    op->inj = np;
-    op->inj_cap = ncap;
-  }
-  ck(cudaMemcpyAsync(op->inj + op->inj_size, g, sizeof(double) * len,
-                     on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, op->stream),
-     "push");
-  ck(cudaStreamSynchronize(op->stream), "sync");
-  op->inj_size += len;
+  inj_append(op, g, len, on_device != 0);
   return HD_OK;
   HD_CATCH
 }
@@ -1741,12 +1791,45 @@ int hd_wait(hd_op* op) {
   HD_CATCH
 }
 
+struct hd_rs {
+  hd::refrng::Source src;
+};
+
+int hd_rs_create(uint64_t seed, uint64_t stream, hd_rs** out) {
+  HD_TRY
+  require(out != nullptr, "hd_rs_create: null argument");
+  *out = new hd_rs{hd::refrng::Source(seed, stream)};
+  return HD_OK;
+  HD_CATCH
+}
+
+void hd_rs_destroy(hd_rs* rs) { delete rs; }
+uint64_t hd_rs_next_u64(hd_rs* rs) { return rs->src.next(); }
+double hd_rs_uniform(hd_rs* rs) { return rs->src.uniform(); }
+double hd_rs_normal(hd_rs* rs) { return rs->src.normal(); }
+
+int hd_rs_normal_vector(hd_rs* rs, int64_t len, double* out) {
+  HD_TRY
+  require(rs && out, "hd_rs_normal_vector: null argument");
+  require(len >= 1, "normal_vector: len must be >= 1");
+  rs->src.normal_fill(out, len);
+  return HD_OK;
+  HD_CATCH
+}
+
+uint64_t hd_derive_seed(uint64_t base, uint64_t index) { return hd::refrng::derive_seed(base, index); }
+
 int hd_reseed(hd_op* op, uint64_t seed) {
   HD_TRY
   require(op, "hd_reseed: null argument");
   require(!op->run_pending, "hd_reseed: a run is in flight (hd_wait first)");
-  require(op->cfg.draw_mode == HD_DRAWS_PHILOX, "hd_reseed: only for HD_DRAWS_PHILOX operators");
+  require(op->cfg.draw_mode != HD_DRAWS_INJECTED, "hd_reseed: injected-draw operators take their draws from the caller");
   cudaSetDevice(op->cfg.device);
+  if (op->cfg.draw_mode == HD_DRAWS_REFERENCE) {  // host generator: a synchronous fresh start
+    op->cfg.seed = seed;
+    hard_reset(op);
+    return HD_OK;
+  }
   // fresh state without a host sync: counters on the host, device words and
   // D tables by kernels on the handle's stream (graph replays reset too)
   op->cfg.seed = seed;

@@ -32,7 +32,7 @@ from .._native import BudgetExhausted, ResourceCapExceeded
 
 __all__ = [
     "BudgetExhausted", "GinibreOperator", "HaarOperator", "GOEOperator", "Reflector", "ResourceCapExceeded",
-    "SubsampledHaarOperator", "USVOperator", "derive_seed", "ista_curves", "make_reflector", "run_trials", "amp_sparse_regression", "spiked_power",
+    "RandomSource", "SubsampledHaarOperator", "USVOperator", "derive_seed", "ista_curves", "make_reflector", "run_trials", "amp_sparse_regression", "spiked_power",
     "sample_dense_haar",
     "spectral_summary", "two_sample_ks",
 ]
@@ -44,10 +44,37 @@ _MASK = (1 << 64) - 1
 
 def derive_seed(base: int, index: int) -> int:
     """random.cpp:73-76: splitmix64(base + index * golden_gamma)."""
-    z = (base + index * 0x9E3779B97F4A7C15 + 0x9E3779B97F4A7C15) & _MASK
-    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _MASK
-    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _MASK
-    return z ^ (z >> 31)
+    return int(N.lib().hd_derive_seed(int(base) & _MASK, int(index) & _MASK))
+
+
+class RandomSource:
+    """The reference's RandomSource(seed, stream) (random.hpp:55-112): xoshiro256++,
+    stream k = k jumps of 2^128, polar normal(), ziggurat normal_vector().
+    Runs on the host inside libhd_b200.so (hd_rs_*)."""
+
+    def __init__(self, seed: int = 1, stream: int = 0):
+        h = C.c_void_p()
+        N.check(N.lib().hd_rs_create(int(seed) & _MASK, int(stream) & _MASK, C.byref(h)))
+        self._h = h.value
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h and N is not None and N._lib is not None:
+            N._lib.hd_rs_destroy(h)
+
+    def next_u64(self) -> int:
+        return int(N.lib().hd_rs_next_u64(self._h))
+
+    def uniform(self) -> float:
+        return float(N.lib().hd_rs_uniform(self._h))
+
+    def normal(self) -> float:
+        return float(N.lib().hd_rs_normal(self._h))
+
+    def normal_vector(self, n: int) -> np.ndarray:
+        out = np.empty(max(int(n), 1), dtype=np.float64)
+        N.check(N.lib().hd_rs_normal_vector(self._h, int(n), out.ctypes.data_as(C.c_void_p)))
+        return out
 
 
 def _side(side: str) -> int:
@@ -76,7 +103,9 @@ class _Operator:
         cfg.seed = int(seed) & _MASK
         cfg.stream = int(stream)
         cfg.capacity = int(capacity)
-        cfg.draw_mode = {"philox": N.HD_DRAWS_PHILOX, "injected": N.HD_DRAWS_INJECTED}[draws]
+        if draws not in N.DRAW_MODES:
+            raise ValueError("draws must be 'philox', 'injected' or 'reference'")
+        cfg.draw_mode = N.DRAW_MODES[draws]
         cfg.skip_reflector = int(bool(skip_reflector))
         cfg.sign_rule = N.SIGN_RULES[sign_rule]
         cfg.device = int(device)

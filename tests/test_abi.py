@@ -9,6 +9,7 @@ import os
 import re
 import subprocess
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -21,7 +22,7 @@ REFERENCE_ALL = ["BudgetExhausted", "GinibreOperator", "HaarOperator", "Resource
 
 def header_functions():
     txt = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(hd_\w+)\s*\(", txt, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*|void|uint64_t|double)\s+(hd_\w+)\s*\(", txt, flags=re.M)))
 
 
 def test_header_declares_the_boundary():
@@ -108,3 +109,35 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"from\s+oracle|import\s+oracle|liboracle|oracle/", txt), f
+
+
+# ------------------------------------------ product RandomSource (host, hd_rs_*)
+def test_product_random_source_golden_words(lm):
+    # test_random.cpp:21-36 golden xoshiro256++ words for seed 1 (as pinned in the oracle tests)
+    rs = lm.RandomSource(1)
+    want = [0xCFC5D07F6F03C29B, 0xBF424132963FE08D, 0x19A37D5757AAF520, 0xBF08119F05CD56D6]
+    assert [rs.next_u64() for _ in range(4)] == want
+
+
+def test_product_random_source_matches_oracle_bitwise(orc, lm):
+    for seed, stream in [(1, 0), (7, 1), (123456789, 3), (2 ** 63 + 5, 2)]:
+        a, b = lm.RandomSource(seed, stream), orc.RandomSource(seed, stream)
+        assert [a.next_u64() for _ in range(8)] == [b.next_u64() for _ in range(8)]
+        assert [a.uniform() for _ in range(5)] == [b.uniform() for _ in range(5)]
+        assert [a.normal() for _ in range(7)] == [b.normal() for _ in range(7)]  # polar, with spare
+        for n in (1, 3, 1000, 65537):
+            assert np.array_equal(a.normal_vector(n), b.normal_vector(n))
+
+
+def test_product_random_source_split_fill_and_errors(lm):
+    a, b = lm.RandomSource(9, 1), lm.RandomSource(9, 1)
+    whole = a.normal_vector(5000)
+    parts = np.concatenate([b.normal_vector(k) for k in (1, 999, 3000, 1000)])
+    assert np.array_equal(whole, parts)  # test_random.cpp:90-98
+    with pytest.raises(ValueError, match="len must be >= 1"):
+        a.normal_vector(0)
+
+
+def test_draw_mode_validation(lm):
+    with pytest.raises(ValueError, match="draws must be"):
+        lm.HaarOperator(4, seed=1, draws="bogus")
