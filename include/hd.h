@@ -201,6 +201,9 @@ uint64_t hd_rs_next_u64(hd_rs* rs);
 double hd_rs_uniform(hd_rs* rs);
 double hd_rs_normal(hd_rs* rs);
 int hd_rs_normal_vector(hd_rs* rs, int64_t len, double* out);
+/* sample_bernoulli_gaussian (experiments.cpp:19-29): per entry one uniform,
+ * 0 when it is < rho, else sigma_s * normal() (polar). */
+int hd_rs_bernoulli_gaussian(hd_rs* rs, int64_t n, double rho, double sigma_s, double* out);
 uint64_t hd_derive_seed(uint64_t base, uint64_t index); /* random.cpp:73-76 */
 const char* hd_version(void);
 

@@ -34,7 +34,7 @@ EXPORTS = (
     "hd_push_draws", "hd_reset", "hd_run", "hd_run_callback", "hd_set_profiling", "hd_get_stats",
     "hd_reset_stats", "hd_launch_count", "hd_last_error", "hd_version", "hd_reflector_apply",
     "hd_run_async", "hd_wait", "hd_reseed", "hd_rs_create", "hd_rs_destroy", "hd_rs_next_u64", "hd_rs_uniform",
-    "hd_rs_normal", "hd_rs_normal_vector", "hd_derive_seed",
+    "hd_rs_normal", "hd_rs_normal_vector", "hd_rs_bernoulli_gaussian", "hd_derive_seed",
 )
 _NON_STATUS = ("hd_last_error", "hd_version", "hd_rs_destroy", "hd_rs_next_u64", "hd_rs_uniform", "hd_rs_normal",
                "hd_derive_seed")
@@ -118,6 +118,7 @@ def lib():
         L.hd_rs_normal.argtypes = [vp]
         L.hd_rs_normal.restype = C.c_double
         L.hd_rs_normal_vector.argtypes = [vp, i64, vp]
+        L.hd_rs_bernoulli_gaussian.argtypes = [vp, i64, C.c_double, C.c_double, vp]
         L.hd_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
         L.hd_derive_seed.restype = C.c_uint64
         for name in EXPORTS:

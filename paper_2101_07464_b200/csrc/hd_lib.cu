@@ -1817,6 +1817,17 @@ int hd_rs_normal_vector(hd_rs* rs, int64_t len, double* out) {
   HD_CATCH
 }
 
+int hd_rs_bernoulli_gaussian(hd_rs* rs, int64_t n, double rho, double sigma_s, double* out) {
+  HD_TRY
+  require(rs && out, "hd_rs_bernoulli_gaussian: null argument");
+  require(n >= 1, "sample_bernoulli_gaussian: n must be positive");  // experiments.cpp:21-23
+  require(rho >= 0.0 && rho <= 1.0, "sample_bernoulli_gaussian: rho in [0,1]");
+  require(sigma_s > 0.0, "sample_bernoulli_gaussian: sigma_s must be positive");
+  rs->src.bernoulli_gaussian(out, n, rho, sigma_s);
+  return HD_OK;
+  HD_CATCH
+}
+
 uint64_t hd_derive_seed(uint64_t base, uint64_t index) { return hd::refrng::derive_seed(base, index); }
 
 int hd_reseed(hd_op* op, uint64_t seed) {

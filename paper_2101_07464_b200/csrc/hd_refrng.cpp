@@ -93,5 +93,9 @@ void Source::normal_fill(double* out, int64_t len) {
   }
 }
 
+void Source::bernoulli_gaussian(double* out, int64_t n, double rho, double sigma_s) {
+  for (int64_t i = 0; i < n; ++i) out[i] = (uniform() < rho) ? 0.0 : sigma_s * normal();
+}
+
 }  // namespace refrng
 }  // namespace hd

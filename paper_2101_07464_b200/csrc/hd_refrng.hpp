@@ -71,6 +71,8 @@ class Source {
   // bit-identical.
   double normal();                               // random.cpp:106-121 (polar)
   void normal_fill(double* out, int64_t len);    // random.cpp:130-176 (ziggurat)
+  // experiments.cpp:19-29: 0 with probability rho, else sigma_s * normal()
+  void bernoulli_gaussian(double* out, int64_t n, double rho, double sigma_s);
 
  private:
   static uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }

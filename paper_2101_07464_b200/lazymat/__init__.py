@@ -16,10 +16,13 @@ Inputs may be numpy arrays (host, like the reference) or CUDA torch tensors
 (zero-copy device path; the result is then a CUDA tensor). Everything runs
 through the C-ABI of libhd_b200.so; there is no CPU fallback.
 
-Out of scope this round: sample_dense_haar,
-ista_curves, spectral_summary, two_sample_ks raise NotImplementedError.
 make_reflector / Reflector (module.cpp:48-66) build and apply the reflector
-on the device through hd_reflector_apply.
+on the device through hd_reflector_apply. ista_curves, spectral_summary,
+sample_dense_haar and two_sample_ks (module.cpp:113-194) run the reference's
+application drivers on the device operators (lazymat/experiments.py).
+``draws="reference"`` makes an operator draw the reference's own
+RandomSource(seed) stream, i.e. the same matrix as the reference's for the
+same seed; ``RandomSource`` is that generator on the host.
 """
 from __future__ import annotations
 
@@ -33,7 +36,7 @@ from .._native import BudgetExhausted, ResourceCapExceeded
 __all__ = [
     "BudgetExhausted", "GinibreOperator", "HaarOperator", "GOEOperator", "Reflector", "ResourceCapExceeded",
     "RandomSource", "SubsampledHaarOperator", "USVOperator", "derive_seed", "ista_curves", "make_reflector", "run_trials", "amp_sparse_regression", "spiked_power",
-    "sample_dense_haar",
+    "sample_dense_haar", "ista_trial", "spectral_trial", "power_iteration", "restarted_krylov", "soft_threshold",
     "spectral_summary", "two_sample_ks",
 ]
 
@@ -74,6 +77,13 @@ class RandomSource:
     def normal_vector(self, n: int) -> np.ndarray:
         out = np.empty(max(int(n), 1), dtype=np.float64)
         N.check(N.lib().hd_rs_normal_vector(self._h, int(n), out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def bernoulli_gaussian(self, n: int, rho: float, sigma_s: float) -> np.ndarray:
+        """sample_bernoulli_gaussian (experiments.cpp:19-29) from this source."""
+        out = np.empty(max(int(n), 1), dtype=np.float64)
+        N.check(N.lib().hd_rs_bernoulli_gaussian(self._h, int(n), float(rho), float(sigma_s),
+                                                 out.ctypes.data_as(C.c_void_p)))
         return out
 
 
@@ -580,17 +590,9 @@ class SubsampledHaarOperator:
         return self.q.probe(padded, "left")
 
 
-def sample_dense_haar(n: int, seed: int = 1):
-    raise NotImplementedError("sample_dense_haar: dense oracle is out of scope (SURVEY.md §8f f4)")
-
-
-def ista_curves(*args, **kwargs):
-    raise NotImplementedError("ista_curves: application driver is out of scope (SURVEY.md §8f f3)")
-
-
-def spectral_summary(*args, **kwargs):
-    raise NotImplementedError("spectral_summary: application driver is out of scope (SURVEY.md §8f f3)")
-
-
-def two_sample_ks(a, b):
-    raise NotImplementedError("two_sample_ks: statistics harness is out of scope (SURVEY.md §8f f4)")
+# Application drivers and the dense direct backend (experiments.cpp,
+# eigensolve.hpp, ensembles.hpp:40-91, stats.cpp) on the device operators.
+from .experiments import (  # noqa: E402
+    ista_curves, ista_trial, power_iteration, restarted_krylov, sample_dense_haar, soft_threshold,
+    spectral_summary, spectral_trial, two_sample_ks,
+)
