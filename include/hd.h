@@ -49,6 +49,10 @@ typedef enum hd_dtype { HD_F64 = 0, HD_F32 = 1 } hd_dtype;
  *            (xoshiro256++ + ziggurat, random.cpp:78-176), generated on the
  *            host and queued: the same seed gives the reference's matrix. */
 typedef enum hd_draw_mode { HD_DRAWS_PHILOX = 0, HD_DRAWS_INJECTED = 1, HD_DRAWS_REFERENCE = 2 } hd_draw_mode;
+/* Exchange of a row-sharded operator group: NCCL across ranks
+ * (one GPU each) or in-process for virtual shards (one host thread each). */
+typedef struct hd_exchange hd_exchange;
+
 /* reflect.hpp:33 SignRule; FaultFlags operators.hpp:16-22 */
 typedef enum hd_sign_rule {
   HD_SIGN_STABLE = 0,
@@ -69,9 +73,33 @@ typedef struct hd_config {
   int32_t skip_reflector;/* FaultFlags::skip_reflector                       */
   int32_t sign_rule;     /* FaultFlags::sign_rule                            */
   int32_t device;        /* CUDA device ordinal                              */
+  /* Row sharding (north star: n beyond one GPU's HBM): shard_count > 1 makes
+   * this handle shard `shard_rank` of an operator whose panels and vectors
+   * are split into tile-aligned row slabs (hd_shard_plan); every shard must
+   * make the same calls with its own rows of x / y (hd_shard_range), and
+   * `capacity` (max probes per chain) is required. 0 or 1 without an
+   * exchange = unsharded; a 1-shard group with an exchange runs the
+   * sharded protocol (exchange after every streaming kernel) on one GPU. */
+  int32_t shard_count;
+  int32_t shard_rank;
+  hd_exchange* exchange; /* the group's exchange (hd_exchange_create_*)     */
 } hd_config;
 
 typedef struct hd_op hd_op;
+
+/* Exchanges and the shard plan. After every streaming kernel
+ * the shards of one operator allreduce one buffer: the partial dot
+ * products, shard 0's head rows and the status flags (NCCL over NVLink for
+ * one rank per GPU; in-process for virtual shards, one host thread each). */
+int hd_exchange_create_local(int32_t nshards, hd_exchange** out);
+int hd_exchange_nccl_id(void* id_out /* 128 bytes, ncclGetUniqueId */);
+int hd_exchange_create_nccl(const void* id, int32_t nranks, int32_t rank, int32_t device, hd_exchange** out);
+int hd_exchange_destroy(hd_exchange* ex);
+/* rows [begin, end) of an N-row dimension owned by shard `rank` of `count`:
+ * tile-aligned slabs, shard 0 holding the head rows [0, head_rows) */
+int hd_shard_plan(int64_t N, int32_t count, int32_t rank, int64_t head_rows, int64_t* begin, int64_t* end);
+/* the rows this handle owns: dim 0 = n (right-probe input), 1 = m (output) */
+int hd_shard_range(const hd_op* op, int32_t dim, int64_t* begin, int64_t* end);
 
 /* Replaces the constructors GinibreOperator(m, n, sigma, RandomSource, faults)
  * (ginibre.hpp:31-42), HaarOperator(n, RandomSource, faults) (haar.hpp:24-31),
@@ -90,7 +118,7 @@ int hd_chain_sizes(const hd_op* op, int64_t* right_chain, int64_t* left_chain);
 
 /* ProbeOperator::probe(x, side) (operators.hpp:41): y = Q x (right) or
  * Q^T x (left). x/y are host pointers (on_device = 0) or device pointers of
- * the operator's dtype (on_device = 1). Validation order follows
+ * the operator's dtype (on_device = 1); a shard passes its own rows only. Validation order follows
  * check_probe_input then the budget check (operators.hpp:44-48,
  * ginibre.hpp:59-62). Synchronous: returns after y is written. `stream` is
  * the caller's cudaStream_t (NULL = the legacy default stream): the probe

@@ -35,6 +35,8 @@ EXPORTS = (
     "hd_reset_stats", "hd_launch_count", "hd_last_error", "hd_version", "hd_reflector_apply",
     "hd_run_async", "hd_wait", "hd_reseed", "hd_rs_create", "hd_rs_destroy", "hd_rs_next_u64", "hd_rs_uniform",
     "hd_rs_normal", "hd_rs_normal_vector", "hd_rs_bernoulli_gaussian", "hd_derive_seed",
+    "hd_exchange_create_local", "hd_exchange_nccl_id", "hd_exchange_create_nccl", "hd_exchange_destroy",
+    "hd_shard_plan", "hd_shard_range",
 )
 _NON_STATUS = ("hd_last_error", "hd_version", "hd_rs_destroy", "hd_rs_next_u64", "hd_rs_uniform", "hd_rs_normal",
                "hd_derive_seed")
@@ -45,7 +47,7 @@ class hd_config(C.Structure):
         ("ensemble", C.c_int32), ("dtype", C.c_int32), ("m", C.c_int64), ("n", C.c_int64),
         ("sigma", C.c_double), ("seed", C.c_uint64), ("stream", C.c_uint64), ("capacity", C.c_int64),
         ("draw_mode", C.c_int32), ("skip_reflector", C.c_int32), ("sign_rule", C.c_int32),
-        ("device", C.c_int32),
+        ("device", C.c_int32), ("shard_count", C.c_int32), ("shard_rank", C.c_int32), ("exchange", C.c_void_p),
     ]
 
 
@@ -120,6 +122,12 @@ def lib():
         L.hd_rs_normal_vector.argtypes = [vp, i64, vp]
         L.hd_rs_bernoulli_gaussian.argtypes = [vp, i64, C.c_double, C.c_double, vp]
         L.hd_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
+        L.hd_exchange_create_local.argtypes = [i32, C.POINTER(vp)]
+        L.hd_exchange_nccl_id.argtypes = [vp]
+        L.hd_exchange_create_nccl.argtypes = [vp, i32, i32, i32, C.POINTER(vp)]
+        L.hd_exchange_destroy.argtypes = [vp]
+        L.hd_shard_plan.argtypes = [i64, i32, i32, i64, C.POINTER(i64), C.POINTER(i64)]
+        L.hd_shard_range.argtypes = [vp, i32, C.POINTER(i64), C.POINTER(i64)]
         L.hd_derive_seed.restype = C.c_uint64
         for name in EXPORTS:
             if name not in _NON_STATUS:

@@ -82,6 +82,7 @@ struct Src {
   const double* D = nullptr;    // D(i) = i < Dlen ? D[i] : *Dtail
   const double* Dtail = nullptr;
   int64_t Dlen = 0;
+  int64_t vbase = 0;  // kSrcVec: x holds global rows [vbase, ...) (row shard)
 };
 
 template <typename T>
@@ -90,20 +91,21 @@ __device__ __forceinline__ double dvalue(const Src<T>& s, int64_t i) {
   return i < s.Dlen ? s.D[i] : *s.Dtail;
 }
 
-// Values of rows (i, i+1), i even; rows >= n read as zero.
+// Values of global rows (i, i+1), i even; rows >= n read as zero.
 template <typename T>
 __device__ __forceinline__ double2 src_pair(const Src<T>& s, int64_t i, int64_t n) {
   double2 v = make_double2(0.0, 0.0);
   if (s.kind == kSrcVec) {
+    const T* xp = s.x + (i - s.vbase);
     if (i + 1 < n) {
       if constexpr (sizeof(T) == 8) {
-        v = *reinterpret_cast<const double2*>(s.x + i);
+        v = *reinterpret_cast<const double2*>(xp);
       } else {
-        const float2 f = *reinterpret_cast<const float2*>(s.x + i);
+        const float2 f = *reinterpret_cast<const float2*>(xp);
         v = make_double2(f.x, f.y);
       }
     } else if (i < n) {
-      v.x = (double)s.x[i];
+      v.x = (double)xp[0];
     }
     if (s.xscale) {
       const double sc = *s.xscale;

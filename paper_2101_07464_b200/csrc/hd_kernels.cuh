@@ -117,6 +117,20 @@ struct ChainDev {
   int64_t Dlen = 0;
 };
 
+// ---------------------------------------------------------- row shards
+// A streaming kernel processes local panel tiles [tile0, tile0 + ntiles);
+// local panel row li is global row li + gdelta, and the row's entry of a
+// dense vector (input x, output y, ...) sits at index (global row - vbase).
+// Unsharded (and shard 0): all zero. A shard s > 0 keeps a replica of the
+// head rows [0, H) in local tiles [0, H/256) for the single-CTA stages and
+// streams only its own rows [lo, hi): tile0 = H/256, gdelta = lo - H,
+// vbase = lo.
+struct RowMap {
+  int64_t tile0 = 0;
+  int64_t gdelta = 0;
+  int64_t vbase = 0;
+};
+
 // ============================================================== k_dots
 template <typename T>
 struct DotJob {
@@ -140,6 +154,7 @@ struct DotArgs {
   DotJob<T> job[2];
   int njobs = 1;
   int64_t n = 0, ntiles = 0;
+  RowMap rm;
   Flush out;
   int nslots = 0;
   int* status = nullptr;
@@ -188,7 +203,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_dots(const __grid_constan
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the slot precede the refill
     mbar_arrive_expect_tx(full + s, bytes);
     bulk_g2s(ring + (size_t)s * kCW * kTile * sizeof(T),
-             J.P + (size_t)p.tile * (size_t)(J.K << kTileShift) + (size_t)p.chunk * kCW * kTile, bytes, full + s);
+             J.P + (size_t)(p.tile + a.rm.tile0) * (size_t)(J.K << kTileShift) + (size_t)p.chunk * kCW * kTile, bytes,
+             full + s);
   };
   // panel chunks written two or more launches back: prefetch, then wait
   if (a.prefetch && lane == 0)
@@ -211,15 +227,16 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_dots(const __grid_constan
       const DotJob<T>& J = a.job[jb];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int64_t i = tile * kTile + 2 * (lane + 32 * q);
+        const int64_t li = (tile + a.rm.tile0) * kTile + 2 * (lane + 32 * q);  // local panel row
+        const int64_t i = li + a.rm.gdelta;                                    // global row
         x[q] = src_pair(J.rhs, i, a.n);
         const double sq = x[q].x * x[q].x + x[q].y * x[q].y;
         if (jb == 0) ss0 += sq;
         else ss1 += sq;
         if (J.check_finite) bad |= !(isfinite(x[q].x) && isfinite(x[q].y));
         if (J.pivot_out && (i == J.pivot_row || i + 1 == J.pivot_row)) *J.pivot_out = (i == J.pivot_row) ? x[q].x : x[q].y;
-        if (J.wcol) st_pair(J.wcol + paddr(i, J.wj, J.wK), x[q].x, x[q].y);
-        pv[q] = (J.pend >= 0) ? ld_pair(J.P + paddr(i, J.pend, J.K)) : make_double2(0.0, 0.0);
+        if (J.wcol) st_pair(J.wcol + paddr(li, J.wj, J.wK), x[q].x, x[q].y);
+        pv[q] = (J.pend >= 0) ? ld_pair(J.P + paddr(li, J.pend, J.K)) : make_double2(0.0, 0.0);
       }
       const int nch = (J.ncols + kCW - 1) / kCW;
       for (int c = 0; c < nch; ++c, ++it) {
@@ -337,19 +354,21 @@ struct Epi {
   int step = 0;
 };
 
+// Epilogue of global rows (i, i + 1); the row's vector entries sit at i - vbase.
 template <typename T>
 __device__ __forceinline__ void epilogue(const Epi<T>& e, int* status, int64_t i, int64_t n, double2 v,
-                                         double* red_s) {
+                                         double* red_s, int64_t vbase) {
   double ss = 0.0;
   bool bad = false;
+  const int64_t vi = i - vbase;
   if (i < n) {
     if (e.yadd) {
       double2 ya;
       if (i + 1 < n) {
-        if constexpr (sizeof(T) == 8) ya = *reinterpret_cast<const double2*>(e.yadd + i);
-        else { const float2 f = *reinterpret_cast<const float2*>(e.yadd + i); ya = make_double2(f.x, f.y); }
+        if constexpr (sizeof(T) == 8) ya = *reinterpret_cast<const double2*>(e.yadd + vi);
+        else { const float2 f = *reinterpret_cast<const float2*>(e.yadd + vi); ya = make_double2(f.x, f.y); }
       } else {
-        ya = make_double2((double)e.yadd[i], 0.0);
+        ya = make_double2((double)e.yadd[vi], 0.0);
       }
       v.x = (ya.x + v.x) * e.add_scale;
       v.y = (ya.y + v.y) * e.add_scale;
@@ -358,19 +377,19 @@ __device__ __forceinline__ void epilogue(const Epi<T>& e, int* status, int64_t i
     if (e.kind == kEpiTanhMix) {
       double2 xp = make_double2(0.0, 0.0);
       if (e.xprev) {
-        if constexpr (sizeof(T) == 8) xp = *reinterpret_cast<const double2*>(e.xprev + i);
-        else { const float2 f = *reinterpret_cast<const float2*>(e.xprev + i); xp = make_double2(f.x, f.y); }
+        if constexpr (sizeof(T) == 8) xp = *reinterpret_cast<const double2*>(e.xprev + vi);
+        else { const float2 f = *reinterpret_cast<const float2*>(e.xprev + vi); xp = make_double2(f.x, f.y); }
         if (e.xprev_scale) { xp.x *= *e.xprev_scale; xp.y *= *e.xprev_scale; }
       }
       const double a = tanh(2.0 * v.x) + 0.1 * xp.x;
       const double b = (i + 1 < n) ? tanh(2.0 * v.y) + 0.1 * xp.y : 0.0;
-      st_pair_guard(e.xnext, i, n, a, b);
+      st_pair_guard(e.xnext - vbase, i, n, a, b);
       bad = !(isfinite(a) && isfinite(b));
     } else {
       bad = !(isfinite(v.x) && isfinite(v.y));
       ss = v.x * v.x + v.y * v.y;
     }
-    if (e.y) st_pair_guard(e.y, i, n, v.x, v.y);
+    if (e.y) st_pair_guard(e.y - vbase, i, n, v.x, v.y);
   }
   if (bad) {
     atomicMin(status + kStBadStep, e.step);
@@ -403,6 +422,7 @@ struct ApplyArgs {
   int ncols = 0;
   const double* beta = nullptr;
   int64_t n = 0, ntiles = 0;
+  RowMap rm;
   const double* D = nullptr;
   const double* Dtail = nullptr;
   int64_t Dlen = 0;
@@ -460,7 +480,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_arrive_expect_tx(full + s, bytes);
     bulk_g2s(ring + (size_t)s * kCW * kTile * sizeof(T),
-             a.P + (size_t)tile * (size_t)(a.K << kTileShift) + (size_t)c * kCW * kTile, bytes, full + s);
+             a.P + (size_t)(tile + a.rm.tile0) * (size_t)(a.K << kTileShift) + (size_t)c * kCW * kTile, bytes,
+             full + s);
   };
   __syncwarp();
   if (a.prefetch && lane == 0)
@@ -483,7 +504,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
     double2 g[4], r[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      g[q] = spec ? src_pair(a.spec, tile * kTile + 2 * (lane + 32 * q), a.n) : make_double2(0.0, 0.0);
+      const int64_t i = (tile + a.rm.tile0) * kTile + a.rm.gdelta + 2 * (lane + 32 * q);
+      g[q] = spec ? src_pair(a.spec, i, a.n) : make_double2(0.0, 0.0);
       r[q] = make_double2(0.0, 0.0);
     }
     for (int c = 0; c < nch; ++c, ++it) {
@@ -516,7 +538,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
     // epilogue on the lane's 8 rows
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int64_t i = tile * kTile + 2 * (lane + 32 * q);
+      const int64_t li = (tile + a.rm.tile0) * kTile + 2 * (lane + 32 * q);  // local panel row
+      const int64_t i = li + a.rm.gdelta;                                    // global row
       const double d0 = (i < a.Dlen) ? a.D[i] : *a.Dtail;
       const double d1 = (i + 1 < a.Dlen) ? a.D[i + 1] : *a.Dtail;
       if constexpr (MODE == kApplyFold) {
@@ -525,7 +548,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
         const double p1 = (i + 1 < a.n) ? d1 * (xv.y - r[q].y) : 0.0;
         const double c0 = (i >= a.off) ? p0 : 0.0, c1 = (i + 1 >= a.off) ? p1 : 0.0;
         const double es = *a.escale;
-        st_pair(a.Pw + paddr(i, a.newj, a.K), c0 * es, c1 * es);
+        st_pair(a.Pw + paddr(li, a.newj, a.K), c0 * es, c1 * es);
         if (i <= a.off) a.head[i] = p0;
         if (i + 1 <= a.off) a.head[i + 1] = p1;
         ss += c0 * c0 + c1 * c1;
@@ -537,11 +560,12 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
         const Epi<T>& e = a.epi;
         if (i < a.n) {
           if (i + 1 >= a.n) y.y = 0.0;
+          const int64_t vi = i - a.rm.vbase;
           if (e.kind == kEpiTanhMix) {
             double2 xp = make_double2(0.0, 0.0);
             if (e.xprev) {
-              xp.x = (double)e.xprev[i];
-              if (i + 1 < a.n) xp.y = (double)e.xprev[i + 1];
+              xp.x = (double)e.xprev[vi];
+              if (i + 1 < a.n) xp.y = (double)e.xprev[vi + 1];
               if (e.xprev_scale) {
                 xp.x *= *e.xprev_scale;
                 xp.y *= *e.xprev_scale;
@@ -549,13 +573,13 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
             }
             const double o0 = tanh(2.0 * y.x) + 0.1 * xp.x;
             const double o1 = (i + 1 < a.n) ? tanh(2.0 * y.y) + 0.1 * xp.y : 0.0;
-            st_pair_guard(e.xnext, i, a.n, o0, o1);
+            st_pair_guard(e.xnext - a.rm.vbase, i, a.n, o0, o1);
             bad |= !(isfinite(o0) && isfinite(o1));
           } else {
             bad |= !(isfinite(y.x) && isfinite(y.y));
             ss += y.x * y.x + y.y * y.y;
           }
-          if (e.y) st_pair_guard(e.y, i, a.n, y.x, y.y);
+          if (e.y) st_pair_guard(e.y - a.rm.vbase, i, a.n, y.x, y.y);
         }
       }
     }
@@ -605,6 +629,7 @@ struct GinArgs {
   const double* coef_cur = nullptr;
   double sigma = 1.0;
   int64_t n = 0;
+  RowMap rm;
   int* status = nullptr;
   Epi<T> epi;
 };
@@ -625,8 +650,9 @@ __global__ void __launch_bounds__(kUpdThreads) k_ginout(const __grid_constant__ 
   }
   for (int j = threadIdx.x; j < a.nS; j += kUpdThreads) cs[j] = a.coefS[j];
   __syncthreads();
-  const int64_t tile = blockIdx.x;
-  const int64_t i = tile * kTile + 2 * threadIdx.x;
+  const int64_t tile = blockIdx.x + a.rm.tile0;              // local panel tile
+  const int64_t li = tile * kTile + 2 * threadIdx.x;
+  const int64_t i = li + a.rm.gdelta;                         // global row
   const double* bp[2] = {b1, b3};
   double2 acc[2];
   panel_accumulate<T, 2>(a.P, a.K, a.ncols, tile, threadIdx.x, bp, acc);
@@ -639,14 +665,14 @@ __global__ void __launch_bounds__(kUpdThreads) k_ginout(const __grid_constant__ 
   double u0 = g.x - acc[0].x, u1 = g.y - acc[0].y;
   if (i >= a.n) u0 = 0.0;
   if (i + 1 >= a.n) u1 = 0.0;
-  st_pair(a.Sw + paddr(i, a.newj, a.KS), u0, u1);
+  st_pair(a.Sw + paddr(li, a.newj, a.KS), u0, u1);
   double c0 = 0.0, c1 = 0.0;
   if (i < a.csplen) c0 = dval(a.D, a.Dtail, a.Dlen, i) * a.csp[i];
   if (i + 1 < a.csplen) c1 = dval(a.D, a.Dtail, a.Dlen, i + 1) * a.csp[i + 1];
   const double cc = *a.coef_cur;
   const double y0 = a.sigma * (accS.x + cc * u0 + (c0 - acc[1].x));
   const double y1 = a.sigma * (accS.y + cc * u1 + (c1 - acc[1].y));
-  epilogue(a.epi, a.status, i, a.n, make_double2(y0, y1), red_s);
+  epilogue(a.epi, a.status, i, a.n, make_double2(y0, y1), red_s, a.rm.vbase);
 }
 
 // Scratch words shared between the small kernels of one probe.

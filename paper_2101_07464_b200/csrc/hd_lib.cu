@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include "hd_refrng.hpp"
+#include "hd_shard.cuh"
 
 #include <algorithm>
 #include <climits>
@@ -116,13 +117,37 @@ struct Counters {
 
 }  // namespace
 
+// Row layout of one dimension (n: right-probe input; m: its output). An
+// unsharded operator owns all rows; a shard owns [lo, hi) plus, on shards
+// > 0, a replica of the head rows [0, H) in its first local tiles.
+struct ShardDim {
+  int64_t N = 0;
+  int64_t lo = 0, hi = 0;
+  int64_t own_tiles = 0;
+  hd::RowMap rm;
+  int64_t rows_pad = 0;  // local panel rows
+  int64_t vlen() const { return hi - lo; }
+};
+
+struct hd_exchange {
+  std::unique_ptr<hd::Exchange> ex;
+};
+
 struct hd_op {
   hd_config cfg{};
   int ens = 0;
   bool f32 = false;
   size_t esz = 8;
   int64_t m = 0, n = 0;  // inner Ginibre m x n (Haar/GOE: n x n)
-  int64_t rows_pad_m = 0, rows_pad_n = 0;
+  int64_t rows_pad_m = 0, rows_pad_n = 0;  // local panel rows (= dm/dn.rows_pad)
+  ShardDim dm, dn;
+  // row sharding: shard_count > 1 => exchange after every
+  // streaming kernel; head_rows H = rows the single-CTA stages read
+  int shard_count = 1, shard_rank = 0;
+  hd::Exchange* ex = nullptr;
+  int64_t head_rows = 0, shard_cap = 0;
+  double* xch[3] = {nullptr, nullptr, nullptr};  // exchange buffers: dots / fold / other
+  int64_t xch_cap = 0;
   int64_t budget = 0;    // inner probes
   Chain R, L;            // right chain (dim n), left chain (dim m)
   Panel U, V;            // Ginibre basis stores: U (m) right probes, V (n) left probes
@@ -637,6 +662,92 @@ Src<T> draw_src(hd_op* op, int64_t len) {
 
 double bytes_of(hd_op* op, double elems) { return elems * (double)op->esz; }
 
+// ------------------------------------------------------------ row shards
+void plan_dim(ShardDim& d, int64_t N, int count, int rank, int64_t head_rows) {
+  d.N = N;
+  if (count <= 1) {
+    d.lo = 0;
+    d.hi = N;
+    d.own_tiles = ceil_div(N, kTile);
+    d.rm = hd::RowMap{};
+    d.rows_pad = d.own_tiles * kTile;
+    return;
+  }
+  hd::shard_plan(N, count, rank, head_rows, &d.lo, &d.hi);
+  d.own_tiles = ceil_div(d.hi - d.lo, kTile);
+  const int64_t htiles = (rank == 0) ? 0 : ceil_div(head_rows, kTile);
+  d.rm.tile0 = htiles;
+  d.rm.gdelta = d.lo - htiles * kTile;
+  d.rm.vbase = d.lo;
+  d.rows_pad = (htiles + d.own_tiles) * kTile;
+}
+
+// An operator with an exchange runs the sharded protocol, even a 1-shard
+// group (which exercises the NCCL path on a single GPU).
+bool sharded(const hd_op* op) { return op->ex != nullptr; }
+
+// One exchange after a streaming kernel (hd_shard.cuh): pack the group
+// partials (fixed order) + shard 0's head payload + status flags into
+// xch[which], allreduce over the shards, unpack the payload on shards > 0.
+// Returns the reduced partials, laid out as [slot][1].
+template <typename T>
+const double* shard_exchange(hd_op* op, cudaStream_t s, int which, const double* partials, int nslots, int ngroups,
+                             std::initializer_list<hd::XItem> items) {
+  hd::XArgs a;
+  a.partials = partials;
+  a.nslots = nslots;
+  a.ngroups = ngroups;
+  int64_t len = nslots + kStWords;
+  for (const hd::XItem& it : items) {
+    if (a.nitems == hd::kXMaxItems) throw HdError(HD_ERR_RUNTIME, "hd: exchange payload overflow");
+    a.item[a.nitems++] = it;
+    len += hd::xitem_len(it, op->head_rows);
+  }
+  if (len > op->xch_cap) {  // grow; xch[2] may hold the speculative dots of the previous probe
+    ck(cudaStreamSynchronize(s), "sync");
+    for (double*& b : op->xch) {
+      double* nb = dmalloc<double>(len * 2);
+      if (b) ck(cudaMemcpy(nb, b, sizeof(double) * op->xch_cap, cudaMemcpyDeviceToDevice), "keep");
+      cudaFree(b);
+      b = nb;
+    }
+    op->xch_cap = len * 2;
+  }
+  a.X = op->xch[which];
+  a.status = op->status;
+  a.lead = (op->shard_rank == 0) ? 1 : 0;
+  {
+    LaunchScope ls(op, s, "xpack", 0.0);
+    launch_k(op, hd::k_xpack<T>, dim3(1), dim3(256), 0, s, a, op->head_rows);
+  }
+  check_launch("k_xpack");
+  {
+    LaunchScope ls(op, s, "allreduce", 8.0 * len);
+    op->ex->allreduce_sum(a.X, len, s, op->shard_rank);
+  }
+  {
+    LaunchScope ls(op, s, "xunpack", 0.0);
+    launch_k(op, hd::k_xunpack<T>, dim3(1), dim3(256), 0, s, a, op->head_rows);
+  }
+  check_launch("k_xunpack");
+  return a.X;
+}
+
+hd::XItem xcol(const Panel& p, int64_t col) {
+  hd::XItem it;
+  it.pan = p.P;
+  it.K = p.K;
+  it.col = col;
+  return it;
+}
+
+hd::XItem xvec(double* v, int64_t len) {
+  hd::XItem it;
+  it.vec = v;
+  it.len = len;
+  return it;
+}
+
 // --------------------------------------------------------------- Haar
 // haar.hpp:40-67. fold = chain of the probed side, other = the opposite.
 // Passes over HBM per probe: GEMV-T over fold (k_dots), GEMV-N over fold
@@ -647,8 +758,10 @@ double bytes_of(hd_op* op, double elems) { return elems * (double)op->esz; }
 template <typename T>
 void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cudaStream_t s) {
   const int64_t n = op->n;
-  const int64_t ntiles = op->rows_pad_n / kTile;
+  const int64_t ntiles = op->dn.own_tiles;
   const bool first = (op->c.t == 0);
+  Src<T> xs = xsrc;
+  xs.vbase = op->dn.rm.vbase;
   op->c.t += 1;
   const int64_t off = op->c.t - 1;
   Chain& F = (side == HD_RIGHT) ? op->R : op->L;
@@ -669,11 +782,12 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   da.njobs = 2;
   da.n = n;
   da.ntiles = ntiles;
+  da.rm = op->dn.rm;
   da.job[0].P = static_cast<const T*>(F.pan.P);
   da.job[0].K = F.pan.K;
   da.job[0].ncols = (int)F.pan.count;
   da.job[0].pend = F.pend;
-  da.job[0].rhs = xsrc;
+  da.job[0].rhs = xs;
   da.job[0].check_finite = 1;
   da.job[1].P = static_cast<const T*>(O.pan.P);
   da.job[1].K = O.pan.K;
@@ -695,6 +809,11 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   SmallArgs sa;
   sa.partials = op->partials;
   sa.nblk = grid;
+  if (sharded(op)) {  // the new mix column's head rows and its pivot draw come from shard 0
+    sa.partials = shard_exchange<T>(op, s, 0, op->partials, da.nslots, grid,
+                                    {xcol(O.pan, O.pan.count), xvec(op->scal + kScPivotG, 1)});
+    sa.nblk = 1;
+  }
   sa.scal = op->scal;
   sa.status = op->status;
   sa.chA = F.dev;
@@ -723,7 +842,7 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   sa.trace = op->trace;
   sa.mix_from_spec = use_spec ? 1 : 0;
   if (use_spec) {
-    sa.spec_parts = op->partsO;
+    sa.spec_parts = sharded(op) ? op->xch[2] : op->partsO;
     sa.spec_nblk = spec_nblk;
     sa.spec_slot0 = spec_slot0;
     sa.spec_count = spec_count;
@@ -748,10 +867,11 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   fa.beta = op->beta1;
   fa.n = n;
   fa.ntiles = ntiles;
+  fa.rm = op->dn.rm;
   fa.D = F.dev.Drow;
   fa.Dtail = F.dev.Dtail;
   fa.Dlen = F.dev.Dlen;
-  fa.x = xsrc;
+  fa.x = xs;
   fa.Pw = static_cast<T*>(F.pan.P);
   fa.newj = F.pan.count;
   fa.off = off;
@@ -762,6 +882,11 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
 
   sa.partials = op->partsF;
   sa.nblk = gridF;
+  if (sharded(op)) {  // the new fold column's head rows and p[0..off] come from shard 0
+    sa.partials = shard_exchange<T>(op, s, 1, op->partsF, fa.nslots, gridF,
+                                    {xcol(F.pan, F.pan.count), xvec(op->head, off + 1)});
+    sa.nblk = 1;
+  }
   sa.fold_slot_ss = fa.slot_ss;
   sa.kA = (int)F.pan.count;
   sa.kB = (int)O.pan.count;
@@ -788,6 +913,7 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   oa.beta = op->beta1;
   oa.n = n;
   oa.ntiles = ntiles;
+  oa.rm = op->dn.rm;
   oa.D = O.dev.Drow;
   oa.Dtail = O.dev.Dtail;
   oa.Dlen = O.dev.Dlen;
@@ -811,7 +937,11 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   }
   double eb = (double)n * (O.pan.count + 1);
   if (epi.kind == kEpiTanhMix) eb += (double)n * ((epi.xprev ? 1 : 0) + (epi.y ? 1 : 0));
-  const int gridO = launch_apply<T, kApplyOther>(op, s, oa, false, bytes_of(op, eb), "other");
+  int gridO = launch_apply<T, kApplyOther>(op, s, oa, false, bytes_of(op, eb), "other");
+  if (sharded(op)) {  // speculative dots and ||y||^2 summed over the shards (kept in xch[2])
+    shard_exchange<T>(op, s, 2, op->partsO, oa.nslots, gridO, {});
+    gridO = 1;
+  }
   op->last_other_grid = gridO;
   op->last_other_slot_ss = oa.slot_ss;
   if (next_ok) {
@@ -837,8 +967,12 @@ void enqueue_ginibre(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi,
   Panel& Sopp = right ? op->V : op->U;    // opposite-side store (input dim)
   const int64_t nin = right ? op->n : op->m;
   const int64_t nout = right ? op->m : op->n;
-  const int64_t tin = (right ? op->rows_pad_n : op->rows_pad_m) / kTile;
-  const int64_t tout = (right ? op->rows_pad_m : op->rows_pad_n) / kTile;
+  const ShardDim& din = right ? op->dn : op->dm;
+  const ShardDim& dout = right ? op->dm : op->dn;
+  const int64_t tin = din.own_tiles;
+  const int64_t tout = dout.own_tiles;
+  Src<T> xs = xsrc;
+  xs.vbase = din.rm.vbase;
   int64_t& cnt = right ? op->c.r : op->c.l;
   const int64_t opp_cnt = right ? op->c.l : op->c.r;
   cnt += 1;
@@ -855,22 +989,27 @@ void enqueue_ginibre(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi,
   da.njobs = 2;
   da.n = nin;
   da.ntiles = tin;
+  da.rm = din.rm;
   da.job[0].P = static_cast<const T*>(F.pan.P);
   da.job[0].K = F.pan.K;
   da.job[0].ncols = (int)F.pan.count;
   da.job[0].pend = F.pend;
-  da.job[0].rhs = xsrc;
+  da.job[0].rhs = xs;
   da.job[0].check_finite = 1;
   da.job[1].P = static_cast<const T*>(Sopp.P);
   da.job[1].K = Sopp.K;
   da.job[1].ncols = (int)Sopp.count;
-  da.job[1].rhs = xsrc;
+  da.job[1].rhs = xs;
   const double b1 = bytes_of(op, (double)nin * (F.pan.count + Sopp.count + (F.pend >= 0) + 1));
   int grid = launch_dots<T>(op, s, da, b1);
 
   SmallArgs sa;
   sa.partials = op->partials;
   sa.nblk = grid;
+  if (sharded(op)) {
+    sa.partials = shard_exchange<T>(op, s, 0, op->partials, da.nslots, grid, {});
+    sa.nblk = 1;
+  }
   sa.scal = op->scal;
   sa.status = op->status;
   sa.chA = F.dev;
@@ -913,10 +1052,11 @@ void enqueue_ginibre(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi,
   fa.beta = op->beta1;
   fa.n = nin;
   fa.ntiles = tin;
+  fa.rm = din.rm;
   fa.D = F.dev.Drow;
   fa.Dtail = F.dev.Dtail;
   fa.Dlen = F.dev.Dlen;
-  fa.x = xsrc;
+  fa.x = xs;
   fa.Pw = static_cast<T*>(F.pan.P);
   fa.newj = F.pan.count;
   fa.off = off;
@@ -925,6 +1065,11 @@ void enqueue_ginibre(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi,
   const int gridF = launch_apply<T, kApplyFold>(op, s, fa, true, bytes_of(op, (double)nin * (F.pan.count + 2)), "fold");
   sa.partials = op->partsF;
   sa.nblk = gridF;
+  if (sharded(op)) {
+    sa.partials = shard_exchange<T>(op, s, 1, op->partsF, fa.nslots, gridF,
+                                    {xcol(F.pan, F.pan.count), xvec(op->head, off + 1)});
+    sa.nblk = 1;
+  }
   sa.fold_slot_ss = fa.slot_ss;
   sa.append = append_fold ? 1 : 0;
   {
@@ -944,6 +1089,7 @@ void enqueue_ginibre(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi,
   db.njobs = 1;
   db.n = nout;
   db.ntiles = tout;
+  db.rm = dout.rm;
   db.job[0].P = static_cast<const T*>(O.pan.P);
   db.job[0].K = O.pan.K;
   db.job[0].ncols = (int)O.pan.count;
@@ -956,6 +1102,10 @@ void enqueue_ginibre(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi,
   SmallArgs sg = sa;
   sg.partials = op->partials;
   sg.nblk = grid;
+  if (sharded(op)) {
+    sg.partials = shard_exchange<T>(op, s, 0, op->partials, db.nslots, grid, {});
+    sg.nblk = 1;
+  }
   sg.chB = O.dev;
   sg.PB = O.pan.P;
   sg.kB = (int)O.pan.count;
@@ -996,6 +1146,7 @@ void enqueue_ginibre(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi,
   ga.coef_cur = op->scal + kScCoefCur;
   ga.sigma = op->cfg.sigma;
   ga.n = nout;
+  ga.rm = dout.rm;
   ga.status = op->status;
   ga.epi = epi;
   double eb = (double)nout * (O.pan.count + S.count + 2 + (g.kind == kSrcInjected ? 1 : 0));
@@ -1124,8 +1275,9 @@ void do_probe(hd_op* op, const void* x, int64_t x_len, void* y, int64_t y_len, i
   require(side == HD_RIGHT || side == HD_LEFT, "side must be 'right' or 'left'");
   const int eff_side = (op->ens == HD_GOE) ? HD_RIGHT : side;  // ensembles.hpp:118-119
   const int64_t rows = op->m, cols = op->n;
-  const int64_t want = (eff_side == HD_RIGHT) ? cols : rows;
-  const int64_t out_len = (eff_side == HD_RIGHT) ? rows : cols;
+  // this shard's rows of x and y (all rows when unsharded)
+  const int64_t want = (eff_side == HD_RIGHT) ? op->dn.vlen() : op->dm.vlen();
+  const int64_t out_len = (eff_side == HD_RIGHT) ? op->dm.vlen() : op->dn.vlen();
   require(x_len == want, "probe: input dimension mismatch");
   require(y_len == out_len, "probe: output dimension mismatch");
   const bool budget_left = remaining(op) > 0;
@@ -1137,6 +1289,14 @@ void do_probe(hd_op* op, const void* x, int64_t x_len, void* y, int64_t y_len, i
       require(host_all_finite(h.data(), x_len, op->f32), "probe: non-finite input");
     }
     throw HdError(HD_ERR_BUDGET_EXHAUSTED, budget_msg(op));
+  }
+  if (sharded(op)) {  // every pivot row must lie in the replicated head rows
+    const int64_t next = (op->ens == HD_HAAR) ? op->c.t + 1
+                         : (op->ens == HD_GOE) ? std::max(op->c.r, op->c.l) + 1
+                                               : (eff_side == HD_RIGHT ? op->c.r : op->c.l) + 1;
+    if (next > op->shard_cap)
+      throw HdError(HD_ERR_RESOURCE_CAP, "hd: sharded operator capacity of " + std::to_string(op->shard_cap) +
+                                             " probes per chain spent (hd_config.capacity)");
   }
   if (op->ens == HD_GOE) ensure_capacity(op, 1, 1);
   else ensure_capacity(op, eff_side == HD_RIGHT ? 1 : 0, eff_side == HD_LEFT ? 1 : 0);
@@ -1164,6 +1324,8 @@ void do_probe(hd_op* op, const void* x, int64_t x_len, void* y, int64_t y_len, i
   epi.step = 1;
   try {
     enqueue_probe<T>(op, eff_side, vec_src<T>(xin, nullptr), epi, s);
+    // k_ginout's status flags (Haar's last kernel already exchanged them)
+    if (sharded(op) && op->ens != HD_HAAR) shard_exchange<T>(op, s, 1, nullptr, 0, 0, {});
   } catch (...) {
     restore(op, snap);
     throw;
@@ -1323,6 +1485,7 @@ const void* final_location(hd_op* op, const hd_run_args& a) {
 template <typename T>
 void do_run_enqueue(hd_op* op, const hd_run_args& a) {
   cudaStream_t s = op->stream;
+  require(!sharded(op), "hd_run: row-sharded operators are driven through hd_probe");
   require(!op->run_pending, "hd_run: the previous hd_run_async was not waited for");
   require(a.iterations >= 0, "run_dynamics: negative iteration count");
   require(a.update >= 0 && a.update <= 2, "run_dynamics: unknown update map");
@@ -1477,6 +1640,7 @@ void do_run(hd_op* op, const hd_run_args& a) {
 template <typename T>
 void do_run_callback(hd_op* op, int64_t T_, int32_t depth, const void* const* initial, hd_side_fn side_of,
                      hd_update_fn update, void* user, void* final_out) {
+  require(!sharded(op), "hd_run_callback: row-sharded operators are driven through hd_probe");
   require(T_ >= 0, "run_dynamics: negative iteration count");
   require(depth >= 0, "run_dynamics: negative history depth");
   require(initial != nullptr, "run_dynamics: initial history must hold d + 1 vectors");
@@ -1546,6 +1710,10 @@ void do_run_callback(hd_op* op, int64_t T_, int32_t depth, const void* const* in
     g_err = e.what();                     \
     return e.code;                        \
   }                                       \
+  catch (const std::invalid_argument& e) { \
+    g_err = e.what();                     \
+    return HD_ERR_INVALID_ARGUMENT;       \
+  }                                       \
   catch (const std::exception& e) {       \
     g_err = e.what();                     \
     return HD_ERR_RUNTIME;                \
@@ -1590,9 +1758,18 @@ int hd_create(const hd_config* cfg, hd_op** out) {
   op->esz = op->f32 ? 4 : 8;
   op->m = m;
   op->n = n;
-  op->rows_pad_m = ceil_div(m, kTile) * kTile;
-  op->rows_pad_n = ceil_div(n, kTile) * kTile;
   op->budget = (c.ensemble == HD_HAAR) ? n : std::min(m, n);
+  if (c.shard_count > 1)
+    require(c.exchange != nullptr, "hd_create: a sharded operator needs an exchange (hd_exchange_create_*)");
+  if (c.exchange != nullptr) {
+    require(c.shard_count >= 1, "hd_create: shard_count must be >= 1 with an exchange");
+    require(c.shard_rank >= 0 && c.shard_rank < c.shard_count, "hd_create: shard_rank out of range");
+    require(c.exchange->ex->size() == c.shard_count, "hd_create: exchange size differs from shard_count");
+    require(c.capacity >= 1, "hd_create: a sharded operator needs capacity (max probes)");
+    op->shard_count = c.shard_count;
+    op->shard_rank = c.shard_rank;
+    op->ex = c.exchange->ex.get();
+  }
   if (const char* e = std::getenv("HD_NO_PDL")) op->pdl = !(e[0] == '1');
   if (const char* e = std::getenv("HD_TRACE")) {
     if (e[0] == '1') {
@@ -1612,6 +1789,14 @@ int hd_create(const hd_config* cfg, hd_op** out) {
   }
   K = std::max<int64_t>(K, 1);
   const int64_t Kside = (c.ensemble == HD_GOE) ? std::max<int64_t>(1, (K + 1) / 2) : K;
+  if (sharded(op.get())) {
+    op->shard_cap = Kside;
+    op->head_rows = ceil_div(Kside + 1, kTile) * kTile;
+  }
+  plan_dim(op->dn, n, op->shard_count, op->shard_rank, op->head_rows);
+  plan_dim(op->dm, m, op->shard_count, op->shard_rank, op->head_rows);
+  op->rows_pad_n = op->dn.rows_pad;
+  op->rows_pad_m = op->dm.rows_pad;
   alloc_chain(op.get(), op->R, op->rows_pad_n, Kside);
   alloc_chain(op.get(), op->L, op->rows_pad_m, Kside);
   if (c.ensemble != HD_HAAR) {
@@ -1665,6 +1850,7 @@ int hd_destroy(hd_op* op) {
     cudaFree(p);
   cudaFree(op->status);
   cudaFree(op->seed_dev);
+  for (double* b : op->xch) cudaFree(b);
   cudaFree(op->xbuf);
   for (auto b : op->ybuf) cudaFree(b);
   cudaFree(op->gtmp);
@@ -1787,6 +1973,66 @@ int hd_wait(hd_op* op) {
     do_run_complete<float>(op);
   else
     do_run_complete<double>(op);
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_exchange_create_local(int32_t nshards, hd_exchange** out) {
+  HD_TRY
+  require(out != nullptr && nshards >= 1, "hd_exchange_create_local: need nshards >= 1");
+  *out = new hd_exchange{std::make_unique<hd::LocalExchange>(nshards)};
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_exchange_nccl_id(void* id_out) {
+  HD_TRY
+  require(id_out != nullptr, "hd_exchange_nccl_id: null argument");
+  try {
+    hd::NcclExchange::unique_id(id_out);
+  } catch (const std::runtime_error& e) {
+    throw HdError(HD_ERR_NCCL, e.what());
+  }
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_exchange_create_nccl(const void* id, int32_t nranks, int32_t rank, int32_t device, hd_exchange** out) {
+  HD_TRY
+  require(id && out && nranks >= 1 && rank >= 0 && rank < nranks, "hd_exchange_create_nccl: bad arguments");
+  try {
+    *out = new hd_exchange{std::make_unique<hd::NcclExchange>(id, nranks, rank, device)};
+  } catch (const std::runtime_error& e) {
+    throw HdError(HD_ERR_NCCL, e.what());
+  }
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_exchange_destroy(hd_exchange* ex) {
+  delete ex;
+  return HD_OK;
+}
+
+int hd_shard_plan(int64_t N, int32_t count, int32_t rank, int64_t head_rows, int64_t* begin, int64_t* end) {
+  HD_TRY
+  require(begin && end, "hd_shard_plan: null argument");
+  try {
+    hd::shard_plan(N, count, rank, head_rows, begin, end);
+  } catch (const std::invalid_argument& e) {
+    throw HdError(HD_ERR_INVALID_ARGUMENT, e.what());
+  }
+  return HD_OK;
+  HD_CATCH
+}
+
+int hd_shard_range(const hd_op* op, int32_t dim, int64_t* begin, int64_t* end) {
+  HD_TRY
+  require(op && begin && end, "hd_shard_range: null argument");
+  require(dim == 0 || dim == 1, "hd_shard_range: dim must be 0 (cols, n) or 1 (rows, m)");
+  const ShardDim& d = dim == 0 ? op->dn : op->dm;
+  *begin = d.lo;
+  *end = d.hi;
   return HD_OK;
   HD_CATCH
 }

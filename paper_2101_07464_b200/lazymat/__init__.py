@@ -35,7 +35,8 @@ from .._native import BudgetExhausted, ResourceCapExceeded
 
 __all__ = [
     "BudgetExhausted", "GinibreOperator", "HaarOperator", "GOEOperator", "Reflector", "ResourceCapExceeded",
-    "RandomSource", "SubsampledHaarOperator", "USVOperator", "derive_seed", "ista_curves", "make_reflector", "run_trials", "amp_sparse_regression", "spiked_power",
+    "RandomSource", "SubsampledHaarOperator", "USVOperator", "derive_seed", "Exchange", "shard_plan",
+    "share_nccl_id", "nccl_exchange", "ista_curves", "make_reflector", "run_trials", "amp_sparse_regression", "spiked_power",
     "sample_dense_haar", "ista_trial", "spectral_trial", "power_iteration", "restarted_krylov", "soft_threshold",
     "spectral_summary", "two_sample_ks",
 ]
@@ -99,12 +100,77 @@ def _is_torch_cuda(x) -> bool:
     return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
 
 
+class Exchange:
+    """The exchange of a row-sharded operator group (hd_exchange_*).
+
+    ``Exchange.local(k)``: k virtual shards in this process, each driven from
+    its own host thread (tests, one GPU). ``Exchange.nccl(uid, world, rank,
+    device)``: one rank per GPU over NCCL; ``Exchange.nccl_id()`` makes the
+    128-byte id on one rank (share it, e.g. with torch.distributed)."""
+
+    def __init__(self, handle: int, size: int):
+        self._h, self.size = handle, size
+
+    @classmethod
+    def local(cls, nshards: int) -> "Exchange":
+        h = C.c_void_p()
+        N.check(N.lib().hd_exchange_create_local(int(nshards), C.byref(h)))
+        return cls(h.value, int(nshards))
+
+    @staticmethod
+    def nccl_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        N.check(N.lib().hd_exchange_nccl_id(buf))
+        return buf.raw
+
+    @classmethod
+    def nccl(cls, uid: bytes, world: int, rank: int, device: int = 0) -> "Exchange":
+        if len(uid) != 128:
+            raise ValueError("Exchange.nccl: uid must be the 128-byte NCCL id")
+        h = C.c_void_p()
+        N.check(N.lib().hd_exchange_create_nccl(C.c_char_p(uid), int(world), int(rank), int(device), C.byref(h)))
+        return cls(h.value, int(world))
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h and N is not None and N._lib is not None:
+            N._lib.hd_exchange_destroy(h)
+
+
+def share_nccl_id(group=None) -> bytes:
+    """Rank 0 of the torch.distributed group makes the NCCL id; every rank
+    receives it (any backend, gloo included)."""
+    import torch.distributed as dist
+
+    obj = [Exchange.nccl_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
+
+
+def nccl_exchange(group=None, device: int = None) -> Exchange:
+    """The NCCL exchange of a row-sharded operator spanning the ranks of a
+    torch.distributed group (one rank per GPU, launched with torchrun)."""
+    import torch
+    import torch.distributed as dist
+
+    uid = share_nccl_id(group)
+    dev = torch.cuda.current_device() if device is None else int(device)
+    return Exchange.nccl(uid, dist.get_world_size(group), dist.get_rank(group), dev)
+
+
+def shard_plan(N_rows: int, count: int, rank: int, head_rows: int = 0):
+    """Rows [begin, end) that shard `rank` of `count` owns (hd_shard_plan)."""
+    b, e = C.c_int64(), C.c_int64()
+    N.check(N.lib().hd_shard_plan(int(N_rows), int(count), int(rank), int(head_rows), C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
 class _Operator:
     _ensemble = -1
 
     def __init__(self, m: int, n: int, sigma: float, seed: int, *, dtype: str = "f64", draws: str = "philox",
                  capacity: int = 0, stream: int = 0, skip_reflector: bool = False, sign_rule: str = "stable",
-                 device: int = 0):
+                 device: int = 0, shard: tuple = None, exchange: "Exchange" = None):
         cfg = N.hd_config()
         cfg.ensemble = self._ensemble
         cfg.dtype = {"f64": N.HD_F64, "f32": N.HD_F32}[dtype]
@@ -119,12 +185,27 @@ class _Operator:
         cfg.skip_reflector = int(bool(skip_reflector))
         cfg.sign_rule = N.SIGN_RULES[sign_rule]
         cfg.device = int(device)
+        if shard is not None:  # (rank, count): this handle is one row shard of the operator
+            cfg.shard_rank, cfg.shard_count = int(shard[0]), int(shard[1])
+            cfg.exchange = exchange._h if exchange is not None else None
         h = C.c_void_p()
         N.check(N.lib().hd_create(C.byref(cfg), C.byref(h)))
         self._h = h
+        self._exchange = exchange  # keep the group's exchange alive
         self._np_dtype = np.float64 if dtype == "f64" else np.float32
         self.dtype = dtype
         self.device = int(device)
+        self._ranges = [self._range(0), self._range(1)]
+
+    def _range(self, dim: int):
+        b, e = C.c_int64(), C.c_int64()
+        N.check(N.lib().hd_shard_range(self._h, dim, C.byref(b), C.byref(e)))
+        return b.value, e.value
+
+    def shard_range(self, dim: str = "cols"):
+        """Global rows [begin, end) of x (dim 'cols', the right-probe input) or
+        of y (dim 'rows') that this handle owns; the whole range when unsharded."""
+        return self._ranges[0 if dim == "cols" else 1]
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -164,8 +245,9 @@ class _Operator:
         N.check(N.lib().hd_chain_sizes(self._h, C.byref(r), C.byref(l)))
         return r.value, l.value
 
-    def _out_len(self, side: int) -> int:
-        return self.rows if side == N.HD_RIGHT else self.cols
+    def _out_len(self, side: int) -> int:  # this shard's rows of the output
+        b, e = self._ranges[1] if side == N.HD_RIGHT else self._ranges[0]
+        return e - b
 
     def probe(self, x, side: str = "right"):
         """Q @ x ('right') or Q.T @ x ('left'), revealing only the randomness

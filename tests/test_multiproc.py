@@ -55,3 +55,49 @@ def test_two_rank_trial_sharding_and_timing():
         assert len(set(seeds)) == world  # independent trials
         assert shards == [(0, 512), (512, 1024)]
         assert val == pytest.approx(2 * 1000 * 55 * 3 / 0.015)
+
+
+# ------------------------------------------------ row-sharded operators (e1)
+def _shard_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2101_07464_b200 import lazymat as lm
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        plans = {}
+        for N, head in [(10 ** 8, 768), (2 * 10 ** 7, 512), (3001, 256), (1800, 256)]:
+            got = [None] * world
+            dist.all_gather_object(got, lm.shard_plan(N, world, rank, head))
+            plans[N] = (head, got)
+        ids = [None] * world
+        dist.all_gather_object(ids, lm.share_nccl_id())
+        q.put((rank, plans, ids))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_shard_plan_and_nccl_id():
+    # host logic of the n-sharded operator: every rank derives the same
+    # tile-aligned row slabs (disjoint, covering [0, N), shard 0 holding the
+    # head rows) and the same NCCL id from rank 0
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (_, plans0, ids0), (_, plans1, ids1) = res
+    assert plans0 == plans1
+    for N, (head, ranges) in plans0.items():
+        assert ranges[0][0] == 0 and ranges[-1][1] == N and ranges[0][1] >= head
+        for (a, b), (c, d) in zip(ranges, ranges[1:]):
+            assert b == c and a < b and b % 256 == 0
+    assert ids0[0] == ids0[1] == ids1[0] and len(ids0[0]) == 128
