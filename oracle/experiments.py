@@ -260,3 +260,80 @@ def spectral_summary(n=256, alpha=2.0, trials=1, seed=1, backend="hd", solver="p
     rhos = [t["rho"] for t in tr]
     return {"rho_mean": mean_of(rhos), "rho_stderr": stderr_of_mean(rhos),
             "lambda_max_mean": mean_of([t["lambda_max"] for t in tr]), "trials": tr}
+
+
+# ----------------------------------------------------- verify.hpp / verify.cpp
+class USV:
+    """USVOperator (ensembles.hpp:133-180) over two oracle Haar operators."""
+
+    def __init__(self, u, v, sv):
+        self.u, self.v, self.sv = u, v, np.asarray(sv, dtype=np.float64)
+        self.rows, self.cols = u.rows, v.cols
+
+    def probe(self, x, side="right"):
+        k = self.sv.size
+        if side == "right":
+            w = np.zeros(self.rows)
+            w[:k] = self.sv * self.v.probe(x, "right")[:k]
+            return self.u.probe(w, "right")
+        w = np.zeros(self.cols)
+        w[:k] = self.sv * self.u.probe(x, "left")[:k]
+        return self.v.probe(w, "left")
+
+
+def consistency_suite(op, m, n, src, rel_tol=1e-10, isometric=False):
+    """verify.hpp:100-160 restated; returns [(name, passed)]."""
+    out = []
+    nrm = np.linalg.norm
+
+    def scale(a, b):
+        return a + b if a + b > 0 else 1.0
+
+    x = src.normal_vector(n)
+    y1, y2 = op.probe(x, "right"), op.probe(x, "right")
+    out.append(("repeat-probe-right", nrm(y1 - y2) / scale(nrm(y1), nrm(y2)) <= rel_tol))
+    if isometric:
+        out.append(("isometry", abs(nrm(y1) - nrm(x)) / nrm(x) <= rel_tol))
+    z = src.normal_vector(m)
+    y1, y2 = op.probe(z, "left"), op.probe(z, "left")
+    out.append(("repeat-probe-left", nrm(y1 - y2) / scale(nrm(y1), nrm(y2)) <= rel_tol))
+    x1, x2 = src.normal_vector(n), src.normal_vector(n)
+    a, b = src.normal_vector(1)[0], src.normal_vector(1)[0]
+    y1, y2 = op.probe(x1, "right"), op.probe(x2, "right")
+    yc = op.probe(a * x1 + b * x2, "right")
+    pred = a * y1 + b * y2
+    out.append(("span-linearity", nrm(yc - pred) / scale(nrm(pred), nrm(yc)) <= rel_tol))
+    for rnd in range(2):
+        x, z = src.normal_vector(n), src.normal_vector(m)
+        qx, qtz = op.probe(x, "right"), op.probe(z, "left")
+        err = abs(float(z @ qx) - float(qtz @ x)) / scale(nrm(z) * nrm(qx), nrm(qtz) * nrm(x))
+        out.append((f"adjoint-bilinear-{rnd + 1}", err <= rel_tol))
+    return out
+
+
+def all_operator_contracts(m, n, seed, mutation="none"):
+    """verify.cpp:47-121 over the oracle operators; returns [(name, passed)]."""
+    kw = {"skip_reflector": mutation == "skip_reflector",
+          "sign_rule": "zero_when_negative" if mutation == "sign_convention" else "stable"}
+    res = []
+    for idx, (name, rows, cols, iso) in enumerate([("ginibre", m, n, False), ("haar", n, n, True),
+                                                   ("goe", n, n, False), ("usv", m, n, False),
+                                                   ("subsampled-haar", n, m, False)]):
+        s = orc.derive_seed(seed, 16 + idx)
+        if name == "ginibre":
+            op = orc.Operator("ginibre", m=rows, n=cols, sigma=1.0, seed=s, **kw)
+        elif name == "haar":
+            op = orc.Operator("haar", n=cols, seed=s, **kw)
+        elif name == "goe":
+            op = orc.Operator("goe", n=cols, sigma=1.0, seed=s, **kw)
+        elif name == "usv":
+            sv_src = orc.RandomSource(orc.derive_seed(s, 3))
+            sv = [0.5 + sv_src.uniform() for _ in range(min(rows, cols))]
+            op = USV(orc.Operator("haar", n=rows, seed=orc.derive_seed(s, 1), **kw),
+                     orc.Operator("haar", n=cols, seed=orc.derive_seed(s, 2), **kw), sv)
+        else:
+            op = Subsampled(orc.Operator("haar", n=cols, seed=orc.derive_seed(s, 1), **kw), rows)
+        for cname, ok in consistency_suite(op, rows, cols, orc.RandomSource(orc.derive_seed(seed, 32 + idx), 1),
+                                           1e-10, iso):
+            res.append((f"{name}/{cname}", ok))
+    return res

@@ -674,6 +674,7 @@ class SubsampledHaarOperator:
 
 # Application drivers and the dense direct backend (experiments.cpp,
 # eigensolve.hpp, ensembles.hpp:40-91, stats.cpp) on the device operators.
+from . import verify  # noqa: E402,F401  (verification harness, lazymat.verify)
 from .experiments import (  # noqa: E402
     ista_curves, ista_trial, power_iteration, restarted_krylov, sample_dense_haar, soft_threshold,
     spectral_summary, spectral_trial, two_sample_ks,

@@ -197,19 +197,27 @@ def ista_trial(n: int = 256, m_ratio: float = 0.5, iterations: int = 50, lambda_
     depth 1 (experiments.cpp:88-104), whose first probe is A 0."""
     from . import GinibreOperator, RandomSource, derive_seed
 
-    torch = _torch()
+    _torch()
     b = _backend(backend)
     _ista_validate(n, m_ratio, iterations, lambda_, tau, rho, sigma_s, sigma_w, 1)
     m = int(math.floor(n * m_ratio))
     if b == 0 and 2 * iterations + 1 > min(m, n):
         raise BudgetExhausted("ista: data generation plus 2T probes exceed the min(m, n) budget")
     base = derive_seed(seed, 2 * trial + b)
-    data = RandomSource(base, 1)
     sigma = 1.0 / math.sqrt(m)
     if b == 0:
         op = GinibreOperator(m, n, sigma, base, draws=draws, capacity=iterations + 1)
     else:
         op = _Dense(_dense_ginibre(m, n, sigma, RandomSource(base, 0)))
+    return ista_on(op, RandomSource(base, 1), iterations, lambda_, tau, rho, sigma_s, sigma_w)
+
+
+def ista_on(op, data, iterations: int, lambda_: float = 2.0, tau: float = 0.3, rho: float = 0.2,
+            sigma_s: float = 2.0, sigma_w: float = 0.1):
+    """ista_trial_on (experiments.cpp:73-111) over a caller-supplied design
+    operator (lazy or dense) and data source: (mse[T] numpy, x_T device)."""
+    torch = _torch()
+    m, n = op.rows, op.cols
     beta = torch.from_numpy(data.bernoulli_gaussian(n, rho, sigma_s)).cuda()
     noise = torch.from_numpy(data.normal_vector(m)).cuda() * sigma_w
     y_obs = op.probe(beta, "right") + noise

@@ -124,3 +124,13 @@ def test_oracle_spectral_matches_dense_diagonalisation():
     for backend in ("hd", "direct"):  # test_experiments.cpp:247-261
         r = ex.spectral_trial(48, 2.0, 1, 0, backend, "krylov")
         assert r["lambda_max"] > 0 and 0.2 < r["rho"] <= 1.0
+
+
+def test_oracle_operator_contracts_and_mutations():
+    # verify.cpp:87-121 restated over the oracle operators: clean operators
+    # satisfy every algebraic contract; the planted construction defects break some
+    ok = ex.all_operator_contracts(96, 64, ex.orc.derive_seed(9, 0))
+    assert len(ok) == 26 and all(p for _, p in ok)
+    for mut in ("skip_reflector", "sign_convention"):
+        res = ex.all_operator_contracts(96, 64, ex.orc.derive_seed(9, 0), mut)
+        assert not all(p for _, p in res), mut
