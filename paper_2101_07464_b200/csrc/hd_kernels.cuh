@@ -439,6 +439,15 @@ struct ApplyArgs {
   // speculative dots with the next draw (kind kSrcNone = off; OTHER only)
   Src<T> spec;
   int slot_spec = 0;  // [ncols]
+  // ... and, when the next probe hits the same side, the next mix column
+  // itself: the draw written to gcol[:, gj], its tail norm^2 (slot_gss =
+  // slot_spec + ncols) and its pivot value (gpivot at global row gpivot_row),
+  // so the next k_dots need not regenerate it
+  T* gcol = nullptr;
+  int64_t gK = 0, gj = 0;
+  double* gpivot = nullptr;
+  int64_t gpivot_row = -1;
+  int slot_gss = -1;
   int slot_ss = 0;    // fold: ||p[off:]||^2; other: ||y||^2
   Flush out;
   int nslots = 0;
@@ -497,16 +506,22 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
     t1 = t0;
   }
 
-  double ss = 0.0;
+  double ss = 0.0, gss = 0.0;
   bool bad = false;
   uint32_t it = 0;
   for (int64_t tile = t0; tile < t1; ++tile) {
     double2 g[4], r[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int64_t i = (tile + a.rm.tile0) * kTile + a.rm.gdelta + 2 * (lane + 32 * q);
+      const int64_t li = (tile + a.rm.tile0) * kTile + 2 * (lane + 32 * q);
+      const int64_t i = li + a.rm.gdelta;
       g[q] = spec ? src_pair(a.spec, i, a.n) : make_double2(0.0, 0.0);
       r[q] = make_double2(0.0, 0.0);
+      if (a.gcol) {  // the next probe's mix column (masked draw), its norm and pivot
+        st_pair(a.gcol + paddr(li, a.gj, a.gK), g[q].x, g[q].y);
+        gss += g[q].x * g[q].x + g[q].y * g[q].y;
+        if (i == a.gpivot_row || i + 1 == a.gpivot_row) *a.gpivot = (i == a.gpivot_row) ? g[q].x : g[q].y;
+      }
     }
     for (int c = 0; c < nch; ++c, ++it) {
       const int s = it % kRing;
@@ -586,6 +601,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
   }
   ss = warp_sum(ss);
   if (lane == 0) acc[a.slot_ss] += ss;
+  if (a.slot_gss >= 0) {
+    gss = warp_sum(gss);
+    if (lane == 0) acc[a.slot_gss] += gss;
+  }
   if constexpr (MODE == kApplyOther) {
     if (bad) {
       atomicMin(a.status + kStBadStep, a.epi.step);
@@ -724,6 +743,7 @@ struct SmallArgs {
   int mix_from_spec = 0;   // Haar mix Gram dots from the speculative pass
   const double* spec_parts = nullptr;  // [slot][spec_nblk] of the previous k_apply(OTHER)
   int spec_nblk = 0, spec_slot0 = 0, spec_count = 0;
+  int spec_ss = 0;         // ... and the mix draw's tail norm^2 (spec row kB)
   int fold_slot_ss = 0;
   int stageA = 0, stageB = 0;  // stage T_A / T_B in shared memory (host: fits the budget)
   int nslots_in = 0;           // slot rows of `partials` staged by the stage
@@ -946,7 +966,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_dots(const __grid_const
   const TView tvB = (HAAR && a.stageB) ? st_stage_T(a.chB, a.kB, tsB, tid, kSmallThreads) : TView{a.chB.Tm, a.chB.K};
   HD_CLK(a, 6);
   st_stage(a.partials, (int64_t)a.nslots_in * a.nblk, ps, tid, kSmallThreads);
-  if (spec) st_stage(a.spec_parts + (size_t)a.spec_slot0 * a.spec_nblk, (int64_t)a.kB * a.spec_nblk, ss, tid, kSmallThreads);
+  if (spec)
+    st_stage(a.spec_parts + (size_t)a.spec_slot0 * a.spec_nblk, (int64_t)(a.kB + a.spec_ss) * a.spec_nblk, ss, tid,
+             kSmallThreads);
   #pragma unroll 1
   for (int j = tid; j < a.kA; j += kSmallThreads) cp_async8(sgA + j, a.chA.sig + j);
   if (HAAR) {
@@ -987,6 +1009,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_dots(const __grid_const
   if (tid == 0) {
     st_reduce(ps, a.nblk, a.slotA_ss, 1, m.sc + 0, 0, 1);
     if (a.slotB_ss >= 0) st_reduce(ps, a.nblk, a.slotB_ss, 1, m.sc + 1, 0, 1);
+    else if (spec && a.spec_ss) st_reduce(ss, a.spec_nblk, a.kB, 1, m.sc + 1, 0, 1);
   }
   __syncthreads();
   HD_CLK(a, 11);

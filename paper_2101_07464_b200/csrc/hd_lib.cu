@@ -113,6 +113,7 @@ struct Counters {
   uint32_t spec_probe = 0;
   int64_t spec_inj = -1;
   int spec_count = 0, spec_nblk = 0, spec_slot0 = 0;
+  int spec_col = 0;  // ... and wrote the next mix column, its norm^2 and pivot
 };
 
 }  // namespace
@@ -275,6 +276,7 @@ void grow_panel(hd_op* op, Panel& p, int64_t rows_pad, int64_t Knew) {
 
 void grow_chain(hd_op* op, Chain& ch, int64_t rows_pad, int64_t Knew) {
   const int64_t Kold = ch.pan.K;
+  op->c.spec_col = 0;  // a mix column pre-written beyond `count` is not carried over
   grow_panel(op, ch.pan, rows_pad, Knew);
   auto grow_vec = [&](double*& v) {
     double* nv = dmalloc<double>(Knew);
@@ -518,6 +520,7 @@ int launch_apply(hd_op* op, cudaStream_t s, ApplyArgs<T>& a, bool fold_buffer, d
   if (a.spec.kind != kSrcNone) {
     a.slot_spec = slot;
     slot += a.ncols + (MODE == kApplyFold ? 1 : 0);
+    if (a.gcol) a.slot_gss = slot++;  // = slot_spec + ncols (k_small_dots reads it as spec row kB)
   }
   a.slot_ss = slot++;
   a.nslots = slot;
@@ -545,7 +548,7 @@ size_t small_smem_bytes(SmallArgs& a, int which, size_t esz) {
   size_t nr = 0;
   if (which == 0) {
     bytes += sizeof(double) * (size_t)a.nslots_in * a.nblk;
-    if (a.is_haar && a.mix_from_spec) bytes += sizeof(double) * (size_t)a.kB * a.spec_nblk;
+    if (a.is_haar && a.mix_from_spec) bytes += sizeof(double) * (size_t)(a.kB + a.spec_ss) * a.spec_nblk;
     needA = true;
     needB = a.is_haar != 0;
   } else if (which == 1) {
@@ -778,8 +781,11 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
 
   // K1: a = P_F^T x (+ pending Gram), g[off:] -> new column of O, ||g_tail||^2,
   // and (no speculation) P_O^T g[off:] (+ pending Gram of O)
+  // with the speculation the previous k_apply(OTHER) also wrote this probe's
+  // mix column, its tail norm^2 and pivot: k_dots streams the fold chain only
+  const bool mix_written = use_spec && op->c.spec_col;
   DotArgs<T> da;
-  da.njobs = 2;
+  da.njobs = mix_written ? 1 : 2;
   da.n = n;
   da.ntiles = ntiles;
   da.rm = op->dn.rm;
@@ -802,8 +808,10 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   da.trace = op->trace;
   // predecessor = previous probe's k_apply(OTHER) (writes y / x_{t+1} only)
   da.prefetch = 1;
-  const double b1 = bytes_of(op, (double)n * (F.pan.count + da.job[1].ncols + (F.pend >= 0) + (da.job[1].pend >= 0) + 2)) +
-                    (g.kind == kSrcInjected ? 8.0 * n : 0.0);
+  const double b1 = mix_written ? bytes_of(op, (double)n * (F.pan.count + (F.pend >= 0) + 1))
+                                 : bytes_of(op, (double)n * (F.pan.count + da.job[1].ncols + (F.pend >= 0) +
+                                                             (da.job[1].pend >= 0) + 2)) +
+                                       (g.kind == kSrcInjected ? 8.0 * n : 0.0);
   const int grid = launch_dots<T>(op, s, da, b1);
 
   SmallArgs sa;
@@ -827,9 +835,10 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
   sa.slotA_dot = da.job[0].slot_dot;
   sa.slotA_pend = da.job[0].slot_pend;
   sa.slotA_ss = da.job[0].slot_sumsq;
-  sa.slotB_dot = da.job[1].slot_dot;
-  sa.slotB_pend = da.job[1].slot_pend;
-  sa.slotB_ss = da.job[1].slot_sumsq;
+  sa.slotB_dot = mix_written ? 0 : da.job[1].slot_dot;
+  sa.slotB_pend = mix_written ? 0 : da.job[1].slot_pend;
+  sa.slotB_ss = mix_written ? -1 : da.job[1].slot_sumsq;
+  sa.spec_ss = mix_written ? 1 : 0;
   sa.off = off;
   sa.rule = op->cfg.sign_rule;
   sa.beta1 = op->beta1;
@@ -934,8 +943,18 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
       oa.spec.probe = op->c.probe_index;
     }
     oa.spec.mask_begin = off + 1;
+    // the next same-side probe's mix column goes to O[:, O.count] (when the
+    // panel has room); if the next probe hits the other side, that column is
+    // simply overwritten by its fold
+    if (O.pan.count < O.pan.K) {
+      oa.gcol = static_cast<T*>(O.pan.P);
+      oa.gK = O.pan.K;
+      oa.gj = O.pan.count;
+      oa.gpivot = op->scal + kScPivotG;
+      oa.gpivot_row = off + 1;
+    }
   }
-  double eb = (double)n * (O.pan.count + 1);
+  double eb = (double)n * (O.pan.count + 1 + (next_ok ? 1 : 0));
   if (epi.kind == kEpiTanhMix) eb += (double)n * ((epi.xprev ? 1 : 0) + (epi.y ? 1 : 0));
   int gridO = launch_apply<T, kApplyOther>(op, s, oa, false, bytes_of(op, eb), "other");
   if (sharded(op)) {  // speculative dots and ||y||^2 summed over the shards (kept in xch[2])
@@ -949,6 +968,7 @@ void enqueue_haar(hd_op* op, int side, const Src<T>& xsrc, const Epi<T>& epi, cu
     op->c.spec_probe = op->c.probe_index;
     op->c.spec_inj = (op->cfg.draw_mode != HD_DRAWS_PHILOX) ? op->c.inj_pos : -1;
     op->c.spec_count = (int)O.pan.count;
+    op->c.spec_col = oa.gcol ? 1 : 0;
     op->c.spec_nblk = gridO;
     op->c.spec_slot0 = oa.slot_spec;
   }
