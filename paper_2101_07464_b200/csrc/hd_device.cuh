@@ -91,9 +91,11 @@ __device__ __forceinline__ double dvalue(const Src<T>& s, int64_t i) {
   return i < s.Dlen ? s.D[i] : *s.Dtail;
 }
 
-// Values of global rows (i, i+1), i even; rows >= n read as zero.
+// The global-load half of src_pair: raw vector values of global rows
+// (i, i+1) (kSrcVec; other kinds return zeros). Issued a tile ahead by the
+// streaming kernels so the load latency overlaps the current tile.
 template <typename T>
-__device__ __forceinline__ double2 src_pair(const Src<T>& s, int64_t i, int64_t n) {
+__device__ __forceinline__ double2 src_raw(const Src<T>& s, int64_t i, int64_t n) {
   double2 v = make_double2(0.0, 0.0);
   if (s.kind == kSrcVec) {
     const T* xp = s.x + (i - s.vbase);
@@ -107,20 +109,30 @@ __device__ __forceinline__ double2 src_pair(const Src<T>& s, int64_t i, int64_t 
     } else if (i < n) {
       v.x = (double)xp[0];
     }
+  }
+  return v;
+}
+
+// Values of global rows (i, i+1), i even, given src_raw's result: vector
+// scale, fresh Philox or injected draws, the mask and D; rows >= n are zero.
+template <typename T>
+__device__ __forceinline__ double2 src_finish(const Src<T>& s, int64_t i, int64_t n, double2 v) {
+  if (s.kind == kSrcVec) {
     if (s.xscale) {
       const double sc = *s.xscale;
       v.x *= sc;
       v.y *= sc;
     }
   } else if (s.kind == kSrcPhilox) {
-    if (i < n) {
-      v = philox_normal_pair(*s.seedp, s.stream, s.probe, (uint64_t)(i >> 1));
-      if constexpr (sizeof(T) == 4) {  // fp32 path consumes fp32-rounded draws
-        v.x = (double)(float)v.x;
-        v.y = (double)(float)v.y;
-      }
-      if (i + 1 >= n) v.y = 0.0;
+    // generated unconditionally (branch-free in i, so the unrolled row pairs
+    // of a lane interleave their Box-Muller chains), zeroed beyond n
+    v = philox_normal_pair(*s.seedp, s.stream, s.probe, (uint64_t)(i >> 1));
+    if constexpr (sizeof(T) == 4) {  // fp32 path consumes fp32-rounded draws
+      v.x = (double)(float)v.x;
+      v.y = (double)(float)v.y;
     }
+    if (i >= n) v.x = 0.0;
+    if (i + 1 >= n) v.y = 0.0;
   } else if (s.kind == kSrcInjected) {
     if (i < n) v.x = s.inj[i];
     if (i + 1 < n) v.y = s.inj[i + 1];
@@ -136,6 +148,12 @@ __device__ __forceinline__ double2 src_pair(const Src<T>& s, int64_t i, int64_t 
     v.y *= dvalue(s, i + 1);
   }
   return v;
+}
+
+// Values of global rows (i, i+1), i even; rows >= n read as zero.
+template <typename T>
+__device__ __forceinline__ double2 src_pair(const Src<T>& s, int64_t i, int64_t n) {
+  return src_finish(s, i, n, src_raw(s, i, n));
 }
 
 // Load two consecutive panel entries as doubles.

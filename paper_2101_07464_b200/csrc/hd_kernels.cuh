@@ -221,22 +221,42 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_dots(const __grid_constan
   double ss0 = 0.0, ss1 = 0.0;
   bool bad = false;
   double2 x[4], pv[4];
+  // software pipeline: job 0's vector rows and pending column of the NEXT
+  // tile are loaded while the current tile is processed
+  double2 nx[4], np[4];
+  auto fetch0 = [&](int64_t tile) {
+    const DotJob<T>& J = a.job[0];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t li = (tile + a.rm.tile0) * kTile + 2 * (lane + 32 * q);
+      nx[q] = src_raw(J.rhs, li + a.rm.gdelta, a.n);
+      np[q] = (J.pend >= 0) ? ld_pair(J.P + paddr(li, J.pend, J.K)) : make_double2(0.0, 0.0);
+    }
+  };
+  if (t0 < t1) fetch0(t0);
   uint32_t it = 0;
   for (int64_t tile = t0; tile < t1; ++tile) {
+    double2 cx[4], cp[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      cx[q] = nx[q];
+      cp[q] = np[q];
+    }
+    if (tile + 1 < t1) fetch0(tile + 1);
     for (int jb = 0; jb < a.njobs; ++jb) {
       const DotJob<T>& J = a.job[jb];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int64_t li = (tile + a.rm.tile0) * kTile + 2 * (lane + 32 * q);  // local panel row
         const int64_t i = li + a.rm.gdelta;                                    // global row
-        x[q] = src_pair(J.rhs, i, a.n);
+        x[q] = (jb == 0) ? src_finish(J.rhs, i, a.n, cx[q]) : src_pair(J.rhs, i, a.n);
         const double sq = x[q].x * x[q].x + x[q].y * x[q].y;
         if (jb == 0) ss0 += sq;
         else ss1 += sq;
         if (J.check_finite) bad |= !(isfinite(x[q].x) && isfinite(x[q].y));
         if (J.pivot_out && (i == J.pivot_row || i + 1 == J.pivot_row)) *J.pivot_out = (i == J.pivot_row) ? x[q].x : x[q].y;
         if (J.wcol) st_pair(J.wcol + paddr(li, J.wj, J.wK), x[q].x, x[q].y);
-        pv[q] = (J.pend >= 0) ? ld_pair(J.P + paddr(li, J.pend, J.K)) : make_double2(0.0, 0.0);
+        pv[q] = (jb == 0) ? cp[q] : (J.pend >= 0) ? ld_pair(J.P + paddr(li, J.pend, J.K)) : make_double2(0.0, 0.0);
       }
       const int nch = (J.ncols + kCW - 1) / kCW;
       for (int c = 0; c < nch; ++c, ++it) {
@@ -508,9 +528,31 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
 
   double ss = 0.0, gss = 0.0;
   bool bad = false;
+  // software pipeline: the next tile's x (fold) or x_{t-1} (tanh mix) rows
+  double2 nv[4];
+  auto fetchv = [&](int64_t tile) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = (tile + a.rm.tile0) * kTile + a.rm.gdelta + 2 * (lane + 32 * q);
+      if constexpr (MODE == kApplyFold) {
+        nv[q] = src_raw(a.x, i, a.n);
+      } else {
+        nv[q] = make_double2(0.0, 0.0);
+        if (a.epi.kind == kEpiTanhMix && a.epi.xprev && i < a.n) {
+          const int64_t vi = i - a.rm.vbase;
+          nv[q].x = (double)a.epi.xprev[vi];
+          if (i + 1 < a.n) nv[q].y = (double)a.epi.xprev[vi + 1];
+        }
+      }
+    }
+  };
+  if (t0 < t1) fetchv(t0);
   uint32_t it = 0;
   for (int64_t tile = t0; tile < t1; ++tile) {
-    double2 g[4], r[4];
+    double2 g[4], r[4], cv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) cv[q] = nv[q];
+    if (tile + 1 < t1) fetchv(tile + 1);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int64_t li = (tile + a.rm.tile0) * kTile + 2 * (lane + 32 * q);
@@ -558,7 +600,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
       const double d0 = (i < a.Dlen) ? a.D[i] : *a.Dtail;
       const double d1 = (i + 1 < a.Dlen) ? a.D[i + 1] : *a.Dtail;
       if constexpr (MODE == kApplyFold) {
-        const double2 xv = src_pair(a.x, i, a.n);
+        const double2 xv = src_finish(a.x, i, a.n, cv[q]);
         const double p0 = (i < a.n) ? d0 * (xv.x - r[q].x) : 0.0;
         const double p1 = (i + 1 < a.n) ? d1 * (xv.y - r[q].y) : 0.0;
         const double c0 = (i >= a.off) ? p0 : 0.0, c1 = (i + 1 >= a.off) ? p1 : 0.0;
@@ -579,8 +621,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
           if (e.kind == kEpiTanhMix) {
             double2 xp = make_double2(0.0, 0.0);
             if (e.xprev) {
-              xp.x = (double)e.xprev[vi];
-              if (i + 1 < a.n) xp.y = (double)e.xprev[vi + 1];
+              xp = cv[q];  // prefetched x_{t-1} rows
               if (e.xprev_scale) {
                 xp.x *= *e.xprev_scale;
                 xp.y *= *e.xprev_scale;
