@@ -72,5 +72,28 @@ def launches(path, out):
         print(f"{k:40s} {v}")
 
 
+def traffic(full_json, out, t=91, n=1_000_000):
+    """DRAM bytes of the captured config-2 probe t vs the library's algorithmic
+    bytes for it (hd_lib.cu LaunchScope accounting, fp64):
+      k_dots   8 n (t + 1): fold chain (t-1 columns) + its pending column + x
+                            (the mix column was written by the previous OTHER)
+      FOLD     8 n (t + 1): fold chain (t-1 columns) + x + the new column
+      OTHER    8 n (t + 3): other chain (t columns) + output + next mix column
+                            + x_{t-1} (tanh mix)"""
+    alg = {"dots": 8 * n * (t + 1), "fold": 8 * n * (t + 1), "other": 8 * n * (t + 3)}
+    kind = {"k_dots": "dots", "k_apply<double, 0>": "fold", "k_apply<double, 1>": "other"}
+    res = {}
+    for d in json.load(open(full_json)):
+        name = d.get("Kernel Name", "")
+        for key, k in kind.items():
+            if key in name and "dram_bytes" in d:
+                us = float(d["gpu__time_duration.sum"]) / (1e3 if d["units"]["gpu__time_duration.sum"] == "nsecond" else 1)
+                res[k] = {"probe_t": t, "dram_bytes": d["dram_bytes"], "alg_bytes": alg[k],
+                          "ratio": d["dram_bytes"] / alg[k], "ncu_us": us,
+                          "source": f"{full_json} (ncu --set full, cold cache, serialised)"}
+    json.dump(res, open(out, "w"), indent=1)
+    print(json.dumps(res, indent=1))
+
+
 if __name__ == "__main__":
-    {"full": full, "launches": launches}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"full": full, "launches": launches, "traffic": traffic}[sys.argv[1]](sys.argv[2], sys.argv[3])
