@@ -75,6 +75,17 @@ def lib():
                                      C.c_int64, C.c_int, _dp]
         L.or_amp.argtypes = [C.c_void_p, _dp, _dp, C.c_int64, C.c_double, _dp, _dp]
         L.or_spiked_power.argtypes = [C.c_void_p, _dp, _dp, C.c_int64, C.c_double, _dp, _dp]
+        L.or_c_last_error.restype = C.c_char_p
+        L.or_c_make_reflector.argtypes = [_dp, C.c_int64, C.c_int64, _dp, C.POINTER(C.c_double), _dp,
+                                          C.POINTER(C.c_int)]
+        L.or_c_reflector_apply.argtypes = [_dp, C.c_int64, C.c_int64, _dp, C.c_int, _dp]
+        L.or_c_chain_apply.argtypes = [_dp, C.c_int64, C.c_int64, _dp, C.c_int, C.c_int, _dp]
+        L.or_c_op_new.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_double, C.c_uint64, C.c_uint64, C.c_int,
+                                  C.POINTER(C.c_void_p)]
+        L.or_c_op_free.argtypes = [C.c_void_p]
+        L.or_c_op_remaining.restype = C.c_int64
+        L.or_c_op_remaining.argtypes = [C.c_void_p]
+        L.or_c_op_probe.argtypes = [C.c_void_p, _dp, C.c_int64, C.c_int, _dp, C.c_int64]
         L.or_bench_workload.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_double, C.c_int, C.c_int,
                                         C.c_int64, C.c_uint64, C.c_int, C.c_int,
                                         C.POINTER(C.c_double), C.POINTER(C.c_double)]
@@ -228,6 +239,89 @@ class Operator:
         _check(lib().or_run_builtin(self._h, UPDATES[kind], SIDE_RULES[side_rule], T, x1, x0p, dim,
                                     int(keep), out.reshape(-1)))
         return out
+
+
+# ------------------------------------------------ complex field
+def _c_check(rc: int):
+    if rc == 0:
+        return
+    msg = lib().or_c_last_error().decode()
+    if rc == 1:
+        raise ValueError(msg)
+    if rc == 2:
+        raise BudgetExhausted(msg)
+    raise OracleError(msg)
+
+
+def _ileave(z) -> np.ndarray:
+    z = np.ascontiguousarray(np.asarray(z, dtype=np.complex128).reshape(-1))
+    return np.ascontiguousarray(z.view(np.float64))
+
+
+def _cplx(a: np.ndarray) -> np.ndarray:
+    return a.view(np.complex128).copy()
+
+
+def c_make_reflector(p, offset: int = 0):
+    """Complex make_reflector (reflect.hpp:142-153): (w, c, s, identity)."""
+    pi = _ileave(p)
+    n = pi.size // 2
+    w = np.zeros(2 * max(n - offset, 1))
+    c, ident = C.c_double(), C.c_int()
+    s = np.zeros(2)
+    _c_check(lib().or_c_make_reflector(pi, n, offset, w, C.byref(c), s, C.byref(ident)))
+    return _cplx(w)[: n - offset], c.value, complex(s[0], s[1]), bool(ident.value)
+
+
+def c_reflector_apply(p, offset: int, x, adjoint: bool = False) -> np.ndarray:
+    pi, xi = _ileave(p), _ileave(x)
+    y = np.empty_like(xi)
+    _c_check(lib().or_c_reflector_apply(pi, pi.size // 2, offset, xi, int(adjoint), y))
+    return _cplx(y)
+
+
+def c_chain_apply(ps, x, reverse: bool = False, adjoint: bool = False) -> np.ndarray:
+    """Chain of reflectors built from rows ps[k] at offsets k (reflect.hpp:193-231)."""
+    ps = np.asarray(ps, dtype=np.complex128)
+    k, n = ps.shape
+    xi = _ileave(x)
+    y = np.empty_like(xi)
+    _c_check(lib().or_c_chain_apply(_ileave(ps), k, n, xi, int(reverse), int(adjoint), y))
+    return _cplx(y)
+
+
+class COperator:
+    """GinibreOperator<complex<double>> / HaarOperator<complex<double>>."""
+
+    def __init__(self, ensemble: str, m: int = 0, n: int = 0, sigma: float = 1.0, seed: int = 1, stream: int = 0,
+                 skip_reflector: bool = False):
+        h = C.c_void_p()
+        _c_check(lib().or_c_op_new({"ginibre": 0, "haar": 1}[ensemble], m if ensemble == "ginibre" else n, n, sigma,
+                                   seed, stream, int(skip_reflector), C.byref(h)))
+        self._h, self.ensemble = h.value, ensemble
+        self.rows, self.cols = (m if ensemble == "ginibre" else n), n
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().or_c_op_free(self._h)
+            self._h = None
+
+    @property
+    def remaining_probes(self) -> int:
+        return int(lib().or_c_op_remaining(self._h))
+
+    def probe(self, x, side: str = "right") -> np.ndarray:
+        xi = _ileave(x)
+        out = self.rows if side == "right" else self.cols
+        y = np.empty(2 * out)
+        _c_check(lib().or_c_op_probe(self._h, xi, xi.size // 2, SIDES[side], y, out))
+        return _cplx(y)
+
+
+def complex_draws_for(seed: int, lengths, stream: int = 0) -> np.ndarray:
+    """The complex draw sequence (normal_complex_vector per probe) as interleaved (re, im) fp64."""
+    rs = RandomSource(seed, stream)
+    return np.concatenate([rs.normal_complex_vector(int(L)) for L in lengths]).view(np.float64).copy()
 
 
 def draws_for(seed: int, lengths, stream: int = 0) -> np.ndarray:
