@@ -40,7 +40,7 @@ typedef enum hd_status {
 
 typedef enum hd_ensemble { HD_GINIBRE = 0, HD_HAAR = 1, HD_GOE = 2 } hd_ensemble;
 typedef enum hd_side { HD_RIGHT = 0, HD_LEFT = 1 } hd_side; /* types.hpp:26 */
-typedef enum hd_dtype { HD_F64 = 0, HD_F32 = 1 } hd_dtype;
+typedef enum hd_dtype { HD_F64 = 0, HD_F32 = 1, HD_C128 = 2 /* complex<double>, interleaved (re, im) */ } hd_dtype;
 /* Gaussian draws:
  *  PHILOX    device Philox4x32-10 keyed by (seed, stream), counter (row, probe):
  *            production, generated inside the streaming kernels;

@@ -21,7 +21,7 @@ HD_ERR_NCCL = 6
 
 HD_GINIBRE, HD_HAAR, HD_GOE = 0, 1, 2
 HD_RIGHT, HD_LEFT = 0, 1
-HD_F64, HD_F32 = 0, 1
+HD_F64, HD_F32, HD_C128 = 0, 1, 2
 HD_DRAWS_PHILOX, HD_DRAWS_INJECTED, HD_DRAWS_REFERENCE = 0, 1, 2
 DRAW_MODES = {"philox": HD_DRAWS_PHILOX, "injected": HD_DRAWS_INJECTED, "reference": HD_DRAWS_REFERENCE}
 SIGN_RULES = {"stable": 0, "negative_at_zero": 1, "zero_when_negative": 2}

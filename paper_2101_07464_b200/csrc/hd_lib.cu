@@ -10,6 +10,7 @@
 //   check_probe_input        include/lazymat/operators.hpp:44-48
 #include <cuda_runtime.h>
 
+#include "hd_complex.cuh"
 #include "hd_refrng.hpp"
 #include "hd_shard.cuh"
 
@@ -134,6 +135,10 @@ struct hd_exchange {
   std::unique_ptr<hd::Exchange> ex;
 };
 
+namespace {
+struct CxState;  // complex-field operator state (hd_complex_host.inc)
+}
+
 struct hd_op {
   hd_config cfg{};
   int ens = 0;
@@ -142,6 +147,7 @@ struct hd_op {
   int64_t m = 0, n = 0;  // inner Ginibre m x n (Haar/GOE: n x n)
   int64_t rows_pad_m = 0, rows_pad_n = 0;  // local panel rows (= dm/dn.rows_pad)
   ShardDim dm, dn;
+  CxState* cx = nullptr;  // set for HD_C128 operators
   // row sharding: shard_count > 1 => exchange after every
   // streaming kernel; head_rows H = rows the single-CTA stages read
   int shard_count = 1, shard_rank = 0;
@@ -1275,6 +1281,10 @@ void clear_status(hd_op* op, cudaStream_t s) {
   check_launch("reset status");
 }
 
+bool host_all_finite(const void* x, int64_t n, bool f32);
+
+#include "hd_complex_host.inc"
+
 bool host_all_finite(const void* x, int64_t n, bool f32) {
   if (f32) {
     const float* p = static_cast<const float*>(x);
@@ -1752,7 +1762,9 @@ int hd_create(const hd_config* cfg, hd_op** out) {
   HD_TRY
   require(cfg != nullptr && out != nullptr, "hd_create: null argument");
   const hd_config& c = *cfg;
-  require(c.dtype == HD_F64 || c.dtype == HD_F32, "hd_create: dtype must be HD_F64 or HD_F32");
+  require(c.dtype == HD_F64 || c.dtype == HD_F32 || c.dtype == HD_C128,
+          "hd_create: dtype must be HD_F64, HD_F32 or HD_C128");
+  require(c.dtype != HD_C128 || c.exchange == nullptr, "hd_create: complex operators are not row-sharded");
   require(c.draw_mode == HD_DRAWS_PHILOX || c.draw_mode == HD_DRAWS_INJECTED || c.draw_mode == HD_DRAWS_REFERENCE,
           "hd_create: unknown draw mode");
   require(c.sign_rule >= 0 && c.sign_rule <= 2, "hd_create: unknown sign rule");
@@ -1817,6 +1829,17 @@ int hd_create(const hd_config* cfg, hd_op** out) {
   plan_dim(op->dm, m, op->shard_count, op->shard_rank, op->head_rows);
   op->rows_pad_n = op->dn.rows_pad;
   op->rows_pad_m = op->dm.rows_pad;
+  if (c.dtype == HD_C128) {  // complex field: its own state (hd_complex_host.inc)
+    op->scal = dmalloc<double>(kScWords);
+    op->status = dmalloc<int>(kStWords);
+    op->seed_dev = dmalloc<unsigned long long>(1);
+    k_set_u64<<<1, 1, 0, op->stream>>>(op->seed_dev, (unsigned long long)c.seed);
+    ck(cudaGetLastError(), "seed");
+    cx_create(op.get(), K);
+    hard_reset(op.get());
+    *out = op.release();
+    return HD_OK;
+  }
   alloc_chain(op.get(), op->R, op->rows_pad_n, Kside);
   alloc_chain(op.get(), op->L, op->rows_pad_m, Kside);
   if (c.ensemble != HD_HAAR) {
@@ -1870,6 +1893,7 @@ int hd_destroy(hd_op* op) {
     cudaFree(p);
   cudaFree(op->status);
   cudaFree(op->seed_dev);
+  cx_free(op->cx);
   for (double* b : op->xch) cudaFree(b);
   cudaFree(op->xbuf);
   for (auto b : op->ybuf) cudaFree(b);
@@ -1920,8 +1944,8 @@ int hd_counts(const hd_op* op, int64_t* right, int64_t* left) {
 int hd_chain_sizes(const hd_op* op, int64_t* rc, int64_t* lc) {
   HD_TRY
   require(op && rc && lc, "hd_chain_sizes: null argument");
-  *rc = op->R.pan.count;
-  *lc = op->L.pan.count;
+  *rc = op->cx ? op->cx->R.count : op->R.pan.count;
+  *lc = op->cx ? op->cx->L.count : op->L.pan.count;
   return HD_OK;
   HD_CATCH
 }
@@ -1932,7 +1956,9 @@ int hd_probe(hd_op* op, const void* x, int64_t x_len, void* y, int64_t y_len, in
   require(op && x && y, "hd_probe: null argument");
   cudaSetDevice(op->cfg.device);
   fork_from(op, static_cast<cudaStream_t>(stream));
-  if (op->f32)
+  if (op->cx)
+    cx_do_probe(op, x, x_len, y, y_len, side, on_device);
+  else if (op->f32)
     do_probe<float>(op, x, x_len, y, y_len, side, on_device, op->stream);
   else
     do_probe<double>(op, x, x_len, y, y_len, side, on_device, op->stream);
@@ -1957,6 +1983,7 @@ int hd_reset(hd_op* op) {
   require(op, "hd_reset: null argument");
   cudaSetDevice(op->cfg.device);
   hard_reset(op);
+  if (op->cx) cx_reset(op);
   return HD_OK;
   HD_CATCH
 }
@@ -1964,6 +1991,7 @@ int hd_reset(hd_op* op) {
 int hd_run(hd_op* op, const hd_run_args* args) {
   HD_TRY
   require(op && args, "hd_run: null argument");
+  require(!op->cx, "hd_run: complex operators are driven through hd_probe");
   cudaSetDevice(op->cfg.device);
   if (op->f32)
     do_run<float>(op, *args);
@@ -1976,6 +2004,7 @@ int hd_run(hd_op* op, const hd_run_args* args) {
 int hd_run_async(hd_op* op, const hd_run_args* args) {
   HD_TRY
   require(op && args, "hd_run_async: null argument");
+  require(!op->cx, "hd_run_async: complex operators are driven through hd_probe");
   cudaSetDevice(op->cfg.device);
   if (op->f32)
     do_run_enqueue<float>(op, *args);
@@ -2099,6 +2128,7 @@ uint64_t hd_derive_seed(uint64_t base, uint64_t index) { return hd::refrng::deri
 int hd_reseed(hd_op* op, uint64_t seed) {
   HD_TRY
   require(op, "hd_reseed: null argument");
+  require(!op->cx, "hd_reseed: complex operators are driven through hd_probe");
   require(!op->run_pending, "hd_reseed: a run is in flight (hd_wait first)");
   require(op->cfg.draw_mode != HD_DRAWS_INJECTED, "hd_reseed: injected-draw operators take their draws from the caller");
   cudaSetDevice(op->cfg.device);
@@ -2124,6 +2154,7 @@ int hd_run_callback(hd_op* op, int64_t iterations, int32_t depth, const void* co
                     hd_update_fn update, void* user, void* final_out_dev) {
   HD_TRY
   require(op, "hd_run_callback: null argument");
+  require(!op->cx, "hd_run_callback: complex operators are driven through hd_probe");
   cudaSetDevice(op->cfg.device);
   if (op->f32)
     do_run_callback<float>(op, iterations, depth, initial_dev, side_of, update, user, final_out_dev);

@@ -173,7 +173,9 @@ class _Operator:
                  device: int = 0, shard: tuple = None, exchange: "Exchange" = None):
         cfg = N.hd_config()
         cfg.ensemble = self._ensemble
-        cfg.dtype = {"f64": N.HD_F64, "f32": N.HD_F32}[dtype]
+        if dtype not in ("f64", "f32", "c128"):
+            raise ValueError("dtype must be 'f64', 'f32' or 'c128'")
+        cfg.dtype = {"f64": N.HD_F64, "f32": N.HD_F32, "c128": N.HD_C128}[dtype]
         cfg.m, cfg.n = int(m), int(n)
         cfg.sigma = float(sigma)
         cfg.seed = int(seed) & _MASK
@@ -192,7 +194,7 @@ class _Operator:
         N.check(N.lib().hd_create(C.byref(cfg), C.byref(h)))
         self._h = h
         self._exchange = exchange  # keep the group's exchange alive
-        self._np_dtype = np.float64 if dtype == "f64" else np.float32
+        self._np_dtype = {"f64": np.float64, "f32": np.float32, "c128": np.complex128}[dtype]
         self.dtype = dtype
         self.device = int(device)
         self._ranges = [self._range(0), self._range(1)]
@@ -257,7 +259,7 @@ class _Operator:
             import torch
 
             xt = x.contiguous()
-            want = torch.float64 if self.dtype == "f64" else torch.float32
+            want = {"f64": torch.float64, "f32": torch.float32, "c128": torch.complex128}[self.dtype]
             if xt.dtype != want:
                 xt = xt.to(want)
             out = torch.empty(self._out_len(s if self._ensemble != N.HD_GOE else N.HD_RIGHT), dtype=want,
@@ -275,7 +277,12 @@ class _Operator:
 
     # parity mode
     def push_draws(self, g) -> None:
-        ga = np.ascontiguousarray(np.asarray(g, dtype=np.float64).reshape(-1))
+        """Queue the next probes' draws (injected mode): fp64 values, or for a
+        complex operator complex values (one normal_complex_vector per probe)."""
+        if np.iscomplexobj(g):
+            ga = np.ascontiguousarray(np.asarray(g, dtype=np.complex128).reshape(-1)).view(np.float64)
+        else:
+            ga = np.ascontiguousarray(np.asarray(g, dtype=np.float64).reshape(-1))
         N.check(N.lib().hd_push_draws(self._h, ga.ctypes.data_as(C.c_void_p), ga.size, 0))
 
     def reset(self) -> None:

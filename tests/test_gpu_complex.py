@@ -1,0 +1,124 @@
+"""Complex-field device operators (dtype "c128") against
+the complex oracle (oracle/hd_oracle_complex.cpp), which restates the
+reference's Scalar = complex<double> instantiation and is pinned by the
+reference's complex tests (tests/test_oracle_complex.py)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(np.asarray(a) - b) / (nb if nb > 0 else 1.0)
+
+
+@pytest.mark.parametrize("n", [1, 7, 300, 2049])
+def test_complex_haar_sequence(orc, lm, n):
+    seed, T = 50 + n, min(n, 20)
+    rng = np.random.default_rng(seed)
+    sides = ["right" if rng.random() < 0.6 else "left" for _ in range(T)]
+    ref = orc.COperator("haar", n=n, seed=seed)
+    op = lm.HaarOperator(n, seed=seed, dtype="c128", draws="injected", capacity=4)
+    op.push_draws(orc.complex_draws_for(seed, [n] * T).view(np.complex128))
+    aux = orc.RandomSource(seed + 1)
+    for t, s in enumerate(sides):
+        x = aux.normal_complex_vector(n)
+        got, want = op.probe(x, s), ref.probe(x, s)
+        assert got.dtype == np.complex128
+        assert rel(got, want) < 1e-10, (t, s, rel(got, want))
+        assert abs(np.linalg.norm(got) - np.linalg.norm(x)) <= 1e-12 * np.linalg.norm(x)  # unitary
+    assert op.remaining_probes == ref.remaining_probes
+
+
+@pytest.mark.parametrize("m,n", [(13, 10), (10, 13), (300, 257), (1000, 2100)])
+def test_complex_ginibre_sequence(orc, lm, m, n):
+    seed, T = 7 + m, min(m, n, 18)
+    rng = np.random.default_rng(seed)
+    sides = ["right" if rng.random() < 0.5 else "left" for _ in range(T)]
+    ref = orc.COperator("ginibre", m=m, n=n, sigma=0.7, seed=seed)
+    op = lm.GinibreOperator(m, n, 0.7, seed, dtype="c128", draws="injected", capacity=3)
+    op.push_draws(orc.complex_draws_for(seed, [m if s == "right" else n for s in sides]).view(np.complex128))
+    aux = orc.RandomSource(seed + 2)
+    for t, s in enumerate(sides):
+        x = aux.normal_complex_vector(n if s == "right" else m)
+        got, want = op.probe(x, s), ref.probe(x, s)
+        assert rel(got, want) < 1e-10, (t, s, rel(got, want))
+    assert op.probe_counts() == (sides.count("right"), sides.count("left"))
+
+
+def test_complex_goe_from_the_inner_ginibre(orc, lm):
+    # GOEOperator over complex: (A x + A^H x) / sqrt(2) (ensembles.hpp:117-127)
+    n, seed, T = 200, 3, 10
+    inner = orc.COperator("ginibre", m=n, n=n, sigma=1.0, seed=seed)
+    op = lm.GOEOperator(n, seed, dtype="c128", draws="injected", capacity=T)
+    op.push_draws(orc.complex_draws_for(seed, [n] * (2 * T)).view(np.complex128))
+    aux = orc.RandomSource(4)
+    for _ in range(T):
+        x = aux.normal_complex_vector(n)
+        want = (inner.probe(x, "right") + inner.probe(x, "left")) * 0.7071067811865475244
+        assert rel(op.probe(x, "right"), want) < 1e-10
+
+
+def test_complex_reference_draws_need_no_injection(orc, lm):
+    for ens, m, n in [("haar", 0, 500), ("ginibre", 400, 300)]:
+        seed = 88
+        if ens == "haar":
+            ref, op = orc.COperator("haar", n=n, seed=seed), lm.HaarOperator(n, seed=seed, dtype="c128",
+                                                                            draws="reference")
+        else:
+            ref = orc.COperator("ginibre", m=m, n=n, sigma=1.0, seed=seed)
+            op = lm.GinibreOperator(m, n, 1.0, seed, dtype="c128", draws="reference")
+        aux = orc.RandomSource(9)
+        for t in range(12):
+            s = "right" if t % 3 else "left"
+            x = aux.normal_complex_vector(n if (s == "right" or ens == "haar") else m)
+            assert rel(op.probe(x, s), ref.probe(x, s)) < 1e-10
+
+
+def test_complex_reference_properties_philox(lm, orc):
+    # test_haar.cpp:113-131 and test_ginibre.cpp:117-132 on the production draws
+    q = lm.HaarOperator(12, seed=92, dtype="c128").reconstruct()
+    assert np.max(np.abs(q.conj().T @ q - np.eye(12))) <= 1e-12
+    op = lm.HaarOperator(9, seed=93, dtype="c128")
+    aux = orc.RandomSource(94)
+    x, w = aux.normal_complex_vector(9), aux.normal_complex_vector(9)
+    qx = op.probe(x, "right")
+    assert abs(np.linalg.norm(qx) - np.linalg.norm(x)) <= 1e-12 * np.linalg.norm(x)
+    assert abs(np.vdot(w, qx) - np.vdot(op.probe(w, "left"), x)) <= 1e-10 * np.linalg.norm(x) * np.linalg.norm(w)
+    op = lm.GinibreOperator(13, 10, 1.0, 21, dtype="c128")
+    x, w = aux.normal_complex_vector(10), aux.normal_complex_vector(13)
+    lhs, rhs = np.vdot(w, op.probe(x, "right")), np.vdot(op.probe(w, "left"), x)
+    assert abs(lhs - rhs) <= 1e-10 * (abs(lhs) + 1.0)
+    op2 = lm.GinibreOperator(13, 10, 1.0, 23, dtype="c128")
+    z1, z2 = op2.probe(x, "right"), op2.probe(x, "right")
+    assert np.linalg.norm(z1 - z2) <= 1e-12 * np.linalg.norm(z1)
+
+
+def test_complex_torch_io_and_errors(lm, orc):
+    import torch
+
+    n = 64
+    op = lm.HaarOperator(n, seed=5, dtype="c128", capacity=8)
+    ref = lm.HaarOperator(n, seed=5, dtype="c128", capacity=8)
+    x = orc.RandomSource(6).normal_complex_vector(n)
+    y = op.probe(torch.from_numpy(x).cuda(), "right")
+    assert y.dtype == torch.complex128 and y.is_cuda
+    assert np.linalg.norm(y.cpu().numpy() - ref.probe(x, "right")) <= 1e-12 * np.linalg.norm(x)
+    bad = x.copy()
+    bad[3] = complex(np.nan, 0)
+    with pytest.raises(ValueError, match="non-finite"):
+        op.probe(bad, "right")
+    with pytest.raises(ValueError, match="non-finite"):
+        op.probe(torch.from_numpy(bad).cuda(), "right")
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        op.probe(np.ones(n + 1, complex), "right")
+    with pytest.raises(ValueError, match="complex operators"):
+        op.run(x, 2)
+    small = lm.HaarOperator(3, seed=1, dtype="c128")
+    for _ in range(3):
+        small.probe(np.ones(3, complex), "right")
+    with pytest.raises(lm.BudgetExhausted):
+        small.probe(np.ones(3, complex), "right")
+    small.reset()
+    assert small.remaining_probes == 3
