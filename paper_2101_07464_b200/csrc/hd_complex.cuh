@@ -80,8 +80,15 @@ __global__ void __launch_bounds__(kCxThreads) kc_gemv_t(const c2* W, int64_t ld,
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int j = wid; j < k; j += nw) {
     const c2* col = W + (size_t)j * ld + b0;
-    c2 acc = cmk(0.0, 0.0);
-    for (int i = lane; i < nr; i += 32) acc = cadd(acc, cconjmul(col[i], vs[i]));
+    c2 acc = cmk(0.0, 0.0), acc2 = cmk(0.0, 0.0);
+    int i = lane;
+#pragma unroll 4
+    for (; i + 32 < nr; i += 64) {  // two independent loads in flight per step
+      acc = cadd(acc, cconjmul(col[i], vs[i]));
+      acc2 = cadd(acc2, cconjmul(col[i + 32], vs[i + 32]));
+    }
+    if (i < nr) acc = cadd(acc, cconjmul(col[i], vs[i]));
+    acc = cadd(acc, acc2);
     for (int o = 16; o > 0; o >>= 1) {
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
@@ -90,13 +97,19 @@ __global__ void __launch_bounds__(kCxThreads) kc_gemv_t(const c2* W, int64_t ld,
   }
 }
 
-// out[j] = sum_b part[b * k + j] (fixed order: deterministic)
+// out[j] = sum_b part[b * k + j]: one warp per column, lane-strided over the
+// blocks then a shuffle tree (fixed order: deterministic)
 __global__ void kc_reduce(const c2* part, int nb, int k, c2* out) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
-    c2 s = cmk(0.0, 0.0);
-    for (int b = 0; b < nb; ++b) s = cadd(s, part[(size_t)b * k + j]);
-    out[j] = s;
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= k) return;
+  c2 s = cmk(0.0, 0.0);
+  for (int b = lane; b < nb; b += 32) s = cadd(s, part[(size_t)b * k + j]);
+  for (int o = 16; o > 0; o >>= 1) {
+    s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+    s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
   }
+  if (lane == 0) out[j] = s;
 }
 
 // beta = T a (herm = 0) or T^H a (herm = 1), T upper triangular k x k (ld K)
@@ -121,8 +134,15 @@ __global__ void kc_gemv_n(const c2* W, int64_t ld, int k, const c2* beta, const 
                           int64_t n, c2* y) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  c2 acc = cmk(0.0, 0.0);
-  for (int j = 0; j < k; ++j) acc = cadd(acc, cmul(W[(size_t)j * ld + i], __ldg(beta + j)));
+  c2 acc = cmk(0.0, 0.0), acc2 = cmk(0.0, 0.0);
+  int j = 0;
+#pragma unroll 4
+  for (; j + 1 < k; j += 2) {  // two independent column loads in flight per step
+    acc = cadd(acc, cmul(W[(size_t)j * ld + i], __ldg(beta + j)));
+    acc2 = cadd(acc2, cmul(W[(size_t)(j + 1) * ld + i], __ldg(beta + j + 1)));
+  }
+  if (j < k) acc = cadd(acc, cmul(W[(size_t)j * ld + i], __ldg(beta + j)));
+  acc = cadd(acc, acc2);
   if (mode == 2) {
     y[i] = acc;
     return;
@@ -145,9 +165,11 @@ __global__ void kc_tail_norm2(const c2* p, int64_t off, int64_t n, double* part)
 // Reflector scalars from the tail norm (reflect.hpp:142-153): scal = {nrm,
 // c, s.re, s.im, phase.re, phase.im}; identity (nrm == 0) -> c = 0, s = 1.
 __global__ void kc_reflector_scalars(const double* part, int nb, const c2* p, int64_t off, double* scal) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  __shared__ double red[32];
   double s2 = 0.0;
-  for (int b = 0; b < nb; ++b) s2 += part[b];
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) s2 += part[b];
+  s2 = block_sum<kCxThreads>(s2, red);  // launched with kCxThreads threads
+  if (threadIdx.x != 0) return;
   const double nrm = sqrt(s2);
   scal[0] = nrm;
   if (nrm == 0.0) {
