@@ -36,6 +36,7 @@ from .._native import BudgetExhausted, ResourceCapExceeded
 __all__ = [
     "BudgetExhausted", "GinibreOperator", "HaarOperator", "GOEOperator", "Reflector", "ResourceCapExceeded",
     "RandomSource", "SubsampledHaarOperator", "USVOperator", "derive_seed", "Exchange", "shard_plan",
+    "DynamicsSpec", "run_dynamics",
     "share_nccl_id", "nccl_exchange", "ista_curves", "make_reflector", "run_trials", "amp_sparse_regression", "spiked_power",
     "sample_dense_haar", "ista_trial", "spectral_trial", "power_iteration", "restarted_krylov", "soft_threshold",
     "spectral_summary", "two_sample_ks",
@@ -520,6 +521,64 @@ def run_trials(ensemble: str, trials: int, n: int, T: int, *, m: int = None, sig
             busy.append(op)
             nxt += 1
     return (out, ops) if return_ops else out
+
+
+class DynamicsSpec:
+    """DynamicsSpec (dynamics.hpp:21-32): T iterations of
+    x_{t+1} = update(t, y_t, history) with y_t = M_t x_t, M_t chosen by
+    side_of(t) ('right' / 'left'); `initial` holds the d + 1 starting vectors
+    newest first; `observer(t, y_t, x_{t+1})` sees the run stream by."""
+
+    def __init__(self, iterations: int = 0, history_depth: int = 0, initial=None, side_of=None, update=None,
+                 observer=None, keep_trajectory: bool = True):
+        self.iterations, self.history_depth = int(iterations), int(history_depth)
+        self.initial = list(initial) if initial is not None else []
+        self.side_of, self.update, self.observer = side_of, update, observer
+        self.keep_trajectory = bool(keep_trajectory)
+
+
+def _all_finite(v) -> bool:
+    if _is_torch_cuda(v):
+        import torch
+
+        return bool(torch.isfinite(v).all())
+    return bool(np.all(np.isfinite(np.asarray(v))))
+
+
+def run_dynamics(op, spec: DynamicsSpec) -> list:
+    """run_dynamics (dynamics.hpp:42-76) over a device operator with user
+    callbacks: the same validation messages, the history window newest first,
+    the non-finite abort and the observer. Vectors are numpy (host) or CUDA
+    tensors (device-resident); every probe runs on the GPU. Returns the
+    iterates x_1..x_{T+1} (or [x_{T+1}] when keep_trajectory is off)."""
+    if spec.iterations < 0:
+        raise ValueError("run_dynamics: negative iteration count")
+    if spec.history_depth < 0:
+        raise ValueError("run_dynamics: negative history depth")
+    if len(spec.initial) != spec.history_depth + 1:
+        raise ValueError("run_dynamics: initial history must hold d + 1 vectors")
+    if spec.side_of is None:
+        raise ValueError("run_dynamics: no side schedule")
+    if spec.update is None:
+        raise ValueError("run_dynamics: no update map")
+    if spec.iterations > op.remaining_probes:
+        raise ValueError("run_dynamics: iteration count exceeds the operator's probe budget")
+    history = list(spec.initial)
+    traj = [history[0]] if spec.keep_trajectory else []
+    for t in range(1, spec.iterations + 1):
+        y = op.probe(history[0], spec.side_of(t))
+        nxt = spec.update(t, y, history)
+        if not _all_finite(nxt):
+            raise RuntimeError(f"run_dynamics: non-finite iterate at step {t}")
+        if spec.observer is not None:
+            spec.observer(t, y, nxt)
+        history.insert(0, nxt)
+        history.pop()
+        if spec.keep_trajectory:
+            traj.append(nxt)
+    if not spec.keep_trajectory:
+        traj.append(history[0])
+    return traj
 
 
 def amp_sparse_regression(op, beta, w, T: int, alpha: float = 1.5):
