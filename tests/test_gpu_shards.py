@@ -160,3 +160,42 @@ def test_one_shard_group_runs_the_exchange_path(orc, lm, kind):
         # needs (+ the final status exchange of Ginibre / GOE probes)
         per_probe = {"haar": 3, "ginibre": 4, "goe": 7}[ens]
         assert op.kernel_stats()["allreduce"]["launches"] == per_probe * T
+
+
+@pytest.mark.parametrize("ens,kw", [("haar", {"skip_reflector": True}), ("ginibre", {"skip_reflector": True}),
+                                    ("haar", {"sign_rule": "negative_at_zero"}), ("goe", {})])
+def test_sharded_faults_and_reference_draws(orc, lm, ens, kw):
+    # fault flags change which columns exist (skip_reflector drops the first
+    # fold) and reference draws make every shard generate the reference's
+    # stream: the stitched shards must still equal the oracle operator built
+    # from the same seed, with no injected draws at all
+    n, m, seed, T = 2600, 2100, 61, 14
+    if ens == "ginibre":
+        ref = orc.Operator("ginibre", m=m, n=n, sigma=0.9, seed=seed, **kw)
+    elif ens == "haar":
+        ref = orc.Operator("haar", n=n, seed=seed, **kw)
+    else:
+        ref = orc.Operator("goe", n=n, sigma=0.9, seed=seed)
+    aux = orc.RandomSource(62)
+    seq = [(aux.normal_vector(n if (t % 3 or ens != "ginibre") else m),
+            "right" if (t % 3 or ens == "goe") else "left") for t in range(T)]
+    want = [ref.probe(x, s) for x, s in seq]
+    ex, outs, errs = lm.Exchange.local(2), [None, None], []
+
+    def worker(r):
+        try:
+            op = make(lm, ens, m, n, seed, 0.9, draws="reference", capacity=T, shard=(r, 2), exchange=ex, **kw)
+            res = []
+            for x, s in seq:
+                lo, hi = op.shard_range("cols" if (s == "right" or ens == "goe") else "rows")
+                res.append(op.probe(np.ascontiguousarray(x[lo:hi]), s))
+            outs[r] = res
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(2)]
+    [t.start() for t in th]
+    [t.join(timeout=300) for t in th]
+    assert not errs, errs
+    for t in range(T):
+        assert rel(np.concatenate([outs[0][t], outs[1][t]]), want[t]) < 1e-10, t
