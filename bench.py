@@ -179,6 +179,66 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def cpu_baselines_all(args):
+    """The reference CPU path (oracle port, -O3 -mavx2 -mfma) timed on this
+    host for the other BASELINE configs, on bounded samples; where the full
+    config exceeds a few seconds (or host RAM) the sample is smaller and the
+    full-config time is extrapolated from the measured element-update rate
+    (the reference's n-slope is ~1, acceptance.cpp:206-218)."""
+    import time
+
+    from oracle import oracle as orc
+
+    orc.build()
+    threads = max(1, min(os.cpu_count() or 1, args.ref_threads))
+    out = []
+
+    def emit(workload, sample, eu, secs, threads_used, full_eu):
+        rate = eu / secs
+        out.append({"impl": "reference", "workload": workload, "sample": sample, "cpu_elem_updates_per_s": rate,
+                    "threads": threads_used, "sample_s": secs, "full_config_elem_updates": full_eu,
+                    "extrapolated_full_config_s": full_eu / rate, "cpu": cpu_model(), "nproc": os.cpu_count()})
+
+    def gin_eu(n, T):  # square Ginibre, alternating: probe k touches n k
+        return n * T * (T + 1) / 2
+
+    # config 1: full size, one trial, one thread (run_dynamics is serial)
+    secs, _ = orc.bench_workload("ginibre", 4096, 4096, 4096 ** -0.5, "normalize", "alternate", 50, 1, 1, 1)
+    emit("config1_ginibre_4096_T50", "full config, 1 trial, 1 thread", gin_eu(4096, 50), secs, 1, gin_eu(4096, 50))
+    # config 3: `threads` trials of the 1024 (one per thread, parallel_for)
+    n, T = 100_000, 100
+    secs, _ = orc.bench_workload("ginibre", n, n, n ** -0.5, "normalize", "alternate", T, 1, threads, threads)
+    emit("config3_ginibre_1e5_T100_B1024", f"{threads} of the 1024 trials, one per thread", gin_eu(n, T) * threads,
+         secs, threads, gin_eu(n, T) * 1024)
+    # config 4: AMP at n = 1e5 (m = 2n), 50 AMP iterations (101 probes), 1 thread
+    n, T = 100_000, 50
+    m = 2 * n
+    rs = orc.RandomSource(4, 1)
+    beta = np.array([(rs.uniform() < 0.1) * rs.normal() for _ in range(n)])
+    w = 0.1 * rs.normal_vector(m)
+    op = orc.Operator("ginibre", m=m, n=n, sigma=m ** -0.5, seed=4)
+    t0 = time.perf_counter()
+    op.amp(beta, w, T)
+    secs = time.perf_counter() - t0
+    eu = lambda nn, TT: sum((nn if k % 2 == 1 else 2 * nn) * k for k in range(1, 2 * TT + 2))  # noqa: E731
+    emit("config4_amp_n1e7_T200", "n = 1e5 (m = 2e5), 50 AMP iterations, 1 thread", eu(n, T), secs, 1,
+         eu(10_000_000, 200))
+    # config 5: spiked GOE at n = 1e5, 64 steps (128 inner probes), 1 thread
+    n, T = 100_000, 64
+    u = orc.RandomSource(5, 1).normal_vector(n)
+    u /= np.linalg.norm(u)
+    x1 = orc.RandomSource(5, 2).normal_vector(n)
+    x1 /= np.linalg.norm(x1)
+    op = orc.Operator("goe", n=n, sigma=n ** -0.5, seed=5)
+    t0 = time.perf_counter()
+    op.spiked_power(u, x1, T)
+    secs = time.perf_counter() - t0
+    emit("config5_spiked_goe_n1e8_T256", "n = 1e5, 64 GOE steps (128 inner probes), 1 thread", gin_eu(n, 2 * T),
+         secs, 1, gin_eu(100_000_000, 512))
+    for line in out:
+        print(json.dumps(line), flush=True)
+
+
 def workload_config(args):
     return {"workload": f"config2_haar_n{args.n}_T{args.T}_tanh_mix", "ensemble": "haar", "n": args.n,
             "T": args.T, "dynamics": "x_{t+1}=tanh(2Qx_t)+0.1x_{t-1}", "draws": "device philox4x32-10",
@@ -200,8 +260,16 @@ def main():
     ap.add_argument("--ref-threads", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--cpu-baselines", action="store_true",
+                    help="time the reference CPU path (oracle) on configs 1, 3, 4, 5 and exit")
     args = ap.parse_args()
 
+    if args.cpu_baselines:
+        import numpy as np  # noqa: F401  (used by cpu_baselines_all)
+
+        globals()["np"] = np
+        cpu_baselines_all(args)
+        return
     if args.impl == "reference":
         run_reference_arm(args)
         return
