@@ -1553,7 +1553,9 @@ void do_run_enqueue(hd_op* op, const hd_run_args& a) {
   const int64_t dim1 = (eff1 == HD_RIGHT) ? op->n : op->m;
   if (a.update == HD_UPDATE_TANH_MIX || a.traj)
     require(op->m == op->n, "run_dynamics: this update map needs a square operator");
-  if (!a.on_device) require(host_all_finite(a.x1, dim1, op->f32), "probe: non-finite input");
+  // x_1 finiteness (check_probe_input, operators.hpp:44-48) is checked by the
+  // first k_dots pass on the device (kStBadInput -> "probe: non-finite input"),
+  // so host inputs are not scanned here
   {
     int64_t nr = 0, nl = 0;
     for (int64_t t = 1; t <= a.iterations; ++t) {

@@ -291,7 +291,7 @@ class _Operator:
 
     # device dynamics (run_dynamics, dynamics.hpp:42-76, built-in maps)
     def run(self, x1, iterations: int, update: str = "normalize", sides: str = "alternate", x0=None,
-            keep_trajectory: bool = False, use_graph: bool = False):
+            keep_trajectory: bool = False, use_graph: bool = False, out=None):
         a = N.hd_run_args()
         a.update = N.UPDATES[update]
         a.side_rule = N.SIDE_RULES[sides]
@@ -325,7 +325,12 @@ class _Operator:
             x0a = np.ascontiguousarray(np.asarray(x0, dtype=self._np_dtype).reshape(-1))
             a.x0 = x0a.ctypes.data
         fdim = self._final_dim(iterations, sides, x1a.size)
-        fin = np.empty(fdim, dtype=self._np_dtype)
+        if out is not None:  # caller's host buffer (e.g. pinned) for x_{T+1}
+            if out.dtype != self._np_dtype or out.size != fdim or not out.flags.c_contiguous:
+                raise ValueError("run: out must be a contiguous host array of the final iterate's size and dtype")
+            fin = out
+        else:
+            fin = np.empty(fdim, dtype=self._np_dtype)
         a.final_out = fin.ctypes.data
         traj = None
         if keep_trajectory:

@@ -414,3 +414,22 @@ def test_spiked_goe_power_parity(orc, lm):
     assert rel(x.cpu().numpy(), xr) < TOL64
     assert np.max(np.abs(ov.cpu().numpy() - ovr)) < 1e-9
     assert abs(ovr[-1]) > 0.5  # theta = 2 > 1: the spike is detected
+
+
+def test_run_rejects_nonfinite_host_x1_on_device(orc, lm):
+    # the finiteness of x_1 (check_probe_input) is checked by the first device
+    # pass: same message, operator state untouched, a valid run afterwards
+    n, T, seed = 2000, 6, 12
+    op = lm.HaarOperator(n, seed=seed, draws="injected", capacity=T)
+    op.push_draws(orc.draws_for(seed, [n] * T))
+    bad = np.ones(n)
+    bad[11] = np.inf
+    for graph in (False, True):
+        with pytest.raises(ValueError, match="probe: non-finite input"):
+            op.run(bad, T, update="normalize", sides="right", use_graph=graph)
+        assert op.remaining_probes == n
+    x1 = orc.RandomSource(seed, 1).normal_vector(n)
+    want = orc.Operator("haar", n=n, seed=seed).run("normalize", "right", T, x1, keep=False)[0]
+    out = np.empty(n)
+    got = op.run(x1, T, update="normalize", sides="right", out=out)
+    assert got is out and rel(out, want) < 1e-9
