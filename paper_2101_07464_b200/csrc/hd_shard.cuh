@@ -39,10 +39,13 @@ class Exchange {
   virtual void allreduce_sum(double* buf, int64_t count, cudaStream_t stream, int rank) = 0;
 };
 
-// Virtual shards in one process (tests / one GPU): one host thread per shard.
-// Each call: sync the caller's stream, publish the buffer, barrier; every
-// shard sums all published buffers in rank order into its scratch, barrier,
-// then copies back. No kernel ever waits on another shard's kernel.
+// Shards in one process, one host thread each — virtual shards on one GPU
+// (tests) or one process driving several GPUs (each shard's hd_config.device;
+// peer access is enabled so the summing kernel reads the other devices'
+// buffers over NVLink). Each call: sync the caller's stream, publish the
+// buffer, barrier; every shard sums all published buffers in rank order into
+// its scratch, barrier, then copies back. No kernel ever waits on another
+// shard's kernel.
 __global__ void k_sum_shards(const double* const* bufs, int nb, int64_t count, double* out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
     double v = 0.0;
@@ -53,7 +56,8 @@ __global__ void k_sum_shards(const double* const* bufs, int nb, int64_t count, d
 
 class LocalExchange final : public Exchange {
  public:
-  explicit LocalExchange(int n) : n_(n), bufs_(n, nullptr), scratch_(n, nullptr), cap_(n, 0), table_(n, nullptr) {}
+  explicit LocalExchange(int n)
+      : n_(n), bufs_(n, nullptr), scratch_(n, nullptr), cap_(n, 0), table_(n, nullptr), devs_(n, 0), peers_(n, 0) {}
   ~LocalExchange() override {
     for (auto p : scratch_) cudaFree(p);
     for (auto p : table_) cudaFree(p);
@@ -68,7 +72,21 @@ class LocalExchange final : public Exchange {
     }
     if (!table_[rank]) check(cudaMalloc(&table_[rank], sizeof(double*) * n_), "exchange table");
     bufs_[rank] = buf;
+    int dev = 0;
+    check(cudaGetDevice(&dev), "device");
+    devs_[rank] = dev;
     barrier();
+    if (!peers_[rank]) {  // first exchange: reach every other shard's device
+      for (int r = 0; r < n_; ++r) {
+        int ok = 0;
+        if (devs_[r] != dev && cudaDeviceCanAccessPeer(&ok, dev, devs_[r]) == cudaSuccess && ok) {
+          const cudaError_t e = cudaDeviceEnablePeerAccess(devs_[r], 0);
+          if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+          else check(e, "peer access");
+        }
+      }
+      peers_[rank] = 1;
+    }
     check(cudaMemcpyAsync(table_[rank], bufs_.data(), sizeof(double*) * n_, cudaMemcpyHostToDevice, stream), "table");
     k_sum_shards<<<64, 256, 0, stream>>>(table_[rank], n_, count, scratch_[rank]);
     check(cudaGetLastError(), "k_sum_shards");
@@ -97,6 +115,7 @@ class LocalExchange final : public Exchange {
   std::vector<double*> bufs_, scratch_;
   std::vector<int64_t> cap_;
   std::vector<double**> table_;
+  std::vector<int> devs_, peers_;
   std::mutex mu_;
   std::condition_variable cv_;
   int arrived_ = 0;
