@@ -122,3 +122,24 @@ def test_complex_torch_io_and_errors(lm, orc):
         small.probe(np.ones(3, complex), "right")
     small.reset()
     assert small.remaining_probes == 3
+
+
+def test_complex_user_dynamics(orc, lm):
+    # run_dynamics over a complex operator (dynamics.hpp is generic in Scalar):
+    # normalised alternating power iteration on a complex Ginibre matrix,
+    # against the complex oracle driven the same way
+    import torch
+
+    m, n, T, seed = 600, 500, 12, 17
+    ref = orc.COperator("ginibre", m=m, n=n, sigma=m ** -0.5, seed=seed)
+    x = orc.RandomSource(seed, 1).normal_complex_vector(n)
+    want = [x]
+    for t in range(1, T + 1):
+        y = ref.probe(want[-1], "right" if t % 2 else "left")
+        want.append(y / np.linalg.norm(y))
+    op = lm.GinibreOperator(m, n, m ** -0.5, seed, dtype="c128", draws="reference")
+    spec = lm.DynamicsSpec(T, 0, [torch.from_numpy(x).cuda()], lambda t: "right" if t % 2 else "left",
+                           lambda t, y, h: y / torch.linalg.vector_norm(y))
+    traj = lm.run_dynamics(op, spec)
+    for t in range(T + 1):
+        assert rel(traj[t].cpu().numpy(), want[t]) < 1e-9, t
