@@ -809,8 +809,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // dst[s] = sum_b parts[(slot0 + s) * nblk + b], thread per slot (fixed order;
 // four independent accumulators so the loads are all in flight together).
-// Inlined: called four times back to back on the critical path of
-// k_small_dots, where the call (cold instruction fetch) cost ~0.7 us per probe.
+// The single-CTA helpers are all inlined: after the stages were restructured
+// the calls (each a jump into not-yet-fetched code at the start of a launch)
+// cost more than the extra code size — measured 23.33 -> 23.14 ms per config-2
+// run and 66 -> 64 us per probe at tiny n.
 __device__ __forceinline__ void st_reduce(const double* parts, int nblk, int slot0, int count, double* dst, int tid,
                                           int nthr) {
 #pragma unroll 1
@@ -832,7 +834,7 @@ __device__ __forceinline__ void st_reduce(const double* parts, int nblk, int slo
 }
 
 // Async-stage `count` contiguous doubles (global -> shared).
-__device__ __noinline__ void st_stage(const double* src, int64_t count, double* dst, int t, int nthr) {
+__device__ __forceinline__ void st_stage(const double* src, int64_t count, double* dst, int t, int nthr) {
 #pragma unroll 1
   for (int64_t e = t; e < count; e += nthr) cp_async8(dst + e, src + e);
 }
@@ -847,7 +849,7 @@ struct TView {
 
 // Stage T[:k, :k] into shared memory (ld = k | 1, conflict-free rows) with
 // one fully parallel coalesced sweep; threads [t0, t0 + nthr).
-__device__ __noinline__ TView st_stage_T(const ChainDev& ch, int k, double* dst, int t, int nthr) {
+__device__ __forceinline__ TView st_stage_T(const ChainDev& ch, int k, double* dst, int t, int nthr) {
   const int64_t ld = k | 1;
   const int w = t >> 5, lane = t & 31, nw = nthr >> 5;  // warp per column, no integer division
 #pragma unroll 1
@@ -860,7 +862,7 @@ __device__ __noinline__ TView st_stage_T(const ChainDev& ch, int k, double* dst,
 // T_new[:k, k] = -c T[:k, :k] g (g in shared memory), T_new[k, k] = c; the
 // new column is written to global memory and to tcol (shared). Warps
 // [w0, w0 + nw) of the CTA, warp per row.
-__device__ __noinline__ void st_T_column(const ChainDev& ch, const TView& tv, int k, double c, const double* g,
+__device__ __forceinline__ void st_T_column(const ChainDev& ch, const TView& tv, int k, double c, const double* g,
                                             double* tcol, int w0, int nw) {
   const int w = (threadIdx.x >> 5) - w0, lane = threadIdx.x & 31;
 #pragma unroll 1
@@ -882,7 +884,7 @@ __device__ __noinline__ void st_T_column(const ChainDev& ch, const TView& tv, in
 
 // out[j] = sum_{i <= j} T[i, j] u[i] for j < k (column p, if >= 0, comes
 // from tcol in shared memory). Warp per column.
-__device__ __noinline__ void st_Tt(const TView& tv, int k, const double* u, double* out, int p,
+__device__ __forceinline__ void st_Tt(const TView& tv, int k, const double* u, double* out, int p,
                                       const double* tcol, int w0, int nw) {
   const int w = (threadIdx.x >> 5) - w0, lane = threadIdx.x & 31;
 #pragma unroll 1
@@ -897,7 +899,7 @@ __device__ __noinline__ void st_Tt(const TView& tv, int k, const double* u, doub
 }
 
 // out[i] = sum_{j >= i} T[i, j] u[j] for i < k (column p from tcol).
-__device__ __noinline__ void st_T(const TView& tv, int k, const double* u, double* out, int p,
+__device__ __forceinline__ void st_T(const TView& tv, int k, const double* u, double* out, int p,
                                      const double* tcol, int w0, int nw) {
   const int w = (threadIdx.x >> 5) - w0, lane = threadIdx.x & 31;
 #pragma unroll 1
@@ -914,7 +916,7 @@ __device__ __noinline__ void st_T(const TView& tv, int k, const double* u, doubl
 // the panel: pivot fix-up, scale, coefficient, leading factor; returns the
 // sign (0 under the zeroing negative control). Single thread.
 template <typename T>
-__device__ __noinline__ double st_reflector(const ChainDev& ch, T* P, int j, int64_t off, double nrm, double pivot,
+__device__ __forceinline__ double st_reflector(const ChainDev& ch, T* P, int j, int64_t off, double nrm, double pivot,
                                                int rule, double colscale, double unscale, bool append) {
   double sign;
   if (rule == 0) sign = (pivot >= 0.0) ? 1.0 : -1.0;
@@ -939,7 +941,7 @@ __device__ __noinline__ double st_reflector(const ChainDev& ch, T* P, int j, int
 
 // D update for a member with offset off and leading factor s: D[i] *= s for
 // i >= off (threads [t0, t0 + nthr)).
-__device__ __noinline__ void st_D_update(const ChainDev& ch, int64_t off, double s, int t, int nthr) {
+__device__ __forceinline__ void st_D_update(const ChainDev& ch, int64_t off, double s, int t, int nthr) {
   for (int64_t i = off + t; i < ch.Dlen; i += nthr) ch.Drow[i] *= s;
   if (t == 0) *ch.Dtail *= s;
 }
