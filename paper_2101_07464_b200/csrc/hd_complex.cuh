@@ -71,6 +71,8 @@ constexpr int kCxThreads = 256;
 // part[b * k + j] = sum_{i in block b} conj(W[i, j]) v(i), i in [r0, r1)
 __global__ void __launch_bounds__(kCxThreads) kc_gemv_t(const c2* W, int64_t ld, int k, CSrc v, int64_t r0, int64_t r1,
                                                         c2* part) {
+  pdl_wait();  // programmatic dependent launch (as the real path)
+  pdl_launch();
   __shared__ c2 vs[kCxRows];
   const int64_t b0 = r0 + (int64_t)blockIdx.x * kCxRows;
   const int64_t rem = r1 - b0;
@@ -100,6 +102,8 @@ __global__ void __launch_bounds__(kCxThreads) kc_gemv_t(const c2* W, int64_t ld,
 // out[j] = sum_b part[b * k + j]: one warp per column, lane-strided over the
 // blocks then a shuffle tree (fixed order: deterministic)
 __global__ void kc_reduce(const c2* part, int nb, int k, c2* out) {
+  pdl_wait();  // programmatic dependent launch (as the real path)
+  pdl_launch();
   const int lane = threadIdx.x & 31;
   const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (j >= k) return;
@@ -114,6 +118,8 @@ __global__ void kc_reduce(const c2* part, int nb, int k, c2* out) {
 
 // beta = T a (herm = 0) or T^H a (herm = 1), T upper triangular k x k (ld K)
 __global__ void kc_tmul(const c2* T, int64_t K, int k, const c2* a, int herm, c2* beta) {
+  pdl_wait();  // programmatic dependent launch (as the real path)
+  pdl_launch();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) {
     c2 s = cmk(0.0, 0.0);
     if (!herm) {
@@ -132,6 +138,8 @@ __global__ void kc_tmul(const c2* T, int64_t K, int k, const c2* a, int herm, c2
 // x rows >= xlen read as zero (sparse inputs)
 __global__ void kc_gemv_n(const c2* W, int64_t ld, int k, const c2* beta, const c2* x, int64_t xlen, DView d, int mode,
                           int64_t n, c2* y) {
+  pdl_wait();  // programmatic dependent launch (as the real path)
+  pdl_launch();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   c2 acc = cmk(0.0, 0.0), acc2 = cmk(0.0, 0.0);
@@ -154,6 +162,8 @@ __global__ void kc_gemv_n(const c2* W, int64_t ld, int k, const c2* beta, const 
 
 // ||p[off:]||^2 partial sums per block
 __global__ void kc_tail_norm2(const c2* p, int64_t off, int64_t n, double* part) {
+  pdl_wait();  // programmatic dependent launch (as the real path)
+  pdl_launch();
   __shared__ double red[32];
   double s = 0.0;
   for (int64_t i = off + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -165,6 +175,8 @@ __global__ void kc_tail_norm2(const c2* p, int64_t off, int64_t n, double* part)
 // Reflector scalars from the tail norm (reflect.hpp:142-153): scal = {nrm,
 // c, s.re, s.im, phase.re, phase.im}; identity (nrm == 0) -> c = 0, s = 1.
 __global__ void kc_reflector_scalars(const double* part, int nb, const c2* p, int64_t off, double* scal) {
+  pdl_wait();  // programmatic dependent launch (as the real path)
+  pdl_launch();
   __shared__ double red[32];
   double s2 = 0.0;
   for (int b = threadIdx.x; b < nb; b += blockDim.x) s2 += part[b];
@@ -194,6 +206,8 @@ __global__ void kc_reflector_scalars(const double* part, int nb, const c2* p, in
 // column k of W: w = p[off:] / nrm (+ phase at off), zero above off and for
 // the identity reflector
 __global__ void kc_write_column(const c2* p, int64_t off, int64_t n, const double* scal, c2* col) {
+  pdl_wait();  // programmatic dependent launch (as the real path)
+  pdl_launch();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double nrm = scal[0];
@@ -209,6 +223,8 @@ __global__ void kc_write_column(const c2* p, int64_t off, int64_t n, const doubl
 // with s from row off on (single block)
 __global__ void kc_append_small(c2* T, int64_t K, int k, const c2* G, const double* scal, double* cs, c2* ss, c2* Dhead,
                                 int64_t Dlen, c2* Dtail, int64_t off) {
+  pdl_wait();  // programmatic dependent launch (as the real path)
+  pdl_launch();
   const double c = scal[1];
   const c2 s = cmk(scal[2], scal[3]);
   for (int i = threadIdx.x; i < k; i += blockDim.x) {  // T[i, k] = -c sum_{j >= i} T[i, j] G[j]
@@ -228,6 +244,8 @@ __global__ void kc_append_small(c2* T, int64_t K, int k, const c2* G, const doub
 // z = H_fold p = [p[0:off], ||p[off:]||, 0, ...] (reflect.hpp: the reflector
 // maps the tail onto +||tail|| e_off)
 __global__ void kc_fold_z(const c2* p, int64_t off, int64_t n, const double* scal, c2* z) {
+  pdl_wait();  // programmatic dependent launch (as the real path)
+  pdl_launch();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   z[i] = (i < off) ? p[i] : (i == off ? cmk(scal[0], 0.0) : cmk(0.0, 0.0));
@@ -237,6 +255,8 @@ __global__ void kc_fold_z(const c2* p, int64_t off, int64_t n, const double* sca
 // queued interleaved draws; rows < mask zero
 __global__ void kc_draw(int philox, const unsigned long long* seedp, uint32_t stream, uint32_t probe, const c2* inj,
                         int64_t n, int64_t mask, c2* g) {
+  pdl_wait();  // programmatic dependent launch (as the real path)
+  pdl_launch();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   c2 v;
@@ -250,11 +270,16 @@ __global__ void kc_draw(int philox, const unsigned long long* seedp, uint32_t st
 }
 
 __global__ void kc_unit(c2* v, int64_t n, int64_t at) {
+  pdl_wait();  // programmatic dependent launch (as the real path)
+  pdl_launch();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) v[i] = (i == at) ? cmk(1.0, 0.0) : cmk(0.0, 0.0);
 }
 
-__global__ void kc_scale(c2* y, int64_t n, double s, const c2* add, double add_s) {  // y = (add + y) * s' / y *= s
+// y = (add + y) * add_s * s, or y *= s without add
+__global__ void kc_scale(c2* y, int64_t n, double s, const c2* add, double add_s) {
+  pdl_wait();  // programmatic dependent launch (as the real path)
+  pdl_launch();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   c2 v = y[i];
@@ -264,6 +289,8 @@ __global__ void kc_scale(c2* y, int64_t n, double s, const c2* add, double add_s
 
 // 1 if any entry is non-finite
 __global__ void kc_check_finite(const c2* x, int64_t n, int* flag) {
+  pdl_wait();  // programmatic dependent launch (as the real path)
+  pdl_launch();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     if (!isfinite(x[i].x) || !isfinite(x[i].y)) atomicOr(flag, 1);
 }
