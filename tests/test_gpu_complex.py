@@ -31,7 +31,7 @@ def test_complex_haar_sequence(orc, lm, n):
     assert op.remaining_probes == ref.remaining_probes
 
 
-@pytest.mark.parametrize("m,n", [(13, 10), (10, 13), (300, 257), (1000, 2100)])
+@pytest.mark.parametrize("m,n", [(1, 1), (1, 3), (3, 1), (13, 10), (10, 13), (300, 257), (1000, 2100)])
 def test_complex_ginibre_sequence(orc, lm, m, n):
     seed, T = 7 + m, min(m, n, 18)
     rng = np.random.default_rng(seed)
