@@ -393,6 +393,10 @@ def main():
                          "frac": achieved / peak, "traffic": traffic, "kernel": dom,
                          "peak_source": peak_kind,
                          "kernel_share_of_step": d["ms"] / tot_ms if tot_ms else None,
+                         "method": "per-launch CUDA events on the operator's stream (the stream the kernels "
+                                   "run on) in an instrumented, non-graph run of the same workload right after "
+                                   "the timed region (events cannot sit between kernels of a graph replay); "
+                                   "achieved = algorithmic bytes per launch / mean launch duration",
                          "step_alg_GBps": tot_bytes / (tot_ms / 1e3) / 1e9 if tot_ms else None,
                          "survey_formula_GBps": alg_bytes_haar(n, T) / (ms_step / 1e3) / 1e9,
                          "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 4),
