@@ -547,17 +547,84 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
     }
   };
   if (t0 < t1) fetchv(t0);
+  // The next draw (Philox + Box-Muller: fp64 transcendentals) of the NEXT
+  // tile is generated one row pair per chunk inside the current tile's
+  // streaming loop, so it overlaps the TMA stream instead of stalling it
+  // at the tile boundary; the first tile's rows are generated up front.
+  double2 gn[4];
+  auto gen = [&](int64_t tile, int q) {
+    const int64_t i = (tile + a.rm.tile0) * kTile + a.rm.gdelta + 2 * (lane + 32 * q);
+    const double2 v = src_pair(a.spec, i, a.n);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (u == q) gn[u] = v;
+  };
+#pragma unroll
+  for (int q = 0; q < 4; ++q) gn[q] = make_double2(0.0, 0.0);
+  if (spec && t0 < t1)
+    for (int q = 0; q < 4; ++q) gen(t0, q);
+  // Epilogue of the lane's rows q of `tile`, given the tile's GEMV-N sums
+  // rq and prefetched rows cvq. (Deferring OTHER's epilogue into the next
+  // tile's streaming loop, like the draw, measured neutral: not done.)
+  auto epi = [&](int64_t tile, int q, double2 rq, double2 cvq) {
+    const int64_t li = (tile + a.rm.tile0) * kTile + 2 * (lane + 32 * q);  // local panel row
+    const int64_t i = li + a.rm.gdelta;                                    // global row
+    const double d0 = (i < a.Dlen) ? a.D[i] : *a.Dtail;
+    const double d1 = (i + 1 < a.Dlen) ? a.D[i + 1] : *a.Dtail;
+    if constexpr (MODE == kApplyFold) {
+      const double2 xv = src_finish(a.x, i, a.n, cvq);
+      const double p0 = (i < a.n) ? d0 * (xv.x - rq.x) : 0.0;
+      const double p1 = (i + 1 < a.n) ? d1 * (xv.y - rq.y) : 0.0;
+      const double c0 = (i >= a.off) ? p0 : 0.0, c1 = (i + 1 >= a.off) ? p1 : 0.0;
+      const double es = *a.escale;
+      st_pair(a.Pw + paddr(li, a.newj, a.K), c0 * es, c1 * es);
+      if (i <= a.off) a.head[i] = p0;
+      if (i + 1 <= a.off) a.head[i + 1] = p1;
+      ss += c0 * c0 + c1 * c1;
+    } else {
+      double z0 = 0.0, z1 = 0.0;
+      if (i < a.zlen) z0 = d0 * a.z[i];
+      if (i + 1 < a.zlen) z1 = d1 * a.z[i + 1];
+      double2 y = make_double2(z0 - rq.x, z1 - rq.y);
+      const Epi<T>& e = a.epi;
+      if (i < a.n) {
+        if (i + 1 >= a.n) y.y = 0.0;
+        const int64_t vi = i - a.rm.vbase;
+        if (e.kind == kEpiTanhMix) {
+          double2 xp = make_double2(0.0, 0.0);
+          if (e.xprev) {
+            xp = cvq;  // prefetched x_{t-1} rows
+            if (e.xprev_scale) {
+              xp.x *= *e.xprev_scale;
+              xp.y *= *e.xprev_scale;
+            }
+          }
+          const double o0 = tanh(2.0 * y.x) + 0.1 * xp.x;
+          const double o1 = (i + 1 < a.n) ? tanh(2.0 * y.y) + 0.1 * xp.y : 0.0;
+          st_pair_guard(e.xnext - a.rm.vbase, i, a.n, o0, o1);
+          bad |= !(isfinite(o0) && isfinite(o1));
+        } else {
+          bad |= !(isfinite(y.x) && isfinite(y.y));
+          ss += y.x * y.x + y.y * y.y;
+        }
+        if (e.y) st_pair_guard(e.y - a.rm.vbase, i, a.n, y.x, y.y);
+      }
+    }
+  };
   uint32_t it = 0;
   for (int64_t tile = t0; tile < t1; ++tile) {
     double2 g[4], r[4], cv[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) cv[q] = nv[q];
+    for (int q = 0; q < 4; ++q) {
+      cv[q] = nv[q];
+      g[q] = gn[q];
+    }
     if (tile + 1 < t1) fetchv(tile + 1);
+    const bool gen_next = spec && tile + 1 < t1;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int64_t li = (tile + a.rm.tile0) * kTile + 2 * (lane + 32 * q);
       const int64_t i = li + a.rm.gdelta;
-      g[q] = spec ? src_pair(a.spec, i, a.n) : make_double2(0.0, 0.0);
       r[q] = make_double2(0.0, 0.0);
       if (a.gcol) {  // the next probe's mix column (masked draw), its norm and pivot
         st_pair(a.gcol + paddr(li, a.gj, a.gK), g[q].x, g[q].y);
@@ -591,54 +658,13 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
         const int u = lane >> 3;
         if ((lane & 7) == 0 && col0 + u < a.ncols) acc[a.slot_spec + col0 + u] += f;
       }
+      if (gen_next && c < 4) gen(tile + 1, c);
     }
+    if (gen_next)
+      for (int q = nch; q < 4; ++q) gen(tile + 1, q);
     // epilogue on the lane's 8 rows
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t li = (tile + a.rm.tile0) * kTile + 2 * (lane + 32 * q);  // local panel row
-      const int64_t i = li + a.rm.gdelta;                                    // global row
-      const double d0 = (i < a.Dlen) ? a.D[i] : *a.Dtail;
-      const double d1 = (i + 1 < a.Dlen) ? a.D[i + 1] : *a.Dtail;
-      if constexpr (MODE == kApplyFold) {
-        const double2 xv = src_finish(a.x, i, a.n, cv[q]);
-        const double p0 = (i < a.n) ? d0 * (xv.x - r[q].x) : 0.0;
-        const double p1 = (i + 1 < a.n) ? d1 * (xv.y - r[q].y) : 0.0;
-        const double c0 = (i >= a.off) ? p0 : 0.0, c1 = (i + 1 >= a.off) ? p1 : 0.0;
-        const double es = *a.escale;
-        st_pair(a.Pw + paddr(li, a.newj, a.K), c0 * es, c1 * es);
-        if (i <= a.off) a.head[i] = p0;
-        if (i + 1 <= a.off) a.head[i + 1] = p1;
-        ss += c0 * c0 + c1 * c1;
-      } else {
-        double z0 = 0.0, z1 = 0.0;
-        if (i < a.zlen) z0 = d0 * a.z[i];
-        if (i + 1 < a.zlen) z1 = d1 * a.z[i + 1];
-        double2 y = make_double2(z0 - r[q].x, z1 - r[q].y);
-        const Epi<T>& e = a.epi;
-        if (i < a.n) {
-          if (i + 1 >= a.n) y.y = 0.0;
-          const int64_t vi = i - a.rm.vbase;
-          if (e.kind == kEpiTanhMix) {
-            double2 xp = make_double2(0.0, 0.0);
-            if (e.xprev) {
-              xp = cv[q];  // prefetched x_{t-1} rows
-              if (e.xprev_scale) {
-                xp.x *= *e.xprev_scale;
-                xp.y *= *e.xprev_scale;
-              }
-            }
-            const double o0 = tanh(2.0 * y.x) + 0.1 * xp.x;
-            const double o1 = (i + 1 < a.n) ? tanh(2.0 * y.y) + 0.1 * xp.y : 0.0;
-            st_pair_guard(e.xnext - a.rm.vbase, i, a.n, o0, o1);
-            bad |= !(isfinite(o0) && isfinite(o1));
-          } else {
-            bad |= !(isfinite(y.x) && isfinite(y.y));
-            ss += y.x * y.x + y.y * y.y;
-          }
-          if (e.y) st_pair_guard(e.y - a.rm.vbase, i, a.n, y.x, y.y);
-        }
-      }
-    }
+    for (int q = 0; q < 4; ++q) epi(tile, q, r[q], cv[q]);
   }
   ss = warp_sum(ss);
   if (lane == 0) acc[a.slot_ss] += ss;
