@@ -256,15 +256,29 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 // global -> shared bulk copy (bytes % 16 == 0, 16 B aligned), evict-first
 // in L2: every panel byte is streamed exactly once per pass.
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "{\n"
-      ".reg .b64 pol;\n"
-      "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n"
-      "}\n" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         bool keep = false) {
+  // streamed panels are read once: evict-first, except chunks the next
+  // kernel re-reads at once (keep: evict-last, see k_dots / ApplyArgs::reverse)
+  if (keep) {
+    asm volatile(
+        "{\n"
+        ".reg .b64 pol;\n"
+        "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n"
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n"
+        "}\n" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n"
+        ".reg .b64 pol;\n"
+        "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n"
+        "}\n" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+  }
 }
 
 // Ampere-style asynchronous 8-byte global -> shared copies (LDGSTS): the

@@ -160,6 +160,9 @@ struct DotArgs {
   int* status = nullptr;
   int prefetch = 0;  // host-asserted: the previous launch writes no panel read here
   unsigned long long* trace = nullptr;  // debug: latest CTA exit time -> trace[8]
+  // bytes of the END of the stream to keep in L2 (evict-last): the fold
+  // that follows streams the same panel last-to-first (ApplyArgs::reverse)
+  int64_t l2_keep = 0;
 };
 
 // Shared-memory carve-up of the streaming kernels (per warp: ring + slots).
@@ -194,6 +197,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_dots(const __grid_constan
   const int nch0 = (a.job[0].ncols + kCW - 1) / kCW;
   const int nch1 = (a.njobs > 1) ? (a.job[1].ncols + kCW - 1) / kCW : 0;
   const uint32_t nst = (uint32_t)((t1 - t0) * (nch0 + nch1));
+  const int64_t keep = a.l2_keep / (W * (int64_t)(kCW * kTile * sizeof(T)));
+  const uint32_t keep_from = keep >= (int64_t)nst ? 0u : nst - (uint32_t)keep;
   auto issue = [&](uint32_t it) {
     const StreamPos p = stream_pos(t0, it, nch0, nch1);
     const DotJob<T>& J = a.job[p.job];
@@ -204,7 +209,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_dots(const __grid_constan
     mbar_arrive_expect_tx(full + s, bytes);
     bulk_g2s(ring + (size_t)s * kCW * kTile * sizeof(T),
              J.P + (size_t)(p.tile + a.rm.tile0) * (size_t)(J.K << kTileShift) + (size_t)p.chunk * kCW * kTile, bytes,
-             full + s);
+             full + s, it >= keep_from);
   };
   // panel chunks written two or more launches back: prefetch, then wait
   if (a.prefetch && lane == 0)
@@ -473,6 +478,14 @@ struct ApplyArgs {
   int nslots = 0;
   int* status = nullptr;
   int prefetch = 0;  // host-asserted: the previous launch writes no panel read here
+  // Stream each warp's tiles (and each tile's chunks) last to first. A fold
+  // right after the k_dots pass over the same panel then starts on the
+  // chunks k_dots read last, which are still in L2.
+  int reverse = 0;
+  // bytes of the END of the stream to keep in L2 (evict-last); for a
+  // reversed fold that is the panel's head of every warp range, which the
+  // next probe's k_dots reads first
+  int64_t l2_keep = 0;
 };
 
 template <typename T, int MODE>
@@ -500,9 +513,13 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
   int64_t t1 = (gw + 1) * a.ntiles / W;
   const int nch = (a.ncols + kCW - 1) / kCW;
   const uint32_t nst = (uint32_t)((t1 - t0) * nch);
+  const int64_t tlast = t1 - 1;
+  const bool rev = a.reverse != 0;
+  const int64_t keep = a.l2_keep / (W * (int64_t)(kCW * kTile * sizeof(T)));
+  const uint32_t keep_from = keep >= (int64_t)nst ? 0u : nst - (uint32_t)keep;
   auto issue = [&](uint32_t it) {
-    const int64_t tile = t0 + it / nch;
-    const int c = (int)(it % nch);
+    const int64_t tile = rev ? tlast - it / nch : t0 + it / nch;
+    const int c = rev ? nch - 1 - (int)(it % nch) : (int)(it % nch);
     const int nc = min(kCW, a.ncols - c * kCW);
     const uint32_t bytes = (uint32_t)(nc * kTile * sizeof(T));
     const int s = it % kRing;
@@ -510,7 +527,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
     mbar_arrive_expect_tx(full + s, bytes);
     bulk_g2s(ring + (size_t)s * kCW * kTile * sizeof(T),
              a.P + (size_t)(tile + a.rm.tile0) * (size_t)(a.K << kTileShift) + (size_t)c * kCW * kTile, bytes,
-             full + s);
+             full + s, it >= keep_from);
   };
   __syncwarp();
   if (a.prefetch && lane == 0)
@@ -546,7 +563,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
       }
     }
   };
-  if (t0 < t1) fetchv(t0);
+  if (t0 < t1) fetchv(rev ? tlast : t0);
   // The next draw (Philox + Box-Muller: fp64 transcendentals) of the NEXT
   // tile is generated one row pair per chunk inside the current tile's
   // streaming loop, so it overlaps the TMA stream instead of stalling it
@@ -562,7 +579,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
 #pragma unroll
   for (int q = 0; q < 4; ++q) gn[q] = make_double2(0.0, 0.0);
   if (spec && t0 < t1)
-    for (int q = 0; q < 4; ++q) gen(t0, q);
+    for (int q = 0; q < 4; ++q) gen(rev ? tlast : t0, q);
   // Epilogue of the lane's rows q of `tile`, given the tile's GEMV-N sums
   // rq and prefetched rows cvq. (Deferring OTHER's epilogue into the next
   // tile's streaming loop, like the draw, measured neutral: not done.)
@@ -612,15 +629,18 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
     }
   };
   uint32_t it = 0;
-  for (int64_t tile = t0; tile < t1; ++tile) {
+  for (int64_t k = 0; k < t1 - t0; ++k) {
+    const int64_t tile = rev ? tlast - k : t0 + k;
+    const int64_t next = rev ? tile - 1 : tile + 1;
+    const bool has_next = k + 1 < t1 - t0;
     double2 g[4], r[4], cv[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       cv[q] = nv[q];
       g[q] = gn[q];
     }
-    if (tile + 1 < t1) fetchv(tile + 1);
-    const bool gen_next = spec && tile + 1 < t1;
+    if (has_next) fetchv(next);
+    const bool gen_next = spec && has_next;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int64_t li = (tile + a.rm.tile0) * kTile + 2 * (lane + 32 * q);
@@ -636,7 +656,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
       const int s = it % kRing;
       mbar_wait(full + s, (it / kRing) & 1);
       const T* sp = reinterpret_cast<const T*>(ring + (size_t)s * kCW * kTile * sizeof(T)) + 2 * lane;
-      const int col0 = c * kCW;
+      const int col0 = (rev ? nch - 1 - c : c) * kCW;
       double d[kCW];
 #pragma unroll
       for (int u = 0; u < kCW; ++u) {
@@ -658,10 +678,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
         const int u = lane >> 3;
         if ((lane & 7) == 0 && col0 + u < a.ncols) acc[a.slot_spec + col0 + u] += f;
       }
-      if (gen_next && c < 4) gen(tile + 1, c);
+      if (gen_next && c < 4) gen(next, c);
     }
     if (gen_next)
-      for (int q = nch; q < 4; ++q) gen(tile + 1, q);
+      for (int q = nch; q < 4; ++q) gen(next, q);
     // epilogue on the lane's 8 rows
 #pragma unroll
     for (int q = 0; q < 4; ++q) epi(tile, q, r[q], cv[q]);

@@ -196,6 +196,9 @@ struct hd_op {
   int spare_sms = 0;  // SMs the persistent streaming grids leave free (HD_SPARE_SMS)
   int max_warps = 8;  // streaming warps per CTA cap (HD_WARPS fixes it)
   bool warps_fixed = false;
+  int fold_reverse = 1;  // fold streams its panel last-to-first (HD_FOLD_FORWARD=1 disables)
+  int64_t l2_keep = 96ll << 20;  // k_dots keeps its last bytes in L2 for that fold (HD_L2_KEEP_MB)
+  int64_t l2_fold_keep = 0;  // ... and the fold its last bytes for the next k_dots (HD_L2_FOLD_KEEP_MB)
   unsigned long long* seed_dev = nullptr;  // Philox key (device word, hd_reseed)
   // hd_run_async bookkeeping, completed by hd_wait
   bool run_pending = false;
