@@ -163,6 +163,7 @@ struct DotArgs {
   // bytes of the END of the stream to keep in L2 (evict-last): the fold
   // that follows streams the same panel last-to-first (ApplyArgs::reverse)
   int64_t l2_keep = 0;
+  int same_rhs = 0;  // host-asserted: job[1].rhs == job[0].rhs (reuse job 0's rows)
 };
 
 // Shared-memory carve-up of the streaming kernels (per warp: ring + slots).
@@ -225,36 +226,55 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_dots(const __grid_constan
 
   double ss0 = 0.0, ss1 = 0.0;
   bool bad = false;
-  double2 x[4], pv[4];
+  double2 x[4], x0[4], pv[4];
   // software pipeline: job 0's vector rows and pending column of the NEXT
-  // tile are loaded while the current tile is processed
-  double2 nx[4], np[4];
+  // tile are loaded while the current tile is processed; the rows are then
+  // finished (scale / mask, or the Philox + Box-Muller draw itself) one row
+  // pair per chunk during the current tile's last job-0 chunks, so draw
+  // generation overlaps the TMA stream instead of stalling it
+  double2 nx[4], np[4], nxf[4];
+  const DotJob<T>& J0 = a.job[0];
+  const int nch0r = (J0.ncols + kCW - 1) / kCW;
   auto fetch0 = [&](int64_t tile) {
-    const DotJob<T>& J = a.job[0];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int64_t li = (tile + a.rm.tile0) * kTile + 2 * (lane + 32 * q);
-      nx[q] = src_raw(J.rhs, li + a.rm.gdelta, a.n);
-      np[q] = (J.pend >= 0) ? ld_pair(J.P + paddr(li, J.pend, J.K)) : make_double2(0.0, 0.0);
+      nx[q] = src_raw(J0.rhs, li + a.rm.gdelta, a.n);
+      np[q] = (J0.pend >= 0) ? ld_pair(J0.P + paddr(li, J0.pend, J0.K)) : make_double2(0.0, 0.0);
     }
   };
-  if (t0 < t1) fetch0(t0);
+  auto finish0 = [&](int64_t tile, int q) {
+    const int64_t i = (tile + a.rm.tile0) * kTile + a.rm.gdelta + 2 * (lane + 32 * q);
+    double2 raw = nx[0];
+#pragma unroll
+    for (int u = 1; u < 4; ++u)
+      if (u == q) raw = nx[u];
+    const double2 v = src_finish(J0.rhs, i, a.n, raw);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (u == q) nxf[u] = v;
+  };
+  if (t0 < t1) {
+    fetch0(t0);
+    for (int q = 0; q < 4; ++q) finish0(t0, q);
+  }
   uint32_t it = 0;
   for (int64_t tile = t0; tile < t1; ++tile) {
-    double2 cx[4], cp[4];
+    double2 cp[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      cx[q] = nx[q];
+      x0[q] = nxf[q];
       cp[q] = np[q];
     }
-    if (tile + 1 < t1) fetch0(tile + 1);
+    const bool has_next = tile + 1 < t1;
+    if (has_next) fetch0(tile + 1);
     for (int jb = 0; jb < a.njobs; ++jb) {
       const DotJob<T>& J = a.job[jb];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int64_t li = (tile + a.rm.tile0) * kTile + 2 * (lane + 32 * q);  // local panel row
         const int64_t i = li + a.rm.gdelta;                                    // global row
-        x[q] = (jb == 0) ? src_finish(J.rhs, i, a.n, cx[q]) : src_pair(J.rhs, i, a.n);
+        x[q] = (jb == 0 || a.same_rhs) ? x0[q] : src_pair(J.rhs, i, a.n);
         const double sq = x[q].x * x[q].x + x[q].y * x[q].y;
         if (jb == 0) ss0 += sq;
         else ss1 += sq;
@@ -290,7 +310,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_dots(const __grid_constan
           const double g = warp_sum4(e[0], e[1], e[2], e[3], lane);
           if ((lane & 7) == 0 && col0 + u <= J.pend) acc[J.slot_pend + col0 + u] += g;
         }
+        if (jb == 0 && has_next && c >= nch0r - 4) finish0(tile + 1, c - (nch0r - 4));
       }
+      if (jb == 0 && has_next)
+        for (int q = 0; q < 4 - nch0r; ++q) finish0(tile + 1, q);
     }
   }
   ss0 = warp_sum(ss0);
