@@ -233,6 +233,12 @@ int hd_rs_normal_vector(hd_rs* rs, int64_t len, double* out);
  * 0 when it is < rho, else sigma_s * normal() (polar). */
 int hd_rs_bernoulli_gaussian(hd_rs* rs, int64_t n, double rho, double sigma_s, double* out);
 uint64_t hd_derive_seed(uint64_t base, uint64_t index); /* random.cpp:73-76 */
+/* The PHILOX draw stream: out[0..n) (device memory) = the Gaussian draw of
+ * probe index `probe` that an operator with (seed, stream) generates on the
+ * device (Philox4x32-10, key = seed, counter = (row pair, probe, stream);
+ * Box-Muller on two 53-bit uniforms). Asynchronous on `stream_ptr`
+ * (cudaStream_t, NULL = legacy default). */
+int hd_philox_normals(uint64_t seed, uint64_t stream, int64_t probe, int64_t n, double* out, void* stream_ptr);
 const char* hd_version(void);
 
 #ifdef __cplusplus

@@ -35,7 +35,7 @@ EXPORTS = (
     "hd_reset_stats", "hd_launch_count", "hd_last_error", "hd_version", "hd_reflector_apply",
     "hd_run_async", "hd_wait", "hd_reseed", "hd_rs_create", "hd_rs_destroy", "hd_rs_next_u64", "hd_rs_uniform",
     "hd_rs_normal", "hd_rs_normal_vector", "hd_rs_bernoulli_gaussian", "hd_derive_seed",
-    "hd_exchange_create_local", "hd_exchange_nccl_id", "hd_exchange_create_nccl", "hd_exchange_destroy",
+    "hd_philox_normals", "hd_exchange_create_local", "hd_exchange_nccl_id", "hd_exchange_create_nccl", "hd_exchange_destroy",
     "hd_shard_plan", "hd_shard_range",
 )
 _NON_STATUS = ("hd_last_error", "hd_version", "hd_rs_destroy", "hd_rs_next_u64", "hd_rs_uniform", "hd_rs_normal",
@@ -122,6 +122,7 @@ def lib():
         L.hd_rs_normal_vector.argtypes = [vp, i64, vp]
         L.hd_rs_bernoulli_gaussian.argtypes = [vp, i64, C.c_double, C.c_double, vp]
         L.hd_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
+        L.hd_philox_normals.argtypes = [C.c_uint64, C.c_uint64, i64, i64, vp, vp]
         L.hd_exchange_create_local.argtypes = [i32, C.POINTER(vp)]
         L.hd_exchange_nccl_id.argtypes = [vp]
         L.hd_exchange_create_nccl.argtypes = [vp, i32, i32, i32, C.POINTER(vp)]

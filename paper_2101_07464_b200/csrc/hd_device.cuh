@@ -46,6 +46,80 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
   return c;
 }
 
+// Straight-line fp64 kernels for the Box-Muller transform (the streaming
+// kernels regenerate draws on the fly, so their instruction count is on the
+// critical path; libdevice's log/sincospi carry special-case branches and
+// range reduction the bounded arguments here never need).
+//
+// ln(x) for x in [2^-53, 1]: x = m 2^e with m in [sqrt(1/2), sqrt(2)),
+// f = m - 1, s = f / (2 + f), ln(1 + f) = f - f^2/2 + s (f^2/2 + R(s^2)) with
+// the degree-14 minimax R of fdlibm's e_log.c (Sun Microsystems, 1993);
+// max error 1 ulp (checked against libm over 2e6 arguments incl. both ends).
+__device__ __forceinline__ double log_unit(double x) {
+  constexpr double Lg1 = 6.666666666666735130e-01, Lg2 = 3.999999999940941908e-01,
+                   Lg3 = 2.857142874366239149e-01, Lg4 = 2.222219843214978396e-01,
+                   Lg5 = 1.818357216161805012e-01, Lg6 = 1.531383769920937332e-01,
+                   Lg7 = 1.479819860511658591e-01;
+  constexpr double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
+  int hi = __double2hiint(x);
+  const int lo = __double2loint(x);
+  int e = (hi >> 20) - 1023;
+  hi = (hi & 0x000fffff) | 0x3ff00000;  // m in [1, 2)
+  if (hi > 0x3ff6a09e) {                // m > sqrt(2): halve it
+    hi -= 0x00100000;
+    e += 1;
+  }
+  const double f = __hiloint2double(hi, lo) - 1.0;  // exact
+  const double d = 2.0 + f;
+  double r;  // d in [1.7, 2.5]: hardware approximation, two Newton steps
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  r = fma(r, fma(-d, r, 1.0), r);
+  r = fma(r, fma(-d, r, 1.0), r);
+  double s = f * r;
+  s = fma(fma(-s, d, f), r, s);
+  const double z = s * s, w = z * z;
+  const double t1 = w * fma(w, fma(w, Lg6, Lg4), Lg2);
+  const double t2 = z * fma(w, fma(w, fma(w, Lg7, Lg5), Lg3), Lg1);
+  const double R = t1 + t2, hfsq = 0.5 * f * f, k = (double)e;
+  return k * ln2_hi - ((hfsq - fma(s, hfsq + R, k * ln2_lo)) - f);
+}
+
+// sqrt(t) for finite t >= 0 without the special-value paths of sqrt():
+// hardware rsqrt approximation, two Newton steps, one residual correction.
+__device__ __forceinline__ double sqrt_nonneg(double t) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(t));
+  const double h = 0.5 * t;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  double r = t * y;
+  r = fma(fma(-r, r, t), 0.5 * y, r);
+  return t > 0.0 ? r : 0.0;
+}
+
+// (sin 2 pi u, cos 2 pi u) for u in [0, 1): u = k/4 + t with |t| <= 1/8 is
+// exact, then fdlibm's __kernel_sin / __kernel_cos minimax polynomials on
+// [-pi/4, pi/4] and a quadrant rotation; max abs error 7e-16.
+__device__ __forceinline__ void sincos_2pi_unit(double u, double* sp, double* cp) {
+  constexpr double S1 = -1.66666666666666324348e-01, S2 = 8.33333333332248946124e-03,
+                   S3 = -1.98412698298579493134e-04, S4 = 2.75573137070700676789e-06,
+                   S5 = -2.50507602534068634195e-08, S6 = 1.58969099521155010221e-10;
+  constexpr double C1 = 4.16666666666666019037e-02, C2 = -1.38888888888741095749e-03,
+                   C3 = 2.48015872894767294178e-05, C4 = -2.75573143513906633035e-07,
+                   C5 = 2.08757232129817482790e-09, C6 = -1.13596475577881948265e-11;
+  const double kq = rint(u * 4.0);
+  const double x = (u - kq * 0.25) * 6.283185307179586232;
+  const double z = x * x;
+  const double ps = fma(z, fma(z, fma(z, fma(z, fma(z, S6, S5), S4), S3), S2), S1);
+  const double pc = fma(z, fma(z, fma(z, fma(z, fma(z, C6, C5), C4), C3), C2), C1);
+  const double sn = fma(x * z, ps, x);
+  const double cs = fma(z * z, pc, fma(-0.5, z, 1.0));
+  const int q = (int)kq & 3;
+  const double a = (q & 1) ? cs : sn, b = (q & 1) ? sn : cs;
+  *sp = (q & 2) ? -a : a;
+  *cp = ((q + 1) & 2) ? -b : b;
+}
+
 // Two N(0,1) draws for rows (2q, 2q+1) of probe `probe` (Box-Muller on two
 // 53-bit uniforms, computed in fp64 for every dtype).
 __device__ __forceinline__ double2 philox_normal_pair(uint64_t seed, uint32_t stream, uint32_t probe, uint64_t q) {
@@ -55,9 +129,9 @@ __device__ __forceinline__ double2 philox_normal_pair(uint64_t seed, uint32_t st
   const uint64_t b = ((uint64_t)w.z << 32) | w.w;
   const double u1 = ((double)(a >> 11) + 1.0) * 0x1.0p-53;  // (0, 1]
   const double u2 = (double)(b >> 11) * 0x1.0p-53;          // [0, 1)
-  const double r = sqrt(-2.0 * log(u1));
+  const double r = sqrt_nonneg(-2.0 * log_unit(u1));
   double s, c;
-  sincospi(2.0 * u2, &s, &c);
+  sincos_2pi_unit(u2, &s, &c);
   return make_double2(r * c, r * s);
 }
 

@@ -1529,6 +1529,16 @@ __global__ void k_reset_chain(ChainDev ch) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *ch.Dtail = 1.0;
 }
 
+// The PHILOX draw stream itself: out[i] = draw i of probe `probe`
+// (hd_philox_normals; the same function the streaming kernels evaluate).
+__global__ void k_philox_normals(uint64_t seed, uint32_t stream, uint32_t probe, int64_t n, double* out) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 2 * q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = philox_normal_pair(seed, stream, probe, (uint64_t)q);
+    out[2 * q] = v.x;
+    if (2 * q + 1 < n) out[2 * q + 1] = v.y;
+  }
+}
+
 __global__ void k_reset_status(int* status) {
   pdl_wait();
   pdl_launch();

@@ -52,6 +52,20 @@ def derive_seed(base: int, index: int) -> int:
     return int(N.lib().hd_derive_seed(int(base) & _MASK, int(index) & _MASK))
 
 
+def philox_normals(seed: int, probe: int, n: int, stream: int = 0, device=None):
+    """The device draw stream of ``draws="philox"`` operators: the length-n
+    Gaussian draw with probe index ``probe`` of an operator built with
+    (seed, stream), as a CUDA float64 tensor (Philox4x32-10, key = seed,
+    counter = (row pair, probe, stream); Box-Muller on 53-bit uniforms)."""
+    import torch
+
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+    out = torch.empty(int(n), dtype=torch.float64, device=dev)
+    N.check(N.lib().hd_philox_normals(int(seed) & _MASK, int(stream) & _MASK, int(probe), int(n),
+                                      C.c_void_p(out.data_ptr()), C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+    return out
+
+
 class RandomSource:
     """The reference's RandomSource(seed, stream) (random.hpp:55-112): xoshiro256++,
     stream k = k jumps of 2^128, polar normal(), ziggurat normal_vector().
