@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libhd_b200.so")
+# HD_LIB overrides the library path (A/B measurements of alternative builds)
+LIB_PATH = os.environ.get("HD_LIB") or os.path.join(_HERE, "lib", "libhd_b200.so")
 
 HD_OK = 0
 HD_ERR_INVALID_ARGUMENT = 1
