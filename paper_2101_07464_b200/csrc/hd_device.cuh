@@ -259,6 +259,28 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Eight warp sums at once (9 shuffles): the full sum of v[(lane >> 2) & 7]
+// in every lane.
+__device__ __forceinline__ double warp_sum8(const double* v, int lane) {
+  const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
+  double e[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const double keep = b16 ? v[u + 4] : v[u], send = b16 ? v[u] : v[u + 4];
+    e[u] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  double f[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const double keep = b8 ? e[u + 2] : e[u], send = b8 ? e[u] : e[u + 2];
+    f[u] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  double g = (b4 ? f[1] : f[0]) + __shfl_xor_sync(0xffffffffu, b4 ? f[0] : f[1], 4);
+  g += __shfl_xor_sync(0xffffffffu, g, 2);
+  g += __shfl_xor_sync(0xffffffffu, g, 1);
+  return g;
+}
+
 // Four warp sums at once (fixed butterfly, 6 shuffles instead of 20).
 // Returns the full sum of d[(lane >> 3) & 3] in every lane.
 __device__ __forceinline__ double warp_sum4(double d0, double d1, double d2, double d3, int lane) {

@@ -167,9 +167,33 @@ struct DotArgs {
 };
 
 // Shared-memory carve-up of the streaming kernels (per warp: ring + slots).
+// Columns per chunk: 4 for fp64, 8 for fp32, so a chunk is 8 KB either way
+// and the per-chunk costs (barrier wait, butterfly, slot update) are spread
+// over the same bytes (fp32: 3.0 -> see DESIGN.md §4.2a).
+template <typename T>
+__host__ __device__ constexpr int chunk_cols() {
+  return sizeof(T) == 8 ? 4 : 8;
+}
+
 template <typename T>
 __host__ __device__ constexpr size_t ring_bytes() {
-  return (size_t)kRing * kCW * kTile * sizeof(T);
+  return (size_t)kRing * chunk_cols<T>() * kTile * sizeof(T);
+}
+
+// Add the warp sums of a chunk's CW per-lane column partials to dst[col0 + u]
+// for col0 + u < lim (fixed butterfly order: deterministic).
+template <int CW>
+__device__ __forceinline__ void add_chunk_sums(const double* d, int lane, int col0, int lim, double* dst) {
+  if constexpr (CW == 4) {
+    const double f = warp_sum4(d[0], d[1], d[2], d[3], lane);
+    const int u = lane >> 3;
+    if ((lane & 7) == 0 && col0 + u < lim) dst[col0 + u] += f;
+  } else {
+    static_assert(CW == 8, "chunk of 4 or 8 columns");
+    const double f = warp_sum8(d, lane);
+    const int u = lane >> 2;
+    if ((lane & 3) == 0 && col0 + u < lim) dst[col0 + u] += f;
+  }
 }
 
 // GEMV-T a = P^T v (k_dots). Lane l holds rows 2(l + 32q) + {0, 1} of the
@@ -177,6 +201,7 @@ __host__ __device__ constexpr size_t ring_bytes() {
 // 32 (or 64 with a pending column) DFMA and one 4-way butterfly.
 template <typename T>
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_dots(const __grid_constant__ DotArgs<T> a) {
+  constexpr int kCW = chunk_cols<T>();
   extern __shared__ __align__(128) unsigned char smem[];
   const int nw = blockDim.x >> 5;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -227,6 +252,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_dots(const __grid_constan
   double ss0 = 0.0, ss1 = 0.0;
   bool bad = false;
   double2 x[4], x0[4], pv[4];
+  float2 xf[4], pf[4];  // fp32 panels: the right-hand sides in fp32 for FFMA
   // software pipeline: job 0's vector rows and pending column of the NEXT
   // tile are loaded while the current tile is processed; the rows are then
   // finished (scale / mask, or the Philox + Box-Muller draw itself) one row
@@ -282,6 +308,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_dots(const __grid_constan
         if (J.pivot_out && (i == J.pivot_row || i + 1 == J.pivot_row)) *J.pivot_out = (i == J.pivot_row) ? x[q].x : x[q].y;
         if (J.wcol) st_pair(J.wcol + paddr(li, J.wj, J.wK), x[q].x, x[q].y);
         pv[q] = (jb == 0) ? cp[q] : (J.pend >= 0) ? ld_pair(J.P + paddr(li, J.pend, J.K)) : make_double2(0.0, 0.0);
+        if constexpr (sizeof(T) == 4) {
+          xf[q] = make_float2((float)x[q].x, (float)x[q].y);
+          pf[q] = make_float2((float)pv[q].x, (float)pv[q].y);
+        }
       }
       const int nch = (J.ncols + kCW - 1) / kCW;
       for (int c = 0; c < nch; ++c, ++it) {
@@ -289,27 +319,41 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_dots(const __grid_constan
         mbar_wait(full + s, (it / kRing) & 1);
         const T* sp = reinterpret_cast<const T*>(ring + (size_t)s * kCW * kTile * sizeof(T)) + 2 * lane;
         double d[kCW], e[kCW];
+        if constexpr (sizeof(T) == 4) {
+          // fp32 panels: the lane's 8 products per column are summed in fp32
+          // (FFMA) and only the partial sums converted, 8 instead of 32
+          // F2F.F64.F32 per chunk; the chunk loop is otherwise conversion-
+          // latency bound at half the fp64 bandwidth
 #pragma unroll
-        for (int u = 0; u < kCW; ++u) {
-          d[u] = 0.0;
-          e[u] = 0.0;
+          for (int u = 0; u < kCW; ++u) {
+            float df = 0.f, ef = 0.f;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const double2 wv = lds_pair(sp + u * kTile + 64 * q);
-            d[u] += wv.x * x[q].x + wv.y * x[q].y;
-            e[u] += wv.x * pv[q].x + wv.y * pv[q].y;
+            for (int q = 0; q < 4; ++q) {
+              const float2 wv = *reinterpret_cast<const float2*>(sp + u * kTile + 64 * q);
+              df = fmaf(wv.x, xf[q].x, fmaf(wv.y, xf[q].y, df));
+              ef = fmaf(wv.x, pf[q].x, fmaf(wv.y, pf[q].y, ef));
+            }
+            d[u] = (double)df;
+            e[u] = (double)ef;
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < kCW; ++u) {
+            d[u] = 0.0;
+            e[u] = 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const double2 wv = lds_pair(sp + u * kTile + 64 * q);
+              d[u] += wv.x * x[q].x + wv.y * x[q].y;
+              e[u] += wv.x * pv[q].x + wv.y * pv[q].y;
+            }
           }
         }
         __syncwarp();
         if (lane == 0 && it + kRing < nst) issue(it + kRing);
         const int col0 = c * kCW;
-        const double f = warp_sum4(d[0], d[1], d[2], d[3], lane);
-        const int u = lane >> 3;
-        if ((lane & 7) == 0 && col0 + u < J.ncols) acc[J.slot_dot + col0 + u] += f;
-        if (J.pend >= 0 && col0 <= J.pend) {
-          const double g = warp_sum4(e[0], e[1], e[2], e[3], lane);
-          if ((lane & 7) == 0 && col0 + u <= J.pend) acc[J.slot_pend + col0 + u] += g;
-        }
+        add_chunk_sums<kCW>(d, lane, col0, J.ncols, acc + J.slot_dot);
+        if (J.pend >= 0 && col0 <= J.pend) add_chunk_sums<kCW>(e, lane, col0, J.pend + 1, acc + J.slot_pend);
         if (jb == 0 && has_next && c >= nch0r - 4) finish0(tile + 1, c - (nch0r - 4));
       }
       if (jb == 0 && has_next)
@@ -513,6 +557,7 @@ struct ApplyArgs {
 
 template <typename T, int MODE>
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_constant__ ApplyArgs<T> a) {
+  constexpr int kCW = chunk_cols<T>();
   extern __shared__ __align__(128) unsigned char smem[];
   const int nw = blockDim.x >> 5;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -664,11 +709,13 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
     }
     if (has_next) fetchv(next);
     const bool gen_next = spec && has_next;
+    float2 gf[4];  // fp32 panels: the next draw in fp32 (exact: fp32 draws are fp32-rounded)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int64_t li = (tile + a.rm.tile0) * kTile + 2 * (lane + 32 * q);
       const int64_t i = li + a.rm.gdelta;
       r[q] = make_double2(0.0, 0.0);
+      gf[q] = make_float2((float)g[q].x, (float)g[q].y);
       if (a.gcol) {  // the next probe's mix column (masked draw), its norm and pivot
         st_pair(a.gcol + paddr(li, a.gj, a.gK), g[q].x, g[q].y);
         gss += g[q].x * g[q].x + g[q].y * g[q].y;
@@ -681,26 +728,51 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
       const T* sp = reinterpret_cast<const T*>(ring + (size_t)s * kCW * kTile * sizeof(T)) + 2 * lane;
       const int col0 = (rev ? nch - 1 - c : c) * kCW;
       double d[kCW];
+      if constexpr (sizeof(T) == 4) {
+        // fp32 panels: chunk-local sums in fp32 (FFMA), converted once per
+        // row pair / column instead of per element (see k_dots)
+        float2 rf[4];
+        float df[kCW];
 #pragma unroll
-      for (int u = 0; u < kCW; ++u) {
-        const double b = (col0 + u < a.ncols) ? beta_s[col0 + u] : 0.0;
-        d[u] = 0.0;
+        for (int q = 0; q < 4; ++q) rf[q] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < kCW; ++u) {
+          const float b = (col0 + u < a.ncols) ? (float)beta_s[col0 + u] : 0.f;
+          df[u] = 0.f;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float2 wv = *reinterpret_cast<const float2*>(sp + u * kTile + 64 * q);
+            if (col0 + u >= a.ncols) wv = make_float2(0.f, 0.f);
+            rf[q].x = fmaf(wv.x, b, rf[q].x);
+            rf[q].y = fmaf(wv.y, b, rf[q].y);
+            df[u] = fmaf(wv.x, gf[q].x, fmaf(wv.y, gf[q].y, df[u]));
+          }
+        }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          double2 wv = lds_pair(sp + u * kTile + 64 * q);
-          if (col0 + u >= a.ncols) wv = make_double2(0.0, 0.0);
-          r[q].x += wv.x * b;
-          r[q].y += wv.y * b;
-          d[u] += wv.x * g[q].x + wv.y * g[q].y;
+          r[q].x += (double)rf[q].x;
+          r[q].y += (double)rf[q].y;
+        }
+#pragma unroll
+        for (int u = 0; u < kCW; ++u) d[u] = (double)df[u];
+      } else {
+#pragma unroll
+        for (int u = 0; u < kCW; ++u) {
+          const double b = (col0 + u < a.ncols) ? beta_s[col0 + u] : 0.0;
+          d[u] = 0.0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            double2 wv = lds_pair(sp + u * kTile + 64 * q);
+            if (col0 + u >= a.ncols) wv = make_double2(0.0, 0.0);
+            r[q].x += wv.x * b;
+            r[q].y += wv.y * b;
+            d[u] += wv.x * g[q].x + wv.y * g[q].y;
+          }
         }
       }
       __syncwarp();
       if (lane == 0 && it + kRing < nst) issue(it + kRing);
-      if (spec) {
-        const double f = warp_sum4(d[0], d[1], d[2], d[3], lane);
-        const int u = lane >> 3;
-        if ((lane & 7) == 0 && col0 + u < a.ncols) acc[a.slot_spec + col0 + u] += f;
-      }
+      if (spec) add_chunk_sums<kCW>(d, lane, col0, a.ncols, acc + a.slot_spec);
       if (gen_next && c < 4) gen(next, c);
     }
     if (gen_next)
