@@ -1,6 +1,7 @@
-"""fp32 storage/streaming (dtype "f32": panels and vectors in fp32, every
-reduction and the k x k algebra in fp64) against the fp64 oracle with the
-north star's fp32 tolerance, 1e-4 relative per iterate."""
+"""fp32 storage/streaming (dtype "f32": panels and vectors in fp32, each
+lane's chunk-local partial sums in fp32, every cross-lane reduction and the
+k x k algebra in fp64) against the fp64 oracle with the north star's fp32
+tolerance, 1e-4 relative per iterate."""
 import threading
 
 import numpy as np
@@ -83,3 +84,21 @@ def test_f32_rectangular_ginibre_and_shards(orc, lm):
     assert not errs, errs
     for t in range(T):
         assert rel(np.concatenate([outs[0][t], outs[1][t]]), want[t]) < TOL32, t
+
+
+def test_f32_config2_scale_against_f64(lm):
+    """Config 2 in fp32 (n = 1e6, T = 100, tanh mix): the fp32 operator (fp32
+    panels, chunk-local fp32 partial sums, fp64 reductions and algebra) tracks
+    the fp64 operator on the same Philox matrix within the fp32 tolerance over
+    the whole trajectory (the fp32 draws are the fp64 draws rounded)."""
+    import torch
+    n, T, seed = 1_000_000, 100, 12
+    x1 = torch.randn(n, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(3))
+    x1 /= x1.norm()
+    x1 = x1.float().double()
+    a = lm.HaarOperator(n, seed=seed, capacity=T)
+    b = lm.HaarOperator(n, seed=seed, dtype="f32", capacity=T)
+    ya = a.run(x1, T, update="tanh_mix", sides="right", keep_trajectory=True)
+    yb = b.run(x1.float(), T, update="tanh_mix", sides="right", keep_trajectory=True)
+    errs = [float((yb[t].double() - ya[t]).norm() / ya[t].norm()) for t in range(T + 1)]
+    assert max(errs) < TOL32, max(errs)
