@@ -79,22 +79,12 @@ __device__ __forceinline__ double2 lds_pair(const T* p) {
   }
 }
 
-// Stage `it` of a warp's stream -> (tile, job, chunk) given per-job chunk
-// counts; the stream is tile-major, then job, then chunk.
+// Position of a chunk in a warp's stream (tile-major, then job, then chunk).
 struct StreamPos {
   int64_t tile;
   int job, chunk;
 };
 
-__device__ __forceinline__ StreamPos stream_pos(int64_t t0, uint32_t it, int nch0, int nch1) {
-  const int per = nch0 + nch1;
-  StreamPos p;
-  p.tile = t0 + it / per;
-  const int r = (int)(it % per);
-  p.job = (r < nch0) ? 0 : 1;
-  p.chunk = (r < nch0) ? r : r - nch0;
-  return p;
-}
 
 // ------------------------------------------------------------------ status
 // status[0]: abort (non-zero: every later kernel of this op returns at once)
@@ -225,8 +215,24 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_dots(const __grid_constan
   const uint32_t nst = (uint32_t)((t1 - t0) * (nch0 + nch1));
   const int64_t keep = a.l2_keep / (W * (int64_t)(kCW * kTile * sizeof(T)));
   const uint32_t keep_from = keep >= (int64_t)nst ? 0u : nst - (uint32_t)keep;
+  // cursor of the next chunk to issue (issue() is called with it = 0, 1, 2, ...):
+  // stream order is tile, then job 0's chunks, then job 1's
+  int64_t cur_k = 0;
+  int cur_j = (nch0 > 0) ? 0 : 1, cur_c = 0;
   auto issue = [&](uint32_t it) {
-    const StreamPos p = stream_pos(t0, it, nch0, nch1);
+    StreamPos p;
+    p.tile = t0 + cur_k;
+    p.job = cur_j;
+    p.chunk = cur_c;
+    if (++cur_c == (cur_j == 0 ? nch0 : nch1)) {
+      cur_c = 0;
+      if (cur_j == 0 && nch1 > 0) {
+        cur_j = 1;
+      } else {
+        cur_j = (nch0 > 0) ? 0 : 1;
+        ++cur_k;
+      }
+    }
     const DotJob<T>& J = a.job[p.job];
     const int nc = min(kCW, J.ncols - p.chunk * kCW);
     const uint32_t bytes = (uint32_t)(nc * kTile * sizeof(T));
@@ -585,9 +591,15 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
   const bool rev = a.reverse != 0;
   const int64_t keep = a.l2_keep / (W * (int64_t)(kCW * kTile * sizeof(T)));
   const uint32_t keep_from = keep >= (int64_t)nst ? 0u : nst - (uint32_t)keep;
+  int64_t cur_k = 0;  // cursor of the next chunk to issue (it = 0, 1, 2, ...)
+  int cur_c = 0;
   auto issue = [&](uint32_t it) {
-    const int64_t tile = rev ? tlast - it / nch : t0 + it / nch;
-    const int c = rev ? nch - 1 - (int)(it % nch) : (int)(it % nch);
+    const int64_t tile = rev ? tlast - cur_k : t0 + cur_k;
+    const int c = rev ? nch - 1 - cur_c : cur_c;
+    if (++cur_c == nch) {
+      cur_c = 0;
+      ++cur_k;
+    }
     const int nc = min(kCW, a.ncols - c * kCW);
     const uint32_t bytes = (uint32_t)(nc * kTile * sizeof(T));
     const int s = it % kRing;
