@@ -960,30 +960,31 @@ __device__ __forceinline__ unsigned long long gtimer() {
     if ((a).trace && threadIdx.x == 0) (a).trace[k] = clock64();   \
   } while (0)
 
-// dst[s] = sum_b parts[(slot0 + s) * nblk + b], thread per slot (fixed order;
-// four independent accumulators so the loads are all in flight together).
 // The single-CTA helpers are all inlined: after the stages were restructured
 // the calls (each a jump into not-yet-fetched code at the start of a launch)
 // cost more than the extra code size — measured 23.33 -> 23.14 ms per config-2
 // run and 66 -> 64 us per probe at tiny n.
-__device__ __forceinline__ void st_reduce(const double* parts, int nblk, int slot0, int count, double* dst, int tid,
-                                          int nthr) {
+
+// One slot's sum over the group partials (fixed order; four independent
+// accumulators so the loads are in flight together).
+// The stages below pick each output's slot from the concatenation of their
+// reduction segments, so all segments reduce in one parallel pass (instead
+// of one st_reduce call after another, with the single-slot sums serialised
+// on thread 0): bitwise identical results.
+__device__ __forceinline__ double st_sum_slot(const double* parts, int nblk, int slot) {
+  const double* ps = parts + (size_t)slot * nblk;
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+  int b = 0;
 #pragma unroll 1
-  for (int s = tid; s < count; s += nthr) {
-    const double* ps = parts + (size_t)(slot0 + s) * nblk;
-    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
-    int b = 0;
-#pragma unroll 1
-    for (; b + 4 <= nblk; b += 4) {
-      v0 += ps[b];
-      v1 += ps[b + 1];
-      v2 += ps[b + 2];
-      v3 += ps[b + 3];
-    }
-#pragma unroll 1
-    for (; b < nblk; ++b) v0 += ps[b];
-    dst[s] = (v0 + v1) + (v2 + v3);
+  for (; b + 4 <= nblk; b += 4) {
+    v0 += ps[b];
+    v1 += ps[b + 1];
+    v2 += ps[b + 2];
+    v3 += ps[b + 3];
   }
+#pragma unroll 1
+  for (; b < nblk; ++b) v0 += ps[b];
+  return (v0 + v1) + (v2 + v3);
 }
 
 // Async-stage `count` contiguous doubles (global -> shared).
@@ -1199,15 +1200,19 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_dots(const __grid_const
   if (HAAR)
     #pragma unroll 1
     for (int j = tid; j < a.kB; j += kSmallThreads) rowB[j] = (double)rowT[j];
-  if (a.kA > 0) st_reduce(ps, a.nblk, a.slotA_dot, a.kA, aA, tid, kSmallThreads);
-  if (a.pendA >= 0) st_reduce(ps, a.nblk, a.slotA_pend, a.pendA + 1, pA, tid, kSmallThreads);
-  if (spec) st_reduce(ss, a.spec_nblk, 0, a.kB, aB, tid, kSmallThreads);
-  else if (a.kB > 0) st_reduce(ps, a.nblk, a.slotB_dot, a.kB, aB, tid, kSmallThreads);
-  if (a.pendB >= 0) st_reduce(ps, a.nblk, a.slotB_pend, a.pendB + 1, pB, tid, kSmallThreads);
-  if (tid == 0) {
-    st_reduce(ps, a.nblk, a.slotA_ss, 1, m.sc + 0, 0, 1);
-    if (a.slotB_ss >= 0) st_reduce(ps, a.nblk, a.slotB_ss, 1, m.sc + 1, 0, 1);
-    else if (spec && a.spec_ss) st_reduce(ss, a.spec_nblk, a.kB, 1, m.sc + 1, 0, 1);
+  {  // all reductions of this stage in one pass (see st_sum_slot)
+    const int nA = a.kA, nPA = a.pendA >= 0 ? a.pendA + 1 : 0, nB = a.kB, nPB = a.pendB >= 0 ? a.pendB + 1 : 0;
+    const bool ssB = a.slotB_ss >= 0 || (spec && a.spec_ss);
+    const int e0 = nA, e1 = e0 + nPA, e2 = e1 + nB, e3 = e2 + nPB, e4 = e3 + 1, e5 = e4 + (ssB ? 1 : 0);
+    #pragma unroll 1
+    for (int t = tid; t < e5; t += kSmallThreads) {
+      if (t < e0) aA[t] = st_sum_slot(ps, a.nblk, a.slotA_dot + t);
+      else if (t < e1) pA[t - e0] = st_sum_slot(ps, a.nblk, a.slotA_pend + t - e0);
+      else if (t < e2) aB[t - e1] = spec ? st_sum_slot(ss, a.spec_nblk, t - e1) : st_sum_slot(ps, a.nblk, a.slotB_dot + t - e1);
+      else if (t < e3) pB[t - e2] = st_sum_slot(ps, a.nblk, a.slotB_pend + t - e2);
+      else if (t < e4) m.sc[0] = st_sum_slot(ps, a.nblk, a.slotA_ss);
+      else m.sc[1] = (a.slotB_ss >= 0) ? st_sum_slot(ps, a.nblk, a.slotB_ss) : st_sum_slot(ss, a.spec_nblk, a.kB);
+    }
   }
   __syncthreads();
   HD_CLK(a, 11);
@@ -1442,8 +1447,14 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_gin(const __grid_consta
   if (tid == 0) m.sc[0] = (a.pendB >= 0) ? a.chB.c[a.pendB] : 0.0;
   cp_async_wait_all();
   __syncthreads();
-  if (a.kB > 0) st_reduce(ps, a.nblk, a.slotB_dot, a.kB, ag, tid, kSmallThreads);
-  if (a.pendB >= 0) st_reduce(ps, a.nblk, a.slotB_pend, a.pendB + 1, pB, tid, kSmallThreads);
+  {  // both reductions in one pass (see st_sum_slot)
+    const int e0 = a.kB, e1 = e0 + (a.pendB >= 0 ? a.pendB + 1 : 0);
+    #pragma unroll 1
+    for (int t = tid; t < e1; t += kSmallThreads) {
+      if (t < e0) ag[t] = st_sum_slot(ps, a.nblk, a.slotB_dot + t);
+      else pB[t - e0] = st_sum_slot(ps, a.nblk, a.slotB_pend + t - e0);
+    }
+  }
   #pragma unroll 1
   for (int64_t i = tid; i < nr; i += kSmallThreads) cps[i] *= dsg[i];
   __syncthreads();
