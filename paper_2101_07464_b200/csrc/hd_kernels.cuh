@@ -969,7 +969,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // accumulators so the loads are in flight together).
 // The stages below pick each output's slot from the concatenation of their
 // reduction segments, so all segments reduce in one parallel pass (instead
-// of one st_reduce call after another, with the single-slot sums serialised
+// of one reduction call after another, with the single-slot sums serialised
 // on thread 0): bitwise identical results.
 __device__ __forceinline__ double st_sum_slot(const double* parts, int nblk, int slot) {
   const double* ps = parts + (size_t)slot * nblk;
