@@ -180,6 +180,24 @@ int hd_wait(hd_op* op);
  * host synchronisation: one captured run graph serves every trial seed. */
 int hd_reseed(hd_op* op, uint64_t seed);
 
+/* Batched independent trials (BASELINE config 3; the reference runs trials
+ * on threads, parallel.hpp): `count` operators of one ensemble, shape and
+ * dtype (device Philox draws, unsharded, real) each run `args` (iterations,
+ * update, side_rule; device vectors) from a fresh state with its own seed,
+ * x_1 = items[i].x1, writing x_{T+1} to items[i].out. Every kernel launch of
+ * the run is issued once for all operators (gridDim.y = count); the launch
+ * sequence is recorded and captured in one CUDA graph on the first call for a
+ * given operator set and replayed afterwards. Asynchronous on args->stream;
+ * the operators must be idle. Results equal `count` separate hd_run calls
+ * bitwise. Non-finite steps are not reported (each operator's status words
+ * hold them). */
+typedef struct hd_batch_item {
+  const void* x1;  /* device x_1 (op dtype) */
+  void* out;       /* device x_{T+1}        */
+  uint64_t seed;   /* RandomSource seed     */
+} hd_batch_item;
+int hd_batch_run(hd_op* const* ops, int32_t count, const hd_run_args* args, const hd_batch_item* items);
+
 /* User update map on device memory: called once per step after the probe
  * with y_t and the history window newest first (device pointers of the op's
  * dtype, each dim elements); must write x_{t+1} into `next` on `stream`.

@@ -36,7 +36,7 @@ EXPORTS = (
     "hd_reset_stats", "hd_launch_count", "hd_last_error", "hd_version", "hd_reflector_apply",
     "hd_run_async", "hd_wait", "hd_reseed", "hd_rs_create", "hd_rs_destroy", "hd_rs_next_u64", "hd_rs_uniform",
     "hd_rs_normal", "hd_rs_normal_vector", "hd_rs_bernoulli_gaussian", "hd_derive_seed",
-    "hd_philox_normals", "hd_exchange_create_local", "hd_exchange_nccl_id", "hd_exchange_create_nccl", "hd_exchange_destroy",
+    "hd_philox_normals", "hd_batch_run", "hd_exchange_create_local", "hd_exchange_nccl_id", "hd_exchange_create_nccl", "hd_exchange_destroy",
     "hd_shard_plan", "hd_shard_range",
 )
 _NON_STATUS = ("hd_last_error", "hd_version", "hd_rs_destroy", "hd_rs_next_u64", "hd_rs_uniform", "hd_rs_normal",
@@ -58,6 +58,10 @@ class hd_run_args(C.Structure):
         ("x0", C.c_void_p), ("on_device", C.c_int32), ("use_graph", C.c_int32), ("traj", C.c_void_p),
         ("final_out", C.c_void_p), ("stream", C.c_void_p),
     ]
+
+
+class hd_batch_item(C.Structure):
+    _fields_ = [("x1", C.c_void_p), ("out", C.c_void_p), ("seed", C.c_uint64)]
 
 
 class hd_kernel_stats(C.Structure):
@@ -124,6 +128,7 @@ def lib():
         L.hd_rs_bernoulli_gaussian.argtypes = [vp, i64, C.c_double, C.c_double, vp]
         L.hd_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
         L.hd_philox_normals.argtypes = [C.c_uint64, C.c_uint64, i64, i64, vp, vp]
+        L.hd_batch_run.argtypes = [C.POINTER(vp), i32, C.POINTER(hd_run_args), C.POINTER(hd_batch_item)]
         L.hd_exchange_create_local.argtypes = [i32, C.POINTER(vp)]
         L.hd_exchange_nccl_id.argtypes = [vp]
         L.hd_exchange_create_nccl.argtypes = [vp, i32, i32, i32, C.POINTER(vp)]

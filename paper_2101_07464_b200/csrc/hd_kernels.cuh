@@ -190,7 +190,7 @@ __device__ __forceinline__ void add_chunk_sums(const double* d, int lane, int co
 // current tile's right-hand side(s); each 4-column chunk costs 16 LDS.128,
 // 32 (or 64 with a pending column) DFMA and one 4-way butterfly.
 template <typename T>
-__global__ void __launch_bounds__(kMaxWarps * 32, 1) k_dots(const __grid_constant__ DotArgs<T> a) {
+__device__ __forceinline__ void k_dots_impl(const DotArgs<T>& a) {
   constexpr int kCW = chunk_cols<T>();
   extern __shared__ __align__(128) unsigned char smem[];
   const int nw = blockDim.x >> 5;
@@ -386,6 +386,16 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_dots(const __grid_constan
     atomicMax(a.trace + 8, t);
   }
 }
+template <typename T>
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) k_dots(const __grid_constant__ DotArgs<T> a) {
+  k_dots_impl<T>(a);
+}
+// batched twin: one launch serves gridDim.y operators, trial blockIdx.y's
+// arguments read from a device table (BatchPlan, hd_batch_run)
+template <typename T>
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) k_dots_b(const DotArgs<T>* __restrict__ argv) {
+  k_dots_impl<T>(argv[blockIdx.y]);
+}
 
 // ============================================================ GEMV-N core
 // Thread layout for the update kernels: one 256-row tile per block of 128
@@ -562,7 +572,7 @@ struct ApplyArgs {
 };
 
 template <typename T, int MODE>
-__global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_constant__ ApplyArgs<T> a) {
+__device__ __forceinline__ void k_apply_impl(const ApplyArgs<T>& a) {
   constexpr int kCW = chunk_cols<T>();
   extern __shared__ __align__(128) unsigned char smem[];
   const int nw = blockDim.x >> 5;
@@ -813,6 +823,16 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_consta
   }
   flush_row(accs, a.nslots, a.out);
 }
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply(const __grid_constant__ ApplyArgs<T> a) {
+  k_apply_impl<T, MODE>(a);
+}
+// batched twin: one launch serves gridDim.y operators, trial blockIdx.y's
+// arguments read from a device table (BatchPlan, hd_batch_run)
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) k_apply_b(const ApplyArgs<T>* __restrict__ argv) {
+  k_apply_impl<T, MODE>(argv[blockIdx.y]);
+}
 
 // ============================================================ k_ginout
 // Ginibre output side (ginibre.hpp:73-83 / 92-102 restated):
@@ -848,7 +868,7 @@ struct GinArgs {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(kUpdThreads) k_ginout(const __grid_constant__ GinArgs<T> a) {
+__device__ __forceinline__ void k_ginout_impl(const GinArgs<T>& a) {
   extern __shared__ double beta_s[];  // [3][K]
   __shared__ double red_s[32];
   pdl_wait();
@@ -886,6 +906,16 @@ __global__ void __launch_bounds__(kUpdThreads) k_ginout(const __grid_constant__ 
   const double y0 = a.sigma * (accS.x + cc * u0 + (c0 - acc[1].x));
   const double y1 = a.sigma * (accS.y + cc * u1 + (c1 - acc[1].y));
   epilogue(a.epi, a.status, i, a.n, make_double2(y0, y1), red_s, a.rm.vbase);
+}
+template <typename T>
+__global__ void __launch_bounds__(kUpdThreads) k_ginout(const __grid_constant__ GinArgs<T> a) {
+  k_ginout_impl<T>(a);
+}
+// batched twin: one launch serves gridDim.y operators, trial blockIdx.y's
+// arguments read from a device table (BatchPlan, hd_batch_run)
+template <typename T>
+__global__ void __launch_bounds__(kUpdThreads) k_ginout_b(const GinArgs<T>* __restrict__ argv) {
+  k_ginout_impl<T>(argv[blockIdx.y]);
 }
 
 // Scratch words shared between the small kernels of one probe.
@@ -1130,7 +1160,7 @@ __device__ __forceinline__ SmallSmem small_smem(double* base, int kv) {
 // H(g, off) appended to chain B or (Ginibre) the opposite-side sparse
 // coefficients (half 2), and the power-of-two fold-column scale.
 template <typename T, bool HAAR>
-__global__ void __launch_bounds__(kSmallThreads) k_small_dots(const __grid_constant__ SmallArgs a) {
+__device__ __forceinline__ void k_small_dots_impl(const SmallArgs& a) {
   extern __shared__ double ssm[];
   HD_STAMP(a, 0);
   pdl_wait();
@@ -1294,12 +1324,22 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_dots(const __grid_const
     HD_STAMP(a, 4);
   }
 }
+template <typename T, bool HAAR>
+__global__ void __launch_bounds__(kSmallThreads) k_small_dots(const __grid_constant__ SmallArgs a) {
+  k_small_dots_impl<T, HAAR>(a);
+}
+// batched twin: one launch serves gridDim.y operators, trial blockIdx.y's
+// arguments read from a device table (BatchPlan, hd_batch_run)
+template <typename T, bool HAAR>
+__global__ void __launch_bounds__(kSmallThreads) k_small_dots_b(const SmallArgs* __restrict__ argv) {
+  k_small_dots_impl<T, HAAR>(argv[blockIdx.y]);
+}
 
 // After k_apply(FOLD): finalise the fold reflector H(p, off) (appended
 // unless the skip fault fires), then (Haar) beta = sig (T_B (W_B^T D_B z))
 // for the sparse folded iterate z = H p, or (Ginibre) the current coefficient.
 template <typename T, bool HAAR>
-__global__ void __launch_bounds__(kSmallThreads) k_small_fold(const __grid_constant__ SmallArgs a) {
+__device__ __forceinline__ void k_small_fold_impl(const SmallArgs& a) {
   extern __shared__ double ssm[];
   pdl_wait();
   pdl_launch();
@@ -1400,12 +1440,22 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_fold(const __grid_const
     for (int j = tid; j < a.kB; j += kSmallThreads) a.beta1[j] = sgB[j] * az[j];
   }
 }
+template <typename T, bool HAAR>
+__global__ void __launch_bounds__(kSmallThreads) k_small_fold(const __grid_constant__ SmallArgs a) {
+  k_small_fold_impl<T, HAAR>(a);
+}
+// batched twin: one launch serves gridDim.y operators, trial blockIdx.y's
+// arguments read from a device table (BatchPlan, hd_batch_run)
+template <typename T, bool HAAR>
+__global__ void __launch_bounds__(kSmallThreads) k_small_fold_b(const SmallArgs* __restrict__ argv) {
+  k_small_fold_impl<T, HAAR>(argv[blockIdx.y]);
+}
 
 // Ginibre, after k_dots over the opposite chain with v = D g_m: pending
 // column, beta1 = sig (T (sig a_g)) for the new basis vector (half 1), beta3
 // for the sparse part L-rev-adj(c) (half 2), same-side store coefficients.
 template <typename T>
-__global__ void __launch_bounds__(kSmallThreads) k_small_gin(const __grid_constant__ SmallArgs a) {
+__device__ __forceinline__ void k_small_gin_impl(const SmallArgs& a) {
   extern __shared__ double ssm[];
   pdl_wait();
   pdl_launch();
@@ -1498,10 +1548,32 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_gin(const __grid_consta
     a.beta3[j] = sg[j] * o3[j];
   }
 }
+template <typename T>
+__global__ void __launch_bounds__(kSmallThreads) k_small_gin(const __grid_constant__ SmallArgs a) {
+  k_small_gin_impl<T>(a);
+}
+// batched twin: one launch serves gridDim.y operators, trial blockIdx.y's
+// arguments read from a device table (BatchPlan, hd_batch_run)
+template <typename T>
+__global__ void __launch_bounds__(kSmallThreads) k_small_gin_b(const SmallArgs* __restrict__ argv) {
+  k_small_gin_impl<T>(argv[blockIdx.y]);
+}
 
 // Normalize dynamics: inv = ||y|| > 0 ? 1/||y|| : 1 (bench.cpp:25-28).
-__global__ void __launch_bounds__(kSmallThreads) k_small_norm(const double* partials, int nblk, double* scal,
-                                                              int* status, int step) {
+struct NormArgs {
+  const double* partials = nullptr;
+  int nblk = 0;
+  double* scal = nullptr;
+  int* status = nullptr;
+  int step = 0;
+};
+
+__device__ __forceinline__ void k_small_norm_impl(const NormArgs& na) {
+  const double* partials = na.partials;
+  const int nblk = na.nblk;
+  double* scal = na.scal;
+  int* status = na.status;
+  const int step = na.step;
   pdl_wait();
   pdl_launch();
   if (aborted(status)) return;
@@ -1523,6 +1595,10 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_norm(const double* part
       atomicOr(status + kStAbort, 1);
     }
   }
+}
+__global__ void __launch_bounds__(kSmallThreads) k_small_norm(const __grid_constant__ NormArgs a) { k_small_norm_impl(a); }
+__global__ void __launch_bounds__(kSmallThreads) k_small_norm_b(const NormArgs* __restrict__ argv) {
+  k_small_norm_impl(argv[blockIdx.y]);
 }
 
 // x = scale * y (materialise a lazily normalised iterate).
@@ -1616,13 +1692,15 @@ __global__ void __launch_bounds__(kReflThreads) k_reflector(const double* p, int
   }
 }
 
-__global__ void k_reset_chain(ChainDev ch) {
+__device__ __forceinline__ void k_reset_chain_impl(const ChainDev& ch) {
   pdl_wait();
   pdl_launch();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ch.Dlen; i += (int64_t)gridDim.x * blockDim.x)
     ch.Drow[i] = 1.0;
   if (blockIdx.x == 0 && threadIdx.x == 0) *ch.Dtail = 1.0;
 }
+__global__ void k_reset_chain(ChainDev ch) { k_reset_chain_impl(ch); }
+__global__ void k_reset_chain_b(const ChainDev* __restrict__ argv) { k_reset_chain_impl(argv[blockIdx.y]); }
 
 // The PHILOX draw stream itself: out[i] = draw i of probe `probe`
 // (hd_philox_normals; the same function the streaming kernels evaluate).
@@ -1634,7 +1712,7 @@ __global__ void k_philox_normals(uint64_t seed, uint32_t stream, uint32_t probe,
   }
 }
 
-__global__ void k_reset_status(int* status) {
+__device__ __forceinline__ void k_reset_status_impl(int* status) {
   pdl_wait();
   pdl_launch();
   if (threadIdx.x == 0) {
@@ -1643,5 +1721,7 @@ __global__ void k_reset_status(int* status) {
     status[kStBadInput] = 0;
   }
 }
+__global__ void k_reset_status(int* status) { k_reset_status_impl(status); }
+__global__ void k_reset_status_b(int* const* __restrict__ argv) { k_reset_status_impl(argv[blockIdx.y]); }
 
 }  // namespace hd

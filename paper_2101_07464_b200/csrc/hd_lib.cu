@@ -24,6 +24,8 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <tuple>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/hd.h"
@@ -139,6 +141,16 @@ namespace {
 struct CxState;  // complex-field operator state (hd_complex_host.inc)
 }
 
+// One recorded launch of a single operator (batched runs, hd_batch_run): the
+// kernel, its launch shape and its one by-value parameter.
+struct BatchRec {
+  const void* fn = nullptr;
+  dim3 grid, block;
+  size_t smem = 0;
+  std::vector<unsigned char> arg;
+};
+struct BatchPlan;
+
 struct hd_op {
   hd_config cfg{};
   int ens = 0;
@@ -193,6 +205,9 @@ struct hd_op {
   std::map<long, int> apply_bps;
   int last_other_grid = 0, last_other_slot_ss = 0;  // normalize partials of k_apply(OTHER)
   bool pdl = true;  // programmatic dependent launch (HD_NO_PDL=1 disables)
+  std::vector<BatchRec>* rec = nullptr;  // recording instead of launching (hd_batch_run)
+  int batch_hint = 1;                    // operators sharing each launch (grid sizing)
+  std::shared_ptr<BatchPlan> batch;      // cached batched run (this op leads it)
   int spare_sms = 0;  // SMs the persistent streaming grids leave free (HD_SPARE_SMS)
   int max_warps = 8;  // streaming warps per CTA cap (HD_WARPS fixes it)
   bool warps_fixed = false;
@@ -221,6 +236,27 @@ struct hd_op {
   std::vector<PendingEv> evq;
   std::vector<cudaEvent_t> evpool;
   int64_t launches = 0;
+};
+
+// A batched run (hd_batch_run): the launch sequence of one run recorded for
+// every operator of the batch, each launch replayed ONCE with gridDim.y =
+// operators and the per-operator parameters in a device table (arena), and
+// the whole sequence captured in one CUDA graph. Operators run in lockstep
+// (same shape, iterations and side schedule), so their sequences match.
+struct BatchPlan {
+  std::string key;
+  std::vector<hd_op*> ops;
+  cudaGraphExec_t graph = nullptr;
+  unsigned char* arena = nullptr;
+  std::vector<Counters> end_state;   // host counters of each operator after the run
+  std::vector<const void*> fin;      // where each operator's x_{T+1} ends up
+  int64_t dim1 = 0, fdim = 0;
+  int64_t launches = 0;              // batched kernels in the graph
+  int64_t op_launches = 0;           // kernels one operator would have launched
+  ~BatchPlan() {
+    if (graph) cudaGraphExecDestroy(graph);
+    if (arena) cudaFree(arena);
+  }
 };
 
 namespace {
@@ -465,6 +501,23 @@ void check_launch(const char* what) {
 template <typename... KArgs, typename... Args>
 void launch_k(hd_op* op, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
               Args&&... args) {
+  if (op->rec) {  // batched-run recording: keep the launch, do not issue it
+    if constexpr (sizeof...(KArgs) == 1) {
+      using A = std::decay_t<std::tuple_element_t<0, std::tuple<KArgs...>>>;
+      const A v(std::forward<Args>(args)...);
+      BatchRec r;
+      r.fn = reinterpret_cast<const void*>(kernel);
+      r.grid = grid;
+      r.block = block;
+      r.smem = smem;
+      r.arg.resize(sizeof(A));
+      std::memcpy(r.arg.data(), &v, sizeof(A));
+      op->rec->push_back(std::move(r));
+      return;
+    } else {
+      throw HdError(HD_ERR_RUNTIME, "hd: this launch cannot be batched");
+    }
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -498,7 +551,8 @@ int launch_tma(hd_op* op, cudaStream_t s, void (*kernel)(Args), Args& args, size
   const size_t budget = (size_t)optin - 1024;
   if (shared_fixed + per_warp > budget) throw HdError(HD_ERR_RESOURCE_CAP, "hd: chain too long for one CTA");
   const int nw_cap = (int)std::min<size_t>(std::min(kMaxWarps, op->max_warps), (budget - shared_fixed) / per_warp);
-  const int sms = std::max(1, op->nsm - op->spare_sms);
+  // a batched launch shares the SMs among its operators
+  const int sms = std::max(1, (op->nsm - op->spare_sms) / std::max(1, op->batch_hint));
   int nw = nw_cap;
   if (!op->warps_fixed) {
     double best = -1.0;

@@ -491,16 +491,53 @@ class Reflector:
         return y
 
 
+def batch_run(ops, x1, out, seeds, iterations: int, update: str = "normalize", sides: str = "alternate",
+              stream=None) -> None:
+    """hd_batch_run: operators of one shape run the same dynamics in lockstep
+    from fresh states (seed per operator), every kernel launch issued once for
+    all of them (include/hd.h). x1 / out: (len(ops), dim) CUDA tensors of the
+    operators' dtype; asynchronous on `stream` (default: torch's current)."""
+    import torch
+
+    B = len(ops)
+    a = N.hd_run_args()
+    a.update = N.UPDATES[update]
+    a.side_rule = N.SIDE_RULES[sides]
+    a.iterations = int(iterations)
+    a.on_device = 1
+    a.use_graph = 1
+    st = stream if stream is not None else torch.cuda.current_stream(x1.device)
+    a.stream = st.cuda_stream
+    handles = (C.c_void_p * B)(*[op._h for op in ops])
+    items = (N.hd_batch_item * B)()
+    for b in range(B):
+        items[b].x1 = x1[b].data_ptr()
+        items[b].out = out[b].data_ptr()
+        items[b].seed = int(seeds[b]) & _MASK
+    N.check(N.lib().hd_batch_run(handles, B, C.byref(a), items))
+
+
 def run_trials(ensemble: str, trials: int, n: int, T: int, *, m: int = None, sigma: float = None, seed: int = 1,
                dtype: str = "f64", update: str = "normalize", sides: str = "alternate", concurrency: int = 16,
-               x1=None, first_trial: int = 0, device: int = 0, return_ops: bool = False):
+               x1=None, first_trial: int = 0, device: int = 0, return_ops: bool = False, batch: int = 1,
+               ops=None):
     """Independent HD trials (BASELINE config 3: trial b uses seed + b). Keeps
     `concurrency` device operators in flight, each on its own CUDA stream
     replaying one captured run graph (reseeded per trial), so the latency of
     one trial's probe sequence overlaps the HBM streaming of the others.
+    batch > 1: `concurrency` groups of `batch` operators, each group's trials
+    sharing every kernel launch (batch_run / hd_batch_run) — the separate-graph
+    mode is bound by the kernel-dispatch rate at config-3 sizes.
     Returns x_{T+1} of every trial as a (trials, dim) CUDA tensor.
-    x1: optional (trials, dim) CUDA tensor; default N(0, I) per trial."""
+    x1: optional (trials, dim) CUDA tensor; default N(0, I) per trial.
+    ops: the operators a previous call returned (return_ops=True) with the same
+    arguments, reused instead of allocating new ones."""
     import torch
+
+    if batch > 1:
+        return _run_trials_batched(ensemble, trials, n, T, m=m, sigma=sigma, seed=seed, dtype=dtype, update=update,
+                                   sides=sides, groups=concurrency, batch=batch, x1=x1, first_trial=first_trial,
+                                   device=device, return_ops=return_ops, pool=ops)
 
     m = n if m is None else m
     if sigma is None:
@@ -512,7 +549,8 @@ def run_trials(ensemble: str, trials: int, n: int, T: int, *, m: int = None, sig
         "haar": lambda: HaarOperator(n, seed, dtype=dtype, capacity=T, device=device),
         "goe": lambda: GOEOperator(n, seed, sigma=sigma, dtype=dtype, capacity=T, device=device),
     }[ensemble]
-    ops = [make() for _ in range(max(1, min(concurrency, trials)))]
+    if ops is None:
+        ops = [make() for _ in range(max(1, min(concurrency, trials)))]
     dim1 = n if (ensemble != "ginibre" or sides != "left") else m
     fdim = ops[0]._final_dim(T, sides, dim1)
     if x1 is None:
@@ -540,6 +578,57 @@ def run_trials(ensemble: str, trials: int, n: int, T: int, *, m: int = None, sig
             busy.append(op)
             nxt += 1
     return (out, ops) if return_ops else out
+
+
+def _run_trials_batched(ensemble, trials, n, T, *, m, sigma, seed, dtype, update, sides, groups, batch, x1,
+                        first_trial, device, return_ops, pool):
+    import torch
+
+    m = n if m is None else m
+    if sigma is None:
+        sigma = 1.0 / float(n) ** 0.5
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    dev = torch.device("cuda", device)
+    make = {
+        "ginibre": lambda: GinibreOperator(m, n, sigma, seed, dtype=dtype, capacity=T, device=device),
+        "haar": lambda: HaarOperator(n, seed, dtype=dtype, capacity=T, device=device),
+        "goe": lambda: GOEOperator(n, seed, sigma=sigma, dtype=dtype, capacity=T, device=device),
+    }[ensemble]
+    batch = max(1, min(batch, trials))
+    ngroups = max(1, min(groups, -(-trials // batch)))
+    tail = trials % batch
+    if pool is not None:  # (groups, tail operators, streams) of a previous call
+        grp, tail_ops, streams = pool
+    else:
+        grp = [[make() for _ in range(batch)] for _ in range(ngroups)]
+        tail_ops = [make() for _ in range(tail)] if tail else []  # a ragged last chunk: its own group
+        streams = [torch.cuda.Stream(device=dev) for _ in range(ngroups)]
+    dim1 = n if (ensemble != "ginibre" or sides != "left") else m
+    fdim = grp[0][0]._final_dim(T, sides, dim1)
+    if x1 is None:
+        x1 = torch.empty((trials, dim1), dtype=tdt, device=dev)
+        for b in range(trials):
+            g = torch.Generator(device=dev).manual_seed(seed + first_trial + b)
+            x1[b] = torch.randn(dim1, dtype=tdt, device=dev, generator=g)
+    out = torch.empty((trials, fdim), dtype=tdt, device=dev)
+    main = torch.cuda.current_stream(dev)
+    for st in streams:
+        st.wait_stream(main)
+    chunk = 0
+    for b0 in range(0, trials - tail, batch):
+        gi = chunk % ngroups
+        with torch.cuda.stream(streams[gi]):
+            seeds = [seed + first_trial + b0 + j for j in range(batch)]
+            batch_run(grp[gi], x1[b0:b0 + batch], out[b0:b0 + batch], seeds, T, update, sides, stream=streams[gi])
+        chunk += 1
+    if tail:
+        b0 = trials - tail
+        with torch.cuda.stream(streams[0]):
+            seeds = [seed + first_trial + b0 + j for j in range(tail)]
+            batch_run(tail_ops, x1[b0:], out[b0:], seeds, T, update, sides, stream=streams[0])
+    for st in streams:
+        main.wait_stream(st)
+    return (out, (grp, tail_ops, streams)) if return_ops else out
 
 
 class DynamicsSpec:
