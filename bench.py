@@ -42,6 +42,13 @@ def alg_bytes_haar(n: int, T: int, s: int = 8) -> float:
     return float(s) * n * (3.0 * T * (T + 1) / 2.0 + 2.0 * T)
 
 
+def alg_bytes_haar_2p(n: int, T: int, s: int = 8) -> float:
+    """Two-pass Haar run: s*n*(2t+5) summed over t = 1..T
+    (both panels read once, the new fold column, x_t, x_{t+1}, x_{t-1} and the
+    next mix column)."""
+    return float(s) * n * (2.0 * T * (T + 1) / 2.0 + 5.0 * T)
+
+
 def rank_seed(base: int, rank: int) -> int:
     """One independent trial per rank (trial sharding)."""
     return base + 1000 * rank
@@ -399,6 +406,7 @@ def main():
                                    "achieved = algorithmic bytes per launch / mean launch duration",
                          "step_alg_GBps": tot_bytes / (tot_ms / 1e3) / 1e9 if tot_ms else None,
                          "survey_formula_GBps": alg_bytes_haar(n, T) / (ms_step / 1e3) / 1e9,
+                         "two_pass_formula_GBps": alg_bytes_haar_2p(n, T) / (ms_step / 1e3) / 1e9,
                          "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 4),
                                          "alg_GB": round(v["alg_bytes"] / 1e9, 4)} for k, v in stats.items()}},
             "clocks": clocks,

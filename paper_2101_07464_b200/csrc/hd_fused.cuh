@@ -1,0 +1,681 @@
+// Two-pass Haar runs: inside a device-resident run with an
+// elementwise update map, probe t's GEMV-N over the fold chain and probe
+// t+1's GEMV-T over the same chain share ONE stream of the fold panel, so a
+// Haar probe reads each panel once (s·n·(2t+5) bytes instead of s·n·(3t+2)).
+//
+// What makes this possible is an early, algebraic ‖p[off:]‖: the fold is an
+// orthogonal map, so ‖p‖ = ‖x‖ and ‖p[off:]‖² = ‖x‖² − Σ_{i<off} p_i², where
+// the head rows p_i (i ≤ off) come from the k x k corner of the panel. With
+// ‖p[off:]‖ known before the pass, z = H p, y = other-rev-adj(z) and the
+// dynamics update x_{t+1} are available row by row inside the pass, so the
+// fold panel's rows can be dotted with x_{t+1} while they are applied to x_t.
+// The new fold column's Gram column follows from the same identity:
+//   W^T p[off:] = D_tail (W^T x − G β̂ − W_h^T (x_h − u_h)),  u = W β̂,
+// h = rows < off (reflect.hpp:120-176 restated in compact-WY form).
+// Both are cancellation-free while ‖p[off:]‖ is not small against ‖x‖; the
+// stage checks that (a priori, and a posteriori against the exact ‖p[off:]‖²
+// the pass reduces) and otherwise flags kStFused, on which the host re-runs
+// the whole run through the three-pass probe sequence.
+#pragma once
+
+#include "hd_kernels.cuh"
+
+namespace hd {
+
+enum { kStFused = 3 };  // status word: the two-pass run lost precision (host re-runs)
+
+// scalar slots of the two-pass stage (after the shared ones)
+enum FusedSlot { kScDold = 7, kScNrm2e = 8, kScWordsUsed = 9 };
+
+// ============================================================ k_haar2p
+// Per warp tile: stream the OTHER chain (GEMV-N y = D_O z − P_O β_O, plus the
+// speculative GEMV-T of the next draw, as k_apply<OTHER>), finish y and the
+// update x_{t+1} for the lane's rows, then stream the FOLD chain: GEMV-N
+// p = D_old (x_t − P_F β_F) and GEMV-T P_F^T x_{t+1} from the same chunks; the
+// new fold column p[off+1:]·2^-e is written and dotted with x_{t+1}.
+template <typename T>
+struct FusedArgs {
+  // other chain
+  const T* PO = nullptr;
+  int64_t KO = 0;
+  int ncolsO = 0;
+  const double* betaO = nullptr;
+  const double* DO = nullptr;
+  const double* DOtail = nullptr;
+  int64_t DOlen = 0;
+  const double* z = nullptr;
+  int64_t zlen = 0;
+  Epi<T> epi;  // kEpiTanhMix (xprev -> xnext) or kEpiPlain (y = x_{t+1})
+  Src<T> spec;  // next probe's draw (kSrcNone: off)
+  T* gcol = nullptr;
+  int64_t gj = 0;
+  double* gpivot = nullptr;
+  int64_t gpivot_row = -1;
+  // fold chain
+  const T* PF = nullptr;
+  int64_t KF = 0;
+  int ncolsF = 0;
+  const double* betaF = nullptr;
+  const double* Dold = nullptr;  // fold D on rows >= off before this probe's member
+  Src<T> x;                      // x_t
+  T* Pw = nullptr;               // = PF, column newj
+  int64_t newj = 0, off = 0;
+  const double* escale = nullptr;
+  // slots: [spec: ncolsO][gss: 1][aF: ncolsF + 1][xss: 1][pss: 1]
+  int slot_spec = 0, slot_gss = 0, slot_aF = 0, slot_xss = 0, slot_pss = 0;
+  int64_t n = 0, ntiles = 0;
+  Flush out;
+  int nslots = 0;
+  int* status = nullptr;
+  int prefetch = 0;
+  int64_t pivot_tile = -1;  // tile holding row off: its warp waits before the first TMA
+};
+
+template <typename T>
+__device__ __forceinline__ void k_haar2p_impl(const FusedArgs<T>& a) {
+  constexpr int kCW = chunk_cols<T>();
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int nw = blockDim.x >> 5;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nsl = (a.nslots + 1) & ~1;
+  const int nbO = (a.ncolsO + 1) & ~1, nbF = (a.ncolsF + 1) & ~1;
+  unsigned char* ring = smem + (size_t)w * ring_bytes<T>();
+  double* bO = reinterpret_cast<double*>(smem + (size_t)nw * ring_bytes<T>());
+  double* bF = bO + nbO;
+  double* accs = bF + nbF;
+  double* acc = accs + (size_t)w * nsl;
+  uint64_t* full = reinterpret_cast<uint64_t*>(accs + (size_t)nw * nsl) + w * kRing;
+  for (int s = lane; s < nsl; s += 32) acc[s] = 0.0;
+  if (lane == 0) {
+    for (int s = 0; s < kRing; ++s) mbar_init(full + s, 1);
+    mbar_fence_init();
+  }
+  const bool spec = (a.spec.kind != kSrcNone);
+  const int64_t W = (int64_t)gridDim.x * nw;
+  const int64_t gw = (int64_t)blockIdx.x * nw + w;
+  const int64_t t0 = gw * a.ntiles / W;
+  int64_t t1 = (gw + 1) * a.ntiles / W;
+  const int nchO = (a.ncolsO + kCW - 1) / kCW;
+  const int nchF = (a.ncolsF + kCW - 1) / kCW;
+  const int nchT = nchO + nchF;
+  const uint32_t nst = (uint32_t)((t1 - t0) * nchT);
+  // issue cursor: tile, then O's chunks, then F's
+  int64_t cur_k = 0;
+  int cur_c = 0;
+  auto issue = [&](uint32_t it) {
+    const int64_t tile = t0 + cur_k;
+    const int c = cur_c;
+    if (++cur_c == nchT) {
+      cur_c = 0;
+      ++cur_k;
+    }
+    const bool isO = c < nchO;
+    const int cc = isO ? c : c - nchO;
+    const int ncols = isO ? a.ncolsO : a.ncolsF;
+    const T* P = isO ? a.PO : a.PF;
+    const int64_t K = isO ? a.KO : a.KF;
+    const int nc = min(kCW, ncols - cc * kCW);
+    const uint32_t bytes = (uint32_t)(nc * kTile * sizeof(T));
+    const int s = it % kRing;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive_expect_tx(full + s, bytes);
+    bulk_g2s(ring + (size_t)s * kCW * kTile * sizeof(T), P + (size_t)tile * (size_t)(K << kTileShift) + (size_t)cc * kCW * kTile,
+             bytes, full + s, false);
+  };
+  __syncwarp();
+  // the stage before this kernel writes the pivot entry of O's new column:
+  // the warp streaming that tile issues only after the wait
+  const bool pf = a.prefetch && !(a.pivot_tile >= t0 && a.pivot_tile < t1);
+  if (pf && lane == 0)
+    for (uint32_t it = 0; it < (uint32_t)kRing && it < nst; ++it) issue(it);
+  pdl_wait();
+  pdl_launch();
+  if (!pf && lane == 0)
+    for (uint32_t it = 0; it < (uint32_t)kRing && it < nst; ++it) issue(it);
+  for (int j = threadIdx.x; j < a.ncolsO; j += blockDim.x) bO[j] = a.betaO[j];
+  for (int j = threadIdx.x; j < a.ncolsF; j += blockDim.x) bF[j] = a.betaF[j];
+  __syncthreads();
+  if (aborted(a.status)) {
+    for (uint32_t it = 0; it < (uint32_t)kRing && it < nst; ++it) mbar_wait(full + it % kRing, 0);
+    t1 = t0;
+  }
+  const double dold = *a.Dold;
+  const double es = *a.escale;
+  const bool tanh_mix = (a.epi.kind == kEpiTanhMix);
+  double ssx = 0.0, ssp = 0.0, gss = 0.0, dnew = 0.0;
+  bool bad = false;
+  // software pipeline: the next tile's x_t rows and x_{t-1} rows
+  double2 nx[4], np[4];
+  auto fetch = [&](int64_t tile) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = tile * kTile + 2 * (lane + 32 * q);
+      nx[q] = src_raw(a.x, i, a.n);
+      np[q] = make_double2(0.0, 0.0);
+      if (tanh_mix && a.epi.xprev && i < a.n) {
+        np[q].x = (double)a.epi.xprev[i];
+        if (i + 1 < a.n) np[q].y = (double)a.epi.xprev[i + 1];
+      }
+    }
+  };
+  if (t0 < t1) fetch(t0);
+  double2 gn[4];
+  auto gen = [&](int64_t tile, int q) {
+    const int64_t i = tile * kTile + 2 * (lane + 32 * q);
+    const double2 v = src_pair(a.spec, i, a.n);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (u == q) gn[u] = v;
+  };
+#pragma unroll
+  for (int q = 0; q < 4; ++q) gn[q] = make_double2(0.0, 0.0);
+  if (spec && t0 < t1)
+    for (int q = 0; q < 4; ++q) gen(t0, q);
+
+  uint32_t it = 0;
+  for (int64_t tile = t0; tile < t1; ++tile) {
+    const bool has_next = tile + 1 < t1;
+    double2 g[4], xt[4], xp[4], r[4], xn[4];
+    float2 gf[4], xnf[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      xt[q] = src_finish(a.x, tile * kTile + 2 * (lane + 32 * q), a.n, nx[q]);
+      xp[q] = np[q];
+      g[q] = gn[q];
+      gf[q] = make_float2((float)g[q].x, (float)g[q].y);
+      r[q] = make_double2(0.0, 0.0);
+    }
+    if (has_next) fetch(tile + 1);
+    const bool gen_next = spec && has_next;
+    if (a.gcol) {  // the next probe's mix column (masked draw), its norm and pivot
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t i = tile * kTile + 2 * (lane + 32 * q);
+        st_pair(a.gcol + paddr(i, a.gj, a.KO), g[q].x, g[q].y);
+        gss += g[q].x * g[q].x + g[q].y * g[q].y;
+        if (i == a.gpivot_row || i + 1 == a.gpivot_row) *a.gpivot = (i == a.gpivot_row) ? g[q].x : g[q].y;
+      }
+    }
+    // ---- other chain: y rows and the speculative dots
+    for (int c = 0; c < nchO; ++c, ++it) {
+      const int s = it % kRing;
+      mbar_wait(full + s, (it / kRing) & 1);
+      const T* sp = reinterpret_cast<const T*>(ring + (size_t)s * kCW * kTile * sizeof(T)) + 2 * lane;
+      const int col0 = c * kCW;
+      double d[kCW];
+      if constexpr (sizeof(T) == 4) {
+        float2 rf[4];
+        float df[kCW];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) rf[q] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < kCW; ++u) {
+          const float b = (col0 + u < a.ncolsO) ? (float)bO[col0 + u] : 0.f;
+          df[u] = 0.f;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float2 wv = *reinterpret_cast<const float2*>(sp + u * kTile + 64 * q);
+            if (col0 + u >= a.ncolsO) wv = make_float2(0.f, 0.f);
+            rf[q].x = fmaf(wv.x, b, rf[q].x);
+            rf[q].y = fmaf(wv.y, b, rf[q].y);
+            df[u] = fmaf(wv.x, gf[q].x, fmaf(wv.y, gf[q].y, df[u]));
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          r[q].x += (double)rf[q].x;
+          r[q].y += (double)rf[q].y;
+        }
+#pragma unroll
+        for (int u = 0; u < kCW; ++u) d[u] = (double)df[u];
+      } else {
+#pragma unroll
+        for (int u = 0; u < kCW; ++u) {
+          const double b = (col0 + u < a.ncolsO) ? bO[col0 + u] : 0.0;
+          d[u] = 0.0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            double2 wv = lds_pair(sp + u * kTile + 64 * q);
+            if (col0 + u >= a.ncolsO) wv = make_double2(0.0, 0.0);
+            r[q].x += wv.x * b;
+            r[q].y += wv.y * b;
+            d[u] += wv.x * g[q].x + wv.y * g[q].y;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0 && it + kRing < nst) issue(it + kRing);
+      if (spec) add_chunk_sums<kCW>(d, lane, col0, a.ncolsO, acc + a.slot_spec);
+      if (gen_next && c < 4) gen(tile + 1, c);
+    }
+    if (gen_next)
+      for (int q = nchO; q < 4; ++q) gen(tile + 1, q);
+    // ---- y = D_O z - acc and the update x_{t+1} (rows >= n stay zero)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = tile * kTile + 2 * (lane + 32 * q);
+      const double d0 = (i < a.DOlen) ? a.DO[i] : *a.DOtail;
+      const double d1 = (i + 1 < a.DOlen) ? a.DO[i + 1] : *a.DOtail;
+      double z0 = 0.0, z1 = 0.0;
+      if (i < a.zlen) z0 = d0 * a.z[i];
+      if (i + 1 < a.zlen) z1 = d1 * a.z[i + 1];
+      double2 y = make_double2(z0 - r[q].x, z1 - r[q].y);
+      double2 o = make_double2(0.0, 0.0);
+      if (i < a.n) {
+        if (i + 1 >= a.n) y.y = 0.0;
+        if (tanh_mix) {
+          o.x = tanh(2.0 * y.x) + 0.1 * xp[q].x;
+          o.y = (i + 1 < a.n) ? tanh(2.0 * y.y) + 0.1 * xp[q].y : 0.0;
+          st_pair_guard(a.epi.xnext, i, a.n, o.x, o.y);
+        } else {
+          o = y;
+        }
+        if (a.epi.y) st_pair_guard(a.epi.y, i, a.n, y.x, y.y);
+        bad |= !(isfinite(o.x) && isfinite(o.y));
+      }
+      if constexpr (sizeof(T) == 4) {  // the iterate as stored (fp32) is what later passes read
+        o.x = (double)(float)o.x;
+        o.y = (double)(float)o.y;
+      }
+      xn[q] = o;
+      xnf[q] = make_float2((float)o.x, (float)o.y);
+      ssx += o.x * o.x + o.y * o.y;
+      r[q] = make_double2(0.0, 0.0);
+    }
+    // ---- fold chain: p = D_old (x_t - P_F beta_F) and P_F^T x_{t+1}
+    for (int c = 0; c < nchF; ++c, ++it) {
+      const int s = it % kRing;
+      mbar_wait(full + s, (it / kRing) & 1);
+      const T* sp = reinterpret_cast<const T*>(ring + (size_t)s * kCW * kTile * sizeof(T)) + 2 * lane;
+      const int col0 = c * kCW;
+      double d[kCW];
+      if constexpr (sizeof(T) == 4) {
+        float2 rf[4];
+        float df[kCW];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) rf[q] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < kCW; ++u) {
+          const float b = (col0 + u < a.ncolsF) ? (float)bF[col0 + u] : 0.f;
+          df[u] = 0.f;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float2 wv = *reinterpret_cast<const float2*>(sp + u * kTile + 64 * q);
+            if (col0 + u >= a.ncolsF) wv = make_float2(0.f, 0.f);
+            rf[q].x = fmaf(wv.x, b, rf[q].x);
+            rf[q].y = fmaf(wv.y, b, rf[q].y);
+            df[u] = fmaf(wv.x, xnf[q].x, fmaf(wv.y, xnf[q].y, df[u]));
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          r[q].x += (double)rf[q].x;
+          r[q].y += (double)rf[q].y;
+        }
+#pragma unroll
+        for (int u = 0; u < kCW; ++u) d[u] = (double)df[u];
+      } else {
+#pragma unroll
+        for (int u = 0; u < kCW; ++u) {
+          const double b = (col0 + u < a.ncolsF) ? bF[col0 + u] : 0.0;
+          d[u] = 0.0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            double2 wv = lds_pair(sp + u * kTile + 64 * q);
+            if (col0 + u >= a.ncolsF) wv = make_double2(0.0, 0.0);
+            r[q].x += wv.x * b;
+            r[q].y += wv.y * b;
+            d[u] += wv.x * xn[q].x + wv.y * xn[q].y;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0 && it + kRing < nst) issue(it + kRing);
+      add_chunk_sums<kCW>(d, lane, col0, a.ncolsF, acc + a.slot_aF);
+    }
+    // ---- the new fold column: rows > off from p (row off: the stage wrote
+    // the pivot entry), its exact ||p[off:]||^2 and its dot with x_{t+1}
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = tile * kTile + 2 * (lane + 32 * q);
+      const double p0 = (i < a.n) ? dold * (xt[q].x - r[q].x) : 0.0;
+      const double p1 = (i + 1 < a.n) ? dold * (xt[q].y - r[q].y) : 0.0;
+      double c0 = (i > a.off) ? (double)(T)(p0 * es) : 0.0;
+      double c1 = (i + 1 > a.off) ? (double)(T)(p1 * es) : 0.0;
+      if (i >= a.off) ssp += p0 * p0;
+      if (i + 1 >= a.off) ssp += p1 * p1;
+      if (i == a.off) {
+        c0 = (double)a.Pw[paddr(i, a.newj, a.KF)];
+        a.Pw[paddr(i + 1, a.newj, a.KF)] = (T)c1;
+      } else if (i + 1 == a.off) {
+        a.Pw[paddr(i, a.newj, a.KF)] = (T)c0;
+        c1 = (double)a.Pw[paddr(i + 1, a.newj, a.KF)];
+      } else {
+        st_pair(a.Pw + paddr(i, a.newj, a.KF), c0, c1);
+      }
+      dnew += c0 * xn[q].x + c1 * xn[q].y;
+    }
+  }
+  ssx = warp_sum(ssx);
+  ssp = warp_sum(ssp);
+  dnew = warp_sum(dnew);
+  if (lane == 0) {
+    acc[a.slot_xss] += ssx;
+    acc[a.slot_pss] += ssp;
+    acc[a.slot_aF + a.ncolsF] += dnew;
+  }
+  if (a.gcol) {
+    gss = warp_sum(gss);
+    if (lane == 0) acc[a.slot_gss] += gss;
+  }
+  if (bad) {
+    atomicMin(a.status + kStBadStep, a.epi.step);
+    atomicOr(a.status + kStAbort, 1);
+  }
+  __syncthreads();
+  for (int s = threadIdx.x; s < a.nslots; s += blockDim.x) {
+    double v = 0.0;
+    for (int u = 0; u < nw; ++u) v += accs[(size_t)u * nsl + s];
+    accs[s] = v;
+  }
+  flush_row(accs, a.nslots, a.out);
+}
+template <typename T>
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) k_haar2p(const __grid_constant__ FusedArgs<T> a) {
+  k_haar2p_impl<T>(a);
+}
+
+// ============================================================ k_small_2p
+// The single-CTA stage of a two-pass Haar probe (replaces k_small_dots +
+// k_small_fold): reduce the previous pass's partials; half 2 appends the mix
+// reflector H(g, off) to the other chain (haar.hpp:57,63) from the
+// speculative dots; half 1 builds the fold coefficients β_F = sig T_F^T (sig a),
+// the head rows p[0..off] from the panel corner, the early ‖p[off:]‖ and the
+// fold reflector H(p, off) with its Gram and T columns (haar.hpp:55-56);
+// then β_O for y = other-rev-adj(z), z = H p (haar.hpp:65).
+struct Small2pArgs {
+  const double* partials = nullptr;  // [slot][nblk]
+  int nblk = 0, nslots_in = 0;
+  int slot_aF = 0, slot_xss = 0, slot_spec = 0, slot_gss = 0, slot_pss = -1;
+  double* scal = nullptr;
+  int* status = nullptr;
+  ChainDev chF, chO;
+  void* PF = nullptr;
+  void* PO = nullptr;
+  int kF = 0, kO = 0;  // member counts before this probe's appends
+  int64_t off = 0;
+  int rule = 0;
+  const void* x = nullptr;  // x_t (dtype by template), head rows read
+  double* head = nullptr;   // p[0..off]
+  double* zbuf = nullptr;
+  double* betaF = nullptr;
+  double* betaO = nullptr;
+  double guard = 1e-4;      // required ||p[off:]||^2 / ||x||^2
+  double check_tol = 1e-8;  // |exact - early| / early of the previous probe's ||p[off:]||^2
+  int stageTF = 0, stageTO = 0, stageCF = 0, stageCO = 0;
+};
+
+template <typename T>
+__device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
+  extern __shared__ double ssm[];
+  pdl_wait();
+  pdl_launch();
+  const int kF = a.kF, kO = a.kO;
+  const int64_t off = a.off, nr = off + 1;
+  const int kv = small_kv(kF + 1, kO + 1);
+  const SmallSmem m = small_smem(ssm, kv);
+  double* aF = m.v0;    // P_F^T x (raw)
+  double* sgF = m.v1;
+  double* uF = m.v2;    // sig a  -> later W^T p_tail
+  double* bh = m.v3;    // beta-hat = T^T uF
+  double* b1 = m.v4;    // sig beta-hat (raw coefficients)
+  double* gF = m.v5;    // new Gram column
+  double* tF = m.v6;    // new T column (F)
+  double* aO = m.v7;    // spec dots (raw)
+  double* sgO = m.v8;
+  double* rowO = m.v9;  // P_O[off, :] incl. the new column
+  double* gO = m.v10;
+  double* tO = m.v11;
+  double* sc = m.sc;
+  double* ps = sc + 16;                                                   // [nslots_in][nblk]
+  double* hp = ps + (size_t)a.nslots_in * a.nblk;                         // [16][nr] head partials
+  double* xh = hp + (size_t)(kHalf / 32) * nr;                            // x[0..off]
+  double* ph = xh + nr;                                                   // p[0..off]
+  double* dF = ph + nr;                                                   // D_F[0..off] (old)
+  double* dO = dF + nr;                                                   // D_O[0..off] (old)
+  double* tsF = dO + nr;                                                  // T_F stage
+  double* tsO = tsF + (a.stageTF ? (size_t)kF * (kF | 1) : 0);            // T_O stage
+  T* cF = reinterpret_cast<T*>(tsO + (a.stageTO ? (size_t)kO * (kO | 1) : 0));  // corner F [kF][nr]
+  T* cO = cF + (a.stageCF ? (size_t)kF * nr : 0);                         // corner O [kO][nr]
+  int* st = reinterpret_cast<int*>(sc + 12);
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const T* PF = (const T*)a.PF;
+  const T* PO = (const T*)a.PO;
+  const T* X = (const T*)a.x;
+  // ---- phase 1: every global load issued asynchronously, one wait
+  const TView tvF = a.stageTF ? st_stage_T(a.chF, kF, tsF, tid, kSmallThreads) : TView{a.chF.Tm, a.chF.K};
+  const TView tvO = a.stageTO ? st_stage_T(a.chO, kO, tsO, tid, kSmallThreads) : TView{a.chO.Tm, a.chO.K};
+  st_stage(a.partials, (int64_t)a.nslots_in * a.nblk, ps, tid, kSmallThreads);
+#pragma unroll 1
+  for (int j = tid; j < kF; j += kSmallThreads) cp_async8(sgF + j, a.chF.sig + j);
+#pragma unroll 1
+  for (int j = tid; j < kO; j += kSmallThreads) cp_async8(sgO + j, a.chO.sig + j);
+#pragma unroll 1
+  for (int64_t i = tid; i < nr; i += kSmallThreads) {
+    cp_async8(dF + i, i < a.chF.Dlen ? a.chF.Drow + i : a.chF.Dtail);
+    cp_async8(dO + i, i < a.chO.Dlen ? a.chO.Drow + i : a.chO.Dtail);
+  }
+  if (a.stageCF)
+#pragma unroll 1
+    for (int j = w; j < kF; j += kSmallThreads / 32)
+#pragma unroll 1
+      for (int64_t i = lane; i < nr; i += 32) cp_async_elem(cF + j * nr + i, PF + paddr(i, j, a.chF.K));
+  if (a.stageCO)
+#pragma unroll 1
+    for (int j = w; j < kO; j += kSmallThreads / 32)
+#pragma unroll 1
+      for (int64_t i = lane; i < nr; i += 32) cp_async_elem(cO + j * nr + i, PO + paddr(i, j, a.chO.K));
+  if (tid == 0) {
+    cp_async8(sc + 4, a.scal + kScPivotG);
+    cp_async8(sc + 7, a.chF.Dtail);
+    cp_async8(sc + 8, a.scal + kScNrm2e);
+    cp_async4(st + 0, a.status + kStAbort);
+    cp_async4(st + 1, a.status + kStBadInput);
+  }
+#pragma unroll 1
+  for (int64_t i = tid; i < nr; i += kSmallThreads) xh[i] = (double)X[i];
+  cp_async_wait_all();
+  __syncthreads();
+  if (st[0] != 0) return;
+  if (st[1] != 0) {  // non-finite probe input seen by the first pass: abort
+    if (tid == 0) *(volatile int*)(a.status + kStAbort) = 1;
+    return;
+  }
+  {  // all reductions in one parallel pass
+    const int e0 = kF, e1 = e0 + kO, e2 = e1 + 1, e3 = e2 + 1, e4 = e3 + (a.slot_pss >= 0 ? 1 : 0);
+#pragma unroll 1
+    for (int t = tid; t < e4; t += kSmallThreads) {
+      if (t < e0) aF[t] = st_sum_slot(ps, a.nblk, a.slot_aF + t);
+      else if (t < e1) aO[t - e0] = st_sum_slot(ps, a.nblk, a.slot_spec + t - e0);
+      else if (t < e2) sc[0] = st_sum_slot(ps, a.nblk, a.slot_xss);
+      else if (t < e3) sc[1] = st_sum_slot(ps, a.nblk, a.slot_gss);
+      else sc[2] = st_sum_slot(ps, a.nblk, a.slot_pss);
+    }
+  }
+#pragma unroll 1
+  for (int j = tid; j < kO; j += kSmallThreads) rowO[j] = a.stageCO ? (double)cO[j * nr + off] : (double)PO[paddr(off, j, a.chO.K)];
+  __syncthreads();
+  if (a.slot_pss >= 0 && tid == 0) {  // a posteriori check of the previous probe's early norm
+    const double ex = sc[2], ea = sc[8];
+    if (!(fabs(ex - ea) <= a.check_tol * ea)) {
+      atomicOr(a.status + kStFused, 1);
+      atomicOr(a.status + kStAbort, 1);
+      st[0] = 1;
+    }
+  }
+  if (tid < kHalf) {
+    // ---- half 1: fold chain
+#pragma unroll 1
+    for (int j = tid; j < kF; j += kHalf) uF[j] = sgF[j] * aF[j];
+    named_sync(1, kHalf);
+    st_Tt(tvF, kF, uF, bh, -1, nullptr, 0, kHalf / 32);
+    named_sync(1, kHalf);
+#pragma unroll 1
+    for (int j = tid; j < kF; j += kHalf) {
+      b1[j] = sgF[j] * bh[j];
+      a.betaF[j] = b1[j];
+    }
+    named_sync(1, kHalf);
+    // head rows p_i = D_i (x_i - sum_j P[i, j] b1_j), i <= off: warp per
+    // column, lanes over rows (coalesced), per-warp partial rows added in
+    // fixed order
+    {
+      double* hw = hp + (size_t)w * nr;
+#pragma unroll 1
+      for (int64_t i = lane; i < nr; i += 32) hw[i] = 0.0;
+#pragma unroll 1
+      for (int j = w; j < kF; j += kHalf / 32) {
+        const double b = b1[j];
+        if (a.stageCF) {
+#pragma unroll 1
+          for (int64_t i = lane; i < nr; i += 32) hw[i] += (double)cF[j * nr + i] * b;
+        } else {
+#pragma unroll 1
+          for (int64_t i = lane; i < nr; i += 32) hw[i] += (double)PF[paddr(i, j, a.chF.K)] * b;
+        }
+      }
+    }
+    named_sync(1, kHalf);
+#pragma unroll 1
+    for (int64_t i = tid; i < nr; i += kHalf) {
+      double v = 0.0;
+#pragma unroll 1
+      for (int u = 0; u < kHalf / 32; ++u) v += hp[(size_t)u * nr + i];
+      ph[i] = dF[i] * (xh[i] - v);
+      a.head[i] = ph[i];
+      if (i < off) a.zbuf[i] = ph[i];
+    }
+    named_sync(1, kHalf);
+    // W^T p[off:] = D_old (uF - G bh - sig W_h^T (D ph)_h)  (normalised W)
+#pragma unroll 1
+    for (int j = w; j < kF; j += kHalf / 32) {
+      double v = 0.0, h = 0.0;
+      const double* Gj = a.chF.G + (int64_t)j * a.chF.K;  // symmetric column j
+#pragma unroll 1
+      for (int l = lane; l < kF; l += 32) v += Gj[l] * bh[l];
+      if (a.stageCF) {
+#pragma unroll 1
+        for (int64_t i = lane; i < off; i += 32) h += (double)cF[j * nr + i] * dF[i] * ph[i];
+      } else {
+#pragma unroll 1
+        for (int64_t i = lane; i < off; i += 32) h += (double)PF[paddr(i, j, a.chF.K)] * dF[i] * ph[i];
+      }
+      v = warp_sum(v);
+      h = warp_sum(h);
+      if (lane == 0) gF[j] = sc[7] * ((uF[j] - v) - sgF[j] * h);
+    }
+    if (w == 0) {
+      double hs = 0.0;
+#pragma unroll 1
+      for (int64_t i = lane; i < off; i += 32) hs += ph[i] * ph[i];
+      hs = warp_sum(hs);
+      if (lane == 0) {
+        const double xss = sc[0];
+        const double nrm2 = xss - hs;
+        double nrm = 0.0;
+        if (!(nrm2 >= a.guard * xss) || !(nrm2 > 0.0 || xss == 0.0)) {
+          atomicOr(a.status + kStFused, 1);
+          atomicOr(a.status + kStAbort, 1);
+        } else {
+          nrm = sqrt(nrm2);
+        }
+        const double xn = sqrt(xss);
+        int e = 0;
+        if (xn > 0.0 && isfinite(xn)) frexp(xn, &e);
+        const double escale = ldexp(1.0, -e), iscale = ldexp(1.0, e);
+        a.scal[kScEscale] = escale;
+        a.scal[kScIscale] = iscale;
+        a.scal[kScDold] = sc[7];
+        a.scal[kScNrm2e] = nrm * nrm;
+        const double piv = ph[off];
+        const double sign = st_reflector<T>(a.chF, (T*)a.PF, kF, off, nrm, piv, a.rule, escale, iscale, true);
+        const double zoff = (nrm == 0.0) ? piv : (sign == 0.0 ? 0.0 : nrm);
+        a.scal[kScNrm] = nrm;
+        a.scal[kScCoefCur] = zoff;
+        a.scal[kScSign] = sign;
+        a.zbuf[off] = zoff;
+        sc[3] = nrm;
+        sc[5] = sign;
+        sc[6] = (nrm == 0.0) ? 0.0 : a.chF.c[kF];
+        sc[9] = zoff;
+      }
+    }
+    named_sync(1, kHalf);
+    const double nrm = sc[3], sign = sc[5], cnew = sc[6];
+#pragma unroll 1
+    for (int j = tid; j < kF; j += kHalf) {
+      const double rowv = a.stageCF ? (double)cF[j * nr + off] : (double)PF[paddr(off, j, a.chF.K)];
+      const double g = (nrm == 0.0) ? 0.0 : gF[j] / nrm + sign * sgF[j] * rowv;
+      gF[j] = g;
+      a.chF.G[j + (int64_t)kF * a.chF.K] = g;
+      a.chF.G[kF + (int64_t)j * a.chF.K] = g;
+    }
+    if (tid == 0) a.chF.G[kF + (int64_t)kF * a.chF.K] = (nrm == 0.0) ? 0.0 : 2.0 / cnew;
+    named_sync(1, kHalf);
+    if (nrm != 0.0) st_D_update(a.chF, off, -sign, tid, kHalf);
+    st_T_column(a.chF, tvF, kF, cnew, gF, tF, 0, kHalf / 32);
+  } else {
+    // ---- half 2: other chain, mix reflector H(g, off) -> column kO
+    const int t2 = tid - kHalf;
+    const double nrm = sqrt(sc[1]);
+    const double piv = sc[4];
+    if (t2 == 0) {
+      const double sign = st_reflector<T>(a.chO, (T*)a.PO, kO, off, nrm, piv, a.rule, 1.0, 1.0, true);
+      sc[10] = sign;
+      sc[11] = (nrm == 0.0) ? 0.0 : a.chO.c[kO];
+      sgO[kO] = (nrm == 0.0) ? 0.0 : 1.0 / nrm;
+      rowO[kO] = (nrm == 0.0) ? 0.0 : (double)(T)(piv + sign * nrm);
+      // D_O[off] after the update (z's row off is scaled by it in the pass)
+      sc[13] = (nrm == 0.0) ? dO[off] : -sign * dO[off];
+    }
+    named_sync(2, kHalf);
+    const double sign = sc[10], cB = sc[11];
+#pragma unroll 1
+    for (int j = t2; j < kO; j += kHalf) {
+      gO[j] = (nrm == 0.0) ? 0.0 : sgO[j] * (aO[j] / nrm + sign * rowO[j]);
+      a.chO.G[j + (int64_t)kO * a.chO.K] = gO[j];
+    }
+    if (t2 == 0) a.chO.G[kO + (int64_t)kO * a.chO.K] = (nrm == 0.0) ? 0.0 : 2.0 / cB;
+    if (nrm != 0.0) st_D_update(a.chO, off, -sign, t2, kHalf);
+    named_sync(2, kHalf);
+    st_T_column(a.chO, tvO, kO, cB, gO, tO, kHalf / 32, kHalf / 32);
+  }
+  __syncthreads();
+  // ---- beta_O = sig_O T_O (sig_O (W_O^T D_O z)) over the sparse z = [p_h, zoff]
+  const int kO1 = kO + 1;
+#pragma unroll 1
+  for (int j = w; j < kO; j += kSmallThreads / 32) {
+    double v = 0.0;
+    if (a.stageCO) {
+#pragma unroll 1
+      for (int64_t i = lane; i < off; i += 32) v += (double)cO[j * nr + i] * dO[i] * ph[i];
+    } else {
+#pragma unroll 1
+      for (int64_t i = lane; i < off; i += 32) v += (double)PO[paddr(i, j, a.chO.K)] * dO[i] * ph[i];
+    }
+    v = warp_sum(v);
+    if (lane == 0) gF[j] = sgO[j] * (v + rowO[j] * sc[13] * sc[9]);
+  }
+  if (tid == 0) gF[kO] = sgO[kO] * rowO[kO] * sc[13] * sc[9];
+  __syncthreads();
+  st_T(tvO, kO1, gF, uF, kO, tO, 0, kSmallThreads / 32);
+  __syncthreads();
+#pragma unroll 1
+  for (int j = tid; j < kO1; j += kSmallThreads) a.betaO[j] = sgO[j] * uF[j];
+}
+template <typename T>
+__global__ void __launch_bounds__(kSmallThreads) k_small_2p(const __grid_constant__ Small2pArgs a) {
+  k_small_2p_impl<T>(a);
+}
+
+}  // namespace hd

@@ -1719,6 +1719,7 @@ __device__ __forceinline__ void k_reset_status_impl(int* status) {
     status[kStAbort] = 0;
     status[kStBadStep] = INT_MAX;
     status[kStBadInput] = 0;
+    status[3] = 0;  // kStFused (hd_fused.cuh)
   }
 }
 __global__ void k_reset_status(int* status) { k_reset_status_impl(status); }

@@ -30,6 +30,7 @@
 
 #include "../../include/hd.h"
 #include "hd_kernels.cuh"
+#include "hd_fused.cuh"
 
 using namespace hd;
 
@@ -211,6 +212,8 @@ struct hd_op {
   int spare_sms = 0;  // SMs the persistent streaming grids leave free (HD_SPARE_SMS)
   int max_warps = 8;  // streaming warps per CTA cap (HD_WARPS fixes it)
   bool warps_fixed = false;
+  int fused = 1;         // two-pass Haar runs (hd_fused.cuh; HD_FUSED=0 disables)
+  bool fused_retry = false;  // the current run fell back to the three-pass sequence
   int fold_reverse = 1;  // fold streams its panel last-to-first (HD_FOLD_FORWARD=1 disables)
   int64_t l2_keep = 96ll << 20;  // k_dots keeps its last bytes in L2 for that fold (HD_L2_KEEP_MB)
   int64_t l2_fold_keep = 0;  // ... and the fold its last bytes for the next k_dots (HD_L2_FOLD_KEEP_MB)
