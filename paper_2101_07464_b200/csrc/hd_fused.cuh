@@ -413,12 +413,38 @@ struct Small2pArgs {
   double guard = 1e-4;      // required ||p[off:]||^2 / ||x||^2
   double check_tol = 1e-8;  // |exact - early| / early of the previous probe's ||p[off:]||^2
   int stageTF = 0, stageTO = 0, stageCF = 0, stageCO = 0;
+  unsigned long long* trace = nullptr;  // HD_TRACE=2: clock64 stamps [16] of this probe's stage
 };
+
+#define HD_T2(k, who)                                                  \
+  do {                                                                 \
+    if (a.trace && threadIdx.x == (who)) a.trace[k] = clock64();       \
+  } while (0)
+
+// sum over l = lane, lane + 32, ... < k of f(l), four loads in flight (the
+// stage is a chain of dependent L2 / shared round trips; fixed order)
+template <class F>
+__device__ __forceinline__ double lane_sum4(int lane, int64_t k, F f) {
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+  int64_t l = lane;
+#pragma unroll 1
+  for (; l + 96 < k; l += 128) {
+    v0 += f(l);
+    v1 += f(l + 32);
+    v2 += f(l + 64);
+    v3 += f(l + 96);
+  }
+#pragma unroll 1
+  for (; l < k; l += 32) v0 += f(l);
+  return (v0 + v1) + (v2 + v3);
+}
 
 template <typename T>
 __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
   extern __shared__ double ssm[];
+  HD_T2(0, 0);
   pdl_wait();
+  HD_T2(1, 0);
   pdl_launch();
   const int kF = a.kF, kO = a.kO;
   const int64_t off = a.off, nr = off + 1;
@@ -455,7 +481,6 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
   // ---- phase 1: every global load issued asynchronously, one wait
   const TView tvF = a.stageTF ? st_stage_T(a.chF, kF, tsF, tid, kSmallThreads) : TView{a.chF.Tm, a.chF.K};
   const TView tvO = a.stageTO ? st_stage_T(a.chO, kO, tsO, tid, kSmallThreads) : TView{a.chO.Tm, a.chO.K};
-  st_stage(a.partials, (int64_t)a.nslots_in * a.nblk, ps, tid, kSmallThreads);
 #pragma unroll 1
   for (int j = tid; j < kF; j += kSmallThreads) cp_async8(sgF + j, a.chF.sig + j);
 #pragma unroll 1
@@ -475,6 +500,7 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
     for (int j = w; j < kO; j += kSmallThreads / 32)
 #pragma unroll 1
       for (int64_t i = lane; i < nr; i += 32) cp_async_elem(cO + j * nr + i, PO + paddr(i, j, a.chO.K));
+  st_stage(a.partials, (int64_t)a.nslots_in * a.nblk, ps, tid, kSmallThreads);
   if (tid == 0) {
     cp_async8(sc + 4, a.scal + kScPivotG);
     cp_async8(sc + 7, a.chF.Dtail);
@@ -486,6 +512,7 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
   for (int64_t i = tid; i < nr; i += kSmallThreads) xh[i] = (double)X[i];
   cp_async_wait_all();
   __syncthreads();
+  HD_T2(2, 0);
   if (st[0] != 0) return;
   if (st[1] != 0) {  // non-finite probe input seen by the first pass: abort
     if (tid == 0) *(volatile int*)(a.status + kStAbort) = 1;
@@ -505,6 +532,7 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
 #pragma unroll 1
   for (int j = tid; j < kO; j += kSmallThreads) rowO[j] = a.stageCO ? (double)cO[j * nr + off] : (double)PO[paddr(off, j, a.chO.K)];
   __syncthreads();
+  HD_T2(3, 0);
   if (a.slot_pss >= 0 && tid == 0) {  // a posteriori check of the previous probe's early norm
     const double ex = sc[2], ea = sc[8];
     if (!(fabs(ex - ea) <= a.check_tol * ea)) {
@@ -520,6 +548,7 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
     named_sync(1, kHalf);
     st_Tt(tvF, kF, uF, bh, -1, nullptr, 0, kHalf / 32);
     named_sync(1, kHalf);
+    HD_T2(4, 0);
 #pragma unroll 1
     for (int j = tid; j < kF; j += kHalf) {
       b1[j] = sgF[j] * bh[j];
@@ -537,10 +566,10 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
       for (int j = w; j < kF; j += kHalf / 32) {
         const double b = b1[j];
         if (a.stageCF) {
-#pragma unroll 1
+#pragma unroll 4
           for (int64_t i = lane; i < nr; i += 32) hw[i] += (double)cF[j * nr + i] * b;
         } else {
-#pragma unroll 1
+#pragma unroll 4
           for (int64_t i = lane; i < nr; i += 32) hw[i] += (double)PF[paddr(i, j, a.chF.K)] * b;
         }
       }
@@ -556,20 +585,16 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
       if (i < off) a.zbuf[i] = ph[i];
     }
     named_sync(1, kHalf);
+    HD_T2(5, 0);
     // W^T p[off:] = D_old (uF - G bh - sig W_h^T (D ph)_h)  (normalised W)
 #pragma unroll 1
     for (int j = w; j < kF; j += kHalf / 32) {
-      double v = 0.0, h = 0.0;
       const double* Gj = a.chF.G + (int64_t)j * a.chF.K;  // symmetric column j
-#pragma unroll 1
-      for (int l = lane; l < kF; l += 32) v += Gj[l] * bh[l];
-      if (a.stageCF) {
-#pragma unroll 1
-        for (int64_t i = lane; i < off; i += 32) h += (double)cF[j * nr + i] * dF[i] * ph[i];
-      } else {
-#pragma unroll 1
-        for (int64_t i = lane; i < off; i += 32) h += (double)PF[paddr(i, j, a.chF.K)] * dF[i] * ph[i];
-      }
+      double v = lane_sum4(lane, kF, [&](int64_t l) { return Gj[l] * bh[l]; });
+      double h = a.stageCF ? lane_sum4(lane, off, [&](int64_t i) { return (double)cF[j * nr + i] * dF[i] * ph[i]; })
+                           : lane_sum4(lane, off, [&](int64_t i) {
+                               return (double)PF[paddr(i, j, a.chF.K)] * dF[i] * ph[i];
+                             });
       v = warp_sum(v);
       h = warp_sum(h);
       if (lane == 0) gF[j] = sc[7] * ((uF[j] - v) - sgF[j] * h);
@@ -611,6 +636,7 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
       }
     }
     named_sync(1, kHalf);
+    HD_T2(6, 0);
     const double nrm = sc[3], sign = sc[5], cnew = sc[6];
 #pragma unroll 1
     for (int j = tid; j < kF; j += kHalf) {
@@ -624,6 +650,8 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
     named_sync(1, kHalf);
     if (nrm != 0.0) st_D_update(a.chF, off, -sign, tid, kHalf);
     st_T_column(a.chF, tvF, kF, cnew, gF, tF, 0, kHalf / 32);
+    named_sync(1, kHalf);
+    HD_T2(7, 0);
   } else {
     // ---- half 2: other chain, mix reflector H(g, off) -> column kO
     const int t2 = tid - kHalf;
@@ -639,6 +667,7 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
       sc[13] = (nrm == 0.0) ? dO[off] : -sign * dO[off];
     }
     named_sync(2, kHalf);
+    HD_T2(8, kHalf);
     const double sign = sc[10], cB = sc[11];
 #pragma unroll 1
     for (int j = t2; j < kO; j += kHalf) {
@@ -649,29 +678,34 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
     if (nrm != 0.0) st_D_update(a.chO, off, -sign, t2, kHalf);
     named_sync(2, kHalf);
     st_T_column(a.chO, tvO, kO, cB, gO, tO, kHalf / 32, kHalf / 32);
+    named_sync(2, kHalf);
+    HD_T2(9, kHalf);
   }
   __syncthreads();
+  HD_T2(10, 0);
   // ---- beta_O = sig_O T_O (sig_O (W_O^T D_O z)) over the sparse z = [p_h, zoff]
   const int kO1 = kO + 1;
 #pragma unroll 1
   for (int j = w; j < kO; j += kSmallThreads / 32) {
-    double v = 0.0;
-    if (a.stageCO) {
-#pragma unroll 1
-      for (int64_t i = lane; i < off; i += 32) v += (double)cO[j * nr + i] * dO[i] * ph[i];
-    } else {
-#pragma unroll 1
-      for (int64_t i = lane; i < off; i += 32) v += (double)PO[paddr(i, j, a.chO.K)] * dO[i] * ph[i];
-    }
+    double v = a.stageCO ? lane_sum4(lane, off, [&](int64_t i) { return (double)cO[j * nr + i] * dO[i] * ph[i]; })
+                         : lane_sum4(lane, off, [&](int64_t i) {
+                             return (double)PO[paddr(i, j, a.chO.K)] * dO[i] * ph[i];
+                           });
     v = warp_sum(v);
     if (lane == 0) gF[j] = sgO[j] * (v + rowO[j] * sc[13] * sc[9]);
   }
   if (tid == 0) gF[kO] = sgO[kO] * rowO[kO] * sc[13] * sc[9];
   __syncthreads();
+  HD_T2(11, 0);
   st_T(tvO, kO1, gF, uF, kO, tO, 0, kSmallThreads / 32);
   __syncthreads();
+  HD_T2(12, 0);
 #pragma unroll 1
   for (int j = tid; j < kO1; j += kSmallThreads) a.betaO[j] = sgO[j] * uF[j];
+  if (a.trace) {
+    __syncthreads();
+    HD_T2(13, 0);
+  }
 }
 template <typename T>
 __global__ void __launch_bounds__(kSmallThreads) k_small_2p(const __grid_constant__ Small2pArgs a) {

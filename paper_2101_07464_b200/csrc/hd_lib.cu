@@ -228,6 +228,8 @@ struct hd_op {
   unsigned long long* trace = nullptr;  // HD_TRACE=1: phase stamps of k_small_dots
   std::vector<double> trace_acc;        // accumulated phase durations (ns)
   int64_t trace_n = 0;
+  unsigned long long* trace2 = nullptr;  // HD_TRACE=2: [probe][16] stage stamps of two-pass runs
+  int64_t trace2_cap = 0, trace2_used = 0;
   // graph cache (hd_run from a fresh state)
   cudaGraphExec_t graph = nullptr;
   std::string graph_key;
@@ -494,6 +496,18 @@ void check_launch(const char* what) {
   if (e != cudaSuccess) throw HdError(HD_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Raise (never lower) a kernel's dynamic shared-memory limit. A captured
+// graph keeps each node's launch size, and a node must stay within the
+// function's limit when the graph is replayed (ncu re-checks it per node), so
+// a later, smaller launch must not shrink the limit an earlier node needs.
+void raise_smem_limit(const void* fn, size_t bytes) {
+  if (bytes <= 48 * 1024) return;
+  cudaFuncAttributes fa{};
+  ck(cudaFuncGetAttributes(&fa, fn), "func attr");
+  if ((size_t)fa.maxDynamicSharedSizeBytes < bytes)
+    ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes), "smem attr");
+}
+
 // =========================================================== launchers
 // Persistent launch of a streaming kernel: grid = SMs x co-resident CTAs
 // (at most one warp-tile per warp); partial sums leave through Flush in
@@ -570,7 +584,7 @@ int launch_tma(hd_op* op, cudaStream_t s, void (*kernel)(Args), Args& args, size
     }
   }
   const size_t smem = shared_fixed + (size_t)nw * per_warp;
-  ck(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+  raise_smem_limit(reinterpret_cast<const void*>(kernel), smem);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ntiles, nw), sms));
   args.out.partials = fb.partials;
   args.out.scratch = fb.scratch;
@@ -674,7 +688,7 @@ size_t small_smem_bytes(SmallArgs& a, int which, size_t esz) {
 
 template <typename K>
 void allow_smem(K kernel, size_t bytes) {
-  if (bytes > 48 * 1024) ck(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes), "smem");
+  raise_smem_limit(reinterpret_cast<const void*>(kernel), bytes);
 }
 
 template <typename T>
