@@ -393,6 +393,11 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_haar2p(const __grid_const
 // the head rows p[0..off] from the panel corner, the early ‖p[off:]‖ and the
 // fold reflector H(p, off) with its Gram and T columns (haar.hpp:55-56);
 // then β_O for y = other-rev-adj(z), z = H p (haar.hpp:65).
+//
+// The stage is a chain of dependent L2 round trips, so nothing k x k is
+// staged: every product reads T, G and the panel corners straight from L2
+// with coalesced column accesses and many loads in flight (warp per column
+// for dots; per-warp partial rows, summed in fixed order, for T v).
 struct Small2pArgs {
   const double* partials = nullptr;  // [slot][nblk]
   int nblk = 0, nslots_in = 0;
@@ -412,7 +417,16 @@ struct Small2pArgs {
   double* betaO = nullptr;
   double guard = 1e-4;      // required ||p[off:]||^2 / ||x||^2
   double check_tol = 1e-8;  // |exact - early| / early of the previous probe's ||p[off:]||^2
-  int stageTF = 0, stageTO = 0, stageCF = 0, stageCO = 0;
+  // k x k state prefetched into shared memory before griddepcontrol.wait
+  // (written by the previous stage, which completed before this launch):
+  // T_F, the fold corner, G_F, T_O, the other corner, as the budget allows
+  int stTF = 0, stCF = 0, stG = 0, stTO = 0, stCO = 0;
+  // where the next pass is triggered (griddepcontrol.launch_dependents):
+  // 1 = before the other chain's corner product (default: the next pass's
+  // early TMA prefetch then no longer competes with the stage's L2 round
+  // trips; 15.98 -> 15.73 ms per config-2 run), 0 = right after the wait,
+  // 2 = before the last writes (HD_2P_LATE)
+  int late_launch = 1;
   unsigned long long* trace = nullptr;  // HD_TRACE=2: clock64 stamps [16] of this probe's stage
 };
 
@@ -421,95 +435,272 @@ struct Small2pArgs {
     if (a.trace && threadIdx.x == (who)) a.trace[k] = clock64();       \
   } while (0)
 
-// sum over l = lane, lane + 32, ... < k of f(l), four loads in flight (the
-// stage is a chain of dependent L2 / shared round trips; fixed order)
-template <class F>
-__device__ __forceinline__ double lane_sum4(int lane, int64_t k, F f) {
-  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
-  int64_t l = lane;
-#pragma unroll 1
-  for (; l + 96 < k; l += 128) {
-    v0 += f(l);
-    v1 += f(l + 32);
-    v2 += f(l + 64);
-    v3 += f(l + 96);
+// Shared-memory layout of k_small_2p (doubles): 20 vectors of kv, 32
+// scalars, 32 partial rows of np, 4 head vectors of nr, then the prefetched
+// matrices in the order T_F, corner F, G_F, T_O, corner O.
+struct Small2pLayout {
+  size_t kv, np, nr, kF, kO;
+  __host__ __device__ Small2pLayout(int kF_, int kO_, int64_t off) {
+    const int km = kF_ > kO_ ? kF_ : kO_;
+    kv = (size_t)small_kv(km + 1, km + 1);
+    nr = (size_t)off + 1;
+    np = kv > nr ? kv : nr;
+    kF = (size_t)kF_;
+    kO = (size_t)kO_;
   }
+  __host__ __device__ size_t fixed() const { return 20 * kv + 32 + 32 * np + 4 * nr; }
+  __host__ __device__ size_t tF() const { return kF * (kF | 1); }
+  __host__ __device__ size_t cF() const { return kF * nr; }
+  __host__ __device__ size_t g() const { return kF * kF; }
+  __host__ __device__ size_t tO() const { return kO * (kO | 1); }
+  __host__ __device__ size_t cO() const { return kO * nr; }
+};
+
+// Sum of one slot's nblk group partials with every load in flight (the stage
+// reads them once, straight from L2); fixed order.
+__device__ __forceinline__ double slot_sum_wide(const double* parts, int nblk, int slot) {
+  const double* p = parts + (size_t)slot * nblk;
+  double acc = 0.0;
 #pragma unroll 1
-  for (; l < k; l += 32) v0 += f(l);
-  return (v0 + v1) + (v2 + v3);
+  for (int b0 = 0; b0 < nblk; b0 += 24) {
+    double x[24];
+#pragma unroll
+    for (int q = 0; q < 24; ++q) x[q] = (b0 + q < nblk) ? p[b0 + q] : 0.0;
+#pragma unroll
+    for (int q = 0; q < 24; q += 4) acc += (x[q] + x[q + 1]) + (x[q + 2] + x[q + 3]);
+  }
+  return acc;
+}
+
+// out[j] = sum_{i < rows(j)} M(i, j) u[i] for j < ncol. Warps [w0, w0 + nw):
+// warp per column, two columns and four rows per lane in flight.
+template <class Acc, class Rows>
+__device__ __forceinline__ void col_dots(Acc M, int ncol, Rows rows, const double* u, double* out, int w0, int nw) {
+  const int wi = (threadIdx.x >> 5) - w0, lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (int j = wi; j < ncol; j += 2 * nw) {
+    const int j2 = j + nw;
+    const int64_t r1 = rows(j), r2 = (j2 < ncol) ? rows(j2) : 0;
+    const int64_t rm = r1 > r2 ? r1 : r2;
+    double sa = 0.0, sb = 0.0;
+#pragma unroll 1
+    for (int64_t i0 = 0; i0 < rm; i0 += 128) {
+      double x[4], y[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t i = i0 + lane + 32 * q;
+        x[q] = (i < r1) ? M(i, j) * u[i] : 0.0;
+        y[q] = (i < r2) ? M(i, j2) * u[i] : 0.0;
+      }
+      sa += (x[0] + x[1]) + (x[2] + x[3]);
+      sb += (y[0] + y[1]) + (y[2] + y[3]);
+    }
+    sa = warp_sum(sa);
+    sb = warp_sum(sb);
+    if (lane == 0) {
+      out[j] = sa;
+      if (j2 < ncol) out[j2] = sb;
+    }
+  }
+}
+
+// Per-warp partial rows of M v: part[wi * nrow + i] = sum over the warp's
+// columns j (j = wi, wi + nw, ...) of M(i, j) v[j], i < min(rows(j), nrow).
+// The caller sums the nw rows in fixed order after a barrier.
+template <class Acc, class Rows>
+__device__ __forceinline__ void col_axpy_part(Acc M, int ncol, Rows rows, const double* v, int64_t nrow, double* part,
+                                              int w0, int nw) {
+  const int wi = (threadIdx.x >> 5) - w0, lane = threadIdx.x & 31;
+  double* pw = part + (size_t)wi * nrow;
+#pragma unroll 1
+  for (int64_t i = lane; i < nrow; i += 32) pw[i] = 0.0;
+  __syncwarp();
+#pragma unroll 1
+  for (int j = wi; j < ncol; j += 2 * nw) {
+    const int j2 = j + nw;
+    int64_t r1 = rows(j), r2 = (j2 < ncol) ? rows(j2) : 0;
+    r1 = r1 < nrow ? r1 : nrow;
+    r2 = r2 < nrow ? r2 : nrow;
+    const int64_t rm = r1 > r2 ? r1 : r2;
+    const double v1 = v[j], v2 = (j2 < ncol) ? v[j2] : 0.0;
+#pragma unroll 4
+    for (int64_t i = lane; i < rm; i += 32) {
+      const double x = (i < r1) ? M(i, j) * v1 : 0.0;
+      const double y = (i < r2) ? M(i, j2) * v2 : 0.0;
+      pw[i] += x + y;
+    }
+    __syncwarp();
+  }
+}
+
+__device__ __forceinline__ double part_sum(const double* part, int64_t nrow, int nw, int64_t i) {
+  double v = 0.0;
+#pragma unroll 4
+  for (int w = 0; w < nw; ++w) v += part[(size_t)w * nrow + i];
+  return v;
+}
+
+// make_reflector scalars (reflect.hpp:120-176) for column j of a chain whose
+// tail was streamed into the panel (see st_reflector); returns sign, sets *c.
+template <typename T>
+__device__ __forceinline__ double refl_scalars(const ChainDev& ch, T* P, int j, int64_t off, double nrm, double pivot,
+                                               int rule, double colscale, double unscale, double* c_out) {
+  double sign;
+  if (rule == 0) sign = (pivot >= 0.0) ? 1.0 : -1.0;
+  else if (rule == 1) sign = (pivot > 0.0) ? 1.0 : -1.0;
+  else sign = (pivot >= 0.0) ? 1.0 : 0.0;
+  if (nrm == 0.0) sign = 1.0;
+  double c = 0.0;
+  if (nrm == 0.0) {  // identity reflector: zero column, c = 0, s = 1
+    ch.sig[j] = 0.0;
+    ch.c[j] = 0.0;
+    ch.s[j] = 1.0;
+  } else {
+    P[paddr(off, j, ch.K)] = (T)((pivot + sign * nrm) * colscale);
+    const double r = pivot / nrm;
+    c = 2.0 / (1.0 + 2.0 * sign * r + sign * sign);
+    ch.sig[j] = unscale / nrm;
+    ch.c[j] = c;
+    ch.s[j] = -sign;
+  }
+  *c_out = c;
+  return sign;
 }
 
 template <typename T>
 __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
   extern __shared__ double ssm[];
   HD_T2(0, 0);
-  pdl_wait();
-  HD_T2(1, 0);
-  pdl_launch();
   const int kF = a.kF, kO = a.kO;
   const int64_t off = a.off, nr = off + 1;
-  const int kv = small_kv(kF + 1, kO + 1);
-  const SmallSmem m = small_smem(ssm, kv);
-  double* aF = m.v0;    // P_F^T x (raw)
-  double* sgF = m.v1;
-  double* uF = m.v2;    // sig a  -> later W^T p_tail
-  double* bh = m.v3;    // beta-hat = T^T uF
-  double* b1 = m.v4;    // sig beta-hat (raw coefficients)
-  double* gF = m.v5;    // new Gram column
-  double* tF = m.v6;    // new T column (F)
-  double* aO = m.v7;    // spec dots (raw)
-  double* sgO = m.v8;
-  double* rowO = m.v9;  // P_O[off, :] incl. the new column
-  double* gO = m.v10;
-  double* tO = m.v11;
-  double* sc = m.sc;
-  double* ps = sc + 16;                                                   // [nslots_in][nblk]
-  double* hp = ps + (size_t)a.nslots_in * a.nblk;                         // [16][nr] head partials
-  double* xh = hp + (size_t)(kHalf / 32) * nr;                            // x[0..off]
-  double* ph = xh + nr;                                                   // p[0..off]
-  double* dF = ph + nr;                                                   // D_F[0..off] (old)
-  double* dO = dF + nr;                                                   // D_O[0..off] (old)
-  double* tsF = dO + nr;                                                  // T_F stage
-  double* tsO = tsF + (a.stageTF ? (size_t)kF * (kF | 1) : 0);            // T_O stage
-  T* cF = reinterpret_cast<T*>(tsO + (a.stageTO ? (size_t)kO * (kO | 1) : 0));  // corner F [kF][nr]
-  T* cO = cF + (a.stageCF ? (size_t)kF * nr : 0);                         // corner O [kO][nr]
-  int* st = reinterpret_cast<int*>(sc + 12);
+  const Small2pLayout L(kF, kO, off);
+  const int kv = (int)L.kv;
+  const int64_t np = (int64_t)L.np;
+  double* v[20];
+  for (int q = 0; q < 20; ++q) v[q] = ssm + (size_t)q * kv;
+  double* aF = v[0];    // P_F^T x (raw)
+  double* sgF = v[1];
+  double* uF = v[2];    // sig a
+  double* bh = v[3];    // beta-hat = T_F^T uF
+  double* b1 = v[4];    // sig beta-hat (raw coefficients)
+  double* gF = v[5];    // G bh, then the new Gram column
+  double* hF = v[6];    // W_h^T (D p)_h (raw)
+  double* rowF = v[8];  // P_F[off, :]
+  double* aO = v[9];    // spec dots (raw)
+  double* sgO = v[10];
+  double* rowO = v[11];  // P_O[off, :] incl. the new column
+  double* gO = v[12];
+  double* tO = v[13];   // new T column (O)
+  double* zO = v[14];   // corner W_O^T (D_O z) -> coefficients
+  double* sc = ssm + 20 * (size_t)kv;
+  double* part = sc + 32;                 // [32][np]
+  double* partA = part;                   // half 1: [16][np]
+  double* partB = part + 16 * (size_t)np; // half 2: [16][np]
+  double* xh = part + 32 * (size_t)np;    // x[0..off], later D_F p
+  double* ph = xh + nr;                   // p[0..off]
+  double* dF = ph + nr;                   // D_F[0..off] (old)
+  double* dO = dF + nr;                   // D_O[0..off] (old)
+  double* mtx = dO + nr;                  // prefetched matrices
+  const int ldF = kF | 1, ldO = kO | 1;
+  double* sTF = mtx;
+  double* sCF = sTF + (a.stTF ? L.tF() : 0);
+  double* sG = sCF + (a.stCF ? L.cF() : 0);
+  double* sTO = sG + (a.stG ? L.g() : 0);
+  double* sCO = sTO + (a.stTO ? L.tO() : 0);
+  int* st = reinterpret_cast<int*>(sc + 28);
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const T* PF = (const T*)a.PF;
-  const T* PO = (const T*)a.PO;
+  T* PF = (T*)a.PF;
+  T* PO = (T*)a.PO;
   const T* X = (const T*)a.x;
-  // ---- phase 1: every global load issued asynchronously, one wait
-  const TView tvF = a.stageTF ? st_stage_T(a.chF, kF, tsF, tid, kSmallThreads) : TView{a.chF.Tm, a.chF.K};
-  const TView tvO = a.stageTO ? st_stage_T(a.chO, kO, tsO, tid, kSmallThreads) : TView{a.chO.Tm, a.chO.K};
+  const int64_t KF = a.chF.K, KO = a.chO.K;
+  // readers of the (possibly prefetched) state
+  auto tF_at = [&](int64_t i, int j) { return a.stTF ? sTF[i + (int64_t)j * ldF] : a.chF.Tm[i + (int64_t)j * KF]; };
+  auto tO_at = [&](int64_t i, int j) { return a.stTO ? sTO[i + (int64_t)j * ldO] : a.chO.Tm[i + (int64_t)j * KO]; };
+  auto g_at = [&](int64_t i, int j) { return a.stG ? sG[i + (int64_t)j * kF] : a.chF.G[i + (int64_t)j * KF]; };
+  auto pF = [&](int64_t i, int j) { return a.stCF ? sCF[i + (int64_t)j * nr] : (double)PF[paddr(i, j, KF)]; };
+  auto pO = [&](int64_t i, int j) { return a.stCO ? sCO[i + (int64_t)j * nr] : (double)PO[paddr(i, j, KO)]; };
+  // ---- phase 0 (before the wait, overlapping the previous pass): state the
+  // previous stage wrote. The fold corner's element (off, kF - 1) is the one
+  // entry the previous pass wrote: read after the wait.
+  {
+    const int nwp = kSmallThreads / 32;
+    if (a.stTF)
 #pragma unroll 1
-  for (int j = tid; j < kF; j += kSmallThreads) cp_async8(sgF + j, a.chF.sig + j);
+      for (int j = w; j < kF; j += nwp)
 #pragma unroll 1
-  for (int j = tid; j < kO; j += kSmallThreads) cp_async8(sgO + j, a.chO.sig + j);
+        for (int i = lane; i <= j; i += 32) cp_async8(sTF + i + (int64_t)j * ldF, a.chF.Tm + i + (int64_t)j * KF);
+    if (a.stCF)
 #pragma unroll 1
-  for (int64_t i = tid; i < nr; i += kSmallThreads) {
-    cp_async8(dF + i, i < a.chF.Dlen ? a.chF.Drow + i : a.chF.Dtail);
-    cp_async8(dO + i, i < a.chO.Dlen ? a.chO.Drow + i : a.chO.Dtail);
+      for (int j = w; j < kF; j += nwp)
+#pragma unroll 1
+        for (int64_t i = lane; i < nr; i += 32) {
+          if (sizeof(T) == 8) cp_async8(sCF + i + (int64_t)j * nr, reinterpret_cast<const double*>(PF) + paddr(i, j, KF));
+          else sCF[i + (int64_t)j * nr] = (double)PF[paddr(i, j, KF)];
+        }
+    if (a.stG)
+#pragma unroll 1
+      for (int j = w; j < kF; j += nwp)
+#pragma unroll 1
+        for (int i = lane; i < kF; i += 32) cp_async8(sG + i + (int64_t)j * kF, a.chF.G + i + (int64_t)j * KF);
+    if (a.stTO)
+#pragma unroll 1
+      for (int j = w; j < kO; j += nwp)
+#pragma unroll 1
+        for (int i = lane; i <= j; i += 32) cp_async8(sTO + i + (int64_t)j * ldO, a.chO.Tm + i + (int64_t)j * KO);
+    if (a.stCO)
+#pragma unroll 1
+      for (int j = w; j < kO; j += nwp)
+#pragma unroll 1
+        for (int64_t i = lane; i < nr; i += 32) {
+          if (sizeof(T) == 8) cp_async8(sCO + i + (int64_t)j * nr, reinterpret_cast<const double*>(PO) + paddr(i, j, KO));
+          else sCO[i + (int64_t)j * nr] = (double)PO[paddr(i, j, KO)];
+        }
+#pragma unroll 1
+    for (int j = tid; j < kF; j += kSmallThreads) cp_async8(sgF + j, a.chF.sig + j);
+#pragma unroll 1
+    for (int j = tid; j < kO; j += kSmallThreads) cp_async8(sgO + j, a.chO.sig + j);
+#pragma unroll 1
+    for (int64_t i = tid; i < nr; i += kSmallThreads) {
+      cp_async8(dF + i, i < a.chF.Dlen ? a.chF.Drow + i : a.chF.Dtail);
+      cp_async8(dO + i, i < a.chO.Dlen ? a.chO.Drow + i : a.chO.Dtail);
+    }
+#pragma unroll 1
+    for (int j = tid; j < kO; j += kSmallThreads) rowO[j] = (double)PO[paddr(off, j, KO)];
+#pragma unroll 1
+    for (int j = tid; j < kF - 1; j += kSmallThreads) rowF[j] = (double)PF[paddr(off, j, KF)];
+    if (tid == 0) {
+      cp_async8(sc + 7, a.chF.Dtail);
+      cp_async8(sc + 8, a.scal + kScNrm2e);
+    }
   }
-  if (a.stageCF)
-#pragma unroll 1
-    for (int j = w; j < kF; j += kSmallThreads / 32)
-#pragma unroll 1
-      for (int64_t i = lane; i < nr; i += 32) cp_async_elem(cF + j * nr + i, PF + paddr(i, j, a.chF.K));
-  if (a.stageCO)
-#pragma unroll 1
-    for (int j = w; j < kO; j += kSmallThreads / 32)
-#pragma unroll 1
-      for (int64_t i = lane; i < nr; i += 32) cp_async_elem(cO + j * nr + i, PO + paddr(i, j, a.chO.K));
-  st_stage(a.partials, (int64_t)a.nslots_in * a.nblk, ps, tid, kSmallThreads);
+  pdl_wait();
+  HD_T2(1, 0);
+  if (!a.late_launch) pdl_launch();
+  // ---- phase 1: what the previous pass wrote
   if (tid == 0) {
     cp_async8(sc + 4, a.scal + kScPivotG);
-    cp_async8(sc + 7, a.chF.Dtail);
-    cp_async8(sc + 8, a.scal + kScNrm2e);
     cp_async4(st + 0, a.status + kStAbort);
     cp_async4(st + 1, a.status + kStBadInput);
   }
 #pragma unroll 1
   for (int64_t i = tid; i < nr; i += kSmallThreads) xh[i] = (double)X[i];
+  if (tid == 32 && kF > 0) {
+    const double e = (double)PF[paddr(off, kF - 1, KF)];
+    rowF[kF - 1] = e;
+    if (a.stCF) sCF[off + (int64_t)(kF - 1) * nr] = e;
+  }
+  {  // all reductions in one parallel pass, every load in flight
+    const int e0 = kF, e1 = e0 + kO, e2 = e1 + 1, e3 = e2 + 1, e4 = e3 + (a.slot_pss >= 0 ? 1 : 0);
+    const double* pr = a.partials;
+#pragma unroll 1
+    for (int t = tid; t < e4; t += kSmallThreads) {
+      if (t < e0) aF[t] = slot_sum_wide(pr, a.nblk, a.slot_aF + t);
+      else if (t < e1) aO[t - e0] = slot_sum_wide(pr, a.nblk, a.slot_spec + t - e0);
+      else if (t < e2) sc[0] = slot_sum_wide(pr, a.nblk, a.slot_xss);
+      else if (t < e3) sc[1] = slot_sum_wide(pr, a.nblk, a.slot_gss);
+      else sc[2] = slot_sum_wide(pr, a.nblk, a.slot_pss);
+    }
+  }
   cp_async_wait_all();
   __syncthreads();
   HD_T2(2, 0);
@@ -518,35 +709,21 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
     if (tid == 0) *(volatile int*)(a.status + kStAbort) = 1;
     return;
   }
-  {  // all reductions in one parallel pass
-    const int e0 = kF, e1 = e0 + kO, e2 = e1 + 1, e3 = e2 + 1, e4 = e3 + (a.slot_pss >= 0 ? 1 : 0);
-#pragma unroll 1
-    for (int t = tid; t < e4; t += kSmallThreads) {
-      if (t < e0) aF[t] = st_sum_slot(ps, a.nblk, a.slot_aF + t);
-      else if (t < e1) aO[t - e0] = st_sum_slot(ps, a.nblk, a.slot_spec + t - e0);
-      else if (t < e2) sc[0] = st_sum_slot(ps, a.nblk, a.slot_xss);
-      else if (t < e3) sc[1] = st_sum_slot(ps, a.nblk, a.slot_gss);
-      else sc[2] = st_sum_slot(ps, a.nblk, a.slot_pss);
-    }
-  }
-#pragma unroll 1
-  for (int j = tid; j < kO; j += kSmallThreads) rowO[j] = a.stageCO ? (double)cO[j * nr + off] : (double)PO[paddr(off, j, a.chO.K)];
-  __syncthreads();
   HD_T2(3, 0);
   if (a.slot_pss >= 0 && tid == 0) {  // a posteriori check of the previous probe's early norm
     const double ex = sc[2], ea = sc[8];
     if (!(fabs(ex - ea) <= a.check_tol * ea)) {
       atomicOr(a.status + kStFused, 1);
       atomicOr(a.status + kStAbort, 1);
-      st[0] = 1;
     }
   }
   if (tid < kHalf) {
-    // ---- half 1: fold chain
+    // ======== half 1: fold chain (warps 0..15)
 #pragma unroll 1
     for (int j = tid; j < kF; j += kHalf) uF[j] = sgF[j] * aF[j];
     named_sync(1, kHalf);
-    st_Tt(tvF, kF, uF, bh, -1, nullptr, 0, kHalf / 32);
+    // beta-hat = T^T uF (column dots over the upper triangle)
+    col_dots(tF_at, kF, [](int j) { return (int64_t)j + 1; }, uF, bh, 0, kHalf / 32);
     named_sync(1, kHalf);
     HD_T2(4, 0);
 #pragma unroll 1
@@ -555,112 +732,94 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
       a.betaF[j] = b1[j];
     }
     named_sync(1, kHalf);
-    // head rows p_i = D_i (x_i - sum_j P[i, j] b1_j), i <= off: warp per
-    // column, lanes over rows (coalesced), per-warp partial rows added in
-    // fixed order
-    {
-      double* hw = hp + (size_t)w * nr;
-#pragma unroll 1
-      for (int64_t i = lane; i < nr; i += 32) hw[i] = 0.0;
-#pragma unroll 1
-      for (int j = w; j < kF; j += kHalf / 32) {
-        const double b = b1[j];
-        if (a.stageCF) {
-#pragma unroll 4
-          for (int64_t i = lane; i < nr; i += 32) hw[i] += (double)cF[j * nr + i] * b;
-        } else {
-#pragma unroll 4
-          for (int64_t i = lane; i < nr; i += 32) hw[i] += (double)PF[paddr(i, j, a.chF.K)] * b;
-        }
-      }
-    }
+    // head rows p_i = D_i (x_i - sum_j P[i, j] b1_j), i <= off
+    col_axpy_part(pF, kF, [&](int) { return nr; }, b1, nr, partA, 0, kHalf / 32);
     named_sync(1, kHalf);
 #pragma unroll 1
     for (int64_t i = tid; i < nr; i += kHalf) {
-      double v = 0.0;
-#pragma unroll 1
-      for (int u = 0; u < kHalf / 32; ++u) v += hp[(size_t)u * nr + i];
-      ph[i] = dF[i] * (xh[i] - v);
-      a.head[i] = ph[i];
-      if (i < off) a.zbuf[i] = ph[i];
+      const double p = dF[i] * (xh[i] - part_sum(partA, nr, kHalf / 32, i));
+      ph[i] = p;
+      xh[i] = dF[i] * p;  // (x - W beta)_i, the h-vector input below
+      a.head[i] = p;
+      if (i < off) a.zbuf[i] = p;
     }
     named_sync(1, kHalf);
     HD_T2(5, 0);
-    // W^T p[off:] = D_old (uF - G bh - sig W_h^T (D ph)_h)  (normalised W)
-#pragma unroll 1
-    for (int j = w; j < kF; j += kHalf / 32) {
-      const double* Gj = a.chF.G + (int64_t)j * a.chF.K;  // symmetric column j
-      double v = lane_sum4(lane, kF, [&](int64_t l) { return Gj[l] * bh[l]; });
-      double h = a.stageCF ? lane_sum4(lane, off, [&](int64_t i) { return (double)cF[j * nr + i] * dF[i] * ph[i]; })
-                           : lane_sum4(lane, off, [&](int64_t i) {
-                               return (double)PF[paddr(i, j, a.chF.K)] * dF[i] * ph[i];
-                             });
-      v = warp_sum(v);
-      h = warp_sum(h);
-      if (lane == 0) gF[j] = sc[7] * ((uF[j] - v) - sgF[j] * h);
-    }
+    // G bh (symmetric G, column j) and W_h^T (x - W beta)_h, h = rows < off
+    col_dots(g_at, kF, [&](int) { return (int64_t)kF; }, bh, gF, 0, kHalf / 32);
+    col_dots(pF, kF, [&](int) { return off; }, xh, hF, 0, kHalf / 32);
     if (w == 0) {
       double hs = 0.0;
 #pragma unroll 1
       for (int64_t i = lane; i < off; i += 32) hs += ph[i] * ph[i];
       hs = warp_sum(hs);
-      if (lane == 0) {
-        const double xss = sc[0];
-        const double nrm2 = xss - hs;
-        double nrm = 0.0;
-        if (!(nrm2 >= a.guard * xss) || !(nrm2 > 0.0 || xss == 0.0)) {
-          atomicOr(a.status + kStFused, 1);
-          atomicOr(a.status + kStAbort, 1);
-        } else {
-          nrm = sqrt(nrm2);
-        }
-        const double xn = sqrt(xss);
-        int e = 0;
-        if (xn > 0.0 && isfinite(xn)) frexp(xn, &e);
-        const double escale = ldexp(1.0, -e), iscale = ldexp(1.0, e);
-        a.scal[kScEscale] = escale;
-        a.scal[kScIscale] = iscale;
-        a.scal[kScDold] = sc[7];
-        a.scal[kScNrm2e] = nrm * nrm;
-        const double piv = ph[off];
-        const double sign = st_reflector<T>(a.chF, (T*)a.PF, kF, off, nrm, piv, a.rule, escale, iscale, true);
-        const double zoff = (nrm == 0.0) ? piv : (sign == 0.0 ? 0.0 : nrm);
-        a.scal[kScNrm] = nrm;
-        a.scal[kScCoefCur] = zoff;
-        a.scal[kScSign] = sign;
-        a.zbuf[off] = zoff;
-        sc[3] = nrm;
-        sc[5] = sign;
-        sc[6] = (nrm == 0.0) ? 0.0 : a.chF.c[kF];
-        sc[9] = zoff;
+      if (lane == 0) sc[3] = hs;
+    }
+    named_sync(1, kHalf);
+    if (tid == 0) {
+      const double xss = sc[0];
+      const double nrm2 = xss - sc[3];
+      double nrm = 0.0;
+      if (!(nrm2 >= a.guard * xss) || !(nrm2 > 0.0 || xss == 0.0)) {
+        atomicOr(a.status + kStFused, 1);
+        atomicOr(a.status + kStAbort, 1);
+      } else {
+        nrm = sqrt(nrm2);
       }
+      const double xn = sqrt(xss);
+      int e = 0;
+      if (xn > 0.0 && isfinite(xn)) frexp(xn, &e);
+      const double escale = ldexp(1.0, -e), iscale = ldexp(1.0, e);
+      a.scal[kScEscale] = escale;
+      a.scal[kScIscale] = iscale;
+      a.scal[kScDold] = sc[7];
+      a.scal[kScNrm2e] = nrm * nrm;
+      const double piv = ph[off];
+      double cnew;
+      const double sign = refl_scalars<T>(a.chF, PF, kF, off, nrm, piv, a.rule, escale, iscale, &cnew);
+      const double zoff = (nrm == 0.0) ? piv : (sign == 0.0 ? 0.0 : nrm);
+      a.scal[kScNrm] = nrm;
+      a.scal[kScCoefCur] = zoff;
+      a.scal[kScSign] = sign;
+      a.zbuf[off] = zoff;
+      sc[5] = nrm;
+      sc[6] = sign;
+      sc[9] = zoff;
+      sc[10] = cnew;
+      // D_F on rows >= off, before this member (the pass's p = D_old (x - P beta))
     }
     named_sync(1, kHalf);
     HD_T2(6, 0);
-    const double nrm = sc[3], sign = sc[5], cnew = sc[6];
+    const double nrm = sc[5], sign = sc[6], cnew = sc[10], dold = sc[7];
+    // Gram column of w_new = (p[off:] + sign nrm e_off) / nrm against W:
+    //   W^T p[off:] = D_old ((W^T x - G bh) - W_h^T (x - W beta)_h)
 #pragma unroll 1
     for (int j = tid; j < kF; j += kHalf) {
-      const double rowv = a.stageCF ? (double)cF[j * nr + off] : (double)PF[paddr(off, j, a.chF.K)];
-      const double g = (nrm == 0.0) ? 0.0 : gF[j] / nrm + sign * sgF[j] * rowv;
+      const double g = (nrm == 0.0) ? 0.0 : dold * ((uF[j] - gF[j]) - sgF[j] * hF[j]) / nrm + sign * sgF[j] * rowF[j];
       gF[j] = g;
-      a.chF.G[j + (int64_t)kF * a.chF.K] = g;
-      a.chF.G[kF + (int64_t)j * a.chF.K] = g;
+      a.chF.G[j + (int64_t)kF * KF] = g;
+      a.chF.G[kF + (int64_t)j * KF] = g;
     }
-    if (tid == 0) a.chF.G[kF + (int64_t)kF * a.chF.K] = (nrm == 0.0) ? 0.0 : 2.0 / cnew;
-    named_sync(1, kHalf);
+    if (tid == 0) a.chF.G[kF + (int64_t)kF * KF] = (nrm == 0.0) ? 0.0 : 2.0 / cnew;
     if (nrm != 0.0) st_D_update(a.chF, off, -sign, tid, kHalf);
-    st_T_column(a.chF, tvF, kF, cnew, gF, tF, 0, kHalf / 32);
     named_sync(1, kHalf);
+    // T column: T[:k, k] = -c T g, T[k, k] = c
+    col_axpy_part(tF_at, kF, [](int j) { return (int64_t)j + 1; }, gF, kF, partA, 0, kHalf / 32);
+    named_sync(1, kHalf);
+#pragma unroll 1
+    for (int i = tid; i < kF; i += kHalf) a.chF.Tm[i + (int64_t)kF * KF] = -cnew * part_sum(partA, kF, kHalf / 32, i);
+    if (tid == 0) a.chF.Tm[kF + (int64_t)kF * KF] = cnew;
     HD_T2(7, 0);
   } else {
-    // ---- half 2: other chain, mix reflector H(g, off) -> column kO
+    // ======== half 2: other chain, mix reflector H(g, off) -> column kO
     const int t2 = tid - kHalf;
     const double nrm = sqrt(sc[1]);
     const double piv = sc[4];
     if (t2 == 0) {
-      const double sign = st_reflector<T>(a.chO, (T*)a.PO, kO, off, nrm, piv, a.rule, 1.0, 1.0, true);
-      sc[10] = sign;
-      sc[11] = (nrm == 0.0) ? 0.0 : a.chO.c[kO];
+      double cB;
+      const double sign = refl_scalars<T>(a.chO, PO, kO, off, nrm, piv, a.rule, 1.0, 1.0, &cB);
+      sc[11] = sign;
+      sc[12] = cB;
       sgO[kO] = (nrm == 0.0) ? 0.0 : 1.0 / nrm;
       rowO[kO] = (nrm == 0.0) ? 0.0 : (double)(T)(piv + sign * nrm);
       // D_O[off] after the update (z's row off is scaled by it in the pass)
@@ -668,40 +827,52 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
     }
     named_sync(2, kHalf);
     HD_T2(8, kHalf);
-    const double sign = sc[10], cB = sc[11];
+    const double sign = sc[11], cB = sc[12];
 #pragma unroll 1
     for (int j = t2; j < kO; j += kHalf) {
       gO[j] = (nrm == 0.0) ? 0.0 : sgO[j] * (aO[j] / nrm + sign * rowO[j]);
-      a.chO.G[j + (int64_t)kO * a.chO.K] = gO[j];
+      a.chO.G[j + (int64_t)kO * KO] = gO[j];
     }
-    if (t2 == 0) a.chO.G[kO + (int64_t)kO * a.chO.K] = (nrm == 0.0) ? 0.0 : 2.0 / cB;
+    if (t2 == 0) a.chO.G[kO + (int64_t)kO * KO] = (nrm == 0.0) ? 0.0 : 2.0 / cB;
     if (nrm != 0.0) st_D_update(a.chO, off, -sign, t2, kHalf);
     named_sync(2, kHalf);
-    st_T_column(a.chO, tvO, kO, cB, gO, tO, kHalf / 32, kHalf / 32);
+    col_axpy_part(tO_at, kO, [](int j) { return (int64_t)j + 1; }, gO, kO, partB,
+                  kHalf / 32, kHalf / 32);
     named_sync(2, kHalf);
+#pragma unroll 1
+    for (int i = t2; i < kO; i += kHalf) {
+      const double tv = -cB * part_sum(partB, kO, kHalf / 32, i);
+      tO[i] = tv;
+      a.chO.Tm[i + (int64_t)kO * KO] = tv;
+    }
+    if (t2 == 0) {
+      tO[kO] = cB;
+      a.chO.Tm[kO + (int64_t)kO * KO] = cB;
+    }
     HD_T2(9, kHalf);
   }
   __syncthreads();
   HD_T2(10, 0);
   // ---- beta_O = sig_O T_O (sig_O (W_O^T D_O z)) over the sparse z = [p_h, zoff]
-  const int kO1 = kO + 1;
 #pragma unroll 1
-  for (int j = w; j < kO; j += kSmallThreads / 32) {
-    double v = a.stageCO ? lane_sum4(lane, off, [&](int64_t i) { return (double)cO[j * nr + i] * dO[i] * ph[i]; })
-                         : lane_sum4(lane, off, [&](int64_t i) {
-                             return (double)PO[paddr(i, j, a.chO.K)] * dO[i] * ph[i];
-                           });
-    v = warp_sum(v);
-    if (lane == 0) gF[j] = sgO[j] * (v + rowO[j] * sc[13] * sc[9]);
-  }
-  if (tid == 0) gF[kO] = sgO[kO] * rowO[kO] * sc[13] * sc[9];
+  for (int64_t i = tid; i < off; i += kSmallThreads) xh[i] = dO[i] * ph[i];
+  __syncthreads();
+  col_dots(pO, kO, [&](int) { return off; }, xh, zO, 0, kSmallThreads / 32);
+  __syncthreads();
+  if (a.late_launch == 1) pdl_launch();
+  const double zc = sc[13] * sc[9];
+#pragma unroll 1
+  for (int j = tid; j <= kO; j += kSmallThreads) zO[j] = (j < kO) ? sgO[j] * (zO[j] + rowO[j] * zc) : sgO[kO] * rowO[kO] * zc;
   __syncthreads();
   HD_T2(11, 0);
-  st_T(tvO, kO1, gF, uF, kO, tO, 0, kSmallThreads / 32);
+  const int kO1 = kO + 1;
+  col_axpy_part([&](int64_t i, int j) { return (j == kO) ? tO[i] : tO_at(i, j); }, kO1, [](int j) { return (int64_t)j + 1; },
+                zO, kO1, part, 0, kSmallThreads / 32);
   __syncthreads();
   HD_T2(12, 0);
+  if (a.late_launch == 2) pdl_launch();
 #pragma unroll 1
-  for (int j = tid; j < kO1; j += kSmallThreads) a.betaO[j] = sgO[j] * uF[j];
+  for (int j = tid; j < kO1; j += kSmallThreads) a.betaO[j] = sgO[j] * part_sum(part, kO1, kSmallThreads / 32, j);
   if (a.trace) {
     __syncthreads();
     HD_T2(13, 0);
