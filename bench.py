@@ -43,10 +43,10 @@ def alg_bytes_haar(n: int, T: int, s: int = 8) -> float:
 
 
 def alg_bytes_haar_2p(n: int, T: int, s: int = 8) -> float:
-    """Two-pass Haar run: s*n*(2t+5) summed over t = 1..T
-    (both panels read once, the new fold column, x_t, x_{t+1}, x_{t-1} and the
-    next mix column)."""
-    return float(s) * n * (2.0 * T * (T + 1) / 2.0 + 5.0 * T)
+    """Two-pass Haar run: s*n*(2t+4) summed over t = 1..T
+    (the other panel's t and the fold panel's t - 1 columns read once, the new
+    fold column, x_t, x_{t+1}, x_{t-1} and the next mix column)."""
+    return float(s) * n * (2.0 * T * (T + 1) / 2.0 + 4.0 * T)
 
 
 def rank_seed(base: int, rank: int) -> int:

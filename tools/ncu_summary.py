@@ -37,10 +37,11 @@ def full(rep, out):
             us = float(d["gpu__time_duration.sum"])
             if d["units"].get("gpu__time_duration.sum") == "nsecond":
                 us /= 1e3
-            mb = float(d["dram__bytes_read.sum"]) + float(d["dram__bytes_write.sum"])
-            scale = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1.0}[d["units"]["dram__bytes_read.sum"]]
-            d["dram_GBps"] = mb * scale / (us * 1e-6) / 1e9
-            d["dram_bytes"] = mb * scale
+            sc = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1.0}
+            b = (float(d["dram__bytes_read.sum"]) * sc[d["units"]["dram__bytes_read.sum"]] +
+                 float(d["dram__bytes_write.sum"]) * sc[d["units"]["dram__bytes_write.sum"]])
+            d["dram_GBps"] = b / (us * 1e-6) / 1e9
+            d["dram_bytes"] = b
         except Exception:
             pass
         res.append(d)
@@ -80,8 +81,12 @@ def traffic(full_json, out, t=91, n=1_000_000):
       FOLD     8 n (t + 1): fold chain (t-1 columns) + x + the new column
       OTHER    8 n (t + 3): other chain (t columns) + output + next mix column
                             + x_{t-1} (tanh mix)"""
-    alg = {"dots": 8 * n * (t + 1), "fold": 8 * n * (t + 1), "other": 8 * n * (t + 3)}
-    kind = {"k_dots": "dots", "k_apply<double, 0>": "fold", "k_apply<double, 1>": "other"}
+    alg = {"dots": 8 * n * (t + 1), "fold": 8 * n * (t + 1), "other": 8 * n * (t + 3),
+           # two-pass pass (DESIGN.md §4.7): other panel t + fold panel t - 1
+           # columns, new fold column, x_t, x_{t+1}, x_{t-1}, next mix column
+           "haar2p": 8 * n * (2 * t + 4)}
+    kind = {"k_dots": "dots", "k_apply<double, 0>": "fold", "k_apply<double, 1>": "other",
+            "k_haar2p<double>": "haar2p"}
     res = {}
     for d in json.load(open(full_json)):
         name = d.get("Kernel Name", "")
