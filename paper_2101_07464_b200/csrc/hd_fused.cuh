@@ -523,11 +523,19 @@ __device__ __forceinline__ void col_axpy_part(Acc M, int ncol, Rows rows, const 
     r2 = r2 < nrow ? r2 : nrow;
     const int64_t rm = r1 > r2 ? r1 : r2;
     const double v1 = v[j], v2 = (j2 < ncol) ? v[j2] : 0.0;
-#pragma unroll 4
-    for (int64_t i = lane; i < rm; i += 32) {
-      const double x = (i < r1) ? M(i, j) * v1 : 0.0;
-      const double y = (i < r2) ? M(i, j2) * v2 : 0.0;
-      pw[i] += x + y;
+#pragma unroll 1
+    for (int64_t i0 = lane; i0 < rm; i0 += 128) {
+      // all eight loads before any store: the partial rows live in shared
+      // memory and the compiler cannot reorder loads across those stores
+      double x[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t i = i0 + 32 * q;
+        x[q] = ((i < r1) ? M(i, j) * v1 : 0.0) + ((i < r2) ? M(i, j2) * v2 : 0.0);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (i0 + 32 * q < rm) pw[i0 + 32 * q] += x[q];
     }
     __syncwarp();
   }
@@ -594,8 +602,11 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
   double* zO = v[14];   // corner W_O^T (D_O z) -> coefficients
   double* sc = ssm + 20 * (size_t)kv;
   double* part = sc + 32;                 // [32][np]
-  double* partA = part;                   // half 1: [16][np]
-  double* partB = part + 16 * (size_t)np; // half 2: [16][np]
+  // the fold chain's part of the CTA (critical path) gets 24 warps, the other
+  // chain's mix reflector and T column (off the critical path) 8
+  constexpr int kN1 = 768, kN2 = kSmallThreads - kN1, kW1 = kN1 / 32, kW2 = kN2 / 32;
+  double* partA = part;                    // part 1: [24][np]
+  double* partB = part + kW1 * (size_t)np; // part 2: [8][np]
   double* xh = part + 32 * (size_t)np;    // x[0..off], later D_F p
   double* ph = xh + nr;                   // p[0..off]
   double* dF = ph + nr;                   // D_F[0..off] (old)
@@ -717,37 +728,38 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
       atomicOr(a.status + kStAbort, 1);
     }
   }
-  if (tid < kHalf) {
-    // ======== half 1: fold chain (warps 0..15)
+  if (tid < kN1) {
+    // ======== part 1: fold chain (warps 0..23, the critical path)
 #pragma unroll 1
-    for (int j = tid; j < kF; j += kHalf) uF[j] = sgF[j] * aF[j];
-    named_sync(1, kHalf);
+    for (int j = tid; j < kF; j += kN1) uF[j] = sgF[j] * aF[j];
+    named_sync(1, kN1);
     // beta-hat = T^T uF (column dots over the upper triangle)
-    col_dots(tF_at, kF, [](int j) { return (int64_t)j + 1; }, uF, bh, 0, kHalf / 32);
-    named_sync(1, kHalf);
+    col_dots(tF_at, kF, [](int j) { return (int64_t)j + 1; }, uF, bh, 0, kW1);
+    named_sync(1, kN1);
     HD_T2(4, 0);
 #pragma unroll 1
-    for (int j = tid; j < kF; j += kHalf) {
+    for (int j = tid; j < kF; j += kN1) {
       b1[j] = sgF[j] * bh[j];
       a.betaF[j] = b1[j];
     }
-    named_sync(1, kHalf);
+    named_sync(1, kN1);
     // head rows p_i = D_i (x_i - sum_j P[i, j] b1_j), i <= off
-    col_axpy_part(pF, kF, [&](int) { return nr; }, b1, nr, partA, 0, kHalf / 32);
-    named_sync(1, kHalf);
+    col_axpy_part(pF, kF, [&](int) { return nr; }, b1, nr, partA, 0, kW1);
+    // G bh (symmetric G, column j) needs only bh: its round trips overlap the head rows'
+    col_dots(g_at, kF, [&](int) { return (int64_t)kF; }, bh, gF, 0, kW1);
+    named_sync(1, kN1);
 #pragma unroll 1
-    for (int64_t i = tid; i < nr; i += kHalf) {
-      const double p = dF[i] * (xh[i] - part_sum(partA, nr, kHalf / 32, i));
+    for (int64_t i = tid; i < nr; i += kN1) {
+      const double p = dF[i] * (xh[i] - part_sum(partA, nr, kW1, i));
       ph[i] = p;
       xh[i] = dF[i] * p;  // (x - W beta)_i, the h-vector input below
       a.head[i] = p;
       if (i < off) a.zbuf[i] = p;
     }
-    named_sync(1, kHalf);
+    named_sync(1, kN1);
     HD_T2(5, 0);
-    // G bh (symmetric G, column j) and W_h^T (x - W beta)_h, h = rows < off
-    col_dots(g_at, kF, [&](int) { return (int64_t)kF; }, bh, gF, 0, kHalf / 32);
-    col_dots(pF, kF, [&](int) { return off; }, xh, hF, 0, kHalf / 32);
+    // W_h^T (x - W beta)_h, h = rows < off
+    col_dots(pF, kF, [&](int) { return off; }, xh, hF, 0, kW1);
     if (w == 0) {
       double hs = 0.0;
 #pragma unroll 1
@@ -755,7 +767,8 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
       hs = warp_sum(hs);
       if (lane == 0) sc[3] = hs;
     }
-    named_sync(1, kHalf);
+    named_sync(1, kN1);
+    HD_T2(14, 0);
     if (tid == 0) {
       const double xss = sc[0];
       const double nrm2 = xss - sc[3];
@@ -788,31 +801,31 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
       sc[10] = cnew;
       // D_F on rows >= off, before this member (the pass's p = D_old (x - P beta))
     }
-    named_sync(1, kHalf);
+    named_sync(1, kN1);
     HD_T2(6, 0);
     const double nrm = sc[5], sign = sc[6], cnew = sc[10], dold = sc[7];
     // Gram column of w_new = (p[off:] + sign nrm e_off) / nrm against W:
     //   W^T p[off:] = D_old ((W^T x - G bh) - W_h^T (x - W beta)_h)
 #pragma unroll 1
-    for (int j = tid; j < kF; j += kHalf) {
+    for (int j = tid; j < kF; j += kN1) {
       const double g = (nrm == 0.0) ? 0.0 : dold * ((uF[j] - gF[j]) - sgF[j] * hF[j]) / nrm + sign * sgF[j] * rowF[j];
       gF[j] = g;
       a.chF.G[j + (int64_t)kF * KF] = g;
       a.chF.G[kF + (int64_t)j * KF] = g;
     }
     if (tid == 0) a.chF.G[kF + (int64_t)kF * KF] = (nrm == 0.0) ? 0.0 : 2.0 / cnew;
-    if (nrm != 0.0) st_D_update(a.chF, off, -sign, tid, kHalf);
-    named_sync(1, kHalf);
+    if (nrm != 0.0) st_D_update(a.chF, off, -sign, tid, kN1);
+    named_sync(1, kN1);
     // T column: T[:k, k] = -c T g, T[k, k] = c
-    col_axpy_part(tF_at, kF, [](int j) { return (int64_t)j + 1; }, gF, kF, partA, 0, kHalf / 32);
-    named_sync(1, kHalf);
+    col_axpy_part(tF_at, kF, [](int j) { return (int64_t)j + 1; }, gF, kF, partA, 0, kW1);
+    named_sync(1, kN1);
 #pragma unroll 1
-    for (int i = tid; i < kF; i += kHalf) a.chF.Tm[i + (int64_t)kF * KF] = -cnew * part_sum(partA, kF, kHalf / 32, i);
+    for (int i = tid; i < kF; i += kN1) a.chF.Tm[i + (int64_t)kF * KF] = -cnew * part_sum(partA, kF, kW1, i);
     if (tid == 0) a.chF.Tm[kF + (int64_t)kF * KF] = cnew;
     HD_T2(7, 0);
   } else {
-    // ======== half 2: other chain, mix reflector H(g, off) -> column kO
-    const int t2 = tid - kHalf;
+    // ======== part 2: other chain (warps 24..31), mix reflector H(g, off) -> column kO
+    const int t2 = tid - kN1;
     const double nrm = sqrt(sc[1]);
     const double piv = sc[4];
     if (t2 == 0) {
@@ -825,23 +838,23 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
       // D_O[off] after the update (z's row off is scaled by it in the pass)
       sc[13] = (nrm == 0.0) ? dO[off] : -sign * dO[off];
     }
-    named_sync(2, kHalf);
-    HD_T2(8, kHalf);
+    named_sync(2, kN2);
+    HD_T2(8, kN1);
     const double sign = sc[11], cB = sc[12];
 #pragma unroll 1
-    for (int j = t2; j < kO; j += kHalf) {
+    for (int j = t2; j < kO; j += kN2) {
       gO[j] = (nrm == 0.0) ? 0.0 : sgO[j] * (aO[j] / nrm + sign * rowO[j]);
       a.chO.G[j + (int64_t)kO * KO] = gO[j];
     }
     if (t2 == 0) a.chO.G[kO + (int64_t)kO * KO] = (nrm == 0.0) ? 0.0 : 2.0 / cB;
-    if (nrm != 0.0) st_D_update(a.chO, off, -sign, t2, kHalf);
-    named_sync(2, kHalf);
+    if (nrm != 0.0) st_D_update(a.chO, off, -sign, t2, kN2);
+    named_sync(2, kN2);
     col_axpy_part(tO_at, kO, [](int j) { return (int64_t)j + 1; }, gO, kO, partB,
-                  kHalf / 32, kHalf / 32);
-    named_sync(2, kHalf);
+                  kW1, kW2);
+    named_sync(2, kN2);
 #pragma unroll 1
-    for (int i = t2; i < kO; i += kHalf) {
-      const double tv = -cB * part_sum(partB, kO, kHalf / 32, i);
+    for (int i = t2; i < kO; i += kN2) {
+      const double tv = -cB * part_sum(partB, kO, kW2, i);
       tO[i] = tv;
       a.chO.Tm[i + (int64_t)kO * KO] = tv;
     }
@@ -849,7 +862,7 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
       tO[kO] = cB;
       a.chO.Tm[kO + (int64_t)kO * KO] = cB;
     }
-    HD_T2(9, kHalf);
+    HD_T2(9, kN1);
   }
   __syncthreads();
   HD_T2(10, 0);
