@@ -69,6 +69,12 @@ struct FusedArgs {
   int* status = nullptr;
   int prefetch = 0;
   int64_t pivot_tile = -1;  // tile holding row off: its warp waits before the first TMA
+  // Consecutive passes stream the same two panels (one column longer each):
+  // every other pass walks each warp's tiles last to first, so it starts on
+  // the chunks the previous pass read last, and every pass marks the last
+  // l2_keep bytes of its stream evict-last for the next one.
+  int reverse = 0;
+  int64_t l2_keep = 0;
 };
 
 template <typename T>
@@ -99,11 +105,15 @@ __device__ __forceinline__ void k_haar2p_impl(const FusedArgs<T>& a) {
   const int nchF = (a.ncolsF + kCW - 1) / kCW;
   const int nchT = nchO + nchF;
   const uint32_t nst = (uint32_t)((t1 - t0) * nchT);
-  // issue cursor: tile, then O's chunks, then F's
+  const bool rev = a.reverse != 0;
+  const int64_t tlast = t1 - 1;
+  const int64_t keep = a.l2_keep / (W * (int64_t)(kCW * kTile * sizeof(T)));
+  const uint32_t keep_from = keep >= (int64_t)nst ? 0u : nst - (uint32_t)keep;
+  // issue cursor: tile (in traversal order), then O's chunks, then F's
   int64_t cur_k = 0;
   int cur_c = 0;
   auto issue = [&](uint32_t it) {
-    const int64_t tile = t0 + cur_k;
+    const int64_t tile = rev ? tlast - cur_k : t0 + cur_k;
     const int c = cur_c;
     if (++cur_c == nchT) {
       cur_c = 0;
@@ -120,7 +130,7 @@ __device__ __forceinline__ void k_haar2p_impl(const FusedArgs<T>& a) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_arrive_expect_tx(full + s, bytes);
     bulk_g2s(ring + (size_t)s * kCW * kTile * sizeof(T), P + (size_t)tile * (size_t)(K << kTileShift) + (size_t)cc * kCW * kTile,
-             bytes, full + s, false);
+             bytes, full + s, it >= keep_from);
   };
   __syncwarp();
   // the stage before this kernel writes the pivot entry of O's new column:
@@ -158,7 +168,7 @@ __device__ __forceinline__ void k_haar2p_impl(const FusedArgs<T>& a) {
       }
     }
   };
-  if (t0 < t1) fetch(t0);
+  if (t0 < t1) fetch(rev ? tlast : t0);
   double2 gn[4];
   auto gen = [&](int64_t tile, int q) {
     const int64_t i = tile * kTile + 2 * (lane + 32 * q);
@@ -170,11 +180,13 @@ __device__ __forceinline__ void k_haar2p_impl(const FusedArgs<T>& a) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) gn[q] = make_double2(0.0, 0.0);
   if (spec && t0 < t1)
-    for (int q = 0; q < 4; ++q) gen(t0, q);
+    for (int q = 0; q < 4; ++q) gen(rev ? tlast : t0, q);
 
   uint32_t it = 0;
-  for (int64_t tile = t0; tile < t1; ++tile) {
-    const bool has_next = tile + 1 < t1;
+  for (int64_t k = 0; k < t1 - t0; ++k) {
+    const int64_t tile = rev ? tlast - k : t0 + k;
+    const int64_t next = rev ? tile - 1 : tile + 1;
+    const bool has_next = k + 1 < t1 - t0;
     double2 g[4], xt[4], xp[4], r[4], xn[4];
     float2 gf[4], xnf[4];
 #pragma unroll
@@ -185,7 +197,7 @@ __device__ __forceinline__ void k_haar2p_impl(const FusedArgs<T>& a) {
       gf[q] = make_float2((float)g[q].x, (float)g[q].y);
       r[q] = make_double2(0.0, 0.0);
     }
-    if (has_next) fetch(tile + 1);
+    if (has_next) fetch(next);
     const bool gen_next = spec && has_next;
     if (a.gcol) {  // the next probe's mix column (masked draw), its norm and pivot
 #pragma unroll
@@ -246,10 +258,10 @@ __device__ __forceinline__ void k_haar2p_impl(const FusedArgs<T>& a) {
       __syncwarp();
       if (lane == 0 && it + kRing < nst) issue(it + kRing);
       if (spec) add_chunk_sums<kCW>(d, lane, col0, a.ncolsO, acc + a.slot_spec);
-      if (gen_next && c < 4) gen(tile + 1, c);
+      if (gen_next && c < 4) gen(next, c);
     }
     if (gen_next)
-      for (int q = nchO; q < 4; ++q) gen(tile + 1, q);
+      for (int q = nchO; q < 4; ++q) gen(next, q);
     // ---- y = D_O z - acc and the update x_{t+1} (rows >= n stay zero)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
