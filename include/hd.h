@@ -172,7 +172,9 @@ int hd_run(hd_op* op, const hd_run_args* args);
  * use_graph) on the handle's own stream, ordered after `args->stream`, and
  * return; hd_wait completes it (status words, error reporting as hd_run, host
  * copies). Device outputs are valid once hd_wait returns. Many handles run
- * concurrently on their own streams (batched independent trials, config 3). */
+ * concurrently on their own streams (batched independent trials, config 3).
+ * x1 / x0 must stay valid until hd_wait: a two-pass Haar run whose precision
+ * guard fires is re-run from them. */
 int hd_run_async(hd_op* op, const hd_run_args* args);
 int hd_wait(hd_op* op);
 
