@@ -439,6 +439,11 @@ struct Small2pArgs {
   // trips; 15.98 -> 15.73 ms per config-2 run), 0 = right after the wait,
   // 2 = before the last writes (HD_2P_LATE)
   int late_launch = 1;
+  // the fold member appended by the previous stage still needs its T column
+  // and its D_F update: done here, before the wait, while the pass streams
+  // (the previous stage had them on its critical path); finish = 1 runs only
+  // that (after a run's last pass)
+  int deferred = 0, finish = 0;
   unsigned long long* trace = nullptr;  // HD_TRACE=2: clock64 stamps [16] of this probe's stage
 };
 
@@ -448,7 +453,7 @@ struct Small2pArgs {
   } while (0)
 
 // Shared-memory layout of k_small_2p (doubles): 20 vectors of kv, 32
-// scalars, 32 partial rows of np, 4 head vectors of nr, then the prefetched
+// scalars, 48 partial rows of np, 5 head vectors of nr, then the prefetched
 // matrices in the order T_F, corner F, G_F, T_O, corner O.
 struct Small2pLayout {
   size_t kv, np, nr, kF, kO;
@@ -460,7 +465,7 @@ struct Small2pLayout {
     kF = (size_t)kF_;
     kO = (size_t)kO_;
   }
-  __host__ __device__ size_t fixed() const { return 20 * kv + 32 + 32 * np + 4 * nr; }
+  __host__ __device__ size_t fixed() const { return 20 * kv + 32 + 48 * np + 5 * nr; }
   __host__ __device__ size_t tF() const { return kF * (kF | 1); }
   __host__ __device__ size_t cF() const { return kF * nr; }
   __host__ __device__ size_t g() const { return kF * kF; }
@@ -553,6 +558,45 @@ __device__ __forceinline__ void col_axpy_part(Acc M, int ncol, Rows rows, const 
   }
 }
 
+// Two right-hand sides sharing the loads of M (see col_axpy_part).
+template <class Acc, class Rows>
+__device__ __forceinline__ void col_axpy2_part(Acc M, int ncol, Rows rows, const double* va, const double* vb,
+                                               int64_t nrow, double* parta, double* partb, int w0, int nw) {
+  const int wi = (threadIdx.x >> 5) - w0, lane = threadIdx.x & 31;
+  double* pa = parta + (size_t)wi * nrow;
+  double* pb = partb + (size_t)wi * nrow;
+#pragma unroll 1
+  for (int64_t i = lane; i < nrow; i += 32) {
+    pa[i] = 0.0;
+    pb[i] = 0.0;
+  }
+  __syncwarp();
+#pragma unroll 1
+  for (int j = wi; j < ncol; j += nw) {
+    int64_t r = rows(j);
+    r = r < nrow ? r : nrow;
+    const double a1 = va[j], b1 = vb[j];
+#pragma unroll 1
+    for (int64_t i0 = lane; i0 < r; i0 += 128) {
+      double m[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) m[q] = (i0 + 32 * q < r) ? M(i0 + 32 * q, j) : 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (i0 + 32 * q < r) {
+          pa[i0 + 32 * q] += m[q] * a1;
+          pb[i0 + 32 * q] += m[q] * b1;
+        }
+    }
+    __syncwarp();
+  }
+}
+
+// Producer side of a named barrier (bar.arrive: no wait; the consumers bar.sync).
+__device__ __forceinline__ void named_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 __device__ __forceinline__ double part_sum(const double* part, int64_t nrow, int nw, int64_t i) {
   double v = 0.0;
 #pragma unroll 4
@@ -611,19 +655,22 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
   double* rowO = v[11];  // P_O[off, :] incl. the new column
   double* gO = v[12];
   double* tO = v[13];   // new T column (O)
-  double* zO = v[14];   // corner W_O^T (D_O z) -> coefficients
+  double* zO = v[14];   // corner W_O^T (D_O p_h)
+  double* zA = v[15];   // T_O zA + zoff T_O zB = T_O (sig_O W_O^T D_O z)
+  double* zB = v[16];
   double* sc = ssm + 20 * (size_t)kv;
   double* part = sc + 32;                 // [32][np]
-  // the fold chain's part of the CTA (critical path) gets 24 warps, the other
-  // chain's mix reflector and T column (off the critical path) 8
-  constexpr int kN1 = 768, kN2 = kSmallThreads - kN1, kW1 = kN1 / 32, kW2 = kN2 / 32;
-  double* partA = part;                    // part 1: [24][np]
-  double* partB = part + kW1 * (size_t)np; // part 2: [8][np]
-  double* xh = part + 32 * (size_t)np;    // x[0..off], later D_F p
+  // part 1 (fold chain) and part 2 (other chain, then beta_O) run side by side
+  constexpr int kN1 = kSmallThreads / 2, kN2 = kSmallThreads - kN1, kW1 = kN1 / 32, kW2 = kN2 / 32;
+  double* partA = part;                     // part 1: [16][np]
+  double* partB = part + kW1 * (size_t)np;  // part 2: [16][np]
+  double* partB2 = partB + kW2 * (size_t)np;  // part 2, second right-hand side: [16][np]
+  double* xh = part + 48 * (size_t)np;    // x[0..off], later D_F p
   double* ph = xh + nr;                   // p[0..off]
   double* dF = ph + nr;                   // D_F[0..off] (old)
   double* dO = dF + nr;                   // D_O[0..off] (old)
-  double* mtx = dO + nr;                  // prefetched matrices
+  double* dz = dO + nr;                   // D_O p, rows < off
+  double* mtx = dz + nr;                  // prefetched matrices
   const int ldF = kF | 1, ldO = kO | 1;
   double* sTF = mtx;
   double* sCF = sTF + (a.stTF ? L.tF() : 0);
@@ -645,11 +692,12 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
   // ---- phase 0 (before the wait, overlapping the previous pass): state the
   // previous stage wrote. The fold corner's element (off, kF - 1) is the one
   // entry the previous pass wrote: read after the wait.
-  {
+  const int kprev = (a.deferred && kF > 0) ? kF - 1 : -1;  // fold member of the previous stage
+  if (!a.finish) {
     const int nwp = kSmallThreads / 32;
     if (a.stTF)
 #pragma unroll 1
-      for (int j = w; j < kF; j += nwp)
+      for (int j = w; j < (kprev >= 0 ? kprev : kF); j += nwp)
 #pragma unroll 1
         for (int i = lane; i <= j; i += 32) cp_async8(sTF + i + (int64_t)j * ldF, a.chF.Tm + i + (int64_t)j * KF);
     if (a.stCF)
@@ -683,19 +731,46 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
 #pragma unroll 1
     for (int j = tid; j < kO; j += kSmallThreads) cp_async8(sgO + j, a.chO.sig + j);
 #pragma unroll 1
-    for (int64_t i = tid; i < nr; i += kSmallThreads) {
-      cp_async8(dF + i, i < a.chF.Dlen ? a.chF.Drow + i : a.chF.Dtail);
-      cp_async8(dO + i, i < a.chO.Dlen ? a.chO.Drow + i : a.chO.Dtail);
-    }
+    for (int64_t i = tid; i < nr; i += kSmallThreads) cp_async8(dO + i, i < a.chO.Dlen ? a.chO.Drow + i : a.chO.Dtail);
 #pragma unroll 1
     for (int j = tid; j < kO; j += kSmallThreads) rowO[j] = (double)PO[paddr(off, j, KO)];
 #pragma unroll 1
     for (int j = tid; j < kF - 1; j += kSmallThreads) rowF[j] = (double)PF[paddr(off, j, KF)];
-    if (tid == 0) {
-      cp_async8(sc + 7, a.chF.Dtail);
-      cp_async8(sc + 8, a.scal + kScNrm2e);
-    }
+    if (tid == 0) cp_async8(sc + 8, a.scal + kScNrm2e);
   }
+  if (kprev >= 0) {  // deferred: T_F[:, kprev] = -c T_F g (g = its Gram column), T[kprev, kprev] = c; D_F update
+#pragma unroll 1
+    for (int j = tid; j < kprev; j += kSmallThreads) gF[j] = a.chF.G[j + (int64_t)kprev * KF];
+    if (tid == 0) {
+      sc[15] = a.chF.c[kprev];
+      sc[16] = a.chF.s[kprev];
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    col_axpy_part(tF_at, kprev, [](int j) { return (int64_t)j + 1; }, gF, kprev, part, 0, kSmallThreads / 32);
+    __syncthreads();
+    const double cp = sc[15], sp = sc[16];
+#pragma unroll 1
+    for (int i = tid; i < kprev; i += kSmallThreads) {
+      const double tv = -cp * part_sum(part, kprev, kSmallThreads / 32, i);
+      a.chF.Tm[i + (int64_t)kprev * KF] = tv;
+      if (a.stTF) sTF[i + (int64_t)kprev * ldF] = tv;
+    }
+    if (tid == 0) {
+      a.chF.Tm[kprev + (int64_t)kprev * KF] = cp;
+      if (a.stTF) sTF[kprev + (int64_t)kprev * ldF] = cp;
+    }
+    if (sp != 1.0) st_D_update(a.chF, off - 1, sp, tid, kSmallThreads);
+    __syncthreads();
+  }
+  if (a.finish) {  // after a run's last pass: only the deferred work (ordered after that pass)
+    pdl_wait();
+    pdl_launch();
+    return;
+  }
+#pragma unroll 1
+  for (int64_t i = tid; i < nr; i += kSmallThreads) cp_async8(dF + i, i < a.chF.Dlen ? a.chF.Drow + i : a.chF.Dtail);
+  if (tid == 0) cp_async8(sc + 7, a.chF.Dtail);
   pdl_wait();
   HD_T2(1, 0);
   if (!a.late_launch) pdl_launch();
@@ -741,7 +816,7 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
     }
   }
   if (tid < kN1) {
-    // ======== part 1: fold chain (warps 0..23, the critical path)
+    // ======== part 1: fold chain (warps 0..15, the critical path)
 #pragma unroll 1
     for (int j = tid; j < kF; j += kN1) uF[j] = sgF[j] * aF[j];
     named_sync(1, kN1);
@@ -769,6 +844,7 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
       if (i < off) a.zbuf[i] = p;
     }
     named_sync(1, kN1);
+    named_arrive(3, kSmallThreads);  // p[0..off] ready for part 2
     HD_T2(5, 0);
     // W_h^T (x - W beta)_h, h = rows < off
     col_dots(pF, kF, [&](int) { return off; }, xh, hF, 0, kW1);
@@ -781,6 +857,7 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
     }
     named_sync(1, kN1);
     HD_T2(14, 0);
+    double escale = 0.0, iscale = 0.0, piv = 0.0;
     if (tid == 0) {
       const double xss = sc[0];
       const double nrm2 = xss - sc[3];
@@ -794,49 +871,65 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
       const double xn = sqrt(xss);
       int e = 0;
       if (xn > 0.0 && isfinite(xn)) frexp(xn, &e);
-      const double escale = ldexp(1.0, -e), iscale = ldexp(1.0, e);
+      escale = ldexp(1.0, -e);
+      iscale = ldexp(1.0, e);
+      piv = ph[off];
+      // make_reflector's sign rule and coefficient (reflect.hpp:157-174); the
+      // global writes follow the arrive below, off part 2's critical path
+      double sign;
+      if (a.rule == 0) sign = (piv >= 0.0) ? 1.0 : -1.0;
+      else if (a.rule == 1) sign = (piv > 0.0) ? 1.0 : -1.0;
+      else sign = (piv >= 0.0) ? 1.0 : 0.0;
+      if (nrm == 0.0) sign = 1.0;
+      const double cnew = (nrm == 0.0) ? 0.0 : 2.0 / (1.0 + 2.0 * sign * (piv / nrm) + sign * sign);
+      const double zoff = (nrm == 0.0) ? piv : (sign == 0.0 ? 0.0 : nrm);
+      sc[9] = zoff;
+      sc[5] = nrm;
+      sc[6] = sign;
+      sc[10] = cnew;
+    }
+    named_arrive(4, kSmallThreads);  // zoff ready for part 2
+    if (tid == 0) {
+      const double nrm = sc[5], sign = sc[6], cnew = sc[10], zoff = sc[9];
+      if (nrm == 0.0) {  // identity reflector: zero column, c = 0, s = 1
+        a.chF.sig[kF] = 0.0;
+        a.chF.c[kF] = 0.0;
+        a.chF.s[kF] = 1.0;
+      } else {
+        PF[paddr(off, kF, KF)] = (T)((piv + sign * nrm) * escale);
+        a.chF.sig[kF] = iscale / nrm;
+        a.chF.c[kF] = cnew;
+        a.chF.s[kF] = -sign;
+      }
       a.scal[kScEscale] = escale;
       a.scal[kScIscale] = iscale;
-      a.scal[kScDold] = sc[7];
+      a.scal[kScDold] = sc[7];  // D_F on rows >= off before this member (the pass's p = D_old (x - P beta))
       a.scal[kScNrm2e] = nrm * nrm;
-      const double piv = ph[off];
-      double cnew;
-      const double sign = refl_scalars<T>(a.chF, PF, kF, off, nrm, piv, a.rule, escale, iscale, &cnew);
-      const double zoff = (nrm == 0.0) ? piv : (sign == 0.0 ? 0.0 : nrm);
       a.scal[kScNrm] = nrm;
       a.scal[kScCoefCur] = zoff;
       a.scal[kScSign] = sign;
       a.zbuf[off] = zoff;
-      sc[5] = nrm;
-      sc[6] = sign;
-      sc[9] = zoff;
-      sc[10] = cnew;
-      // D_F on rows >= off, before this member (the pass's p = D_old (x - P beta))
     }
     named_sync(1, kN1);
     HD_T2(6, 0);
     const double nrm = sc[5], sign = sc[6], cnew = sc[10], dold = sc[7];
     // Gram column of w_new = (p[off:] + sign nrm e_off) / nrm against W:
     //   W^T p[off:] = D_old ((W^T x - G bh) - W_h^T (x - W beta)_h)
+    // (its T column and the D_F update are deferred to the next stage's
+    // prologue, which overlaps the pass: see the top of this kernel)
 #pragma unroll 1
     for (int j = tid; j < kF; j += kN1) {
       const double g = (nrm == 0.0) ? 0.0 : dold * ((uF[j] - gF[j]) - sgF[j] * hF[j]) / nrm + sign * sgF[j] * rowF[j];
-      gF[j] = g;
       a.chF.G[j + (int64_t)kF * KF] = g;
       a.chF.G[kF + (int64_t)j * KF] = g;
     }
     if (tid == 0) a.chF.G[kF + (int64_t)kF * KF] = (nrm == 0.0) ? 0.0 : 2.0 / cnew;
-    if (nrm != 0.0) st_D_update(a.chF, off, -sign, tid, kN1);
-    named_sync(1, kN1);
-    // T column: T[:k, k] = -c T g, T[k, k] = c
-    col_axpy_part(tF_at, kF, [](int j) { return (int64_t)j + 1; }, gF, kF, partA, 0, kW1);
-    named_sync(1, kN1);
-#pragma unroll 1
-    for (int i = tid; i < kF; i += kN1) a.chF.Tm[i + (int64_t)kF * KF] = -cnew * part_sum(partA, kF, kW1, i);
-    if (tid == 0) a.chF.Tm[kF + (int64_t)kF * KF] = cnew;
     HD_T2(7, 0);
   } else {
-    // ======== part 2: other chain (warps 24..31), mix reflector H(g, off) -> column kO
+    // ======== part 2: other chain (warps 16..31): mix reflector H(g, off) ->
+    // column kO, its T column, then beta_O = sig_O T_O (sig_O W_O^T D_O z),
+    // z = [p_h, zoff], split as T_O zA + zoff T_O zB so that only the last
+    // step waits for zoff
     const int t2 = tid - kN1;
     const double nrm = sqrt(sc[1]);
     const double piv = sc[4];
@@ -861,8 +954,7 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
     if (t2 == 0) a.chO.G[kO + (int64_t)kO * KO] = (nrm == 0.0) ? 0.0 : 2.0 / cB;
     if (nrm != 0.0) st_D_update(a.chO, off, -sign, t2, kN2);
     named_sync(2, kN2);
-    col_axpy_part(tO_at, kO, [](int j) { return (int64_t)j + 1; }, gO, kO, partB,
-                  kW1, kW2);
+    col_axpy_part(tO_at, kO, [](int j) { return (int64_t)j + 1; }, gO, kO, partB, kW1, kW2);
     named_sync(2, kN2);
 #pragma unroll 1
     for (int i = t2; i < kO; i += kN2) {
@@ -875,29 +967,38 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
       a.chO.Tm[kO + (int64_t)kO * KO] = cB;
     }
     HD_T2(9, kN1);
+    named_sync(3, kSmallThreads);  // p[0..off] from part 1
+    HD_T2(10, kN1);
+#pragma unroll 1
+    for (int64_t i = t2; i < off; i += kN2) dz[i] = dO[i] * ph[i];
+    named_sync(2, kN2);
+    col_dots(pO, kO, [&](int) { return off; }, dz, zO, kW1, kW2);
+    named_sync(2, kN2);
+    if (a.late_launch == 1) pdl_launch();
+    const double doff = sc[13];
+#pragma unroll 1
+    for (int j = t2; j <= kO; j += kN2) {
+      zA[j] = (j < kO) ? sgO[j] * zO[j] : 0.0;
+      zB[j] = sgO[j] * rowO[j] * doff;
+    }
+    named_sync(2, kN2);
+    HD_T2(11, kN1);
+    const int kO1 = kO + 1;
+    col_axpy2_part([&](int64_t i, int j) { return (j == kO) ? tO[i] : tO_at(i, j); }, kO1,
+                   [](int j) { return (int64_t)j + 1; }, zA, zB, kO1, partB, partB2, kW1, kW2);
+    named_sync(2, kN2);
+#pragma unroll 1
+    for (int j = t2; j < kO1; j += kN2) {
+      zA[j] = part_sum(partB, kO1, kW2, j);
+      zB[j] = part_sum(partB2, kO1, kW2, j);
+    }
+    HD_T2(12, kN1);
+    named_sync(4, kSmallThreads);  // zoff from part 1
+    if (a.late_launch == 2) pdl_launch();
+    const double zoff = sc[9];
+#pragma unroll 1
+    for (int j = t2; j < kO1; j += kN2) a.betaO[j] = sgO[j] * (zA[j] + zoff * zB[j]);
   }
-  __syncthreads();
-  HD_T2(10, 0);
-  // ---- beta_O = sig_O T_O (sig_O (W_O^T D_O z)) over the sparse z = [p_h, zoff]
-#pragma unroll 1
-  for (int64_t i = tid; i < off; i += kSmallThreads) xh[i] = dO[i] * ph[i];
-  __syncthreads();
-  col_dots(pO, kO, [&](int) { return off; }, xh, zO, 0, kSmallThreads / 32);
-  __syncthreads();
-  if (a.late_launch == 1) pdl_launch();
-  const double zc = sc[13] * sc[9];
-#pragma unroll 1
-  for (int j = tid; j <= kO; j += kSmallThreads) zO[j] = (j < kO) ? sgO[j] * (zO[j] + rowO[j] * zc) : sgO[kO] * rowO[kO] * zc;
-  __syncthreads();
-  HD_T2(11, 0);
-  const int kO1 = kO + 1;
-  col_axpy_part([&](int64_t i, int j) { return (j == kO) ? tO[i] : tO_at(i, j); }, kO1, [](int j) { return (int64_t)j + 1; },
-                zO, kO1, part, 0, kSmallThreads / 32);
-  __syncthreads();
-  HD_T2(12, 0);
-  if (a.late_launch == 2) pdl_launch();
-#pragma unroll 1
-  for (int j = tid; j < kO1; j += kSmallThreads) a.betaO[j] = sgO[j] * part_sum(part, kO1, kSmallThreads / 32, j);
   if (a.trace) {
     __syncthreads();
     HD_T2(13, 0);
