@@ -973,6 +973,10 @@ struct SmallArgs {
   int nslots_in = 0;           // slot rows of `partials` staged by the stage
   int stageC = 0;              // stage the sparse-input corner of P_B in shared memory
   unsigned long long* trace = nullptr;  // debug: %globaltimer stamps per phase (HD_TRACE)
+  // 1: do not trigger the next launch early (griddepcontrol.launch_dependents
+  // right after the wait); it then starts when this stage exits, and its
+  // early TMA prefetch no longer competes with the stage (HD_LATE_LAUNCH)
+  int late_launch = 0;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -1165,7 +1169,7 @@ __device__ __forceinline__ void k_small_dots_impl(const SmallArgs& a) {
   HD_STAMP(a, 0);
   pdl_wait();
   HD_STAMP(a, 1);
-  pdl_launch();
+  if (!a.late_launch) pdl_launch();
   const int kv = small_kv(a.kA, a.kB);
   const SmallSmem m = small_smem(ssm, kv);
   double* aA = m.v0;     // red A dot
@@ -1342,7 +1346,7 @@ template <typename T, bool HAAR>
 __device__ __forceinline__ void k_small_fold_impl(const SmallArgs& a) {
   extern __shared__ double ssm[];
   pdl_wait();
-  pdl_launch();
+  if (!a.late_launch) pdl_launch();
   const int kv = small_kv(a.kA, a.kB);
   const SmallSmem m = small_smem(ssm, kv);
   double* az = m.v0;    // corner partial sum_{i<off} P_B[i,j] D_B(i) p_i
@@ -1458,7 +1462,7 @@ template <typename T>
 __device__ __forceinline__ void k_small_gin_impl(const SmallArgs& a) {
   extern __shared__ double ssm[];
   pdl_wait();
-  pdl_launch();
+  if (!a.late_launch) pdl_launch();
   if (aborted(a.status)) return;
   const int kv = small_kv(0, a.kB);
   const SmallSmem m = small_smem(ssm, kv);

@@ -212,6 +212,7 @@ struct hd_op {
   int spare_sms = 0;  // SMs the persistent streaming grids leave free (HD_SPARE_SMS)
   int max_warps = 8;  // streaming warps per CTA cap (HD_WARPS fixes it)
   bool warps_fixed = false;
+  int late_launch = 0;   // three-pass single-CTA stages trigger the next launch on exit (HD_LATE_LAUNCH=1)
   int fused = 1;         // two-pass Haar runs (hd_fused.cuh; HD_FUSED=0 disables)
   bool fused_retry = false;  // the current run fell back to the three-pass sequence
   int fold_reverse = 1;  // fold streams its panel last-to-first (HD_FOLD_FORWARD=1 disables)
