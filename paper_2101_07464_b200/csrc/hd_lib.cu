@@ -215,6 +215,11 @@ struct hd_op {
   int late_launch = 0;   // three-pass single-CTA stages trigger the next launch on exit (HD_LATE_LAUNCH=1)
   int fused = 1;         // two-pass Haar runs (hd_fused.cuh; HD_FUSED=0 disables)
   bool fused_retry = false;  // the current run fell back to the three-pass sequence
+  // two-pass tuning / A/B knobs, read at hd_create (hd_fused_host.inc)
+  double fused_guard = -1.0, fused_check = -1.0;  // HD_FUSED_GUARD / HD_FUSED_CHECK (< 0: defaults)
+  int fused_late = -1;                             // HD_2P_LATE (< 0: default)
+  bool fused_reverse = false;                      // HD_2P_REVERSE=1
+  std::string fused_stage_order;                   // HD_2P_STAGE_ORDER
   int fold_reverse = 1;  // fold streams its panel last-to-first (HD_FOLD_FORWARD=1 disables)
   int64_t l2_keep = 96ll << 20;  // k_dots keeps its last bytes in L2 for that fold (HD_L2_KEEP_MB)
   int64_t l2_fold_keep = 0;  // ... and the fold its last bytes for the next k_dots (HD_L2_FOLD_KEEP_MB)
