@@ -1009,4 +1009,427 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_2p(const __grid_constan
   k_small_2p_impl<T>(a);
 }
 
+// ============================================================ k_small_2pc
+// The same stage on a cluster of two CTAs (two SMs): CTA 0 the fold chain,
+// CTA 1 the other chain and beta_O, each with all 32 warps and its own shared
+// memory for its chain's k x k state (prefetched before the wait). CTA 1 reads
+// p[0..off] and zoff from CTA 0's shared memory (distributed shared memory),
+// ordered by cluster barrier phases: A = p ready, B = zoff ready, C = done.
+struct Small2pcLayout {
+  size_t kv, np, nr;
+  __host__ __device__ Small2pcLayout(int kF, int kO, int64_t off) {
+    const int km = kF > kO ? kF : kO;
+    kv = (size_t)small_kv(km + 1, km + 1);
+    nr = (size_t)off + 1;
+    np = kv > nr ? kv : nr;
+  }
+  // 10 vectors, 32 scalars, 5 head vectors, 16 (CTA 0) or 32 (CTA 1) partial
+  // rows; then the CTA's own matrices. p[0..off] (CTA 0) is read by CTA 1 at
+  // the same offset (ph()).
+  __host__ __device__ size_t ph() const { return 10 * kv + 32 + nr; }
+  __host__ __device__ size_t fixed(int rank) const { return 10 * kv + 32 + 5 * nr + (rank == 0 ? 16 : 32) * np; }
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+// load a double from the same shared-memory offset in CTA `rank` of the cluster
+__device__ __forceinline__ double ld_dsmem(const double* local, uint32_t rank) {
+  uint32_t a = smem_u32(local), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(r) : "memory");
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ void k_small_2pc_impl(const Small2pArgs& a) {
+  extern __shared__ double ssm[];
+  const uint32_t rank = cluster_rank();
+  HD_T2(0, 0);
+  const int kF = a.kF, kO = a.kO;
+  const int64_t off = a.off, nr = off + 1;
+  const Small2pcLayout L(kF, kO, off);
+  const int kv = (int)L.kv;
+  const int64_t np = (int64_t)L.np;
+  double* v[10];
+  for (int q = 0; q < 10; ++q) v[q] = ssm + (size_t)q * kv;
+  double* sc = ssm + 10 * (size_t)kv;
+  double* xh = sc + 32;                       // x[0..off], later D_F p
+  double* ph = ssm + L.ph();                  // p[0..off] (CTA 0's, read by CTA 1 remotely)
+  double* dF = ph + nr;                       // D_F[0..off] (old)
+  double* dO = dF + nr;                       // D_O[0..off] (old)
+  double* dz = dO + nr;                       // D_O p, rows < off
+  double* part = dz + nr;                     // [16][np]
+  double* part2 = part + 16 * (size_t)np;     // [16][np] (CTA 1)
+  double* mtx = ssm + L.fixed((int)rank);     // this CTA's prefetched matrices
+  int* st = reinterpret_cast<int*>(sc + 28);
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  constexpr int NW = kSmallThreads / 32, NP = 16;  // warps; partial rows of the T v products
+  T* PF = (T*)a.PF;
+  T* PO = (T*)a.PO;
+  const int64_t KF = a.chF.K, KO = a.chO.K;
+  const int ldF = kF | 1, ldO = kO | 1;
+  if (rank == 0) {
+    // ================================================= CTA 0: fold chain
+    double* aF = v[0];
+    double* sgF = v[1];
+    double* uF = v[2];
+    double* bh = v[3];
+    double* b1 = v[4];
+    double* gF = v[5];
+    double* hF = v[6];
+    double* rowF = v[7];
+    double* sCF = mtx;
+    double* sTF = sCF + (a.stCF ? (size_t)kF * nr : 0);
+    double* sG = sTF + (a.stTF ? (size_t)kF * ldF : 0);
+    auto tF_at = [&](int64_t i, int j) { return a.stTF ? sTF[i + (int64_t)j * ldF] : a.chF.Tm[i + (int64_t)j * KF]; };
+    auto g_at = [&](int64_t i, int j) { return a.stG ? sG[i + (int64_t)j * kF] : a.chF.G[i + (int64_t)j * KF]; };
+    auto pF = [&](int64_t i, int j) { return a.stCF ? sCF[i + (int64_t)j * nr] : (double)PF[paddr(i, j, KF)]; };
+    const int kprev = (a.deferred && kF > 0) ? kF - 1 : -1;
+    // ---- before the wait: the previous stage's state
+    if (!a.finish) {
+      if (a.stTF)
+#pragma unroll 1
+        for (int j = w; j < (kprev >= 0 ? kprev : kF); j += NW)
+#pragma unroll 1
+          for (int i = lane; i <= j; i += 32) cp_async8(sTF + i + (int64_t)j * ldF, a.chF.Tm + i + (int64_t)j * KF);
+      if (a.stCF)
+#pragma unroll 1
+        for (int j = w; j < kF; j += NW)
+#pragma unroll 1
+          for (int64_t i = lane; i < nr; i += 32) {
+            if (sizeof(T) == 8) cp_async8(sCF + i + (int64_t)j * nr, reinterpret_cast<const double*>(PF) + paddr(i, j, KF));
+            else sCF[i + (int64_t)j * nr] = (double)PF[paddr(i, j, KF)];
+          }
+      if (a.stG)
+#pragma unroll 1
+        for (int j = w; j < kF; j += NW)
+#pragma unroll 1
+          for (int i = lane; i < kF; i += 32) cp_async8(sG + i + (int64_t)j * kF, a.chF.G + i + (int64_t)j * KF);
+#pragma unroll 1
+      for (int j = tid; j < kF; j += kSmallThreads) cp_async8(sgF + j, a.chF.sig + j);
+#pragma unroll 1
+      for (int j = tid; j < kF - 1; j += kSmallThreads) rowF[j] = (double)PF[paddr(off, j, KF)];
+      if (tid == 0) cp_async8(sc + 8, a.scal + kScNrm2e);
+    }
+    if (kprev >= 0) {  // deferred: T_F[:, kprev] = -c T_F g, T[kprev, kprev] = c; D_F update
+#pragma unroll 1
+      for (int j = tid; j < kprev; j += kSmallThreads) gF[j] = a.chF.G[j + (int64_t)kprev * KF];
+      if (tid == 0) {
+        sc[15] = a.chF.c[kprev];
+        sc[16] = a.chF.s[kprev];
+      }
+      cp_async_wait_all();
+      __syncthreads();
+      if (w < NP) col_axpy_part(tF_at, kprev, [](int j) { return (int64_t)j + 1; }, gF, kprev, part, 0, NP);
+      __syncthreads();
+      const double cp = sc[15], sp = sc[16];
+#pragma unroll 1
+      for (int i = tid; i < kprev; i += kSmallThreads) {
+        const double tv = -cp * part_sum(part, kprev, NP, i);
+        a.chF.Tm[i + (int64_t)kprev * KF] = tv;
+        if (a.stTF) sTF[i + (int64_t)kprev * ldF] = tv;
+      }
+      if (tid == 0) {
+        a.chF.Tm[kprev + (int64_t)kprev * KF] = cp;
+        if (a.stTF) sTF[kprev + (int64_t)kprev * ldF] = cp;
+      }
+      if (sp != 1.0) st_D_update(a.chF, off - 1, sp, tid, kSmallThreads);
+      __syncthreads();
+    }
+    if (a.finish) {  // after a run's last pass: only the deferred work
+      pdl_wait();
+      pdl_launch();
+      return;
+    }
+#pragma unroll 1
+    for (int64_t i = tid; i < nr; i += kSmallThreads) cp_async8(dF + i, i < a.chF.Dlen ? a.chF.Drow + i : a.chF.Dtail);
+    if (tid == 0) cp_async8(sc + 7, a.chF.Dtail);
+    pdl_wait();
+    HD_T2(1, 0);
+    // ---- after the wait: what the previous pass wrote
+    if (tid == 0) {
+      cp_async4(st + 0, a.status + kStAbort);
+      cp_async4(st + 1, a.status + kStBadInput);
+    }
+    const T* X = (const T*)a.x;
+#pragma unroll 1
+    for (int64_t i = tid; i < nr; i += kSmallThreads) xh[i] = (double)X[i];
+    if (tid == 32 && kF > 0) {
+      const double e = (double)PF[paddr(off, kF - 1, KF)];
+      rowF[kF - 1] = e;
+      if (a.stCF) sCF[off + (int64_t)(kF - 1) * nr] = e;
+    }
+    {
+      const int e0 = kF, e1 = e0 + 1, e2 = e1 + (a.slot_pss >= 0 ? 1 : 0);
+#pragma unroll 1
+      for (int t = tid; t < e2; t += kSmallThreads) {
+        if (t < e0) aF[t] = slot_sum_wide(a.partials, a.nblk, a.slot_aF + t);
+        else if (t < e1) sc[0] = slot_sum_wide(a.partials, a.nblk, a.slot_xss);
+        else sc[2] = slot_sum_wide(a.partials, a.nblk, a.slot_pss);
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    HD_T2(2, 0);
+    // no early exit past this point in either CTA (they meet at cluster
+    // barriers): an aborted probe computes on, and every later kernel no-ops
+    if (st[0] == 0 && st[1] != 0 && tid == 0) *(volatile int*)(a.status + kStAbort) = 1;
+    if (a.slot_pss >= 0 && tid == 0) {  // a posteriori check of the previous probe's early norm
+      const double ex = sc[2], ea = sc[8];
+      if (!(fabs(ex - ea) <= a.check_tol * ea)) {
+        atomicOr(a.status + kStFused, 1);
+        atomicOr(a.status + kStAbort, 1);
+      }
+    }
+    HD_T2(3, 0);
+#pragma unroll 1
+    for (int j = tid; j < kF; j += kSmallThreads) uF[j] = sgF[j] * aF[j];
+    __syncthreads();
+    col_dots(tF_at, kF, [](int j) { return (int64_t)j + 1; }, uF, bh, 0, NW);
+    __syncthreads();
+    HD_T2(4, 0);
+#pragma unroll 1
+    for (int j = tid; j < kF; j += kSmallThreads) b1[j] = sgF[j] * bh[j];
+    __syncthreads();
+    // head rows p_i = D_i (x_i - sum_j P[i, j] b1_j), i <= off (warps 0..15),
+    // G bh beside them (warps 16..31)
+    if (w < NP) col_axpy_part(pF, kF, [&](int) { return nr; }, b1, nr, part, 0, NP);
+    else col_dots(g_at, kF, [&](int) { return (int64_t)kF; }, bh, gF, NP, NW - NP);
+    __syncthreads();
+#pragma unroll 1
+    for (int64_t i = tid; i < nr; i += kSmallThreads) {
+      const double p = dF[i] * (xh[i] - part_sum(part, nr, NP, i));
+      ph[i] = p;
+      xh[i] = dF[i] * p;  // (x - W beta)_i, the h-vector input below
+    }
+    __syncthreads();
+    // A: p[0..off] ready for CTA 1 (the arrive releases this CTA's pending
+    // writes, so the global ones follow it)
+    cluster_arrive();
+#pragma unroll 1
+    for (int64_t i = tid; i < nr; i += kSmallThreads) {
+      a.head[i] = ph[i];
+      if (i < off) a.zbuf[i] = ph[i];
+    }
+#pragma unroll 1
+    for (int j = tid; j < kF; j += kSmallThreads) a.betaF[j] = b1[j];
+    HD_T2(5, 0);
+    col_dots(pF, kF, [&](int) { return off; }, xh, hF, 0, NW - 1);
+    if (w == NW - 1) {
+      double hs = 0.0;
+#pragma unroll 1
+      for (int64_t i = lane; i < off; i += 32) hs += ph[i] * ph[i];
+      hs = warp_sum(hs);
+      if (lane == 0) sc[3] = hs;
+    }
+    __syncthreads();
+    HD_T2(14, 0);
+    double escale = 0.0, iscale = 0.0, piv = 0.0;
+    if (tid == 0) {
+      const double xss = sc[0];
+      const double nrm2 = xss - sc[3];
+      double nrm = 0.0;
+      if (!(nrm2 >= a.guard * xss) || !(nrm2 > 0.0 || xss == 0.0)) {
+        atomicOr(a.status + kStFused, 1);
+        atomicOr(a.status + kStAbort, 1);
+      } else {
+        nrm = sqrt(nrm2);
+      }
+      const double xn = sqrt(xss);
+      int e = 0;
+      if (xn > 0.0 && isfinite(xn)) frexp(xn, &e);
+      escale = ldexp(1.0, -e);
+      iscale = ldexp(1.0, e);
+      piv = ph[off];
+      double sign;  // make_reflector's sign rule and coefficient (reflect.hpp:157-174)
+      if (a.rule == 0) sign = (piv >= 0.0) ? 1.0 : -1.0;
+      else if (a.rule == 1) sign = (piv > 0.0) ? 1.0 : -1.0;
+      else sign = (piv >= 0.0) ? 1.0 : 0.0;
+      if (nrm == 0.0) sign = 1.0;
+      sc[9] = (nrm == 0.0) ? piv : (sign == 0.0 ? 0.0 : nrm);  // zoff
+      sc[5] = nrm;
+      sc[6] = sign;
+      sc[10] = (nrm == 0.0) ? 0.0 : 2.0 / (1.0 + 2.0 * sign * (piv / nrm) + sign * sign);
+    }
+    __syncthreads();
+    cluster_wait();    // (A complete)
+    cluster_arrive();  // B: zoff ready for CTA 1
+    if (a.late_launch == 1) pdl_launch();
+    HD_T2(6, 0);
+    const double nrm = sc[5], sign = sc[6], cnew = sc[10], dold = sc[7], zoff = sc[9];
+    if (tid == 0) {
+      if (nrm == 0.0) {  // identity reflector: zero column, c = 0, s = 1
+        a.chF.sig[kF] = 0.0;
+        a.chF.c[kF] = 0.0;
+        a.chF.s[kF] = 1.0;
+      } else {
+        PF[paddr(off, kF, KF)] = (T)((piv + sign * nrm) * escale);
+        a.chF.sig[kF] = iscale / nrm;
+        a.chF.c[kF] = cnew;
+        a.chF.s[kF] = -sign;
+      }
+      a.scal[kScEscale] = escale;
+      a.scal[kScIscale] = iscale;
+      a.scal[kScDold] = dold;  // D_F on rows >= off before this member (the pass's p = D_old (x - P beta))
+      a.scal[kScNrm2e] = nrm * nrm;
+      a.scal[kScNrm] = nrm;
+      a.scal[kScCoefCur] = zoff;
+      a.scal[kScSign] = sign;
+      a.zbuf[off] = zoff;
+    }
+    // Gram column of w_new = (p[off:] + sign nrm e_off) / nrm against W:
+    //   W^T p[off:] = D_old ((W^T x - G bh) - W_h^T (x - W beta)_h)
+#pragma unroll 1
+    for (int j = tid; j < kF; j += kSmallThreads) {
+      const double g = (nrm == 0.0) ? 0.0 : dold * ((uF[j] - gF[j]) - sgF[j] * hF[j]) / nrm + sign * sgF[j] * rowF[j];
+      a.chF.G[j + (int64_t)kF * KF] = g;
+      a.chF.G[kF + (int64_t)j * KF] = g;
+    }
+    if (tid == 0) a.chF.G[kF + (int64_t)kF * KF] = (nrm == 0.0) ? 0.0 : 2.0 / cnew;
+    HD_T2(7, 0);
+    cluster_wait();    // (B complete)
+    if (a.late_launch != 1) pdl_launch();
+    cluster_arrive();  // C: CTA 1 is done reading our shared memory
+    cluster_wait();
+    if (a.trace) HD_T2(13, 0);
+  } else {
+    // ================================================= CTA 1: other chain
+    double* aO = v[0];
+    double* sgO = v[1];
+    double* rowO = v[2];
+    double* gO = v[3];
+    double* tO = v[4];
+    double* zO = v[5];
+    double* zA = v[6];
+    double* zB = v[7];
+    double* sCO = mtx;
+    double* sTO = sCO + (a.stCO ? (size_t)kO * nr : 0);
+    auto tO_at = [&](int64_t i, int j) { return a.stTO ? sTO[i + (int64_t)j * ldO] : a.chO.Tm[i + (int64_t)j * KO]; };
+    auto pO = [&](int64_t i, int j) { return a.stCO ? sCO[i + (int64_t)j * nr] : (double)PO[paddr(i, j, KO)]; };
+    if (a.finish) return;
+    if (a.stTO)
+#pragma unroll 1
+      for (int j = w; j < kO; j += NW)
+#pragma unroll 1
+        for (int i = lane; i <= j; i += 32) cp_async8(sTO + i + (int64_t)j * ldO, a.chO.Tm + i + (int64_t)j * KO);
+    if (a.stCO)
+#pragma unroll 1
+      for (int j = w; j < kO; j += NW)
+#pragma unroll 1
+        for (int64_t i = lane; i < nr; i += 32) {
+          if (sizeof(T) == 8) cp_async8(sCO + i + (int64_t)j * nr, reinterpret_cast<const double*>(PO) + paddr(i, j, KO));
+          else sCO[i + (int64_t)j * nr] = (double)PO[paddr(i, j, KO)];
+        }
+#pragma unroll 1
+    for (int j = tid; j < kO; j += kSmallThreads) cp_async8(sgO + j, a.chO.sig + j);
+#pragma unroll 1
+    for (int64_t i = tid; i < nr; i += kSmallThreads) cp_async8(dO + i, i < a.chO.Dlen ? a.chO.Drow + i : a.chO.Dtail);
+#pragma unroll 1
+    for (int j = tid; j < kO; j += kSmallThreads) rowO[j] = (double)PO[paddr(off, j, KO)];
+    pdl_wait();
+    if (tid == 0) {
+      cp_async8(sc + 4, a.scal + kScPivotG);
+      cp_async4(st + 0, a.status + kStAbort);
+      cp_async4(st + 1, a.status + kStBadInput);
+    }
+    {
+      const int e0 = kO, e1 = e0 + 1;
+#pragma unroll 1
+      for (int t = tid; t < e1; t += kSmallThreads) {
+        if (t < e0) aO[t] = slot_sum_wide(a.partials, a.nblk, a.slot_spec + t);
+        else sc[1] = slot_sum_wide(a.partials, a.nblk, a.slot_gss);
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    HD_T2(8, 0);
+    // mix reflector H(g, off) -> column kO
+    const double nrmg = sqrt(sc[1]);
+    const double pivg = sc[4];
+    if (tid == 0) {
+      double cB;
+      const double sign = refl_scalars<T>(a.chO, PO, kO, off, nrmg, pivg, a.rule, 1.0, 1.0, &cB);
+      sc[11] = sign;
+      sc[12] = cB;
+      sgO[kO] = (nrmg == 0.0) ? 0.0 : 1.0 / nrmg;
+      rowO[kO] = (nrmg == 0.0) ? 0.0 : (double)(T)(pivg + sign * nrmg);
+      sc[13] = (nrmg == 0.0) ? dO[off] : -sign * dO[off];  // D_O[off] after the update
+    }
+    __syncthreads();
+    const double signg = sc[11], cB = sc[12];
+#pragma unroll 1
+    for (int j = tid; j < kO; j += kSmallThreads) {
+      gO[j] = (nrmg == 0.0) ? 0.0 : sgO[j] * (aO[j] / nrmg + signg * rowO[j]);
+      a.chO.G[j + (int64_t)kO * KO] = gO[j];
+    }
+    if (tid == 0) a.chO.G[kO + (int64_t)kO * KO] = (nrmg == 0.0) ? 0.0 : 2.0 / cB;
+    if (nrmg != 0.0) st_D_update(a.chO, off, -signg, tid, kSmallThreads);
+    __syncthreads();
+    // warps 0..15: the new T column -c T_O g; warps 16..31: T_O zB over the
+    // old columns (zB needs nothing from CTA 0; the new column's share is
+    // added after)
+    const double doff = sc[13];
+#pragma unroll 1
+    for (int j = tid; j <= kO; j += kSmallThreads) zB[j] = sgO[j] * rowO[j] * doff;
+    __syncthreads();
+    if (w < NP) col_axpy_part(tO_at, kO, [](int j) { return (int64_t)j + 1; }, gO, kO, part, 0, NP);
+    else col_axpy_part(tO_at, kO, [](int j) { return (int64_t)j + 1; }, zB, kO, part2, NP, NW - NP);
+    __syncthreads();
+#pragma unroll 1
+    for (int i = tid; i < kO; i += kSmallThreads) {
+      const double tv = -cB * part_sum(part, kO, NP, i);
+      tO[i] = tv;
+      a.chO.Tm[i + (int64_t)kO * KO] = tv;
+    }
+    if (tid == 0) {
+      tO[kO] = cB;
+      a.chO.Tm[kO + (int64_t)kO * KO] = cB;
+    }
+    __syncthreads();
+    const int kO1 = kO + 1;
+    double* vB = gO;  // T_O zB (gO is no longer needed)
+#pragma unroll 1
+    for (int i = tid; i < kO1; i += kSmallThreads)
+      vB[i] = ((i < kO) ? part_sum(part2, kO, NW - NP, i) : 0.0) + tO[i] * zB[kO];
+    HD_T2(9, 0);
+    cluster_arrive();  // A
+    cluster_wait();    // p[0..off] of CTA 0 ready
+    HD_T2(10, 0);
+#pragma unroll 1
+    for (int64_t i = tid; i < off; i += kSmallThreads) dz[i] = dO[i] * ld_dsmem(ph + i, 0);
+    __syncthreads();
+    col_dots(pO, kO, [&](int) { return off; }, dz, zO, 0, NW);
+    __syncthreads();
+    if (a.late_launch == 1) pdl_launch();
+#pragma unroll 1
+    for (int j = tid; j < kO; j += kSmallThreads) zA[j] = sgO[j] * zO[j];
+    __syncthreads();
+    HD_T2(11, 0);
+    // T_O zA: zA's row kO is zero, so only the old columns contribute
+    if (w < NP) col_axpy_part(tO_at, kO, [](int j) { return (int64_t)j + 1; }, zA, kO, part, 0, NP);
+    __syncthreads();
+#pragma unroll 1
+    for (int j = tid; j < kO1; j += kSmallThreads) zO[j] = (j < kO) ? part_sum(part, kO, NP, j) : 0.0;
+    HD_T2(12, 0);
+    cluster_arrive();  // B
+    cluster_wait();    // zoff of CTA 0 ready
+    if (a.late_launch == 2) pdl_launch();
+    const double zoff = ld_dsmem(sc + 9, 0);
+#pragma unroll 1
+    for (int j = tid; j < kO1; j += kSmallThreads) a.betaO[j] = sgO[j] * (zO[j] + zoff * vB[j]);
+    cluster_arrive();  // C: done with CTA 0's shared memory
+    cluster_wait();
+  }
+}
+template <typename T>
+__global__ void __launch_bounds__(kSmallThreads) k_small_2pc(const __grid_constant__ Small2pArgs a) {
+  k_small_2pc_impl<T>(a);
+}
+
 }  // namespace hd

@@ -219,6 +219,7 @@ struct hd_op {
   double fused_guard = -1.0, fused_check = -1.0;  // HD_FUSED_GUARD / HD_FUSED_CHECK (< 0: defaults)
   int fused_late = -1;                             // HD_2P_LATE (< 0: default)
   bool fused_reverse = false;                      // HD_2P_REVERSE=1
+  bool fused_cluster = true;                       // stage on a 2-CTA cluster (HD_2P_CLUSTER=0: one CTA)
   std::string fused_stage_order;                   // HD_2P_STAGE_ORDER
   int fold_reverse = 1;  // fold streams its panel last-to-first (HD_FOLD_FORWARD=1 disables)
   int64_t l2_keep = 96ll << 20;  // k_dots keeps its last bytes in L2 for that fold (HD_L2_KEEP_MB)
