@@ -177,3 +177,19 @@ def test_fused_async_run(lm):
     a.wait()
     yb = b.run(x1, T, update="tanh_mix", sides="right")
     assert rel(out.cpu(), yb.cpu()) < 1e-12
+
+
+@pytest.mark.parametrize("cluster", ["1", "0"])
+def test_fused_stage_variants_match(orc, lm, monkeypatch, cluster):
+    # the stage on a 2-CTA cluster (default) and on one CTA (HD_2P_CLUSTER=0)
+    # both match the oracle; the one-CTA variant stays covered
+    monkeypatch.setenv("HD_2P_CLUSTER", cluster)
+    n, T, seed = 12000, 40, 29
+    x1 = orc.RandomSource(seed, 1).normal_vector(n)
+    x1 /= np.linalg.norm(x1)
+    want = orc.Operator("haar", n=n, seed=seed).run("tanh_mix", "right", T, x1, keep=False)[0]
+    op = haar(lm, n, seed=seed, draws="injected", capacity=T)
+    op.push_draws(orc.draws_for(seed, [n] * T))
+    got = op.run(x1, T, update="tanh_mix", sides="right")
+    assert per_probe_launches(op, T) < 2.5
+    assert rel(got, want) < TOL64
