@@ -25,7 +25,7 @@ namespace hd {
 enum { kStFused = 3 };  // status word: the two-pass run lost precision (host re-runs)
 
 // scalar slots of the two-pass stage (after the shared ones)
-enum FusedSlot { kScDold = 7, kScNrm2e = 8, kScWordsUsed = 9 };
+enum FusedSlot { kScDold = 7, kScNrm2e = 8 };
 
 // ============================================================ k_haar2p
 // Per warp tile: stream the OTHER chain (GEMV-N y = D_O z − P_O β_O, plus the
@@ -151,6 +151,7 @@ __device__ __forceinline__ void k_haar2p_impl(const FusedArgs<T>& a) {
   }
   const double dold = *a.Dold;
   const double es = *a.escale;
+  const double dOt = *a.DOtail;  // D_O below its head rows (one load, not one per row pair)
   const bool tanh_mix = (a.epi.kind == kEpiTanhMix);
   double ssx = 0.0, ssp = 0.0, gss = 0.0, dnew = 0.0;
   bool bad = false;
@@ -266,8 +267,8 @@ __device__ __forceinline__ void k_haar2p_impl(const FusedArgs<T>& a) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int64_t i = tile * kTile + 2 * (lane + 32 * q);
-      const double d0 = (i < a.DOlen) ? a.DO[i] : *a.DOtail;
-      const double d1 = (i + 1 < a.DOlen) ? a.DO[i + 1] : *a.DOtail;
+      const double d0 = (i < a.DOlen) ? a.DO[i] : dOt;
+      const double d1 = (i + 1 < a.DOlen) ? a.DO[i + 1] : dOt;
       double z0 = 0.0, z1 = 0.0;
       if (i < a.zlen) z0 = d0 * a.z[i];
       if (i + 1 < a.zlen) z1 = d1 * a.z[i + 1];
