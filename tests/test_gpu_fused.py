@@ -193,3 +193,59 @@ def test_fused_stage_variants_match(orc, lm, monkeypatch, cluster):
     got = op.run(x1, T, update="tanh_mix", sides="right")
     assert per_probe_launches(op, T) < 2.5
     assert rel(got, want) < TOL64
+
+
+@pytest.mark.parametrize("n,T,update", [(1, 1, "tanh_mix"), (2, 2, "identity"), (3, 3, "tanh_mix"), (255, 40, "tanh_mix"),
+                                        (513, 60, "identity")])
+def test_fused_tiny_and_ragged_shapes(orc, lm, n, T, update):
+    seed = 101 + n
+    x1 = orc.RandomSource(seed, 1).normal_vector(n)
+    want = orc.Operator("haar", n=n, seed=seed).run(update, "right", T, x1, keep=True)
+    op = haar(lm, n, seed=seed, draws="injected", capacity=4)
+    op.push_draws(orc.draws_for(seed, [n] * T))
+    got = op.run(x1, T, update=update, sides="right", keep_trajectory=True)
+    for t in range(T + 1):
+        assert rel(got[t], want[t]) < TOL64, (t, rel(got[t], want[t]))
+    assert op.remaining_probes == n - T
+
+
+@pytest.mark.parametrize("T", [300, 480])
+def test_fused_long_run_crosses_tiles(orc, lm, T):
+    # off beyond the first 256-row tile: the pivot tile moves, the stage's head
+    # rows span several tiles, and the k x k state outgrows shared memory
+    n, seed = 6000, 7
+    x1 = orc.RandomSource(seed, 1).normal_vector(n)
+    x1 /= np.linalg.norm(x1)
+    want = orc.Operator("haar", n=n, seed=seed).run("tanh_mix", "right", T, x1, keep=False)[0]
+    op = haar(lm, n, seed=seed, draws="injected", capacity=16)
+    op.push_draws(orc.draws_for(seed, [n] * T))
+    got = op.run(x1, T, update="tanh_mix", sides="right")
+    assert per_probe_launches(op, T) < 2.5
+    assert rel(got, want) < TOL64
+
+
+def test_fused_fp32_matches_oracle(orc, lm):
+    n, T, seed = 8192, 50, 13
+    x1 = orc.RandomSource(seed, 1).normal_vector(n)
+    x1 /= np.linalg.norm(x1)
+    want = orc.Operator("haar", n=n, seed=seed).run("tanh_mix", "right", T, x1, keep=False)[0]
+    op = haar(lm, n, seed=seed, draws="injected", dtype="f32", capacity=T)
+    op.push_draws(orc.draws_for(seed, [n] * T))
+    got = op.run(x1.astype(np.float32), T, update="tanh_mix", sides="right")
+    assert per_probe_launches(op, T) < 2.5
+    assert rel(got, want) < TOL32
+
+
+def test_fused_graph_replays_across_reseeds(lm):
+    torch = pytest.importorskip("torch")
+    n, T = 50000, 30
+    x1 = torch.randn(n, dtype=torch.float64, device="cuda")
+    a = haar(lm, n, True, seed=1)
+    outs = []
+    for sd in (11, 12, 11):
+        a.reseed(sd)
+        outs.append(a.run(x1, T, update="tanh_mix", sides="right", use_graph=True).cpu())
+    assert torch.equal(outs[0], outs[2]) and not torch.equal(outs[0], outs[1])
+    b = haar(lm, n, False, seed=12)
+    yb = b.run(x1, T, update="tanh_mix", sides="right").cpu()
+    assert rel(outs[1], yb) < 1e-12
