@@ -445,6 +445,11 @@ struct Small2pArgs {
   // (the previous stage had them on its critical path); finish = 1 runs only
   // that (after a run's last pass)
   int deferred = 0, finish = 0;
+  // normalize dynamics (x_t = y_{t-1} / ||y_{t-1}||, bench.cpp:25-28): the
+  // previous pass left y_{t-1} and ||y||^2; this stage scales the dots, ||x||^2
+  // and the head rows by inv = 1/||y|| and publishes inv (kScInv) for the
+  // pass's x rows. step_prev: the step that produced y (non-finite abort)
+  int normalize = 0, step_prev = 0;
   unsigned long long* trace = nullptr;  // HD_TRACE=2: clock64 stamps [16] of this probe's stage
 };
 
@@ -809,6 +814,26 @@ __device__ __forceinline__ void k_small_2p_impl(const Small2pArgs& a) {
     return;
   }
   HD_T2(3, 0);
+  if (a.normalize) {
+    if (tid == 0) {
+      const double ny = sqrt(sc[0]);
+      const double inv = ny > 0.0 ? 1.0 / ny : 1.0;  // (k_small_norm)
+      a.scal[kScInv] = inv;
+      if (!isfinite(inv)) {
+        atomicMin(a.status + kStBadStep, a.step_prev);
+        atomicOr(a.status + kStAbort, 1);
+      }
+      sc[18] = inv;
+      sc[0] = sc[0] * inv * inv;
+    }
+    __syncthreads();
+    const double inv = sc[18];
+#pragma unroll 1
+    for (int j = tid; j < kF; j += kSmallThreads) aF[j] *= inv;
+#pragma unroll 1
+    for (int64_t i = tid; i < nr; i += kSmallThreads) xh[i] *= inv;
+    __syncthreads();
+  }
   if (a.slot_pss >= 0 && tid == 0) {  // a posteriori check of the previous probe's early norm
     const double ex = sc[2], ea = sc[8];
     if (!(fabs(ex - ea) <= a.check_tol * ea)) {
@@ -1189,6 +1214,26 @@ __device__ __forceinline__ void k_small_2pc_impl(const Small2pArgs& a) {
       }
     }
     HD_T2(3, 0);
+    if (a.normalize) {
+      if (tid == 0) {
+        const double ny = sqrt(sc[0]);
+        const double inv = ny > 0.0 ? 1.0 / ny : 1.0;  // (k_small_norm)
+        a.scal[kScInv] = inv;
+        if (!isfinite(inv)) {
+          atomicMin(a.status + kStBadStep, a.step_prev);
+          atomicOr(a.status + kStAbort, 1);
+        }
+        sc[18] = inv;
+        sc[0] = sc[0] * inv * inv;
+      }
+      __syncthreads();
+      const double inv = sc[18];
+  #pragma unroll 1
+      for (int j = tid; j < kF; j += kSmallThreads) aF[j] *= inv;
+  #pragma unroll 1
+      for (int64_t i = tid; i < nr; i += kSmallThreads) xh[i] *= inv;
+      __syncthreads();
+    }
 #pragma unroll 1
     for (int j = tid; j < kF; j += kSmallThreads) uF[j] = sgF[j] * aF[j];
     __syncthreads();

@@ -249,3 +249,33 @@ def test_fused_graph_replays_across_reseeds(lm):
     b = haar(lm, n, False, seed=12)
     yb = b.run(x1, T, update="tanh_mix", sides="right").cpu()
     assert rel(outs[1], yb) < 1e-12
+
+
+@pytest.mark.parametrize("T,sides", [(1, "right"), (2, "left"), (17, "right"), (40, "left")])
+def test_fused_normalize_matches_oracle(orc, lm, T, sides):
+    # normalize dynamics (bench.cpp:25-28): y_t and ||y_t||^2 from the pass, the
+    # scaling by the next stage (x_{T+1} checked; trajectories take the
+    # three-pass sequence for this map)
+    n, seed = 5003, 57 + T
+    x1 = orc.RandomSource(seed, 1).normal_vector(n)
+    want = orc.Operator("haar", n=n, seed=seed).run("normalize", sides, T, x1, keep=False)[0]
+    op = haar(lm, n, seed=seed, draws="injected", capacity=T)
+    op.push_draws(orc.draws_for(seed, [n] * T))
+    got = op.run(x1, T, update="normalize", sides=sides)
+    # two-pass: resets (at creation and at the run) + k_dots + 2 per probe + the
+    # closing stage + k_small_norm + the final scaled copy
+    assert op.launch_count() <= 2 * T + 10
+    assert rel(got, want) < TOL64
+    assert abs(np.linalg.norm(got) - 1.0) < 1e-12
+
+
+def test_fused_normalize_equals_three_pass_philox(lm):
+    torch = pytest.importorskip("torch")
+    n, T = 65536, 100
+    x1 = torch.randn(n, dtype=torch.float64, device="cuda")
+    a = haar(lm, n, True, seed=8)
+    b = haar(lm, n, False, seed=8)
+    ya = a.run(x1, T, update="normalize", sides="right")
+    yb = b.run(x1, T, update="normalize", sides="right")
+    assert per_probe_launches(a, T) < 2.5 and per_probe_launches(b, T) > 4.5
+    assert rel(ya.cpu(), yb.cpu()) < 1e-12
