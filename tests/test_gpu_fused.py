@@ -279,3 +279,36 @@ def test_fused_normalize_equals_three_pass_philox(lm):
     yb = b.run(x1, T, update="normalize", sides="right")
     assert per_probe_launches(a, T) < 2.5 and per_probe_launches(b, T) > 4.5
     assert rel(ya.cpu(), yb.cpu()) < 1e-12
+
+
+def test_fused_runs_match_dense_haar_in_law(lm):
+    # production path (device Philox, two-pass runs) against a dense
+    # simulation with Haar matrices (batched QR with sign correction): the law
+    # of x_{T+1} under x_{t+1} = tanh(2 Q x_t) + 0.1 x_{t-1} from x_1 = e_1 (KS)
+    torch = pytest.importorskip("torch")
+    stats = pytest.importorskip("scipy.stats")
+    n, T, trials = 6, 5, 3000
+    x1 = np.zeros(n)
+    x1[0] = 1.0
+    op = haar(lm, n, True, seed=1, capacity=T)
+    lazy = np.empty((trials, n))
+    for b in range(trials):
+        op.reseed(1000 + b)
+        lazy[b] = op.run(x1, T, update="tanh_mix", sides="right")
+    assert op.launch_count() < trials * (2 * T + 12)  # two-pass runs (no fallback storm)
+    g = torch.Generator().manual_seed(5)
+    G = torch.randn(trials, n, n, generator=g, dtype=torch.float64)
+    Q, R = torch.linalg.qr(G)
+    Q = Q * torch.sign(torch.diagonal(R, dim1=1, dim2=2))[:, None, :]
+    x = torch.zeros(trials, n, dtype=torch.float64)
+    x[:, 0] = 1.0
+    xp = torch.zeros_like(x)
+    for _ in range(T):
+        y = torch.einsum("bij,bj->bi", Q, x)
+        x, xp = torch.tanh(2.0 * y) + 0.1 * xp, x
+    dense = x.numpy()
+    alpha = 1e-3 / 3
+    for name, a, d in [("coord0", lazy[:, 0], dense[:, 0]), ("coord_last", lazy[:, -1], dense[:, -1]),
+                       ("sqnorm", (lazy ** 2).sum(1), (dense ** 2).sum(1))]:
+        p = stats.ks_2samp(a, d).pvalue
+        assert p > alpha, (name, p)
