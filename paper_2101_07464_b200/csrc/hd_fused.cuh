@@ -1248,6 +1248,7 @@ __device__ __forceinline__ void k_small_2pc_impl(const Small2pArgs& a) {
     if (w < NP) col_axpy_part(pF, kF, [&](int) { return nr; }, b1, nr, part, 0, NP);
     else col_dots(g_at, kF, [&](int) { return (int64_t)kF; }, bh, gF, NP, NW - NP);
     __syncthreads();
+    HD_T2(15, 0);
 #pragma unroll 1
     for (int64_t i = tid; i < nr; i += kSmallThreads) {
       const double p = dF[i] * (xh[i] - part_sum(part, nr, NP, i));
