@@ -16,6 +16,10 @@
 // stage checks that (a priori, and a posteriori against the exact ‖p[off:]‖²
 // the pass reduces) and otherwise flags kStFused, on which the host re-runs
 // the whole run through the three-pass probe sequence.
+//
+// Kernels: k_haar2p (the pass, TMA-streamed like k_apply), k_small_2pc (the
+// stage on a 2-CTA cluster: fold chain | other chain, default) and
+// k_small_2p (the same stage on one CTA, HD_2P_CLUSTER=0).
 #pragma once
 
 #include "hd_kernels.cuh"
