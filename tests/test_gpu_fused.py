@@ -312,3 +312,23 @@ def test_fused_runs_match_dense_haar_in_law(lm):
                        ("sqnorm", (lazy ** 2).sum(1), (dense ** 2).sum(1))]:
         p = stats.ks_2samp(a, d).pvalue
         assert p > alpha, (name, p)
+
+
+def test_fused_run_then_second_run_continues(orc, lm):
+    # a second run on the same operator (no longer fresh) takes the three-pass
+    # sequence from the two-pass run's end state; both match the oracle
+    n, T1, T2, seed = 3000, 12, 9, 45
+    x1 = orc.RandomSource(seed, 1).normal_vector(n)
+    x1 /= np.linalg.norm(x1)
+    ref = orc.Operator("haar", n=n, seed=seed)
+    w1 = ref.run("tanh_mix", "right", T1, x1, keep=False)[0]
+    w2 = ref.run("normalize", "right", T2, w1, keep=False)[0]
+    op = haar(lm, n, seed=seed, draws="injected", capacity=4)
+    op.push_draws(orc.draws_for(seed, [n] * (T1 + T2)))
+    g1 = op.run(x1, T1, update="tanh_mix", sides="right")
+    assert rel(g1, w1) < TOL64
+    before = op.launch_count()
+    g2 = op.run(g1, T2, update="normalize", sides="right")
+    assert op.launch_count() - before > 4 * T2  # three-pass sequence
+    assert rel(g2, w2) < TOL64
+    assert op.chain_sizes() == ref.chain_sizes()
