@@ -1167,9 +1167,6 @@ template <typename T, bool HAAR>
 __device__ __forceinline__ void k_small_dots_impl(const SmallArgs& a) {
   extern __shared__ double ssm[];
   HD_STAMP(a, 0);
-  pdl_wait();
-  HD_STAMP(a, 1);
-  if (!a.late_launch) pdl_launch();
   const int kv = small_kv(a.kA, a.kB);
   const SmallSmem m = small_smem(ssm, kv);
   double* aA = m.v0;     // red A dot
@@ -1193,12 +1190,15 @@ __device__ __forceinline__ void k_small_dots_impl(const SmallArgs& a) {
   const int tid = threadIdx.x;
   const bool spec = HAAR && a.mix_from_spec && a.kB > 0;
   // ---- phase 1: every global load issued asynchronously (no register round
-  // trips: the panel row and scalars miss L2 right after a streaming pass)
+  // trips: the panel row and scalars miss L2 right after a streaming pass).
+  // What earlier stages / the previous probe's passes wrote (T, sig, the pivot
+  // row of the existing members, the speculative dots, c of the pending
+  // members) is issued before griddepcontrol.wait: those kernels completed
+  // before this launch; only k_dots' outputs wait.
   HD_CLK(a, 5);
   const TView tvA = a.stageA ? st_stage_T(a.chA, a.kA, tsA, tid, kSmallThreads) : TView{a.chA.Tm, a.chA.K};
   const TView tvB = (HAAR && a.stageB) ? st_stage_T(a.chB, a.kB, tsB, tid, kSmallThreads) : TView{a.chB.Tm, a.chB.K};
   HD_CLK(a, 6);
-  st_stage(a.partials, (int64_t)a.nslots_in * a.nblk, ps, tid, kSmallThreads);
   if (spec)
     st_stage(a.spec_parts + (size_t)a.spec_slot0 * a.spec_nblk, (int64_t)(a.kB + a.spec_ss) * a.spec_nblk, ss, tid,
              kSmallThreads);
@@ -1215,6 +1215,12 @@ __device__ __forceinline__ void k_small_dots_impl(const SmallArgs& a) {
   if (tid == 0) {
     if (a.pendA >= 0) cp_async8(m.sc + 2, a.chA.c + a.pendA);
     if (a.pendB >= 0) cp_async8(m.sc + 3, a.chB.c + a.pendB);
+  }
+  pdl_wait();
+  HD_STAMP(a, 1);
+  if (!a.late_launch) pdl_launch();
+  st_stage(a.partials, (int64_t)a.nslots_in * a.nblk, ps, tid, kSmallThreads);
+  if (tid == 0) {
     cp_async8(m.sc + 4, a.scal + kScPivotG);
     cp_async4(st + 0, a.status + kStAbort);
     cp_async4(st + 1, a.status + kStBadInput);
@@ -1345,8 +1351,6 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_dots_b(const SmallArgs*
 template <typename T, bool HAAR>
 __device__ __forceinline__ void k_small_fold_impl(const SmallArgs& a) {
   extern __shared__ double ssm[];
-  pdl_wait();
-  if (!a.late_launch) pdl_launch();
   const int kv = small_kv(a.kA, a.kB);
   const SmallSmem m = small_smem(ssm, kv);
   double* az = m.v0;    // corner partial sum_{i<off} P_B[i,j] D_B(i) p_i
@@ -1361,16 +1365,15 @@ __device__ __forceinline__ void k_small_fold_impl(const SmallArgs& a) {
   double* hs = tsB + (a.stageB ? (size_t)a.kB * (a.kB | 1) : 0);  // head p[0..off]
   double* ds = hs + nr;                                               // D_B[0..off]
   T* cs = reinterpret_cast<T*>(ds + nr);                              // corner [kB][nr]
-  // ---- phase 1: every global load issued asynchronously, one wait
+  // ---- phase 1: every global load issued asynchronously, one wait; what
+  // the earlier stages wrote (T_B, the scales, D_B, sig, the corner) before
+  // griddepcontrol.wait, the fold pass's outputs after it
   const TView tvB = (HAAR && a.stageB) ? st_stage_T(a.chB, a.kB, tsB, tid, kSmallThreads)
                                             : TView{a.chB.Tm, a.chB.K};
-  st_stage(a.partials + (size_t)a.fold_slot_ss * a.nblk, a.nblk, psf, tid, kSmallThreads);
-  st_stage(a.head, nr, hs, tid, kSmallThreads);
   int* st = reinterpret_cast<int*>(m.sc + 12);
   if (tid == 0) {
     cp_async8(m.sc + 8, a.scal + kScEscale);
     cp_async8(m.sc + 9, a.scal + kScIscale);
-    cp_async4(st, a.status + kStAbort);
   }
   if (HAAR) {
     #pragma unroll 1
@@ -1383,6 +1386,11 @@ __device__ __forceinline__ void k_small_fold_impl(const SmallArgs& a) {
         #pragma unroll 1
         for (int64_t i = lane; i < nr; i += 32) cp_async_elem(cs + j * nr + i, PB + paddr(i, j, a.chB.K));
   }
+  pdl_wait();
+  if (!a.late_launch) pdl_launch();
+  st_stage(a.partials + (size_t)a.fold_slot_ss * a.nblk, a.nblk, psf, tid, kSmallThreads);
+  st_stage(a.head, nr, hs, tid, kSmallThreads);
+  if (tid == 0) cp_async4(st, a.status + kStAbort);
   cp_async_wait_all();
   __syncthreads();
   if (st[0] != 0) return;
@@ -1461,9 +1469,6 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_fold_b(const SmallArgs*
 template <typename T>
 __device__ __forceinline__ void k_small_gin_impl(const SmallArgs& a) {
   extern __shared__ double ssm[];
-  pdl_wait();
-  if (!a.late_launch) pdl_launch();
-  if (aborted(a.status)) return;
   const int kv = small_kv(0, a.kB);
   const SmallSmem m = small_smem(ssm, kv);
   double* ag = m.v0;
@@ -1483,9 +1488,10 @@ __device__ __forceinline__ void k_small_gin_impl(const SmallArgs& a) {
   double* cps = ps + (size_t)a.nslots_in * a.nblk;                  // D_B(i) c_i, i < nr
   double* dsg = cps + nr;                                           // D_B rows (staging)
   T* cs = reinterpret_cast<T*>(dsg + nr);                           // corner [kB][nr]
-  // ---- phase 1: every global load issued asynchronously, one wait
+  // ---- phase 1: every global load issued asynchronously, one wait; what
+  // the earlier stages / passes wrote before griddepcontrol.wait, the dots
+  // pass's partials after it
   const TView tvB = a.stageB ? st_stage_T(a.chB, a.kB, tsB, tid, kSmallThreads) : TView{a.chB.Tm, a.chB.K};
-  st_stage(a.partials, (int64_t)a.nslots_in * a.nblk, ps, tid, kSmallThreads);
   st_stage(a.csp, nr, cps, tid, kSmallThreads);
   #pragma unroll 1
   for (int64_t i = tid; i < nr; i += kSmallThreads) cp_async8(dsg + i, i < a.chB.Dlen ? a.chB.Drow + i : a.chB.Dtail);
@@ -1499,6 +1505,13 @@ __device__ __forceinline__ void k_small_gin_impl(const SmallArgs& a) {
   #pragma unroll 1
   for (int q = tid; q < a.nS; q += kSmallThreads) a.coefS[q] = a.head[q];
   if (tid == 0) m.sc[0] = (a.pendB >= 0) ? a.chB.c[a.pendB] : 0.0;
+  pdl_wait();
+  if (!a.late_launch) pdl_launch();
+  if (aborted(a.status)) {
+    cp_async_wait_all();
+    return;
+  }
+  st_stage(a.partials, (int64_t)a.nslots_in * a.nblk, ps, tid, kSmallThreads);
   cp_async_wait_all();
   __syncthreads();
   {  // both reductions in one pass (see st_sum_slot)
