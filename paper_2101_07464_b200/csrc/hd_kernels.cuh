@@ -154,6 +154,11 @@ struct DotArgs {
   // that follows streams the same panel last-to-first (ApplyArgs::reverse)
   int64_t l2_keep = 0;
   int same_rhs = 0;  // host-asserted: job[1].rhs == job[0].rhs (reuse job 0's rows)
+  // > 1: few tiles (small n): `split` warps share each tile, warp g of a tile
+  // streaming the g-th of `split` contiguous chunk ranges of each job (the
+  // per-column sums add up in the flush); the row side effects (sums of
+  // squares, pivot, column write) belong to warp 0 of the tile
+  int split = 1;
 };
 
 // Shared-memory carve-up of the streaming kernels (per warp: ring + slots).
@@ -208,10 +213,24 @@ __device__ __forceinline__ void k_dots_impl(const DotArgs<T>& a) {
   __syncwarp();
   const int64_t W = (int64_t)gridDim.x * nw;
   const int64_t gw = (int64_t)blockIdx.x * nw + w;
-  const int64_t t0 = gw * a.ntiles / W;
-  int64_t t1 = (gw + 1) * a.ntiles / W;
-  const int nch0 = (a.job[0].ncols + kCW - 1) / kCW;
-  const int nch1 = (a.njobs > 1) ? (a.job[1].ncols + kCW - 1) / kCW : 0;
+  int64_t t0, t1;
+  int grp = 0;
+  if (a.split > 1) {
+    const int64_t tile = gw / a.split;
+    grp = (int)(gw % a.split);
+    t0 = tile < a.ntiles ? tile : a.ntiles;
+    t1 = tile < a.ntiles ? tile + 1 : a.ntiles;
+  } else {
+    t0 = gw * a.ntiles / W;
+    t1 = (gw + 1) * a.ntiles / W;
+  }
+  const bool owner = (grp == 0);
+  const int nchA = (a.job[0].ncols + kCW - 1) / kCW;
+  const int nchB = (a.njobs > 1) ? (a.job[1].ncols + kCW - 1) / kCW : 0;
+  // this warp's chunks of each job: [lo, lo + count)
+  const int lo0 = grp * nchA / a.split, lo1 = grp * nchB / a.split;
+  const int nch0 = (grp + 1) * nchA / a.split - lo0;
+  const int nch1 = (grp + 1) * nchB / a.split - lo1;
   const uint32_t nst = (uint32_t)((t1 - t0) * (nch0 + nch1));
   const int64_t keep = a.l2_keep / (W * (int64_t)(kCW * kTile * sizeof(T)));
   const uint32_t keep_from = keep >= (int64_t)nst ? 0u : nst - (uint32_t)keep;
@@ -234,6 +253,7 @@ __device__ __forceinline__ void k_dots_impl(const DotArgs<T>& a) {
       }
     }
     const DotJob<T>& J = a.job[p.job];
+    p.chunk += (p.job == 0) ? lo0 : lo1;
     const int nc = min(kCW, J.ncols - p.chunk * kCW);
     const uint32_t bytes = (uint32_t)(nc * kTile * sizeof(T));
     const int s = it % kRing;
@@ -307,19 +327,22 @@ __device__ __forceinline__ void k_dots_impl(const DotArgs<T>& a) {
         const int64_t li = (tile + a.rm.tile0) * kTile + 2 * (lane + 32 * q);  // local panel row
         const int64_t i = li + a.rm.gdelta;                                    // global row
         x[q] = (jb == 0 || a.same_rhs) ? x0[q] : src_pair(J.rhs, i, a.n);
-        const double sq = x[q].x * x[q].x + x[q].y * x[q].y;
-        if (jb == 0) ss0 += sq;
-        else ss1 += sq;
-        if (J.check_finite) bad |= !(isfinite(x[q].x) && isfinite(x[q].y));
-        if (J.pivot_out && (i == J.pivot_row || i + 1 == J.pivot_row)) *J.pivot_out = (i == J.pivot_row) ? x[q].x : x[q].y;
-        if (J.wcol) st_pair(J.wcol + paddr(li, J.wj, J.wK), x[q].x, x[q].y);
+        if (owner) {
+          const double sq = x[q].x * x[q].x + x[q].y * x[q].y;
+          if (jb == 0) ss0 += sq;
+          else ss1 += sq;
+          if (J.check_finite) bad |= !(isfinite(x[q].x) && isfinite(x[q].y));
+          if (J.pivot_out && (i == J.pivot_row || i + 1 == J.pivot_row)) *J.pivot_out = (i == J.pivot_row) ? x[q].x : x[q].y;
+          if (J.wcol) st_pair(J.wcol + paddr(li, J.wj, J.wK), x[q].x, x[q].y);
+        }
         pv[q] = (jb == 0) ? cp[q] : (J.pend >= 0) ? ld_pair(J.P + paddr(li, J.pend, J.K)) : make_double2(0.0, 0.0);
         if constexpr (sizeof(T) == 4) {
           xf[q] = make_float2((float)x[q].x, (float)x[q].y);
           pf[q] = make_float2((float)pv[q].x, (float)pv[q].y);
         }
       }
-      const int nch = (J.ncols + kCW - 1) / kCW;
+      const int nch = (jb == 0) ? nch0 : nch1;
+      const int clo = (jb == 0) ? lo0 : lo1;
       for (int c = 0; c < nch; ++c, ++it) {
         const int s = it % kRing;
         mbar_wait(full + s, (it / kRing) & 1);
@@ -357,7 +380,7 @@ __device__ __forceinline__ void k_dots_impl(const DotArgs<T>& a) {
         }
         __syncwarp();
         if (lane == 0 && it + kRing < nst) issue(it + kRing);
-        const int col0 = c * kCW;
+        const int col0 = (c + clo) * kCW;
         add_chunk_sums<kCW>(d, lane, col0, J.ncols, acc + J.slot_dot);
         if (J.pend >= 0 && col0 <= J.pend) add_chunk_sums<kCW>(e, lane, col0, J.pend + 1, acc + J.slot_pend);
         if (jb == 0 && has_next && c >= nch0r - 4) finish0(tile + 1, c - (nch0r - 4));

@@ -213,6 +213,7 @@ struct hd_op {
   int max_warps = 8;  // streaming warps per CTA cap (HD_WARPS fixes it)
   bool warps_fixed = false;
   int late_launch = 0;   // three-pass single-CTA stages trigger the next launch on exit (HD_LATE_LAUNCH=1)
+  bool dots_split = true;  // k_dots shares tiles among warps at small n (HD_DOTS_SPLIT=0 disables)
   int fused = 1;         // two-pass Haar runs (hd_fused.cuh; HD_FUSED=0 disables)
   bool fused_retry = false;  // the current run fell back to the three-pass sequence
   // two-pass tuning / A/B knobs, read at hd_create (hd_fused_host.inc)
@@ -617,10 +618,24 @@ int launch_dots(hd_op* op, cudaStream_t s, DotArgs<T>& a, double bytes) {
   a.nslots = slot;
   a.status = op->status;
   const size_t per_warp = ring_bytes<T>() + sizeof(double) * ((a.nslots + 1) & ~1) + 8 * kRing;
+  // few tiles (small n): split each tile's chunks over several warps, up to
+  // about half the warp slots of the SMs this launch may use
+  {
+    const int64_t chunks = (a.job[0].ncols + chunk_cols<T>() - 1) / chunk_cols<T>() +
+                           ((a.njobs > 1) ? (a.job[1].ncols + chunk_cols<T>() - 1) / chunk_cols<T>() : 0);
+    const int64_t slots = (int64_t)std::max(1, (op->nsm - op->spare_sms) / std::max(1, op->batch_hint)) * kMaxWarps / 2;
+    // the single-CTA stage stages nslots x (CTAs / kGroup) partial rows:
+    // keep that under 64 KB (at >= 6 warps per CTA)
+    const int64_t max_groups = std::max<int64_t>(1, 65536 / (8 * std::max(1, a.nslots)));
+    const int64_t max_warps = max_groups * kGroup * 6;
+    a.split = 1;
+    if (op->dots_split && a.ntiles > 0 && a.ntiles * 2 <= slots && chunks >= 2)
+      a.split = (int)std::max<int64_t>(1, std::min<int64_t>({chunks, slots / a.ntiles, max_warps / a.ntiles, 64}));
+  }
   int grid;
   {
     LaunchScope ls(op, s, "dots", bytes);
-    grid = launch_tma(op, s, k_dots<T>, a, 0, per_warp, a.ntiles, op->fbD);
+    grid = launch_tma(op, s, k_dots<T>, a, 0, per_warp, a.ntiles * a.split, op->fbD);
   }
   check_launch("k_dots");
   return grid;
