@@ -592,6 +592,10 @@ struct ApplyArgs {
   // reversed fold that is the panel's head of every warp range, which the
   // next probe's k_dots reads first
   int64_t l2_keep = 0;
+  // 1: few tiles (small n): one CTA per tile, warp w streaming the w-th
+  // contiguous range of its chunks; the row partial sums meet in shared
+  // memory (fixed order) and warp 0 runs the epilogue
+  int cta_split = 0;
 };
 
 template <typename T, int MODE>
@@ -607,6 +611,8 @@ __device__ __forceinline__ void k_apply_impl(const ApplyArgs<T>& a) {
   double* accs = beta_s + nb;
   double* acc = accs + (size_t)w * nsl;
   uint64_t* full = reinterpret_cast<uint64_t*>(accs + (size_t)nw * nsl) + w * kRing;
+  // cta_split: [nw][128] row pairs after the barriers (16-byte aligned)
+  double2* red = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(full + (nw - w) * kRing) + 15) & ~(uintptr_t)15);
   for (int j = threadIdx.x; j < a.ncols; j += blockDim.x) beta_s[j] = a.beta[j];
   for (int s = lane; s < nsl; s += 32) acc[s] = 0.0;
   if (lane == 0) {
@@ -616,9 +622,13 @@ __device__ __forceinline__ void k_apply_impl(const ApplyArgs<T>& a) {
   const bool spec = (a.spec.kind != kSrcNone);
   const int64_t W = (int64_t)gridDim.x * nw;
   const int64_t gw = (int64_t)blockIdx.x * nw + w;
-  const int64_t t0 = gw * a.ntiles / W;
-  int64_t t1 = (gw + 1) * a.ntiles / W;
-  const int nch = (a.ncols + kCW - 1) / kCW;
+  const bool cs = a.cta_split != 0;
+  int64_t t0 = cs ? (int64_t)blockIdx.x : gw * a.ntiles / W;
+  int64_t t1 = cs ? t0 + 1 : (gw + 1) * a.ntiles / W;
+  const int ncht = (a.ncols + kCW - 1) / kCW;
+  const int clo = cs ? w * ncht / nw : 0;  // this warp's chunks [clo, clo + nch)
+  const int nch = cs ? (w + 1) * ncht / nw - clo : ncht;
+  const bool epi_warp = !cs || w == 0;     // runs the row epilogue and side effects
   const uint32_t nst = (uint32_t)((t1 - t0) * nch);
   const int64_t tlast = t1 - 1;
   const bool rev = a.reverse != 0;
@@ -628,7 +638,7 @@ __device__ __forceinline__ void k_apply_impl(const ApplyArgs<T>& a) {
   int cur_c = 0;
   auto issue = [&](uint32_t it) {
     const int64_t tile = rev ? tlast - cur_k : t0 + cur_k;
-    const int c = rev ? nch - 1 - cur_c : cur_c;
+    const int c = clo + (rev ? nch - 1 - cur_c : cur_c);
     if (++cur_c == nch) {
       cur_c = 0;
       ++cur_k;
@@ -650,8 +660,10 @@ __device__ __forceinline__ void k_apply_impl(const ApplyArgs<T>& a) {
   if (!a.prefetch && lane == 0)
     for (uint32_t it = 0; it < (uint32_t)kRing && it < nst; ++it) issue(it);
   for (int j = threadIdx.x; j < a.ncols; j += blockDim.x) beta_s[j] = a.beta[j];
+  __shared__ int s_abort;  // one decision per CTA (cta_split warps meet at barriers)
+  if (threadIdx.x == 0) s_abort = aborted(a.status) ? 1 : 0;
   __syncthreads();
-  if (aborted(a.status)) {
+  if (s_abort) {
     for (uint32_t it = 0; it < (uint32_t)kRing && it < nst; ++it) mbar_wait(full + it % kRing, 0);
     t1 = t0;
   }
@@ -761,7 +773,7 @@ __device__ __forceinline__ void k_apply_impl(const ApplyArgs<T>& a) {
       const int64_t i = li + a.rm.gdelta;
       r[q] = make_double2(0.0, 0.0);
       gf[q] = make_float2((float)g[q].x, (float)g[q].y);
-      if (a.gcol) {  // the next probe's mix column (masked draw), its norm and pivot
+      if (a.gcol && epi_warp) {  // the next probe's mix column (masked draw), its norm and pivot
         st_pair(a.gcol + paddr(li, a.gj, a.gK), g[q].x, g[q].y);
         gss += g[q].x * g[q].x + g[q].y * g[q].y;
         if (i == a.gpivot_row || i + 1 == a.gpivot_row) *a.gpivot = (i == a.gpivot_row) ? g[q].x : g[q].y;
@@ -771,7 +783,7 @@ __device__ __forceinline__ void k_apply_impl(const ApplyArgs<T>& a) {
       const int s = it % kRing;
       mbar_wait(full + s, (it / kRing) & 1);
       const T* sp = reinterpret_cast<const T*>(ring + (size_t)s * kCW * kTile * sizeof(T)) + 2 * lane;
-      const int col0 = (rev ? nch - 1 - c : c) * kCW;
+      const int col0 = (clo + (rev ? nch - 1 - c : c)) * kCW;
       double d[kCW];
       if constexpr (sizeof(T) == 4) {
         // fp32 panels: chunk-local sums in fp32 (FFMA), converted once per
@@ -822,9 +834,27 @@ __device__ __forceinline__ void k_apply_impl(const ApplyArgs<T>& a) {
     }
     if (gen_next)
       for (int q = nch; q < 4; ++q) gen(next, q);
-    // epilogue on the lane's 8 rows
+    if (cs) {  // row partial sums of the CTA's warps, fixed order, to warp 0
 #pragma unroll
-    for (int q = 0; q < 4; ++q) epi(tile, q, r[q], cv[q]);
+      for (int q = 0; q < 4; ++q) red[w * 128 + lane + 32 * q] = r[q];
+      __syncthreads();
+      if (w == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          double2 v = red[lane + 32 * q];
+          for (int u = 1; u < nw; ++u) {
+            const double2 o = red[u * 128 + lane + 32 * q];
+            v.x += o.x;
+            v.y += o.y;
+          }
+          r[q] = v;
+        }
+      }
+    }
+    // epilogue on the lane's 8 rows
+    if (epi_warp)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) epi(tile, q, r[q], cv[q]);
   }
   ss = warp_sum(ss);
   if (lane == 0) acc[a.slot_ss] += ss;

@@ -214,6 +214,7 @@ struct hd_op {
   bool warps_fixed = false;
   int late_launch = 0;   // three-pass single-CTA stages trigger the next launch on exit (HD_LATE_LAUNCH=1)
   bool dots_split = true;  // k_dots shares tiles among warps at small n (HD_DOTS_SPLIT=0 disables)
+  bool apply_split = true; // k_apply: one CTA per tile at small n (HD_APPLY_SPLIT=0 disables)
   int fused = 1;         // two-pass Haar runs (hd_fused.cuh; HD_FUSED=0 disables)
   bool fused_retry = false;  // the current run fell back to the three-pass sequence
   // two-pass tuning / A/B knobs, read at hd_create (hd_fused_host.inc)
@@ -570,7 +571,7 @@ void launch_k(hd_op* op, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t
 // 23.3 ms; at n = 1e7 8 warps (0.9998) stays best. HD_WARPS fixes the count.
 template <typename Args>
 int launch_tma(hd_op* op, cudaStream_t s, void (*kernel)(Args), Args& args, size_t shared_fixed, size_t per_warp,
-               int64_t ntiles, const FlushBufs& fb) {
+               int64_t ntiles, const FlushBufs& fb, int64_t fixed_grid = 0) {
   int optin = 0;
   ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, op->cfg.device), "attr");
   const size_t budget = (size_t)optin - 1024;
@@ -593,7 +594,7 @@ int launch_tma(hd_op* op, cudaStream_t s, void (*kernel)(Args), Args& args, size
   }
   const size_t smem = shared_fixed + (size_t)nw * per_warp;
   raise_smem_limit(reinterpret_cast<const void*>(kernel), smem);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ntiles, nw), sms));
+  const int grid = fixed_grid > 0 ? (int)fixed_grid : (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ntiles, nw), sms));
   args.out.partials = fb.partials;
   args.out.scratch = fb.scratch;
   args.out.counters = fb.counters;
@@ -652,12 +653,16 @@ int launch_apply(hd_op* op, cudaStream_t s, ApplyArgs<T>& a, bool fold_buffer, d
   a.slot_ss = slot++;
   a.nslots = slot;
   a.status = op->status;
-  const size_t per_warp = ring_bytes<T>() + sizeof(double) * ((a.nslots + 1) & ~1) + 8 * kRing;
+  // few tiles (small n): one CTA per tile, its warps splitting the chunks
+  const int sms = std::max(1, (op->nsm - op->spare_sms) / std::max(1, op->batch_hint));
+  a.cta_split = (op->apply_split && a.ntiles * 2 <= sms && a.ncols >= 2 * chunk_cols<T>()) ? 1 : 0;
+  const size_t per_warp = ring_bytes<T>() + sizeof(double) * ((a.nslots + 1) & ~1) + 8 * kRing +
+                          (a.cta_split ? sizeof(double2) * 128 : 0);
   int grid;
   {
     LaunchScope ls(op, s, kind, bytes);
-    grid = launch_tma(op, s, k_apply<T, MODE>, a, sizeof(double) * ((a.ncols + 1) & ~1), per_warp, a.ntiles,
-                      fold_buffer ? op->fbF : op->fbO);
+    grid = launch_tma(op, s, k_apply<T, MODE>, a, sizeof(double) * ((a.ncols + 1) & ~1) + 16, per_warp, a.ntiles,
+                      fold_buffer ? op->fbF : op->fbO, a.cta_split ? a.ntiles : 0);
   }
   check_launch("k_apply");
   return grid;
