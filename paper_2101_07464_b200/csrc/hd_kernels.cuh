@@ -141,7 +141,7 @@ struct DotJob {
 
 template <typename T>
 struct DotArgs {
-  DotJob<T> job[2];
+  DotJob<T> job[3];  // up to three panels (Ginibre: fold chain + opposite store with x, other chain with g)
   int njobs = 1;
   int64_t n = 0, ntiles = 0;
   RowMap rm;
@@ -225,35 +225,44 @@ __device__ __forceinline__ void k_dots_impl(const DotArgs<T>& a) {
     t1 = (gw + 1) * a.ntiles / W;
   }
   const bool owner = (grp == 0);
-  const int nchA = (a.job[0].ncols + kCW - 1) / kCW;
-  const int nchB = (a.njobs > 1) ? (a.job[1].ncols + kCW - 1) / kCW : 0;
-  // this warp's chunks of each job: [lo, lo + count)
-  const int lo0 = grp * nchA / a.split, lo1 = grp * nchB / a.split;
-  const int nch0 = (grp + 1) * nchA / a.split - lo0;
-  const int nch1 = (grp + 1) * nchB / a.split - lo1;
-  const uint32_t nst = (uint32_t)((t1 - t0) * (nch0 + nch1));
+  // this warp's chunks of each job: [lo[j], lo[j] + nchw[j])
+  int lo[3], nchw[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const int nc = (j < a.njobs) ? (a.job[j].ncols + kCW - 1) / kCW : 0;
+    lo[j] = grp * nc / a.split;
+    nchw[j] = (grp + 1) * nc / a.split - lo[j];
+  }
+  const uint32_t nst = (uint32_t)((t1 - t0) * (nchw[0] + nchw[1] + nchw[2]));
   const int64_t keep = a.l2_keep / (W * (int64_t)(kCW * kTile * sizeof(T)));
   const uint32_t keep_from = keep >= (int64_t)nst ? 0u : nst - (uint32_t)keep;
   // cursor of the next chunk to issue (issue() is called with it = 0, 1, 2, ...):
   // stream order is tile, then job 0's chunks, then job 1's
   int64_t cur_k = 0;
-  int cur_j = (nch0 > 0) ? 0 : 1, cur_c = 0;
+  auto first_job = [&]() {
+    int j = 0;
+    while (j < 2 && nchw[j] == 0) ++j;
+    return j;
+  };
+  int cur_j = first_job(), cur_c = 0;
   auto issue = [&](uint32_t it) {
     StreamPos p;
     p.tile = t0 + cur_k;
     p.job = cur_j;
     p.chunk = cur_c;
-    if (++cur_c == (cur_j == 0 ? nch0 : nch1)) {
+    if (++cur_c == nchw[cur_j]) {
       cur_c = 0;
-      if (cur_j == 0 && nch1 > 0) {
-        cur_j = 1;
+      int nj = cur_j + 1;
+      while (nj < 3 && nchw[nj] == 0) ++nj;
+      if (nj < 3) {
+        cur_j = nj;
       } else {
-        cur_j = (nch0 > 0) ? 0 : 1;
+        cur_j = first_job();
         ++cur_k;
       }
     }
     const DotJob<T>& J = a.job[p.job];
-    p.chunk += (p.job == 0) ? lo0 : lo1;
+    p.chunk += lo[p.job];
     const int nc = min(kCW, J.ncols - p.chunk * kCW);
     const uint32_t bytes = (uint32_t)(nc * kTile * sizeof(T));
     const int s = it % kRing;
@@ -275,7 +284,7 @@ __device__ __forceinline__ void k_dots_impl(const DotArgs<T>& a) {
     t1 = t0;
   }
 
-  double ss0 = 0.0, ss1 = 0.0;
+  double ss0 = 0.0, ss1 = 0.0, ss2 = 0.0;
   bool bad = false;
   double2 x[4], x0[4], pv[4];
   float2 xf[4], pf[4];  // fp32 panels: the right-hand sides in fp32 for FFMA
@@ -326,11 +335,12 @@ __device__ __forceinline__ void k_dots_impl(const DotArgs<T>& a) {
       for (int q = 0; q < 4; ++q) {
         const int64_t li = (tile + a.rm.tile0) * kTile + 2 * (lane + 32 * q);  // local panel row
         const int64_t i = li + a.rm.gdelta;                                    // global row
-        x[q] = (jb == 0 || a.same_rhs) ? x0[q] : src_pair(J.rhs, i, a.n);
+        x[q] = (jb == 0 || (jb == 1 && a.same_rhs)) ? x0[q] : src_pair(J.rhs, i, a.n);
         if (owner) {
           const double sq = x[q].x * x[q].x + x[q].y * x[q].y;
           if (jb == 0) ss0 += sq;
-          else ss1 += sq;
+          else if (jb == 1) ss1 += sq;
+          else ss2 += sq;
           if (J.check_finite) bad |= !(isfinite(x[q].x) && isfinite(x[q].y));
           if (J.pivot_out && (i == J.pivot_row || i + 1 == J.pivot_row)) *J.pivot_out = (i == J.pivot_row) ? x[q].x : x[q].y;
           if (J.wcol) st_pair(J.wcol + paddr(li, J.wj, J.wK), x[q].x, x[q].y);
@@ -341,8 +351,8 @@ __device__ __forceinline__ void k_dots_impl(const DotArgs<T>& a) {
           pf[q] = make_float2((float)pv[q].x, (float)pv[q].y);
         }
       }
-      const int nch = (jb == 0) ? nch0 : nch1;
-      const int clo = (jb == 0) ? lo0 : lo1;
+      const int nch = nchw[jb];
+      const int clo = lo[jb];
       for (int c = 0; c < nch; ++c, ++it) {
         const int s = it % kRing;
         mbar_wait(full + s, (it / kRing) & 1);
@@ -391,9 +401,11 @@ __device__ __forceinline__ void k_dots_impl(const DotArgs<T>& a) {
   }
   ss0 = warp_sum(ss0);
   ss1 = warp_sum(ss1);
+  ss2 = warp_sum(ss2);
   if (lane == 0) {
     if (a.job[0].slot_sumsq >= 0) acc[a.job[0].slot_sumsq] += ss0;
     if (a.njobs > 1 && a.job[1].slot_sumsq >= 0) acc[a.job[1].slot_sumsq] += ss1;
+    if (a.njobs > 2 && a.job[2].slot_sumsq >= 0) acc[a.job[2].slot_sumsq] += ss2;
   }
   if (bad) atomicOr(a.status + kStBadInput, 1);
   __syncthreads();

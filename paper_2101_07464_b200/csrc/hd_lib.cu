@@ -622,8 +622,8 @@ int launch_dots(hd_op* op, cudaStream_t s, DotArgs<T>& a, double bytes) {
   // few tiles (small n): split each tile's chunks over several warps, up to
   // about half the warp slots of the SMs this launch may use
   {
-    const int64_t chunks = (a.job[0].ncols + chunk_cols<T>() - 1) / chunk_cols<T>() +
-                           ((a.njobs > 1) ? (a.job[1].ncols + chunk_cols<T>() - 1) / chunk_cols<T>() : 0);
+    int64_t chunks = 0;
+    for (int j = 0; j < a.njobs; ++j) chunks += (a.job[j].ncols + chunk_cols<T>() - 1) / chunk_cols<T>();
     const int64_t slots = (int64_t)std::max(1, (op->nsm - op->spare_sms) / std::max(1, op->batch_hint)) * kMaxWarps / 2;
     // the single-CTA stage stages nslots x (CTAs / kGroup) partial rows:
     // keep that under 64 KB (at >= 6 warps per CTA)
