@@ -215,6 +215,7 @@ struct hd_op {
   int late_launch = 0;   // three-pass single-CTA stages trigger the next launch on exit (HD_LATE_LAUNCH=1)
   bool dots_split = true;  // k_dots shares tiles among warps at small n (HD_DOTS_SPLIT=0 disables)
   bool apply_split = true; // k_apply: one CTA per tile at small n (HD_APPLY_SPLIT=0 disables)
+  bool gin_merge = true;   // square Ginibre: draw dots as k_dots' third job (HD_GIN_MERGE=0 disables)
   int fused = 1;         // two-pass Haar runs (hd_fused.cuh; HD_FUSED=0 disables)
   bool fused_retry = false;  // the current run fell back to the three-pass sequence
   // two-pass tuning / A/B knobs, read at hd_create (hd_fused_host.inc)
