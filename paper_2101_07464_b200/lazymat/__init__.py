@@ -306,6 +306,9 @@ class _Operator:
     # device dynamics (run_dynamics, dynamics.hpp:42-76, built-in maps)
     def run(self, x1, iterations: int, update: str = "normalize", sides: str = "alternate", x0=None,
             keep_trajectory: bool = False, use_graph: bool = False, out=None):
+        """run_dynamics with a built-in update map on the device; returns x_{T+1}
+        (or the trajectory). A fresh Haar operator on a fixed side takes the
+        two-pass sequence (each panel read once per probe)."""
         a = N.hd_run_args()
         a.update = N.UPDATES[update]
         a.side_rule = N.SIDE_RULES[sides]
