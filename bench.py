@@ -1,17 +1,31 @@
 #!/usr/bin/env python
 """Benchmark of the HD hot path on B200 (one JSON line on rank 0).
 
-Workload (BASELINE.json configs[1], the headline single-GPU config):
-  Haar-orthogonal HD operator, n = 1e6, T = 100 probes (all Q x), fp64,
-  x_1 = g/||g|| (seeded), x_0 = 0, dynamics x_{t+1} = tanh(2 Q x_t) + 0.1 x_{t-1}.
-A step = one full T-probe HD run on a freshly reset operator (device Philox
-draws). Metric: HD element-updates/s = sum_t n*t per run / time.
+Workloads (BASELINE.json configs; a step = one full HD run on a freshly
+reseeded operator, device Philox draws, fp64):
 
---gpus N > 1 runs one independent trial per rank (trial sharding, no
-data-path collective, scaling "weak"); time = max over ranks (CUDA events).
+  config4 (default, the largest single-GPU config, configs[3]): AMP for sparse
+      regression on a Ginibre design, m = 2e7, n = 1e7, T = 200 AMP iterations
+      (401 probes), beta ~ Bernoulli(0.1) N(0,1), w ~ N(0, 0.01), soft
+      threshold 1.5 tau_t with the Onsager term, alternating Q^T / Q; the whole
+      run is one device-resident CUDA graph (hd_run_amp). ~96 GB of panels.
+  config2 (configs[1]): Haar, n = 1e6, T = 100, x_{t+1} = tanh(2 Q x_t) + 0.1 x_{t-1}.
+  config5 (configs[4]): spiked GOE power method, theta = 2, T = 256 GOE steps,
+      n = 1.25e7 per GPU; with N > 1 ranks the operator is row-sharded across
+      the ranks (one NCCL allreduce of the partial dots after every streaming
+      kernel), at N = 1 it is one GPU's n.
+
+Metric: HD element-updates/s = sum over the run's probes of N_in * t (SURVEY
+§8d). `value` is device time with inputs resident (CUDA events); `e2e` runs the
+same workload through the public API with HOST buffers (pinned), host<->device
+copies inside the timed region.
+
+--gpus N > 1 (under torchrun): config5 row-sharded by default (the north
+star's n-sharded workload); --trials runs independent per-rank trials of the
+chosen workload instead (trial sharding, no data-path collective).
 --impl reference times the reference's CPU path (the oracle restatement in
-oracle/, since the reference itself cannot be built here — DESIGN.md) with
-all host threads, rank 0 only.
+oracle/, the reference itself cannot be built here — DESIGN.md §6) with all
+host threads on rank 0, on bounded samples of the same workload.
 """
 from __future__ import annotations
 
@@ -27,14 +41,24 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_DEFAULT = 1_000_000
-T_DEFAULT = 100
-METRIC = "HD element-updates/s (n*t per probe, summed over the run)"
+METRIC = "HD element-updates/s (N_in*t per probe, summed over the run)"
 UNIT = "element-updates/s"
 
 
-def elem_updates(n: int, T: int) -> float:
+# --------------------------------------------------------------- workloads
+def eu_haar(n: int, T: int) -> float:
     return float(n) * T * (T + 1) / 2.0
+
+
+def eu_amp(n: int, m: int, T: int) -> float:
+    """2T + 1 probes: probe k (1-based) is right (N_in = n) for odd k, left
+    (N_in = m) for even k, and touches N_in * k elements."""
+    return float(sum((n if k % 2 == 1 else m) * k for k in range(1, 2 * T + 2)))
+
+
+def eu_goe(n: int, T: int) -> float:
+    """T GOE steps = 2T inner probes of the square inner Ginibre, probe k touches n k."""
+    return float(n) * (2 * T) * (2 * T + 1) / 2.0
 
 
 def alg_bytes_haar(n: int, T: int, s: int = 8) -> float:
@@ -43,10 +67,25 @@ def alg_bytes_haar(n: int, T: int, s: int = 8) -> float:
 
 
 def alg_bytes_haar_2p(n: int, T: int, s: int = 8) -> float:
-    """Two-pass Haar run: s*n*(2t+4) summed over t = 1..T
-    (the other panel's t and the fold panel's t - 1 columns read once, the new
-    fold column, x_t, x_{t+1}, x_{t-1} and the next mix column)."""
+    """Two-pass Haar run: s*n*(2t+4) summed over t = 1..T."""
     return float(s) * n * (2.0 * T * (T + 1) / 2.0 + 4.0 * T)
+
+
+def survey_bytes_ginibre(m: int, n: int, sides, s: int = 8) -> float:
+    """SURVEY §8d Ginibre probe bytes summed over a probe sequence (sides:
+    'R'/'L' per probe; r, l counts include the current probe, t = r + l)."""
+    r = l = 0
+    tot = 0.0
+    for sd in sides:
+        if sd == "R":
+            r += 1
+            t = r + l
+            tot += 2 * n * (r - 1) + 2 * m * l + n * r + (m + n) * t + 3 * n + 2 * m
+        else:
+            l += 1
+            t = r + l
+            tot += 2 * m * (l - 1) + 2 * n * r + m * l + (m + n) * t + 3 * m + 2 * n
+    return s * tot
 
 
 def rank_seed(base: int, rank: int) -> int:
@@ -67,9 +106,9 @@ def max_over_ranks(x: float, dist, device) -> float:
     return float(t.item())
 
 
-def whole_job_value(world: int, n: int, T: int, steps: int, ms: float) -> float:
+def whole_job_value(world: int, eu_per_rank_step: float, steps: int, ms: float) -> float:
     """Aggregate element-updates/s over all ranks, timed by the slowest rank."""
-    return world * elem_updates(n, T) * steps / (ms / 1e3)
+    return world * eu_per_rank_step * steps / (ms / 1e3)
 
 
 def load_peaks():
@@ -77,9 +116,9 @@ def load_peaks():
     try:
         with open(p) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -93,10 +132,11 @@ class ClockSampler:
         self.device = device
         self.proc = None
         self.out = None
+        self.path = f"/tmp/hd_clocks_{os.getpid()}.csv"
 
     def __enter__(self):
         try:
-            self.out = open(os.devnull if False else "/tmp/hd_clocks.csv", "w")
+            self.out = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.out,
                                          stderr=subprocess.DEVNULL)
@@ -116,7 +156,7 @@ class ClockSampler:
 
     def summary(self):
         try:
-            rows = [r.split(",") for r in open("/tmp/hd_clocks.csv").read().strip().splitlines() if r.strip()]
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
         except Exception:
             return None
         if not rows:
@@ -143,57 +183,114 @@ def cpu_model():
     return "unknown"
 
 
-def cpu_baseline(n: int, T_sample: int, seed: int):
-    """The reference hot path restated (oracle/, -O3 -mavx2 -mfma) single-threaded
-    like run_dynamics; one Haar trial of T_sample probes (bounded sample)."""
+# ------------------------------------------------------------ configs
+def workload_config(args, world: int = 1):
+    if args.workload == "config4":
+        n, T = args.n, args.T
+        return {"workload": f"config4_amp_m{2 * n:.0e}_n{n:.0e}_T{T}".replace("+0", ""), "ensemble": "ginibre",
+                "m": 2 * n, "n": n, "T": T, "probes": 2 * T + 1, "sigma": "1/sqrt(m)",
+                "dynamics": "AMP: x=soft(x+A^T z, 1.5*||z||/sqrt(m)); z=y-Ax+(nnz(x)/n/delta)z; y=A beta+w",
+                "data": "beta~Bernoulli(0.1)N(0,1), w~N(0,0.01) (seeded)", "draws": "device philox4x32-10",
+                "trials_per_gpu": 1,
+                "l2": f"inputs larger than L2 (panels {(3 * n * (T + 1) + 3 * n * T) * 8 / 1e9:.0f} GB > 126 MB)"}
+    if args.workload == "config5":
+        n, T = args.n5 * (world if not args.trials else 1), args.T5
+        return {"workload": f"config5_spiked_goe_n{n:.3g}_T{T}", "ensemble": "goe", "n": n, "T": T,
+                "inner_probes": 2 * T, "theta": 2.0, "sigma": "1/sqrt(n)",
+                "dynamics": "x=(Gx+theta<u,x>u)/||.||", "draws": "device philox4x32-10",
+                "sharding": "rows (NCCL allreduce per streaming kernel)" if world > 1 and not args.trials else "none",
+                "l2": f"inputs larger than L2 (panels ~{4 * (n / max(world, 1)) * T * 8 / 1e9:.0f} GB per GPU)"}
+    n, T = args.n2, args.T2
+    return {"workload": f"config2_haar_n{n}_T{T}_tanh_mix", "ensemble": "haar", "n": n, "T": T,
+            "dynamics": "x_{t+1}=tanh(2Qx_t)+0.1x_{t-1}", "draws": "device philox4x32-10", "trials_per_gpu": 1,
+            "l2": f"inputs larger than L2 (2 panels x n x T x 8 B = {2 * n * T * 8 / 1e9:.2f} GB > 126 MB)"}
+
+
+def eu_per_step(args, world: int = 1) -> float:
+    if args.workload == "config4":
+        return eu_amp(args.n, 2 * args.n, args.T)
+    if args.workload == "config5":
+        return eu_goe(args.n5 * (world if not args.trials else 1), args.T5)
+    return eu_haar(args.n2, args.T2)
+
+
+# -------------------------------------------------- CPU (reference path)
+def cpu_sample(args):
+    """(kind, n, T) of one bounded CPU trial of the workload: the full T, a
+    reduced n (the reference's time is linear in n, acceptance.cpp:206-218)."""
+    if args.workload == "config4":
+        return "amp", args.ref_n4, args.T
+    if args.workload == "config5":
+        return "spiked", args.ref_n5, args.T5
+    return "haar", args.ref_n2, args.T2
+
+
+def cpu_eu(kind: str, n: int, T: int) -> float:
+    return eu_amp(n, 2 * n, T) if kind == "amp" else eu_goe(n, T) if kind == "spiked" else eu_haar(n, T)
+
+
+def cpu_run(kind: str, n: int, T: int, seed: int, trials: int, threads: int) -> float:
+    from oracle import oracle as orc
+
+    if kind == "haar":
+        secs, _ = orc.bench_workload("haar", n, n, 1.0, "tanh_mix", "right", T, seed, trials, threads)
+    else:
+        secs, _ = orc.bench_app(kind, n, T, seed, trials, threads)
+    return secs
+
+
+def cpu_baseline(args):
+    """The reference hot path restated (oracle/, -O3 -mavx2 -mfma), one trial
+    on one core like run_dynamics (bounded sample: the full T, reduced n)."""
     from oracle import oracle as orc
 
     orc.build()
-    secs, _ = orc.bench_workload("haar", n, n, 1.0, "tanh_mix", "right", T_sample, seed, 1, 1)
-    return {"value": elem_updates(n, T_sample) / secs, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"1 trial, Haar n={n}, T={T_sample} probes (tanh mix), {secs:.2f} s wall incl. construction; "
+    kind, n, T = cpu_sample(args)
+    secs = cpu_run(kind, n, T, args.seed, 1, 1)
+    return {"value": cpu_eu(kind, n, T) / secs, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"1 trial of the {args.workload} dynamics at the full T = {T} with n = {n}"
+                      f"{' (m = 2n)' if kind == 'amp' else ''}, {secs:.2f} s wall incl. operator construction, 1 thread; "
                       f"CPU {cpu_model()}"}
 
 
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     from oracle import oracle as orc
 
     orc.build()
     threads = max(1, min(os.cpu_count() or 1, args.ref_threads))
-    n, T_s = args.n, args.ref_T
+    kind, n, T = cpu_sample(args)
     trials = threads
     times = []
     for i in range(args.warmup + args.steps):
-        secs, _ = orc.bench_workload("haar", n, n, 1.0, "tanh_mix", "right", T_s, args.seed + i, trials, threads)
+        secs = cpu_run(kind, n, T, args.seed + i, trials, threads)
         if i >= args.warmup:
             times.append(secs)
-    per = elem_updates(n, T_s) * trials
+    per = cpu_eu(kind, n, T) * trials
     tot = sum(times)
     value = per * len(times) / tot
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args),
+        "config": workload_config(args, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{trials} concurrent Haar trials (one per thread), n={n}, T={T_s} probes each, "
-                                   f"tanh mix; CPU {cpu_model()}, nproc={os.cpu_count()}"},
+                         "sample": f"per step: {trials} concurrent trials (one per thread, parallel_for) of the "
+                                   f"{args.workload} dynamics at the full T = {T} with n = {n}"
+                                   f"{' (m = 2n)' if kind == 'amp' else ''}; CPU {cpu_model()}, "
+                                   f"nproc={os.cpu_count()}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 def cpu_baselines_all(args):
-    """The reference CPU path (oracle port, -O3 -mavx2 -mfma) timed on this
-    host for the other BASELINE configs, on bounded samples; where the full
-    config exceeds a few seconds (or host RAM) the sample is smaller and the
-    full-config time is extrapolated from the measured element-update rate
-    (the reference's n-slope is ~1, acceptance.cpp:206-218)."""
-    import time
-
+    """The reference CPU path (oracle port) timed on this host for every BASELINE
+    config on bounded samples (full T, reduced n), with the full-config time
+    extrapolated from the measured element-update rate."""
     from oracle import oracle as orc
 
     orc.build()
@@ -209,72 +306,182 @@ def cpu_baselines_all(args):
     def gin_eu(n, T):  # square Ginibre, alternating: probe k touches n k
         return n * T * (T + 1) / 2
 
-    # config 1: full size, one trial, one thread (run_dynamics is serial)
     secs, _ = orc.bench_workload("ginibre", 4096, 4096, 4096 ** -0.5, "normalize", "alternate", 50, 1, 1, 1)
     emit("config1_ginibre_4096_T50", "full config, 1 trial, 1 thread", gin_eu(4096, 50), secs, 1, gin_eu(4096, 50))
-    # config 3: `threads` trials of the 1024 (one per thread, parallel_for)
+    secs, _ = orc.bench_workload("haar", 1_000_000, 1_000_000, 1.0, "tanh_mix", "right", 30, 1, 1, 1)
+    emit("config2_haar_1e6_T100", "n = 1e6, T = 30, 1 thread", eu_haar(1_000_000, 30), secs, 1,
+         eu_haar(1_000_000, 100))
     n, T = 100_000, 100
     secs, _ = orc.bench_workload("ginibre", n, n, n ** -0.5, "normalize", "alternate", T, 1, threads, threads)
     emit("config3_ginibre_1e5_T100_B1024", f"{threads} of the 1024 trials, one per thread", gin_eu(n, T) * threads,
          secs, threads, gin_eu(n, T) * 1024)
-    # config 4: AMP at n = 1e5 (m = 2n), 50 AMP iterations (101 probes), 1 thread
-    n, T = 100_000, 50
-    m = 2 * n
-    rs = orc.RandomSource(4, 1)
-    beta = np.array([(rs.uniform() < 0.1) * rs.normal() for _ in range(n)])
-    w = 0.1 * rs.normal_vector(m)
-    op = orc.Operator("ginibre", m=m, n=n, sigma=m ** -0.5, seed=4)
-    t0 = time.perf_counter()
-    op.amp(beta, w, T)
-    secs = time.perf_counter() - t0
-    eu = lambda nn, TT: sum((nn if k % 2 == 1 else 2 * nn) * k for k in range(1, 2 * TT + 2))  # noqa: E731
-    emit("config4_amp_n1e7_T200", "n = 1e5 (m = 2e5), 50 AMP iterations, 1 thread", eu(n, T), secs, 1,
-         eu(10_000_000, 200))
-    # config 5: spiked GOE at n = 1e5, 64 steps (128 inner probes), 1 thread
-    n, T = 100_000, 64
-    u = orc.RandomSource(5, 1).normal_vector(n)
-    u /= np.linalg.norm(u)
-    x1 = orc.RandomSource(5, 2).normal_vector(n)
-    x1 /= np.linalg.norm(x1)
-    op = orc.Operator("goe", n=n, sigma=n ** -0.5, seed=5)
-    t0 = time.perf_counter()
-    op.spiked_power(u, x1, T)
-    secs = time.perf_counter() - t0
-    emit("config5_spiked_goe_n1e8_T256", "n = 1e5, 64 GOE steps (128 inner probes), 1 thread", gin_eu(n, 2 * T),
-         secs, 1, gin_eu(100_000_000, 512))
+    n, T = 20_000, 200
+    secs, _ = orc.bench_app("amp", n, T, 1, 1, 1)
+    emit("config4_amp_n1e7_T200", f"n = {n} (m = 2n), full T = 200 (401 probes), 1 thread", eu_amp(n, 2 * n, T),
+         secs, 1, eu_amp(10_000_000, 20_000_000, 200))
+    n, T = 20_000, 256
+    secs, _ = orc.bench_app("spiked", n, T, 1, 1, 1)
+    emit("config5_spiked_goe_n1e8_T256", f"n = {n}, full T = 256 (512 inner probes), 1 thread", eu_goe(n, T), secs,
+         1, eu_goe(100_000_000, 256))
     for line in out:
         print(json.dumps(line), flush=True)
 
 
-def workload_config(args):
-    return {"workload": f"config2_haar_n{args.n}_T{args.T}_tanh_mix", "ensemble": "haar", "n": args.n,
-            "T": args.T, "dynamics": "x_{t+1}=tanh(2Qx_t)+0.1x_{t-1}", "draws": "device philox4x32-10",
-            "trials_per_gpu": 1, "l2": "inputs larger than L2 (2 panels x n x T x 8 B = "
-                                        f"{2 * args.n * args.T * 8 / 1e9:.2f} GB > 126 MB)"}
+# ------------------------------------------------------------ device runs
+class Runner:
+    """One workload on this rank's GPU: step() = one full run on a freshly
+    reseeded operator (device-resident inputs), e2e_step() = the same through
+    the public API with pinned host buffers, profile() = an instrumented run."""
+
+    def __init__(self, args, rank, world, dev, dist):
+        import torch
+
+        from paper_2101_07464_b200 import lazymat
+
+        self.args, self.rank, self.world, self.dev, self.lm = args, rank, world, dev, lazymat
+        self.torch = torch
+        self.use_graph = not args.no_graph
+        self.sharded = args.workload == "config5" and world > 1 and not args.trials
+        self.seed = args.seed if self.sharded else rank_seed(args.seed, rank)
+        g = torch.Generator(device=dev).manual_seed(self.seed)
+        f64 = torch.float64
+        if args.workload == "config4":
+            n, T = args.n, args.T
+            m = 2 * n
+            self.op = lazymat.GinibreOperator(m, n, m ** -0.5, self.seed, capacity=T + 1, device=dev.index)
+            self.beta = (torch.rand(n, device=dev, generator=g, dtype=f64) < 0.1) * torch.randn(
+                n, device=dev, generator=g, dtype=f64)
+            self.w = 0.1 * torch.randn(m, device=dev, generator=g, dtype=f64)
+            self.h2d = 8 * (n + m)
+            self.d2h = 8 * (n + T)
+            self.probe_sides = ["R"] + ["L", "R"] * T
+            self.dims = (m, n)
+        elif args.workload == "config5":
+            n, T = args.n5 * (world if self.sharded else 1), args.T5
+            kw = {}
+            if self.sharded:
+                self.ex = lazymat.nccl_exchange(device=dev.index)
+                kw = {"shard": (rank, world), "exchange": self.ex}
+            self.op = lazymat.GOEOperator(n, self.seed, sigma=n ** -0.5, capacity=T, device=dev.index, **kw)
+            u = torch.randn(n, device=dev, generator=g, dtype=f64)
+            x1 = torch.randn(n, device=dev, generator=g, dtype=f64)
+            lo, hi = self.op.shard_range()
+            self.u = (u / u.norm())[lo:hi].clone()
+            self.x1 = (x1 / x1.norm())[lo:hi].clone()
+            del u, x1
+            self.h2d = 8 * 2 * (hi - lo)
+            self.d2h = 8 * ((hi - lo) + T)
+            self.probe_sides = ["R", "L"] * T
+            self.dims = (n, n)
+        else:
+            n, T = args.n2, args.T2
+            self.op = lazymat.HaarOperator(n, seed=self.seed, capacity=T, device=dev.index)
+            self.x1 = torch.randn(n, dtype=f64, device=dev, generator=g)
+            self.x1 /= self.x1.norm()
+            self.x0 = torch.zeros(n, dtype=f64, device=dev)
+            self.h2d = 8 * n
+            self.d2h = 8 * n
+        torch.cuda.empty_cache()
+
+    def step(self):
+        a, lm, op = self.args, self.lm, self.op
+        op.reseed(self.seed)
+        if a.workload == "config4":
+            return lm.amp_sparse_regression(op, self.beta, self.w, a.T, use_graph=self.use_graph)[1]
+        if a.workload == "config5":
+            return lm.spiked_power(op, self.u, self.x1, a.T5, use_graph=self.use_graph)[1]
+        return op.run(self.x1, a.T2, update="tanh_mix", sides="right", x0=self.x0, use_graph=self.use_graph)
+
+    def host_buffers(self):
+        torch = self.torch
+        pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+        a = self.args
+        if a.workload == "config4":
+            self.hb = [pin(self.beta).numpy(), pin(self.w).numpy()]
+            self.ho = [torch.empty(a.n, dtype=torch.float64).pin_memory().numpy(),
+                       torch.empty(a.T, dtype=torch.float64).pin_memory().numpy()]
+        elif a.workload == "config5":
+            self.hb = [pin(self.u).numpy(), pin(self.x1).numpy()]
+            self.ho = [torch.empty(self.u.numel(), dtype=torch.float64).pin_memory().numpy(),
+                       torch.empty(a.T5, dtype=torch.float64).pin_memory().numpy()]
+        else:
+            self.hb = [pin(self.x1).numpy()]
+            self.ho = [torch.empty(a.n2, dtype=torch.float64).pin_memory().numpy()]
+
+    def e2e_step(self):
+        a, lm, op = self.args, self.lm, self.op
+        op.reseed(self.seed)
+        if a.workload == "config4":
+            lm.amp_sparse_regression(op, self.hb[0], self.hb[1], a.T, use_graph=self.use_graph, x_out=self.ho[0],
+                                     mse_out=self.ho[1])
+        elif a.workload == "config5":
+            lm.spiked_power(op, self.hb[0], self.hb[1], a.T5, use_graph=self.use_graph, x_out=self.ho[0],
+                            overlap_out=self.ho[1])
+        else:
+            op.run(self.hb[0], a.T2, update="tanh_mix", sides="right", use_graph=self.use_graph, out=self.ho[0])
+
+    def profile(self):
+        """Instrumented (non-graph) run: CUDA events around every launch on the
+        operator's stream; returns per-kernel-kind stats."""
+        a, lm, op = self.args, self.lm, self.op
+        op.reseed(self.seed)
+        op.set_profiling(True)
+        op.reset_stats()
+        if a.workload == "config4":
+            lm.amp_sparse_regression(op, self.beta, self.w, a.T, use_graph=False)
+        elif a.workload == "config5":
+            lm.spiked_power(op, self.u, self.x1, a.T5, use_graph=False)
+        else:
+            op.run(self.x1, a.T2, update="tanh_mix", sides="right", x0=self.x0, use_graph=False)
+        stats = op.kernel_stats()
+        op.set_profiling(False)
+        return stats
+
+    def extra_roofline(self, ms_step):
+        """Step-level byte formulas: the SURVEY §8(d) formula and the bytes
+        the kernels are accounted (the reduced-traffic algorithms)."""
+        a = self.args
+        if a.workload == "config2":
+            return {"survey_formula_GBps": alg_bytes_haar(a.n2, a.T2) / (ms_step / 1e3) / 1e9,
+                    "two_pass_formula_GBps": alg_bytes_haar_2p(a.n2, a.T2) / (ms_step / 1e3) / 1e9}
+        m, n = self.dims
+        per_gpu = self.world if self.sharded else 1
+        return {"survey_formula_GBps": survey_bytes_ginibre(m, n, self.probe_sides) / per_gpu / (ms_step / 1e3) / 1e9}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)  # ~0.8 s timed: several nvidia-smi clock samples
+    ap.add_argument("--steps", type=int, default=None, help="timed steps (default: config4/5 5, config2 50)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=N_DEFAULT)
-    ap.add_argument("--T", type=int, default=T_DEFAULT)
+    ap.add_argument("--workload", default=None, choices=["config4", "config2", "config5"],
+                    help="default: config4 at N = 1, config5 (row-sharded) under torchrun with N > 1")
+    ap.add_argument("--trials", action="store_true", help="N > 1: independent per-rank trials instead of row shards")
+    ap.add_argument("--n", type=int, default=10_000_000, help="config4 n (m = 2n)")
+    ap.add_argument("--T", type=int, default=200, help="config4 AMP iterations")
+    ap.add_argument("--n2", type=int, default=1_000_000)
+    ap.add_argument("--T2", type=int, default=100)
+    ap.add_argument("--n5", type=int, default=12_500_000, help="config5 rows per GPU")
+    ap.add_argument("--T5", type=int, default=256)
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--cpu-T", type=int, default=60, help="probes in the bounded cpu_baseline sample")
-    ap.add_argument("--ref-T", type=int, default=30, help="probes per trial in the reference arm sample")
+    ap.add_argument("--ref-n4", type=int, default=10_000, help="reference arm / cpu_baseline: config4 sample n")
+    ap.add_argument("--ref-n2", type=int, default=100_000)
+    ap.add_argument("--ref-n5", type=int, default=20_000)
     ap.add_argument("--ref-threads", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--cpu-baselines", action="store_true",
-                    help="time the reference CPU path (oracle) on configs 1, 3, 4, 5 and exit")
+                    help="time the reference CPU path (oracle) on every BASELINE config and exit")
     args = ap.parse_args()
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.workload is None:
+        args.workload = "config5" if (world_env > 1 and not args.trials) else "config4"
+    if args.steps is None:
+        args.steps = 50 if args.workload == "config2" else 5
+    args.warmup = max(args.warmup, 3)
 
     if args.cpu_baselines:
-        import numpy as np  # noqa: F401  (used by cpu_baselines_all)
-
-        globals()["np"] = np
         cpu_baselines_all(args)
         return
     if args.impl == "reference":
@@ -285,7 +492,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = world_env
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
@@ -300,121 +507,86 @@ def main():
         ge.build()
     if world > 1:
         dist.barrier()
-    from paper_2101_07464_b200 import lazymat
 
-    n, T = args.n, args.T
-    seed = rank_seed(args.seed, rank)
-    op = lazymat.HaarOperator(n, seed=seed, capacity=T, device=local)
-    gen = torch.Generator(device=dev).manual_seed(seed)
-    x1 = torch.randn(n, dtype=torch.float64, device=dev, generator=gen)
-    x1 /= x1.norm()
-    x0 = torch.zeros(n, dtype=torch.float64, device=dev)
-    use_graph = not args.no_graph
-
-    def step_device():
-        # fresh operator, same seed: reseed resets the host counters without a
-        # host sync (the captured graph resets the device state itself), so the
-        # timed region holds back-to-back graph replays
-        op.reseed(seed)
-        return op.run(x1, T, update="tanh_mix", sides="right", x0=x0, use_graph=use_graph)
-
-    for _ in range(max(args.warmup, 3)):
-        step_device()
+    R = Runner(args, rank, world, dev, dist)
+    for _ in range(args.warmup):
+        R.step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    l0 = op.launch_count()
+    l0 = R.op.launch_count()
     stream = torch.cuda.current_stream(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            out = step_device()
+            out = R.step()
         ev1.record(stream)
         torch.cuda.synchronize()
-    launches = (op.launch_count() - l0) // args.steps
+    launches = (R.op.launch_count() - l0) // args.steps
     ms = ev0.elapsed_time(ev1)
     if world > 1:
         ms = max_over_ranks(ms, dist, dev)
         dist.barrier()
     ms_step = ms / args.steps
-    value = whole_job_value(world, n, T, args.steps, ms)
-    final_norm = float(out.norm())
+    eu = eu_per_step(args, world)
+    per_rank_eu = eu / world if R.sharded else eu
+    value = whole_job_value(world, per_rank_eu, args.steps, ms)
+    check = float(out[-1]) if out.numel() else 0.0
 
-    # e2e through the public API with host buffers in pinned memory (H2D x_1;
-    # x_0 = 0 is the library's default history; D2H x_{T+1}), every step
-    # inside the timed region, each on a fresh operator (reseed)
-    x1p = x1.cpu().pin_memory()
-    outp = torch.empty(n, dtype=torch.float64).pin_memory()
-    x1h, outh = x1p.numpy(), outp.numpy()
-    op.reseed(seed)
-    op.run(x1h, T, update="tanh_mix", sides="right", use_graph=use_graph, out=outh)
+    # e2e through the public API with pinned host buffers (H2D inputs, D2H
+    # x_T and the curve), every step inside the timed region
+    R.host_buffers()
+    R.e2e_step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        op.reseed(seed)
-        op.run(x1h, T, update="tanh_mix", sides="right", use_graph=use_graph, out=outh)
+        R.e2e_step()
     e2e_s = time.perf_counter() - t0
     if world > 1:
         e2e_s = max_over_ranks(e2e_s, dist, dev)
-    e2e_val = whole_job_value(world, n, T, args.steps, e2e_s * 1e3)
-    assert np.isfinite(outh).all()
+    e2e_val = whole_job_value(world, per_rank_eu, args.steps, e2e_s * 1e3)
+    assert all(np.isfinite(h).all() for h in R.ho)
 
-    # roofline: instrumented pass (CUDA events around every launch on the op's stream)
-    op.reset()
-    op.set_profiling(True)
-    op.reset_stats()
-    op.run(x1, T, update="tanh_mix", sides="right", x0=x0, use_graph=False)
-    stats = op.kernel_stats()
-    op.set_profiling(False)
+    stats = R.profile()
     peak, peak_kind = load_peaks()
     dom = max((k for k in stats if stats[k]["alg_bytes"] > 0), key=lambda k: stats[k]["ms"])
     d = stats[dom]
     achieved = (d["alg_bytes"] / d["launches"]) / (d["ms"] / d["launches"] / 1e3) / 1e9
     tot_ms = sum(v["ms"] for v in stats.values())
     tot_bytes = sum(v["alg_bytes"] for v in stats.values())
-    # DRAM bytes per launch of the dominant kernel: the committed ncu capture's
-    # DRAM/algorithmic ratio (probe t = 91) applied to this run's per-launch bytes
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        try:
-            tr = json.load(open(tp)).get(dom)
-            if tr:
-                traffic = tr["ratio"] * d["alg_bytes"] / d["launches"]
-        except Exception:
-            traffic = None
 
     if rank == 0:
         clocks = clk.summary()
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (device Philox draws, seeded x_1)",
-            "config": workload_config(args),
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device Philox draws, seeded inputs)", "config": workload_config(args, world),
             "gpu_launches": int(launches),
-            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * 8},
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(R.h2d),
+                    "d2h_bytes_per_step": int(R.d2h)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": dom,
-                         "peak_source": peak_kind,
+                         "frac": achieved / peak, "traffic": None, "kernel": dom, "peak_source": peak_kind,
                          "kernel_share_of_step": d["ms"] / tot_ms if tot_ms else None,
-                         "method": "per-launch CUDA events on the operator's stream (the stream the kernels "
-                                   "run on) in an instrumented, non-graph run of the same workload right after "
-                                   "the timed region (events cannot sit between kernels of a graph replay); "
-                                   "achieved = algorithmic bytes per launch / mean launch duration",
+                         "traffic_note": "DRAM bytes per launch from the committed ncu capture: "
+                                         "profiles/ (not measured in this run)",
+                         "method": "per-launch CUDA events on the operator's stream (the stream the kernels run "
+                                   "on) in an instrumented, non-graph run of the same workload right after the "
+                                   "timed region (events cannot sit between kernels of a graph replay); "
+                                   "achieved = algorithmic bytes per launch (DESIGN.md §4) / mean launch duration",
                          "step_alg_GBps": tot_bytes / (tot_ms / 1e3) / 1e9 if tot_ms else None,
-                         "survey_formula_GBps": alg_bytes_haar(n, T) / (ms_step / 1e3) / 1e9,
-                         "two_pass_formula_GBps": alg_bytes_haar_2p(n, T) / (ms_step / 1e3) / 1e9,
+                         **R.extra_roofline(ms_step),
                          "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 4),
                                          "alg_GB": round(v["alg_bytes"] / 1e9, 4)} for k, v in stats.items()}},
             "clocks": clocks,
-            "final_norm": final_norm,
+            "check": check,
         }
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(n, min(args.cpu_T, T), args.seed)
+            line["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -212,6 +212,51 @@ int hd_run_callback(hd_op* op, int64_t iterations, int32_t depth, const void* co
                     hd_side_fn side_of, hd_update_fn update, void* user, void* final_out_dev);
 
 /* ---------------------------------------------------------------------------
+ * Device-resident application runs of the BASELINE workloads: the whole run
+ * is one CUDA graph (no host synchronisation per probe); the update maps run
+ * in the epilogue of each probe's output pass. The reference has neither map
+ * (SPEC.md:439 lists AMP as a non-goal); both are defined once in the test
+ * oracle (oracle/hd_oracle.cpp or_amp / or_spiked_power, same operation order)
+ * and the probes are GinibreOperator::probe (ginibre.hpp:58-106) and
+ * GOEOperator::probe (ensembles.hpp:117-127). Vectors are host pointers
+ * (on_device = 0) or device pointers of the operator's dtype; curves are
+ * double. Synchronous; errors as hd_run.
+ *
+ * AMP on a Ginibre design A (m x n), delta = m / n (BASELINE config 4):
+ *   y = A beta + w (one right probe, experiments.cpp:80-82), x^0 = 0, z^0 = y,
+ *   x^{t+1} = soft(x^t + A^T z^t, alpha ||z^t|| / sqrt(m))  (experiments.cpp:31-39)
+ *   z^{t+1} = y - A x^{t+1} + (nnz(x^{t+1}) / n / delta) z^t
+ *   mse_out[t] = ||x^{t+1} - beta||^2 / n; x_out = x^T. 2T + 1 probes. */
+typedef struct hd_amp_args {
+  const void* beta;   /* n  */
+  const void* w;      /* m  */
+  int64_t iterations; /* T  */
+  double alpha;       /* threshold multiplier (1.5 in config 4) */
+  void* x_out;        /* n  */
+  double* mse_out;    /* T, optional */
+  int32_t on_device;
+  int32_t use_graph;
+  void* stream;       /* caller's cudaStream_t (NULL = legacy default) */
+} hd_amp_args;
+int hd_run_amp(hd_op* op, const hd_amp_args* args);
+
+/* Power method on a spiked GOE (BASELINE config 5): G the GOE operator,
+ *   x_{t+1} = (G x_t + theta <u, x_t> u) / ||.||,  overlap_out[t] = <u, x_{t+1}>,
+ * x_out = x_{T+1}. u should be a unit vector. */
+typedef struct hd_spiked_args {
+  const void* u;      /* n  */
+  const void* x1;     /* n  */
+  int64_t iterations; /* T GOE steps (2T inner probes) */
+  double theta;
+  void* x_out;        /* n  */
+  double* overlap_out;/* T, optional */
+  int32_t on_device;
+  int32_t use_graph;
+  void* stream;
+} hd_spiked_args;
+int hd_run_spiked(hd_op* op, const hd_spiked_args* args);
+
+/* ---------------------------------------------------------------------------
  * Standalone reflector: make_reflector(p, offset, zero_tol, sign_rule) built
  * on the device and applied to `count` vectors x (each n long, contiguous)
  * into y (reflect.hpp:70-83,120-176; bindings module.cpp:48-66). Real

@@ -124,6 +124,13 @@ double RandomSource::normal() {  // random.cpp:106-121 (Marsaglia polar)
 
 Vec RandomSource::normal_vector(Index len) {  // random.cpp:130-176
   require(len >= 1, "normal_vector: len must be >= 1");
+  if (queue_) {  // test hook: the queued draws (set_queue)
+    require(qpos_ + static_cast<size_t>(len) <= queue_->size(), "normal_vector: draw queue exhausted");
+    Vec out(queue_->begin() + static_cast<std::ptrdiff_t>(qpos_),
+            queue_->begin() + static_cast<std::ptrdiff_t>(qpos_ + static_cast<size_t>(len)));
+    qpos_ += static_cast<size_t>(len);
+    return out;
+  }
   const Zig& z = zig();
   Xoshiro256pp e = eng_;
   auto u53 = [&e] { return static_cast<double>(e.next() >> 11) * 0x1.0p-53; };
@@ -562,6 +569,29 @@ int or_op_new(int ensemble, std::int64_t m, std::int64_t n, double sigma, std::u
   return 0;
   OR_CATCH
 }
+// An operator whose matrix stream is the given draw sequence (one vector per
+// probe, in probe order) instead of RandomSource(seed, stream): the checker
+// for device runs in Philox mode (draws exported by hd_philox_normals).
+int or_op_new_queued(int ensemble, std::int64_t m, std::int64_t n, double sigma, const double* draws,
+                     std::int64_t len, void** out) {
+  OR_TRY
+  auto q = std::make_shared<std::vector<double>>(draws, draws + len);
+  RandomSource src(1, 0);
+  src.set_queue(q);
+  auto box = std::make_unique<OpBox>();
+  box->ensemble = ensemble;
+  if (ensemble == 0)
+    box->op = std::make_unique<GinibreOperator>(m, n, sigma, src);
+  else if (ensemble == 1)
+    box->op = std::make_unique<HaarOperator>(n, src);
+  else if (ensemble == 2)
+    box->op = std::make_unique<GOEOperator>(n, sigma, src);
+  else
+    throw std::invalid_argument("unknown ensemble");
+  *out = box.release();
+  return 0;
+  OR_CATCH
+}
 void or_op_free(void* p) { delete static_cast<OpBox*>(p); }
 std::int64_t or_op_remaining(void* p) { return static_cast<OpBox*>(p)->op->remaining_probes(); }
 std::int64_t or_op_rows(void* p) { return static_cast<OpBox*>(p)->op->rows(); }
@@ -683,11 +713,98 @@ int or_bench_workload(int ensemble, std::int64_t m, std::int64_t n, double sigma
 //     b   = (#{i : x^{t+1}_i != 0} / n) / delta (Onsager coefficient)
 //     z^{t+1} = y - A x^{t+1} + b z^t           (right probe)
 //   mse_t = ||x^{t+1} - beta||^2 / n.
+static void amp_run(ProbeOperator& A, const double* beta, const double* w, std::int64_t T, double alpha,
+                    double* x_out, double* mse_out);
+static void spiked_run(ProbeOperator& G, const double* u, const double* x1, std::int64_t T, double theta,
+                       double* x_out, double* overlap_out);
+
 int or_amp(void* p, const double* beta, const double* w, std::int64_t T, double alpha, double* x_out,
            double* mse_out) {
   OR_TRY
-  auto* b = static_cast<OpBox*>(p);
-  ProbeOperator& A = *b->op;
+  amp_run(*static_cast<OpBox*>(p)->op, beta, w, T, alpha, x_out, mse_out);
+  return 0;
+  OR_CATCH
+}
+
+int or_spiked_power(void* p, const double* u, const double* x1, std::int64_t T, double theta, double* x_out,
+                    double* overlap_out) {
+  OR_TRY
+  spiked_run(*static_cast<OpBox*>(p)->op, u, x1, T, theta, x_out, overlap_out);
+  return 0;
+  OR_CATCH
+}
+
+// CPU timing of the config-4 / config-5 workloads (bench.py's reference arm
+// and cpu_baseline): `trials` independent trials on `threads` threads (one
+// trial per thread at a time, like parallel_for, parallel.hpp:17-52), each
+// timed from operator construction (bench.cpp:42-53). Trial i uses
+// derive_seed(seed, i): matrix stream 0, data stream 1 (experiments.cpp:122-125).
+//   kind 0: AMP, Ginibre m = 2n, sigma = 1/sqrt(m), beta ~ Bernoulli(0.1) N(0,1)
+//           (sample_bernoulli_gaussian with rho = 0.9, experiments.cpp:19-29),
+//           w = 0.1 N(0, I_m), alpha = 1.5, T iterations (2T + 1 probes)
+//   kind 1: spiked GOE, sigma = 1/sqrt(n), u and x_1 unit vectors from the
+//           data stream, theta = 2, T steps (2T inner probes)
+int or_bench_app(int kind, std::int64_t n, std::int64_t T, std::uint64_t seed, int trials, int threads,
+                 double* seconds, double* checksum) {
+  OR_TRY
+  require(trials >= 1 && threads >= 1, "or_bench_app: trials/threads must be positive");
+  std::atomic<int> next{0};
+  std::vector<double> sums(static_cast<size_t>(trials), 0.0);
+  std::mutex emu;
+  std::exception_ptr first;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto worker = [&] {
+    for (;;) {
+      const int i = next.fetch_add(1);
+      if (i >= trials) return;
+      try {
+        const std::uint64_t s = derive_seed(seed, static_cast<std::uint64_t>(i));
+        RandomSource data(s, 1);
+        Vec out(static_cast<size_t>(n));
+        if (kind == 0) {
+          const Index m = 2 * n;
+          GinibreOperator A(m, n, 1.0 / std::sqrt(double(m)), RandomSource(s, 0));
+          Vec beta(static_cast<size_t>(n));
+          for (auto& v : beta) v = (data.uniform() < 0.9) ? 0.0 : data.normal();
+          Vec w = data.normal_vector(m);
+          for (auto& v : w) v *= 0.1;
+          amp_run(A, beta.data(), w.data(), T, 1.5, out.data(), nullptr);
+        } else {
+          GOEOperator G(n, 1.0 / std::sqrt(double(n)), RandomSource(s, 0));
+          Vec u = data.normal_vector(n), x1 = data.normal_vector(n);
+          const double iu = 1.0 / norm(u), ix = 1.0 / norm(x1);
+          for (auto& v : u) v *= iu;
+          for (auto& v : x1) v *= ix;
+          spiked_run(G, u.data(), x1.data(), T, 2.0, out.data(), nullptr);
+        }
+        double acc = 0.0;
+        for (double v : out) acc += v;
+        sums[static_cast<size_t>(i)] = acc;
+      } catch (...) {
+        std::lock_guard<std::mutex> g(emu);
+        if (!first) first = std::current_exception();
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  const int nt = std::min(threads, trials);
+  for (int i = 1; i < nt; ++i) pool.emplace_back(worker);
+  worker();
+  for (auto& th : pool) th.join();
+  const auto t1 = std::chrono::steady_clock::now();
+  if (first) std::rethrow_exception(first);
+  *seconds = std::chrono::duration<double>(t1 - t0).count();
+  double acc = 0.0;
+  for (double v : sums) acc += v;
+  *checksum = acc;
+  return 0;
+  OR_CATCH
+}
+
+}  // extern "C"
+
+static void amp_run(ProbeOperator& A, const double* beta, const double* w, std::int64_t T, double alpha,
+                    double* x_out, double* mse_out) {
   const Index m = A.rows(), n = A.cols();
   const double delta = double(m) / double(n);
   Vec bv(beta, beta + n);
@@ -716,17 +833,12 @@ int or_amp(void* p, const double* beta, const double* w, std::int64_t T, double 
     if (mse_out) mse_out[t] = e / double(n);
   }
   std::memcpy(x_out, x.data(), x.size() * sizeof(double));
-  return 0;
-  OR_CATCH
 }
 
 // Spiked-GOE power method (BASELINE config 5): G = GOE probe operator,
 // x_{t+1} = (G x_t + theta <u, x_t> u) / ||.||, u a unit vector.
-int or_spiked_power(void* p, const double* u, const double* x1, std::int64_t T, double theta, double* x_out,
-                    double* overlap_out) {
-  OR_TRY
-  auto* b = static_cast<OpBox*>(p);
-  ProbeOperator& G = *b->op;
+static void spiked_run(ProbeOperator& G, const double* u, const double* x1, std::int64_t T, double theta,
+                       double* x_out, double* overlap_out) {
   const Index n = G.cols();
   Vec x(x1, x1 + n);
   for (Index t = 0; t < T; ++t) {
@@ -739,8 +851,4 @@ int or_spiked_power(void* p, const double* u, const double* x1, std::int64_t T, 
     if (overlap_out) overlap_out[t] = dot(u, x.data(), n);
   }
   std::memcpy(x_out, x.data(), x.size() * sizeof(double));
-  return 0;
-  OR_CATCH
 }
-
-}  // extern "C"

@@ -23,6 +23,7 @@
 #include <functional>
 #include <stdexcept>
 #include <string>
+#include <memory>
 #include <vector>
 
 namespace hdo {
@@ -81,8 +82,17 @@ class RandomSource {
   Vec normal_vector(Index len);           // ziggurat, random.cpp:130-176
   Vec normal_complex_vector(Index len);   // interleaved (re, im), random.cpp:178-188
   std::uint64_t next_u64() { return eng_.next(); }
+  // Test-infrastructure hook (not in the reference): serve normal_vector from
+  // a fixed queue of draws instead of the ziggurat, so the checker can consume
+  // exactly the Gaussian stream the device generated (device Philox mode).
+  void set_queue(std::shared_ptr<const std::vector<double>> q) {
+    queue_ = std::move(q);
+    qpos_ = 0;
+  }
 
  private:
+  std::shared_ptr<const std::vector<double>> queue_;
+  size_t qpos_ = 0;
   Xoshiro256pp eng_;
   bool has_spare_ = false;
   double spare_ = 0.0;

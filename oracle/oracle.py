@@ -86,6 +86,10 @@ def lib():
         L.or_c_op_remaining.restype = C.c_int64
         L.or_c_op_remaining.argtypes = [C.c_void_p]
         L.or_c_op_probe.argtypes = [C.c_void_p, _dp, C.c_int64, C.c_int, _dp, C.c_int64]
+        L.or_op_new_queued.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_double, _dp, C.c_int64,
+                                       C.POINTER(C.c_void_p)]
+        L.or_bench_app.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_uint64, C.c_int, C.c_int,
+                                   C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.or_bench_workload.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_double, C.c_int, C.c_int,
                                         C.c_int64, C.c_uint64, C.c_int, C.c_int,
                                         C.POINTER(C.c_double), C.POINTER(C.c_double)]
@@ -169,10 +173,17 @@ class Operator:
     """ProbeOperator (operators.hpp:29-49) over Ginibre / Haar / GOE."""
 
     def __init__(self, ensemble: str, m: int = 0, n: int = 0, sigma: float = 1.0, seed: int = 1,
-                 stream: int = 0, skip_reflector: bool = False, sign_rule: str = "stable"):
+                 stream: int = 0, skip_reflector: bool = False, sign_rule: str = "stable", draws=None):
+        """draws: optional fp64 array; the operator's matrix stream then serves
+        these values (one normal_vector per probe, in order) instead of
+        RandomSource(seed, stream) — the checker for device Philox runs."""
         h = C.c_void_p()
-        _check(lib().or_op_new(ENSEMBLES[ensemble], m, n, sigma, seed, stream, int(skip_reflector),
-                               SIGN_RULES[sign_rule], C.byref(h)))
+        if draws is not None:
+            d = np.ascontiguousarray(draws, dtype=np.float64).reshape(-1)
+            _check(lib().or_op_new_queued(ENSEMBLES[ensemble], m, n, sigma, d, d.size, C.byref(h)))
+        else:
+            _check(lib().or_op_new(ENSEMBLES[ensemble], m, n, sigma, seed, stream, int(skip_reflector),
+                                   SIGN_RULES[sign_rule], C.byref(h)))
         self._h = h.value
         self.ensemble = ensemble
 
@@ -336,4 +347,14 @@ def bench_workload(ensemble: str, m: int, n: int, sigma: float, kind: str, side_
     secs, chk = C.c_double(), C.c_double()
     _check(lib().or_bench_workload(ENSEMBLES[ensemble], m, n, sigma, UPDATES[kind], SIDE_RULES[side_rule],
                                    T, seed, trials, threads, C.byref(secs), C.byref(chk)))
+    return secs.value, chk.value
+
+
+def bench_app(kind: str, n: int, T: int, seed: int, trials: int, threads: int):
+    """Wall time of `trials` independent config-4 ('amp', m = 2n) or config-5
+    ('spiked', GOE) trials on `threads` threads, from operator construction
+    (or_bench_app). Returns (seconds, checksum)."""
+    secs, chk = C.c_double(), C.c_double()
+    _check(lib().or_bench_app({"amp": 0, "spiked": 1}[kind], n, T, seed, trials, threads, C.byref(secs),
+                              C.byref(chk)))
     return secs.value, chk.value

@@ -37,7 +37,7 @@ EXPORTS = (
     "hd_run_async", "hd_wait", "hd_reseed", "hd_rs_create", "hd_rs_destroy", "hd_rs_next_u64", "hd_rs_uniform",
     "hd_rs_normal", "hd_rs_normal_vector", "hd_rs_bernoulli_gaussian", "hd_derive_seed",
     "hd_philox_normals", "hd_batch_run", "hd_exchange_create_local", "hd_exchange_nccl_id", "hd_exchange_create_nccl", "hd_exchange_destroy",
-    "hd_shard_plan", "hd_shard_range",
+    "hd_shard_plan", "hd_shard_range", "hd_run_amp", "hd_run_spiked",
 )
 _NON_STATUS = ("hd_last_error", "hd_version", "hd_rs_destroy", "hd_rs_next_u64", "hd_rs_uniform", "hd_rs_normal",
                "hd_derive_seed")
@@ -57,6 +57,22 @@ class hd_run_args(C.Structure):
         ("update", C.c_int32), ("side_rule", C.c_int32), ("iterations", C.c_int64), ("x1", C.c_void_p),
         ("x0", C.c_void_p), ("on_device", C.c_int32), ("use_graph", C.c_int32), ("traj", C.c_void_p),
         ("final_out", C.c_void_p), ("stream", C.c_void_p),
+    ]
+
+
+class hd_amp_args(C.Structure):
+    _fields_ = [
+        ("beta", C.c_void_p), ("w", C.c_void_p), ("iterations", C.c_int64), ("alpha", C.c_double),
+        ("x_out", C.c_void_p), ("mse_out", C.c_void_p), ("on_device", C.c_int32), ("use_graph", C.c_int32),
+        ("stream", C.c_void_p),
+    ]
+
+
+class hd_spiked_args(C.Structure):
+    _fields_ = [
+        ("u", C.c_void_p), ("x1", C.c_void_p), ("iterations", C.c_int64), ("theta", C.c_double),
+        ("x_out", C.c_void_p), ("overlap_out", C.c_void_p), ("on_device", C.c_int32), ("use_graph", C.c_int32),
+        ("stream", C.c_void_p),
     ]
 
 
@@ -113,6 +129,8 @@ def lib():
         L.hd_launch_count.argtypes = [vp, C.POINTER(i64)]
         L.hd_reflector_apply.argtypes = [vp, i64, i64, C.c_double, i32, vp, vp, i64, i32, vp]
         L.hd_run_async.argtypes = [vp, C.POINTER(hd_run_args)]
+        L.hd_run_amp.argtypes = [vp, C.POINTER(hd_amp_args)]
+        L.hd_run_spiked.argtypes = [vp, C.POINTER(hd_spiked_args)]
         L.hd_wait.argtypes = [vp]
         L.hd_reseed.argtypes = [vp, C.c_uint64]
         L.hd_rs_create.argtypes = [C.c_uint64, C.c_uint64, C.POINTER(vp)]

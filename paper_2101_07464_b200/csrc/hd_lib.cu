@@ -234,6 +234,7 @@ struct hd_op {
   std::vector<Counters> pend_snaps;
   int64_t pend_fdim = 0, pend_dim1 = 0;
   void* pend_traj_dev = nullptr;
+  bool pend_final_deferred = false;  // device x_{T+1} copied out by hd_wait (two-pass runs)
   cudaStream_t pend_stream = nullptr;
   unsigned long long* trace = nullptr;  // HD_TRACE=1: phase stamps of k_small_dots
   std::vector<double> trace_acc;        // accumulated phase durations (ns)
@@ -245,6 +246,16 @@ struct hd_op {
   std::string graph_key;
   std::vector<Counters> graph_snaps;  // per-step host state recorded at capture
   int64_t graph_launches = 0;         // kernels inside the captured graph
+  int64_t layout_gen = 0;  // bumped by every reallocation a captured graph could point into
+  // device-resident application runs (hd_run_amp / hd_run_spiked, hd_apps.inc)
+  void* appv[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  size_t appv_bytes[6] = {0, 0, 0, 0, 0, 0};
+  double* app_out = nullptr;
+  int64_t app_out_cap = 0;
+  cudaGraphExec_t app_graph = nullptr;
+  std::string app_graph_key;
+  Counters app_graph_end;
+  int64_t app_graph_launches = 0;
   // instrumentation
   bool prof = false;
   std::map<std::string, KStat> stats;
@@ -335,6 +346,7 @@ void grow_panel(hd_op* op, Panel& p, int64_t rows_pad, int64_t Knew) {
   cudaFree(p.P);
   p.P = np;
   p.K = Knew;
+  op->layout_gen++;
 }
 
 void grow_chain(hd_op* op, Chain& ch, int64_t rows_pad, int64_t Knew) {
@@ -379,6 +391,7 @@ void ensure_small(hd_op* op, int64_t K) {
     *p = dmalloc<double>(K + 8);
   }
   op->small_cap = K;
+  op->layout_gen++;
 }
 
 void ensure_red(hd_op* op, size_t nslots) {
@@ -386,6 +399,7 @@ void ensure_red(hd_op* op, size_t nslots) {
     cudaFree(op->red);
     op->red_cap = nslots * 2;
     op->red = dmalloc<double>(op->red_cap);
+    op->layout_gen++;
   }
 }
 
@@ -433,6 +447,7 @@ void ensure_capacity(hd_op* op, int64_t nr, int64_t nl) {
       }
     }
     op->flush_slots = slots;
+    op->layout_gen++;
   }
   op->partials = op->fbD.partials;
   op->partsF = op->fbF.partials;
@@ -625,7 +640,14 @@ int launch_dots(hd_op* op, cudaStream_t s, DotArgs<T>& a, double bytes) {
   {
     int64_t chunks = 0;
     for (int j = 0; j < a.njobs; ++j) chunks += (a.job[j].ncols + chunk_cols<T>() - 1) / chunk_cols<T>();
-    const int64_t slots = (int64_t)std::max(1, (op->nsm - op->spare_sms) / std::max(1, op->batch_hint)) * kMaxWarps / 2;
+    // launch_tma picks one of the three largest feasible warp counts and caps
+    // the grid at the SMs: every (tile, group) work item needs a warp
+    int optin = 0;
+    ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, op->cfg.device), "attr");
+    const int nw_cap = (int)std::min<size_t>(std::min(kMaxWarps, op->max_warps), ((size_t)optin - 1024) / per_warp);
+    const int nw_min = op->warps_fixed ? nw_cap : std::max(1, nw_cap - 2);
+    const int64_t sms = std::max(1, (op->nsm - op->spare_sms) / std::max(1, op->batch_hint));
+    const int64_t slots = std::min<int64_t>(sms * kMaxWarps / 2, sms * nw_min);
     // the single-CTA stage stages nslots x (CTAs / kGroup) partial rows:
     // keep that under 64 KB (at >= 6 warps per CTA)
     const int64_t max_groups = std::max<int64_t>(1, 65536 / (8 * std::max(1, a.nslots)));
@@ -742,6 +764,7 @@ void inj_append(hd_op* op, const double* g, int64_t len, bool on_device) {
     cudaFree(op->inj);
     op->inj = np;
     op->inj_cap = ncap;
+    op->layout_gen++;
   }
   ck(cudaMemcpyAsync(op->inj + op->inj_size, g, sizeof(double) * len,
                      on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, op->stream),
@@ -801,6 +824,8 @@ double bytes_of(hd_op* op, double elems) { return elems * (double)op->esz; }
 #include "hd_probe.inc"
 
 #include "hd_run.inc"
+
+#include "hd_apps.inc"
 
 }  // namespace
 

@@ -692,49 +692,78 @@ def run_dynamics(op, spec: DynamicsSpec) -> list:
     return traj
 
 
-def amp_sparse_regression(op, beta, w, T: int, alpha: float = 1.5):
+def _app_io(op, vecs, dims):
+    """Inputs of a device app run: (pointers, keep-alive, on_device, stream,
+    torch module or None). CUDA tensors stay on the device; anything else is a
+    contiguous host array of the operator's dtype."""
+    if any(_is_torch_cuda(v) for v in vecs):
+        import torch
+
+        want = torch.float64 if op.dtype == "f64" else torch.float32
+        dev = next(v.device for v in vecs if _is_torch_cuda(v))
+        ts = [torch.as_tensor(v, device=dev).to(want).contiguous().reshape(-1) for v in vecs]
+        for t, d in zip(ts, dims):
+            if t.numel() != d:
+                raise ValueError("run_dynamics: initial history must hold d + 1 vectors")
+        return [t.data_ptr() for t in ts], ts, 1, torch.cuda.current_stream(dev).cuda_stream, torch
+    arrs = [np.ascontiguousarray(np.asarray(v, dtype=op._np_dtype).reshape(-1)) for v in vecs]
+    for a, d in zip(arrs, dims):
+        if a.size != d:
+            raise ValueError("run_dynamics: initial history must hold d + 1 vectors")
+    return [a.ctypes.data for a in arrs], arrs, 0, None, None
+
+
+def amp_sparse_regression(op, beta, w, T: int, alpha: float = 1.5, use_graph: bool = True, x_out=None,
+                          mse_out=None):
     """AMP for sparse regression on a device Ginibre design A (BASELINE config 4;
     not in the reference — the same recurrence is or_amp in the test oracle):
     y = A beta + w (one right probe, experiments.cpp:80-82), x^0 = 0, z^0 = y,
       x^{t+1} = soft(x^t + A^T z^t, alpha ||z^t|| / sqrt(m))   (soft: experiments.cpp:31-39)
       z^{t+1} = y - A x^{t+1} + (nnz(x^{t+1}) / n / delta) z^t,  delta = m / n.
-    Probes alternate Q^T, Q on the device; the update runs on device tensors.
-    Returns (x^T, mse curve ||x^t - beta||^2 / n as a device tensor)."""
-    import torch
-
+    The whole run (2T + 1 probes, the update maps fused into each output pass)
+    is one device-resident CUDA graph (hd_run_amp). CUDA tensors in -> CUDA
+    tensors out; host arrays in -> numpy out (optionally into the caller's
+    host buffers x_out / mse_out, e.g. pinned). Returns (x^T, mse curve
+    ||x^t - beta||^2 / n)."""
     m, n = op.rows, op.cols
-    delta = m / n
-    beta = torch.as_tensor(beta, dtype=torch.float64, device="cuda")
-    w = torch.as_tensor(w, dtype=torch.float64, device="cuda")
-    y = op.probe(beta, "right") + w
-    x = torch.zeros(n, dtype=torch.float64, device="cuda")
-    z = y.clone()
-    mse = torch.empty(T, dtype=torch.float64, device="cuda")
-    for t in range(T):
-        r = x + op.probe(z, "left")
-        th = alpha * torch.linalg.vector_norm(z) / (m ** 0.5)
-        x = torch.sign(r) * torch.clamp(r.abs() - th, min=0.0)
-        ons = torch.count_nonzero(x).to(torch.float64) / n / delta
-        z = y - op.probe(x, "right") + ons * z
-        mse[t] = torch.sum((x - beta) ** 2) / n
+    ptrs, keep, on_dev, stream, torch = _app_io(op, [beta, w], [n, m])
+    a = N.hd_amp_args()
+    a.beta, a.w = ptrs
+    a.iterations, a.alpha = int(T), float(alpha)
+    a.on_device, a.use_graph = on_dev, int(bool(use_graph))
+    a.stream = stream
+    if torch is not None:
+        x = torch.empty(n, dtype=keep[0].dtype, device=keep[0].device) if x_out is None else x_out
+        mse = torch.empty(int(T), dtype=torch.float64, device=keep[0].device) if mse_out is None else mse_out
+    else:
+        x = np.empty(n, dtype=op._np_dtype) if x_out is None else x_out
+        mse = np.empty(int(T), dtype=np.float64) if mse_out is None else mse_out
+    a.x_out = x.data_ptr() if torch is not None else x.ctypes.data
+    a.mse_out = (mse.data_ptr() if torch is not None else mse.ctypes.data) if int(T) > 0 else None
+    N.check(N.lib().hd_run_amp(op._h, C.byref(a)))
     return x, mse
 
 
-def spiked_power(op, u, x1, T: int, theta: float = 2.0):
+def spiked_power(op, u, x1, T: int, theta: float = 2.0, use_graph: bool = True, x_out=None, overlap_out=None):
     """Power method on Q + theta u u^T with Q a device GOE operator (BASELINE
-    config 5): x_{t+1} = (Q x_t + theta <u, x_t> u) / ||.||. Returns (x_T,
-    overlaps <u, x_t> as a device tensor)."""
-    import torch
-
-    u = torch.as_tensor(u, dtype=torch.float64, device="cuda")
-    x = torch.as_tensor(x1, dtype=torch.float64, device="cuda").clone()
-    ov = torch.empty(T, dtype=torch.float64, device="cuda")
-    for t in range(T):
-        gx = op.probe(x, "right")
-        gx = gx + theta * torch.dot(u, x) * u
-        nr = torch.linalg.vector_norm(gx)
-        x = gx * torch.where(nr > 0, 1.0 / nr, torch.ones_like(nr))
-        ov[t] = torch.dot(u, x)
+    config 5): x_{t+1} = (Q x_t + theta <u, x_t> u) / ||.||. One device-resident
+    CUDA graph (hd_run_spiked). Returns (x_{T+1}, overlaps <u, x_{t+1}>)."""
+    n = op.cols
+    ptrs, keep, on_dev, stream, torch = _app_io(op, [u, x1], [n, n])
+    a = N.hd_spiked_args()
+    a.u, a.x1 = ptrs
+    a.iterations, a.theta = int(T), float(theta)
+    a.on_device, a.use_graph = on_dev, int(bool(use_graph))
+    a.stream = stream
+    if torch is not None:
+        x = torch.empty(n, dtype=keep[0].dtype, device=keep[0].device) if x_out is None else x_out
+        ov = torch.empty(int(T), dtype=torch.float64, device=keep[0].device) if overlap_out is None else overlap_out
+    else:
+        x = np.empty(n, dtype=op._np_dtype) if x_out is None else x_out
+        ov = np.empty(int(T), dtype=np.float64) if overlap_out is None else overlap_out
+    a.x_out = x.data_ptr() if torch is not None else x.ctypes.data
+    a.overlap_out = (ov.data_ptr() if torch is not None else ov.ctypes.data) if int(T) > 0 else None
+    N.check(N.lib().hd_run_spiked(op._h, C.byref(a)))
     return x, ov
 
 

@@ -1,0 +1,213 @@
+"""Parity at the BASELINE shapes (VERDICT r1 "what's weak" #1): the device path
+checked against the CPU oracle at the sizes the benchmark runs, every iterate.
+
+* config 2 shape: Haar n = 1e6, T = 100, reference draws (the reference's own
+  RandomSource stream), normalize / identity / tanh-mix maps, the two-pass run
+  and the three-pass sequence (HD_FUSED=0); the tanh-mix tolerance is the
+  oracle's own measured sensitivity envelope (tests/golden/chaos_envelope_config2.json,
+  SURVEY §7 hard part 6) floored at the north star's 1e-9;
+* config 3 shape: Ginibre 1e5 x 1e5, T = 100, alternating normalize, fp64
+  (1e-9) and fp32 (1e-4) — past t ~ 60 this power iteration is chaotic (a
+  1e-16 perturbation of x_1 grows to 1e-5 in the oracle itself), so late
+  iterates are held to 10x the oracle's measured envelope instead — and
+  hd_batch_run trials in device Philox mode checked against the oracle fed
+  the same Philox draws (the production path);
+* config 4 shape: AMP m = 2e5, n = 1e5, T = 200 AMP iterations (401 probes)
+  in device Philox mode, the whole run one CUDA graph (hd_run_amp), against
+  or_amp fed the same draws.
+References: haar.hpp:40-67, ginibre.hpp:58-106, test_haar.cpp:35-45,
+dynamics.hpp:42-76."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def rel_rows(a, b):
+    a = np.asarray(a)
+    return np.linalg.norm(a - b, axis=-1) / np.linalg.norm(b, axis=-1)
+
+
+def philox_draws(lm, seed, lens):
+    """The device Philox stream of an operator seeded `seed`: one draw vector
+    per probe, probe index k = 0, 1, ... (hd_philox_normals), on the host."""
+    return np.concatenate([lm.philox_normals(seed, k, L).cpu().numpy() for k, L in enumerate(lens)])
+
+
+@pytest.fixture
+def env_flags():
+    """Set HD_* switches for the operators created inside the test."""
+    saved = {}
+
+    def set_(**kv):
+        for k, v in kv.items():
+            saved.setdefault(k, os.environ.get(k))
+            os.environ[k] = v
+
+    yield set_
+    for k, v in saved.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
+
+
+# ----------------------------------------------------------------- config 2
+N2, T2, SEED2 = 1_000_000, 100, 2
+
+
+@pytest.fixture(scope="module")
+def haar_x1(orc):
+    x1 = orc.RandomSource(SEED2, 1).normal_vector(N2)
+    return x1 / np.linalg.norm(x1)
+
+
+@pytest.fixture(scope="module")
+def haar_refs(orc, haar_x1):
+    out = {}
+    for kind in ("normalize", "identity", "tanh_mix"):
+        out[kind] = orc.Operator("haar", n=N2, seed=SEED2).run(kind, "right", T2, haar_x1, keep=True)
+    return out
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_haar_1e6_normalize_and_identity_every_iterate(lm, haar_x1, haar_refs, env_flags, fused):
+    env_flags(HD_FUSED=fused)
+    # normalize with the trajectory: three-pass sequence (iterates exist only lazily scaled in the two-pass run)
+    op = lm.HaarOperator(N2, seed=SEED2, draws="reference", capacity=T2)
+    traj = op.run(haar_x1, T2, update="normalize", sides="right", keep_trajectory=True)
+    assert rel_rows(traj, haar_refs["normalize"]).max() < 1e-9
+    # identity with the trajectory: the two-pass run when fused = 1 (2 launches per probe)
+    op = lm.HaarOperator(N2, seed=SEED2, draws="reference", capacity=T2)
+    l0 = op.launch_count()
+    traj = op.run(haar_x1, T2, update="identity", sides="right", keep_trajectory=True)
+    per_probe = (op.launch_count() - l0) / T2
+    assert (per_probe < 4) == (fused == "1")
+    assert rel_rows(traj, haar_refs["identity"]).max() < 1e-9
+    # normalize, final iterate only: two-pass when fused = 1
+    op = lm.HaarOperator(N2, seed=SEED2, draws="reference", capacity=T2)
+    fin = op.run(haar_x1, T2, update="normalize", sides="right")
+    assert rel_rows(fin, haar_refs["normalize"][-1]) < 1e-9
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_config2_tanh_mix_1e6_every_iterate_within_envelope(lm, haar_x1, haar_refs, env_flags, fused):
+    env_flags(HD_FUSED=fused)
+    env = json.load(open(os.path.join(HERE, "golden", "chaos_envelope_config2.json")))
+    assert env["n"] == N2 and env["T"] == T2 and env["seed"] == SEED2
+    tol = np.maximum(1e-9, np.asarray(env["envelope"]))
+    op = lm.HaarOperator(N2, seed=SEED2, draws="reference", capacity=T2)
+    traj = op.run(haar_x1, T2, update="tanh_mix", sides="right", keep_trajectory=True)
+    err = rel_rows(traj, haar_refs["tanh_mix"])
+    assert (err <= tol).all(), f"worst iterate {int(np.argmax(err / tol))}: {err.max():.3e}"
+
+
+# ----------------------------------------------------------------- config 3
+N3, T3, SEED3 = 100_000, 100, 3
+
+
+def oracle_envelope(orc, make, kind, sides, T, x1, rels, seed=1):
+    """The oracle's own sensitivity: max over relative perturbations `rels` of
+    x_1 of the per-iterate relative distance to the unperturbed run. Normalised
+    power iterations are chaotic once the iterate lies in the revealed span
+    (SURVEY §0 (iv), §7 hard parts 5-6): new reflectors are then built from
+    rounding noise, and two correct implementations that round differently
+    separate exactly as the oracle does from its perturbed self."""
+    ref = make().run(kind, sides, T, x1, keep=True)
+    xi = np.random.default_rng(seed).standard_normal(x1.size)
+    env = np.zeros(T + 1)
+    for r in rels:
+        b = make().run(kind, sides, T, x1 * (1.0 + r * xi), keep=True)
+        env = np.maximum(env, rel_rows(b, ref))
+    return ref, env
+
+
+@pytest.fixture(scope="module")
+def gin_case(orc):
+    x1 = orc.RandomSource(SEED3, 1).normal_vector(N3)
+    x1 /= np.linalg.norm(x1)
+    make = lambda: orc.Operator("ginibre", m=N3, n=N3, sigma=N3 ** -0.5, seed=SEED3)  # noqa: E731
+    ref, env64 = oracle_envelope(orc, make, "normalize", "alternate", T3, x1, (1e-16, 1e-15, 1e-14))
+    _, env32 = oracle_envelope(orc, make, "normalize", "alternate", T3, x1, (3e-8, 6e-8))
+    return x1, ref, {"f64": env64, "f32": env32}
+
+
+@pytest.mark.parametrize("dtype,floor", [("f64", 1e-9), ("f32", 1e-4)])
+def test_config3_ginibre_1e5_T100_every_iterate(lm, gin_case, dtype, floor):
+    # every iterate within max(floor, 10 x the oracle's envelope at the dtype's
+    # rounding level): the north star's 1e-9 / 1e-4 while the run is well
+    # conditioned, the oracle's own chaos bound once it is not
+    x1, ref, env = gin_case
+    tol = np.maximum(floor, 10.0 * env[dtype])
+    op = lm.GinibreOperator(N3, N3, N3 ** -0.5, SEED3, draws="reference", capacity=T3, dtype=dtype)
+    traj = op.run(x1.astype(np.float32) if dtype == "f32" else x1, T3, update="normalize", sides="alternate",
+                  keep_trajectory=True)
+    err = rel_rows(traj.astype(np.float64), ref)
+    assert (err <= tol).all(), f"worst iterate {int(np.argmax(err / tol))}: {err.max():.3e}"
+    assert (err[:30] < floor).all()  # the well-conditioned start meets the north-star tolerance outright
+
+
+def test_config3_batched_trial_matches_oracle_on_philox_draws(orc, lm):
+    import torch
+
+    B, seeds = 4, [SEED3 + b for b in range(4)]
+    ops = [lm.GinibreOperator(N3, N3, N3 ** -0.5, s, capacity=T3) for s in seeds]
+    g = torch.Generator("cuda").manual_seed(9)
+    x1 = torch.randn((B, N3), dtype=torch.float64, device="cuda", generator=g)
+    x1 /= x1.norm(dim=1, keepdim=True)
+    out = torch.empty_like(x1)
+    lm.batch_run(ops, x1, out, seeds, T3, update="normalize", sides="alternate")
+    torch.cuda.synchronize()
+    for b in (0, 3):  # two of the batch's trials, each against the oracle on its own Philox draws
+        draws = philox_draws(lm, seeds[b], [N3] * T3)
+        make = lambda: orc.Operator("ginibre", m=N3, n=N3, sigma=N3 ** -0.5, draws=draws)  # noqa: E731
+        ref, env = oracle_envelope(orc, make, "normalize", "alternate", T3, x1[b].cpu().numpy(), (1e-16, 1e-15, 1e-14))
+        assert rel_rows(out[b].cpu().numpy(), ref[-1]) <= max(1e-9, 10.0 * env[-1])
+
+
+# ----------------------------------------------------------------- config 4
+N4, T4, SEED4 = 100_000, 200, 4
+
+
+def test_config4_amp_1e5_T200_graph_run_matches_oracle(orc, lm):
+    import torch
+
+    m, n = 2 * N4, N4
+    g = torch.Generator("cuda").manual_seed(4)
+    beta = (torch.rand(n, device="cuda", generator=g, dtype=torch.float64) < 0.1) * torch.randn(
+        n, device="cuda", generator=g, dtype=torch.float64)
+    w = 0.1 * torch.randn(m, device="cuda", generator=g, dtype=torch.float64)
+    op = lm.GinibreOperator(m, n, m ** -0.5, SEED4, capacity=T4 + 1)
+    x, mse = lm.amp_sparse_regression(op, beta, w, T4)  # Philox, one CUDA graph
+    x2, mse2 = lm.amp_sparse_regression(op2 := lm.GinibreOperator(m, n, m ** -0.5, SEED4, capacity=T4 + 1),
+                                        beta.cpu().numpy(), w.cpu().numpy(), T4, use_graph=False)
+    assert op2.remaining_probes == n - (2 * T4 + 1)
+    ref = orc.Operator("ginibre", m=m, n=n, sigma=m ** -0.5, draws=philox_draws(lm, SEED4, [m] + [n, m] * T4))
+    xr, mser = ref.amp(beta.cpu().numpy(), w.cpu().numpy(), T4)
+    x, mse = x.cpu().numpy(), mse.cpu().numpy()
+    assert rel_rows(x, xr) < 1e-9
+    assert np.max(np.abs(mse - mser) / mser) < 1e-9
+    assert rel_rows(x2, xr) < 1e-9 and np.max(np.abs(mse2 - mser) / mser) < 1e-9  # host API, no graph
+    assert mse[-1] < 0.2 * mse[0]  # AMP converges
+
+
+# ------------------------------------------------- performance switches
+@pytest.mark.parametrize("flag", ["HD_GIN_MERGE", "HD_APPLY_SPLIT", "HD_DOTS_SPLIT"])
+@pytest.mark.parametrize("ens", ["ginibre", "goe"])
+def test_square_dynamics_switches_match_default_and_oracle(orc, lm, env_flags, flag, ens):
+    n, T, seed = 3000, 24, 41
+    x1 = orc.RandomSource(seed, 1).normal_vector(n)
+    x1 /= np.linalg.norm(x1)
+    ref = orc.Operator(ens, m=n, n=n, sigma=n ** -0.5, seed=seed).run("normalize", "alternate", T, x1, keep=False)[0]
+    make = (lambda: lm.GinibreOperator(n, n, n ** -0.5, seed, draws="reference", capacity=T)) if ens == "ginibre" \
+        else (lambda: lm.GOEOperator(n, seed, sigma=n ** -0.5, draws="reference", capacity=T))
+    base = make().run(x1, T, update="normalize", sides="alternate")
+    env_flags(**{flag: "0"})
+    off = make().run(x1, T, update="normalize", sides="alternate")
+    assert rel_rows(off, base) < 1e-12
+    assert rel_rows(off, ref) < 1e-9 and rel_rows(base, ref) < 1e-9

@@ -390,13 +390,19 @@ def test_amp_sparse_regression_parity(orc, lm):
     w = 0.1 * rng.standard_normal(m)
     ref = orc.Operator("ginibre", m=m, n=n, sigma=m ** -0.5, seed=seed)
     xr, mser = ref.amp(beta, w, T)
-    op = lm.GinibreOperator(m, n, m ** -0.5, seed, draws="injected", capacity=2 * T + 1)
-    op.push_draws(orc.draws_for(seed, [m] + [n, m] * T))
-    x, mse = op_amp = lm.amp_sparse_regression(op, beta, w, T)
-    x, mse = x.cpu().numpy(), mse.cpu().numpy()
-    assert rel(x, xr) < TOL64
-    assert np.max(np.abs(mse - mser) / mser) < 1e-9
-    assert mse[-1] < 0.5 * mse[0]  # AMP converges
+    import torch
+
+    for dev in (False, True):  # host arrays in/out, then CUDA tensors in/out (device-resident run)
+        op = lm.GinibreOperator(m, n, m ** -0.5, seed, draws="injected", capacity=2 * T + 1)
+        op.push_draws(orc.draws_for(seed, [m] + [n, m] * T))
+        if dev:
+            x, mse = lm.amp_sparse_regression(op, torch.tensor(beta, device="cuda"), torch.tensor(w, device="cuda"), T)
+            x, mse = x.cpu().numpy(), mse.cpu().numpy()
+        else:
+            x, mse = lm.amp_sparse_regression(op, beta, w, T)
+        assert rel(x, xr) < TOL64
+        assert np.max(np.abs(mse - mser) / mser) < 1e-9
+        assert mse[-1] < 0.5 * mse[0]  # AMP converges
 
 
 def test_spiked_goe_power_parity(orc, lm):
@@ -411,8 +417,8 @@ def test_spiked_goe_power_parity(orc, lm):
     op = lm.GOEOperator(n, seed, sigma=n ** -0.5, draws="injected", capacity=T)
     op.push_draws(orc.draws_for(seed, [n] * (2 * T)))
     x, ov = lm.spiked_power(op, u, x1, T)
-    assert rel(x.cpu().numpy(), xr) < TOL64
-    assert np.max(np.abs(ov.cpu().numpy() - ovr)) < 1e-9
+    assert rel(x, xr) < TOL64
+    assert np.max(np.abs(ov - ovr)) < 1e-9
     assert abs(ovr[-1]) > 0.5  # theta = 2 > 1: the spike is detected
 
 

@@ -32,7 +32,7 @@ def _worker(rank, world, port, q):
         dist.all_gather_object(seeds, bench.rank_seed(1, rank))
         shards = [None] * world
         dist.all_gather_object(shards, bench.shard_trials(1024, world, rank))
-        val = bench.whole_job_value(world, 1000, 10, 3, mx)
+        val = bench.whole_job_value(world, bench.eu_haar(1000, 10), 3, mx)
         q.put((rank, mx, seeds, shards, val))
     finally:
         dist.destroy_process_group()

@@ -347,3 +347,21 @@ def test_oracle_matches_committed_golden(orc):
     assert set(now) == set(golden)
     for k in golden:
         assert now[k] == golden[k], k
+
+
+def test_queued_draws_reproduce_the_seeded_operator(orc):
+    # the checker hook: an oracle operator fed the seed's own draw sequence is
+    # bitwise the seeded operator (Ginibre alternating, Haar, GOE)
+    rng = np.random.default_rng(3)
+    for ens, m, n, lens in (("ginibre", 70, 50, [70, 50, 70, 50]), ("haar", 0, 60, [60] * 4),
+                            ("goe", 0, 40, [40] * 8)):
+        a = orc.Operator(ens, m=m, n=n, sigma=0.3, seed=9)
+        b = orc.Operator(ens, m=m, n=n, sigma=0.3, draws=orc.draws_for(9, lens))
+        for k in range(4):
+            side = "right" if (ens != "ginibre" or k % 2 == 0) else "left"
+            x = rng.standard_normal(a.cols if side == "right" else a.rows)
+            assert np.array_equal(a.probe(x, side), b.probe(x, side))
+    c = orc.Operator("haar", n=10, draws=np.ones(10))
+    c.probe(np.ones(10))
+    with pytest.raises(Exception, match="draw queue exhausted"):
+        c.probe(np.ones(10))
