@@ -1,0 +1,663 @@
+// Two-pass Ginibre / GOE probes: every panel is streamed
+// ONCE per probe, and each pass does a GEMV-N and a GEMV-T over the same
+// bytes.
+//
+// Per probe (ginibre.hpp:58-106; F = the probed side's chain, O = the other
+// chain, S = the same-side basis store):
+//   pass A (k_nt<FOLD>) over F:  N: p = D_F (x - W_F beta1) -> new column
+//       p[off:] 2^-e, head p[0..off], ||p[off:]||^2;
+//     T: W_F^T w_new (the new reflector's Gram column, rows > off; the pivot
+//       row is added by the stage) and W_F^T g' for the NEXT probe's draw g'
+//       (it lands on this chain when the next probe is on the other side:
+//       the dots k_dots would otherwise stream F again for).
+//   pass B (k_nt<GIN>) over O and S:  N: u = D_O g - W_O beta1 -> S's new
+//       column, y = sigma (S coef + c u + D_O c - W_O beta3) -> update map;
+//     T: O^T x_{t+1} and S^T x_{t+1} — the next probe's K1 dots (its F is
+//       this O, its opposite store this S) — with x_{t+1} the update map's
+//       output row (or, for the GOE inner right probe, the step's input x).
+// The GEMV-T needs the GEMV-N's result row by row, so the panel cannot be a
+// 256-row tile per warp streamed in column chunks as in k_dots/k_apply: a
+// CTA stages a row SUB-TILE of all columns of the pass's panels in shared
+// memory (3-D TMA box {Rs rows, columns, 1 tile} of the tile-major panel,
+// SASS UTMALDG), runs the GEMV-N (thread = row, column groups), the epilogue
+// (thread = row), then the GEMV-T (thread = column, rows rotated by lane:
+// conflict-free) from the same shared bytes. A producer warp keeps the stage
+// ring full (mbarrier full/empty pairs); consumer warps never wait on HBM
+// while a stage is ready. Partial column sums stay in registers across the
+// CTA's contiguous sub-tile range and leave through the deterministic group
+// flush (flush_row), in the slot layouts the single-CTA stages read.
+#pragma once
+
+#include <cuda.h>
+
+#include "hd_kernels.cuh"
+
+namespace hd {
+
+constexpr int kNtConsumers = 256;                   // 8 consumer warps
+constexpr int kNtThreads = kNtConsumers + 32;       // + 1 producer warp
+constexpr int kNtMaxMaps = 4;
+constexpr int kNtMaxVecs = 5;
+constexpr int kNtMaxStages = 16;
+constexpr int kNtMaxCols = 512;                     // columns of a pass (T-phase: <= 2 per consumer)
+constexpr int kNtBarId = 1;                         // named barrier of the consumer warps
+
+enum NtMode : int { kNtFold = 0, kNtGin = 1 };
+enum NtRhs : int { kRhsEpi = 0, kRhsSrc = 1 };
+
+// One 3-D TMA box family: panel `panel`, stage columns [scol, scol + cols),
+// panel columns [pcol, pcol + cols).
+struct NtMapInfo {
+  int scol = 0, pcol = 0, cols = 0;
+};
+
+template <typename T>
+struct NtArgs {
+  CUtensorMap maps[kNtMaxMaps];  // __grid_constant__ parameter space (64-B aligned)
+  NtMapInfo mi[kNtMaxMaps];
+  int nmaps = 0;
+  int rs = 32;        // rows per sub-tile (16..256, divides 256)
+  int nst = 2;        // stages
+  int C = 0;          // columns of the pass (stage layout [C][rs])
+  int kP0 = 0;        // columns of panel 0 (F or O); panel 1 (S) = C - kP0
+  int64_t n = 0;      // rows of the dimension (global)
+  int64_t nsub = 0;   // sub-tiles of this shard's rows
+  RowMap rm;
+  // vectors bulk-copied per sub-tile (rs elements each; 8 B slots): x / g_inj /
+  // yadd / state / aux / xprev, by role index below
+  const void* vec[kNtMaxVecs] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  int vesz[kNtMaxVecs] = {0, 0, 0, 0, 0};
+  int nvec = 0;
+  int64_t stage_bytes = 0;  // per stage
+  int64_t tx_bytes = 0;     // TMA bytes per stage (boxes + vectors)
+  // N-phase coefficients: fold beta1 (F); gin beta1, beta3 (O), coefS (S)
+  const double* beta1 = nullptr;
+  const double* beta3 = nullptr;
+  const double* coefS = nullptr;
+  // D of the panel's chain (fold: F; gin: O)
+  const double* D = nullptr;
+  const double* Dtail = nullptr;
+  int64_t Dlen = 0;
+  // ---- fold
+  int vx = -1;                      // vector role: x (dtype T)
+  const double* xscale = nullptr;   // x * scale (lazily normalised iterate)
+  T* Pw = nullptr;                  // panel F (new column newj)
+  int64_t K = 0, newj = 0, off = 0;
+  const double* escale = nullptr;
+  double* head = nullptr;
+  Src<T> spec;                      // next probe's draw (kSrcPhilox / kSrcInjected via vinj2) or none
+  int vspec = -1;                   // vector role of injected spec draws
+  // ---- gin
+  Src<T> g;                         // this probe's draw (mask, D of O)
+  int vg = -1;                      // vector role of injected draws
+  T* Sw = nullptr;                  // store S (new column newjS)
+  int64_t KS = 0, newjS = 0;
+  const double* csp = nullptr;
+  int64_t csplen = 0;
+  const double* coef_cur = nullptr;
+  double sigma = 1.0;
+  Epi<T> epi;
+  int vyadd = -1, vstate = -1, vaux = -1, vxprev = -1;
+  int rhs_mode = kRhsEpi;           // T-phase right-hand side: epilogue output or the Src below
+  int vrhs = -1;                    // vector role of that Src (dtype T, times rhs_scale)
+  const double* rhs_scale = nullptr;
+  int do_t = 1;                     // run the T phase at all
+  // ---- output slots
+  int slot_t0 = 0;    // T-phase column sums of RHS 0: columns [0, kP0) at slot_t0 + c, columns >= kP0 at slot_t1 + c - kP0
+  int slot_t1 = 0;
+  int slot_t2 = -1;   // fold: RHS 1 (spec draw) column sums at slot_t2 + c
+  int slot_r0 = -1, slot_r1 = -1, slot_r2 = -1, slot_r3 = -1, slot_r4 = -1;  // scalar reductions
+  int nslots = 0;
+  Flush out;
+  int* status = nullptr;
+  int prefetch = 0;
+};
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .b64 pol;\n"
+      "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], pol;\n"
+      "}\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// mbarrier wait that backs off between probes: the producer warp waits for
+// stages to drain most of the time and must not steal issue slots from the
+// consumer warps of its SM partition.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  while (!done) {
+    __nanosleep(64);
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ double ld_vec(const unsigned char* slot, int esz, int r) {
+  if (esz == 8) return reinterpret_cast<const double*>(slot)[r];
+  return (double)reinterpret_cast<const float*>(slot)[r];
+}
+
+// Warp roles of a k_nt CTA (kNtThreads = 9 warps):
+//   warps [0, E)      epilogue warps: one sub-tile row per thread (rs <= 32 E)
+//   warps [E, 8)      workers: GEMV-N of sub-tile j + 1 and GEMV-T of j - 1
+//   warp 8            producer: the TMA ring
+// In "slot" j the epilogue warps finish sub-tile j while the workers run the
+// N phase of j + 1 and the T phase of j - 1 — one barrier per slot, so the
+// row-serial epilogue is off the critical path.
+__host__ __device__ inline int nt_ewarps(int rs) { return rs <= 32 ? 1 : rs / 32; }
+__host__ __device__ inline int nt_workers(int rs) { return kNtConsumers - 32 * nt_ewarps(rs); }
+
+// Shared-memory carve-up (sized per launch): [stages][stage_bytes] | beta1
+// [kP0] | beta3 [kP0] | coefS [C - kP0] | N-phase partials [2][1 or 3][2 WT] |
+// rhs [2][2][rs] | Philox draw batches [2][2 WT] | barriers. The T-phase
+// partials, the scalar partials and the slot row reuse the stages at the end.
+struct NtSmem {
+  unsigned char* stages;
+  double *b1, *b3, *bs;   // bs is indexed by the stage column (c >= kP0)
+  double* red;
+  double* rhs;
+  double* draw;
+  uint64_t* full;
+  uint64_t* empty;
+};
+
+__host__ __device__ inline size_t nt_fixed_doubles(int mode, int C, int kP0, int rs) {
+  const size_t b = (size_t)((kP0 + 1) & ~1) + (mode == kNtGin ? (size_t)((kP0 + 1) & ~1) + (size_t)((C - kP0 + 1) & ~1) : 0);
+  const size_t wt2 = 2 * (size_t)nt_workers(rs);
+  return b + 2 * (mode == kNtGin ? 3 : 1) * wt2 + 4 * (size_t)rs + 2 * wt2;
+}
+
+__host__ __device__ inline size_t nt_fixed_bytes(int mode, int C, int kP0, int rs, int nst) {
+  return sizeof(double) * nt_fixed_doubles(mode, C, kP0, rs) + 2 * (size_t)nst * sizeof(uint64_t) + 128;
+}
+
+// Bytes of the stage ring the final flush reuses: T partials [WT][6], scalar
+// partials [4][kNtConsumers], the slot row.
+__host__ __device__ inline size_t nt_flush_bytes(int nslots) {
+  return sizeof(double) * (6 * (size_t)kNtConsumers + 4 * (size_t)kNtConsumers + (size_t)nslots + 8);
+}
+
+__device__ __forceinline__ NtSmem nt_smem(unsigned char* base, int mode, int C, int kP0, int rs, int nst,
+                                          int64_t stage_bytes) {
+  NtSmem m;
+  m.stages = base;
+  double* p = reinterpret_cast<double*>(base + (size_t)nst * stage_bytes);
+  m.b1 = p; p += (kP0 + 1) & ~1;
+  m.b3 = p;
+  m.bs = p;
+  if (mode == kNtGin) {
+    p += (kP0 + 1) & ~1;
+    m.bs = p - kP0;
+    p += (C - kP0 + 1) & ~1;
+  }
+  const int wt2 = 2 * nt_workers(rs);
+  m.red = p; p += 2 * (mode == kNtGin ? 3 : 1) * wt2;
+  m.rhs = p; p += 4 * rs;
+  m.draw = p; p += 2 * wt2;
+  m.full = reinterpret_cast<uint64_t*>(p);
+  m.empty = m.full + nst;
+  return m;
+}
+
+template <typename T, int MODE>
+__device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const NtSmem m = nt_smem(smem, MODE, a.C, a.kP0, a.rs, a.nst, a.stage_bytes);
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const bool producer = (w == kNtConsumers / 32);
+  const int rs = a.rs, C = a.C, nst = a.nst;
+  const int E = nt_ewarps(rs), WT = nt_workers(rs);
+  const bool epi_thr = !producer && tid < 32 * E;
+  const bool worker = !producer && !epi_thr;
+  const int wt = tid - 32 * E;  // worker index
+  // sub-tiles dealt round robin: at any moment the CTAs stream neighbouring
+  // sub-tiles, so each column's contiguous 2 KB tile segment is read by
+  // neighbouring CTAs close together in time (DRAM row-buffer locality)
+  const int64_t nk = (a.nsub > (int64_t)blockIdx.x) ? (a.nsub - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (tid == 0) {
+    for (int q = 0; q < nst; ++q) {
+      mbar_init(m.full + q, 1);
+      mbar_init(m.empty + q, 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const size_t vec_off = (size_t)C * rs * sizeof(T);  // vector slots after the panel columns (8 B each)
+  auto row_of = [&](int64_t k) { return a.rm.tile0 * kTile + ((int64_t)blockIdx.x + k * gridDim.x) * rs; };
+  auto issue = [&](int64_t k, int q) {  // producer lane 0: sub-tile k into stage q
+    unsigned char* st = m.stages + (size_t)q * a.stage_bytes;
+    const int64_t li = row_of(k);  // local panel row
+    const int tile = (int)(li >> kTileShift), rin = (int)(li & (kTile - 1));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive_expect_tx(m.full + q, (uint32_t)a.tx_bytes);
+    for (int b = 0; b < a.nmaps; ++b)
+      tma_load_3d(st + (size_t)a.mi[b].scol * rs * sizeof(T), &a.maps[b], rin, a.mi[b].pcol, tile, m.full + q);
+    const int64_t vi = li + a.rm.gdelta - a.rm.vbase;  // vector index of the sub-tile's first row
+    for (int v = 0; v < a.nvec; ++v)
+      bulk_g2s(st + vec_off + (size_t)v * rs * 8, static_cast<const unsigned char*>(a.vec[v]) + vi * a.vesz[v],
+               (uint32_t)(rs * a.vesz[v]), m.full + q);
+  };
+  int64_t prefetched = 0;
+  if (producer && lane == 0) {
+    for (int b = 0; b < a.nmaps; ++b) prefetch_map(&a.maps[b]);
+    if (a.prefetch)
+      for (; prefetched < nk && prefetched < nst; ++prefetched) issue(prefetched, (int)prefetched);
+  }
+  pdl_wait();
+  pdl_launch();
+  __shared__ int s_abort;
+  if (tid == 0) s_abort = aborted(a.status) ? 1 : 0;
+  __syncthreads();
+  const bool abort_all = s_abort != 0;
+  if (producer && lane == 0) {
+    int64_t k = prefetched;
+    int q = (int)(k % nst);
+    uint32_t ph = (uint32_t)((k / nst) & 1);  // phase of the empty barrier to wait for: use (k / nst) - 1
+    if (!abort_all) {
+      for (; k < nk; ++k) {
+        if (k >= nst) mbar_wait(m.empty + q, ph ^ 1u);
+        issue(k, q);
+        if (++q == nst) {
+          q = 0;
+          ph ^= 1u;
+        }
+      }
+    } else {
+      for (int64_t j = 0; j < prefetched; ++j) mbar_wait(m.full + j, 0);  // drain what was prefetched
+    }
+  }
+  // ------------------------------------------------------------ consumers
+  const int kP0 = a.kP0;
+  if (!producer) {
+    for (int c = tid; c < kP0; c += kNtConsumers) {
+      m.b1[c] = a.beta1[c];
+      if (MODE == kNtGin) m.b3[c] = a.beta3[c];
+    }
+    if (MODE == kNtGin)
+      for (int c = kP0 + tid; c < C; c += kNtConsumers) m.bs[c] = a.coefS[c - kP0];
+  }
+  // worker T-phase mapping: C >= WT: columns wt, wt + WT, wt + 2 WT; else
+  // G (a power of two) workers per column, column c = wt / G, phase g = wt % G
+  int G = (C >= WT || C == 0) ? 1 : min(WT / C, rs / 2);
+  while (G & (G - 1)) G &= G - 1;
+  const int c0 = (C >= WT) ? wt : wt / G, tg = (C >= WT) ? 0 : wt % G;
+  const int c1 = (C >= WT && wt + WT < C) ? wt + WT : -1;
+  const int c2 = (C >= WT && wt + 2 * WT < C) ? wt + 2 * WT : -1;
+  const bool t_active = worker && C > 0 && c0 < C && a.do_t;
+  double tA0 = 0.0, tA1 = 0.0, tA2 = 0.0, tB0 = 0.0, tB1 = 0.0, tB2 = 0.0;
+  // worker N-phase mapping: row pair nrp, column group ncg (CG groups)
+  const int RP = rs / 2;
+  const int CG = WT / RP;
+  const int nrp = wt % RP, ncg = wt / RP;
+  const int cga = (int)((int64_t)C * ncg / CG), cgb = (int)((int64_t)C * (ncg + 1) / CG);
+  const int nred = (MODE == kNtGin) ? 3 : 1;
+  const int red_stride = 2 * WT;  // one partial array: CG x rs = 2 WT doubles
+  // epilogue scalar accumulators
+  double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+  bool bad = false;
+  const double dtail = (a.Dtail != nullptr) ? *a.Dtail : 1.0;
+  double escale = 1.0, xsc = 1.0, rsc = 1.0, cc = 0.0, esc = 0.0;
+  if (MODE == kNtFold) {
+    escale = *a.escale;
+    if (a.xscale) xsc = *a.xscale;
+  } else {
+    cc = *a.coef_cur;
+    if (a.rhs_scale) rsc = *a.rhs_scale;
+    if (a.epi.sc) esc = *a.epi.sc;
+  }
+  const bool need_draw = (MODE == kNtGin) ? (a.g.kind == kSrcPhilox) : (a.spec.kind == kSrcPhilox);
+  const Src<T>& dsrc = (MODE == kNtGin) ? a.g : a.spec;
+  // Philox batches: batch b covers the CTA's sub-tiles [b CG, (b + 1) CG),
+  // one row pair per worker (sub-tile q = wt / RP, pair wt % RP)
+  auto gen_batch = [&](int64_t b) {
+    if (!need_draw || !worker) return;
+    const int64_t k = b * CG + ncg;
+    if (k >= nk) return;
+    const int64_t i = row_of(k) + a.rm.gdelta + 2 * nrp;
+    const double2 v = philox_normal_pair(*dsrc.seedp, dsrc.stream, dsrc.probe, (uint64_t)(i >> 1));
+    double vx = v.x, vy = v.y;
+    if constexpr (sizeof(T) == 4) {
+      vx = (double)(float)vx;
+      vy = (double)(float)vy;
+    }
+    double* d = m.draw + (b & 1) * 2 * WT;
+    d[2 * wt] = vx;
+    d[2 * wt + 1] = vy;
+  };
+  auto stage_ptr = [&](int q) { return m.stages + (size_t)q * a.stage_bytes; };
+  // ---- N phase of sub-tile k (stage q): workers -> red[k & 1]
+  auto nphase = [&](int64_t k, int q, uint32_t ph) {
+    mbar_wait(m.full + q, ph);
+    const T* sp = reinterpret_cast<const T*>(stage_ptr(q)) + 2 * nrp;
+    double2 n1 = make_double2(0.0, 0.0), n3 = make_double2(0.0, 0.0), ns = make_double2(0.0, 0.0);
+    const int ce = min(cgb, kP0);
+#pragma unroll 4
+    for (int c = cga; c < ce; ++c) {  // one 2-row load per column, coefficients broadcast
+      const double2 v = lds_pair(sp + c * rs);
+      const double b = m.b1[c];
+      n1.x = fma(v.x, b, n1.x);
+      n1.y = fma(v.y, b, n1.y);
+      if (MODE == kNtGin) {
+        const double b3 = m.b3[c];
+        n3.x = fma(v.x, b3, n3.x);
+        n3.y = fma(v.y, b3, n3.y);
+      }
+    }
+    if (MODE == kNtGin) {
+#pragma unroll 4
+      for (int c = max(cga, kP0); c < cgb; ++c) {
+        const double2 v = lds_pair(sp + c * rs);
+        const double b = m.bs[c];
+        ns.x = fma(v.x, b, ns.x);
+        ns.y = fma(v.y, b, ns.y);
+      }
+    }
+    double* red = m.red + (k & 1) * nred * red_stride + ncg * rs + 2 * nrp;  // [cg][rs]
+    *reinterpret_cast<double2*>(red) = n1;
+    if (MODE == kNtGin) {
+      *reinterpret_cast<double2*>(red + red_stride) = n3;
+      *reinterpret_cast<double2*>(red + 2 * red_stride) = ns;
+    }
+  };
+  // ---- epilogue of sub-tile k (stage q): epilogue threads, one row each -> rhs[k & 1]
+  auto epilogue = [&](int64_t k, int q, uint32_t ph, int64_t kb, uint32_t bpar) {
+    const int et = tid;
+    if (et >= rs) return;
+    mbar_wait(m.full + q, ph);  // complete (the workers waited for it a slot ago): orders the vector reads
+    const unsigned char* vs = stage_ptr(q) + vec_off;
+    double* rb = m.rhs + (k & 1) * 2 * rs;
+    const double* red = m.red + (k & 1) * nred * red_stride;
+    double r1 = 0.0, r3 = 0.0, rS = 0.0;
+    {  // column-group partials, fixed order (deterministic), two chains each
+      double r1b = 0.0, r3b = 0.0, rSb = 0.0;
+      int g = 0;
+      for (; g + 1 < CG; g += 2) {
+        r1 += red[g * rs + et];
+        r1b += red[(g + 1) * rs + et];
+        if (MODE == kNtGin) {
+          r3 += red[red_stride + g * rs + et];
+          r3b += red[red_stride + (g + 1) * rs + et];
+          rS += red[2 * red_stride + g * rs + et];
+          rSb += red[2 * red_stride + (g + 1) * rs + et];
+        }
+      }
+      if (g < CG) {
+        r1 += red[g * rs + et];
+        if (MODE == kNtGin) {
+          r3 += red[red_stride + g * rs + et];
+          rS += red[2 * red_stride + g * rs + et];
+        }
+      }
+      r1 += r1b;
+      r3 += r3b;
+      rS += rSb;
+    }
+    const int64_t li = row_of(k) + et;
+    const int64_t i = li + a.rm.gdelta;
+    const double d = (i < a.Dlen) ? a.D[i] : dtail;
+    const double* draw = m.draw + bpar * 2 * WT + kb * rs + et;
+    if (MODE == kNtFold) {
+      const double xv = ld_vec<T>(vs + (size_t)a.vx * rs * 8, sizeof(T), et) * xsc;
+      const double p = (i < a.n) ? d * (xv - r1) : 0.0;
+      const double cv = (i >= a.off) ? p : 0.0;
+      const double wv = cv * escale;
+      a.Pw[paddr(li, a.newj, a.K)] = (T)wv;
+      if (i <= a.off) a.head[i] = p;
+      e0 += cv * cv;  // ||p[off:]||^2
+      const double g_rhs0 = (i > a.off) ? (double)(T)wv : 0.0;  // Gram RHS (the stored values)
+      double g_rhs1 = 0.0;
+      if (a.spec.kind != kSrcNone && i < a.n && i >= a.spec.mask_begin) {
+        g_rhs1 = (a.spec.kind == kSrcPhilox) ? *draw : a.spec.inj[i];  // injected: parity mode only
+        if constexpr (sizeof(T) == 4) g_rhs1 = (double)(float)g_rhs1;
+      }
+      e1 += g_rhs0 * g_rhs1;  // new column . next draw
+      rb[et] = g_rhs0;
+      rb[rs + et] = g_rhs1;
+    } else {
+      double gv = 0.0;
+      if (i < a.n && i >= a.g.mask_begin) {
+        gv = (a.g.kind == kSrcPhilox) ? *draw : a.g.inj[i];  // injected: parity mode only
+        if constexpr (sizeof(T) == 4) gv = (double)(float)gv;
+        gv *= d;
+      }
+      const double u = (i < a.n) ? gv - r1 : 0.0;
+      a.Sw[paddr(li, a.newjS, a.KS)] = (T)u;
+      const double uu = (double)(T)u;
+      const double cs = (i < a.csplen) ? d * a.csp[i] : 0.0;
+      double y = a.sigma * (rS + cc * u + (cs - r3));  // k_ginout's order
+      const Epi<T>& e = a.epi;
+      const int64_t vi = i - a.rm.vbase;
+      double out = 0.0;
+      if (i < a.n) {
+        if (e.yadd) y = (ld_vec<T>(vs + (size_t)a.vyadd * rs * 8, sizeof(T), et) + y) * e.add_scale;
+        if (e.kind >= kEpiAmpInit) {
+          const double stv =
+              (e.state && e.kind != kEpiAmpInit) ? ld_vec<T>(vs + (size_t)a.vstate * rs * 8, sizeof(T), et) : 0.0;
+          const double axv = e.aux ? ld_vec<T>(vs + (size_t)a.vaux * rs * 8, sizeof(T), et) : 0.0;
+          double q0, q1;
+          const double o = epi_row(e.kind, y, stv, axv, esc, q0, q1);
+          if (e.state) e.state[vi] = (T)o;
+          if (e.kind == kEpiAmpInit || e.kind == kEpiSpike) y = o;
+          out = (double)(T)o;
+          e2 += q0;
+          e3 += q1;
+          bad |= !isfinite(o);
+        } else if (e.kind == kEpiTanhMix) {
+          double xp = e.xprev ? ld_vec<T>(vs + (size_t)a.vxprev * rs * 8, sizeof(T), et) : 0.0;
+          if (e.xprev_scale) xp *= *e.xprev_scale;
+          const double o = tanh(2.0 * y) + 0.1 * xp;
+          e.xnext[vi] = (T)o;
+          out = (double)(T)o;
+          bad |= !isfinite(o);
+        } else {
+          out = (double)(T)y;
+          bad |= !isfinite(y);
+          e2 += y * y;  // normalize: ||y||^2 (also the plain map's)
+        }
+        if (e.y) e.y[vi] = (T)y;
+      }
+      const double rhs =
+          (a.rhs_mode == kRhsSrc) ? ((i < a.n) ? ld_vec<T>(vs + (size_t)a.vrhs * rs * 8, sizeof(T), et) * rsc : 0.0)
+                                  : out;
+      e0 += rhs * rhs;  // ||x_{t+1}||^2 (the next probe's K1 sum of squares)
+      e1 += uu * rhs;   // new S column . x_{t+1}
+      rb[et] = rhs;
+    }
+  };
+  // ---- T phase of sub-tile k (stage q): workers; column loads of 2 rows,
+  // the row pair XOR-rotated by the lane (a quarter warp reads 8 distinct
+  // 16-B chunks: conflict-free); small C: G workers per column split the pairs
+  auto tphase = [&](int64_t k, int q) {
+    if (!t_active) return;
+    const T* sp = reinterpret_cast<const T*>(stage_ptr(q));
+    const double* r0 = m.rhs + (k & 1) * 2 * rs;
+    const T* pc0 = sp + (size_t)c0 * rs;
+    if (G == 1) {
+      const int pm = RP - 1;
+      const T* pc1 = sp + (size_t)(c1 >= 0 ? c1 : 0) * rs;
+      const T* pc2 = sp + (size_t)(c2 >= 0 ? c2 : 0) * rs;
+      double2 a0 = make_double2(0.0, 0.0), a1 = a0, a2 = a0, b0 = a0, b1 = a0, b2 = a0;
+#pragma unroll 4
+      for (int jp = 0; jp < RP; ++jp) {
+        const int o = 2 * ((jp ^ lane) & pm);
+        const double2 x = *reinterpret_cast<const double2*>(r0 + o);
+        double2 z = make_double2(0.0, 0.0);
+        if (MODE == kNtFold) z = *reinterpret_cast<const double2*>(r0 + rs + o);
+        const double2 v = lds_pair(pc0 + o);
+        a0.x = fma(v.x, x.x, a0.x);
+        a0.y = fma(v.y, x.y, a0.y);
+        if (MODE == kNtFold) {
+          b0.x = fma(v.x, z.x, b0.x);
+          b0.y = fma(v.y, z.y, b0.y);
+        }
+        if (c1 >= 0) {
+          const double2 u = lds_pair(pc1 + o);
+          a1.x = fma(u.x, x.x, a1.x);
+          a1.y = fma(u.y, x.y, a1.y);
+          if (MODE == kNtFold) {
+            b1.x = fma(u.x, z.x, b1.x);
+            b1.y = fma(u.y, z.y, b1.y);
+          }
+        }
+        if (c2 >= 0) {
+          const double2 u = lds_pair(pc2 + o);
+          a2.x = fma(u.x, x.x, a2.x);
+          a2.y = fma(u.y, x.y, a2.y);
+          if (MODE == kNtFold) {
+            b2.x = fma(u.x, z.x, b2.x);
+            b2.y = fma(u.y, z.y, b2.y);
+          }
+        }
+      }
+      tA0 += a0.x + a0.y;
+      tA1 += a1.x + a1.y;
+      tA2 += a2.x + a2.y;
+      tB0 += b0.x + b0.y;
+      tB1 += b1.x + b1.y;
+      tB2 += b2.x + b2.y;
+    } else {
+      const int npg = RP / G;  // row pairs per phase (a power of two)
+      double2 a0 = make_double2(0.0, 0.0), b0 = a0;
+      for (int jp = 0; jp < npg; ++jp) {
+        const int o = 2 * (tg * npg + ((jp ^ c0) & (npg - 1)));
+        const double2 x = *reinterpret_cast<const double2*>(r0 + o);
+        const double2 v = lds_pair(pc0 + o);
+        a0.x = fma(v.x, x.x, a0.x);
+        a0.y = fma(v.y, x.y, a0.y);
+        if (MODE == kNtFold) {
+          const double2 z = *reinterpret_cast<const double2*>(r0 + rs + o);
+          b0.x = fma(v.x, z.x, b0.x);
+          b0.y = fma(v.y, z.y, b0.y);
+        }
+      }
+      tA0 += a0.x + a0.y;
+      tB0 += b0.x + b0.y;
+    }
+  };
+  // ---- the slot loop (see the warp roles above)
+  if (!producer) named_sync(kNtBarId, kNtConsumers);  // coefficients staged
+  if (!producer && !abort_all && nk > 0) {
+    // stage / phase of sub-tile k, advanced without divisions
+    int qN = 0, qE = 0, qT = 0;          // stages of N (k + 1), epilogue (k), T (k - 1)
+    uint32_t phN = 0, phE = 0;
+    int64_t kbE = 0;                     // epilogue: sub-tile index within its draw batch
+    uint32_t bparE = 0;                  // ... and the batch buffer it reads
+    gen_batch(0);
+    if (worker) nphase(0, 0, 0);
+    qN = (nst > 1) ? 1 : 0;
+    phN = (nst > 1) ? 0u : 1u;
+    named_sync(kNtBarId, kNtConsumers);
+    for (int64_t j = 0; j <= nk; ++j) {
+      if (epi_thr && j < nk) epilogue(j, qE, phE, kbE, bparE);
+      if (worker) {
+        if (j + 1 < nk) {
+          if (kbE + 1 == CG) gen_batch((j + 1) / CG);  // the batch the next epilogue starts (its other buffer)
+          nphase(j + 1, qN, phN);
+        }
+        if (j >= 1) tphase(j - 1, qT);
+      }
+      named_sync(kNtBarId, kNtConsumers);  // red of j + 1, rhs of j ready; stage of j - 1 free
+      if (j >= 1) {
+        if (tid == 0) mbar_arrive(m.empty + qT);
+        if (++qT == nst) qT = 0;
+      }
+      if (++qE == nst) {
+        qE = 0;
+        phE ^= 1u;
+      }
+      if (++kbE == CG) {
+        kbE = 0;
+        bparE ^= 1u;
+      }
+      if (++qN == nst) {
+        qN = 0;
+        phN ^= 1u;
+      }
+    }
+  }
+  // ---- partial sums -> slot row (fixed order) -> group flush; the stages
+  // are free now: [T partials: 6 x 256][scalar partials: 4 x 256][slot row]
+  __syncthreads();
+  double* part = reinterpret_cast<double*>(m.stages);
+  double* sc = part + 6 * kNtConsumers;
+  double* acc = sc + 4 * kNtConsumers;
+  if (worker) {
+    part[6 * wt + 0] = tA0;
+    part[6 * wt + 1] = tA1;
+    part[6 * wt + 2] = tA2;
+    part[6 * wt + 3] = tB0;
+    part[6 * wt + 4] = tB1;
+    part[6 * wt + 5] = tB2;
+  }
+  if (!producer) {
+    sc[tid] = e0;
+    sc[kNtConsumers + tid] = e1;
+    sc[2 * kNtConsumers + tid] = e2;
+    sc[3 * kNtConsumers + tid] = e3;
+  }
+  for (int sl = tid; sl < a.nslots; sl += kNtThreads) acc[sl] = 0.0;
+  __syncthreads();
+  if (C > 0 && a.do_t) {
+    for (int c = tid; c < C; c += kNtThreads) {
+      double s0 = 0.0, s1 = 0.0;
+      if (C >= WT) {
+        const int t = c % WT, u = c / WT;
+        s0 = part[6 * t + u];
+        s1 = part[6 * t + 3 + u];
+      } else {
+        for (int g = 0; g < G; ++g) {  // fixed order: deterministic
+          s0 += part[6 * (c * G + g) + 0];
+          s1 += part[6 * (c * G + g) + 3];
+        }
+      }
+      acc[(c < kP0) ? a.slot_t0 + c : a.slot_t1 + (c - kP0)] = s0;
+      if (MODE == kNtFold && a.slot_t2 >= 0) acc[a.slot_t2 + c] = s1;
+    }
+  }
+  if (tid < 4) {  // scalar reductions of the epilogue threads, fixed order
+    const int slot = tid == 0 ? a.slot_r0 : tid == 1 ? a.slot_r1 : tid == 2 ? a.slot_r2 : a.slot_r3;
+    if (slot >= 0) {
+      double v = 0.0;
+      for (int t = 0; t < rs; ++t) v += sc[tid * kNtConsumers + t];
+      acc[slot] = v;
+    }
+  }
+  if (bad && MODE == kNtGin) {
+    atomicMin(a.status + kStBadStep, a.epi.step);
+    atomicOr(a.status + kStAbort, 1);
+  }
+  flush_row(acc, a.nslots, a.out);
+}
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kNtThreads, 1) k_nt(const __grid_constant__ NtArgs<T> a) {
+  k_nt_impl<T, MODE>(a);
+}
+
+}  // namespace hd

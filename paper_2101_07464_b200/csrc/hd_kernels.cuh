@@ -1128,6 +1128,13 @@ struct SmallArgs {
   // right after the wait); it then starts when this stage exits, and its
   // early TMA prefetch no longer competes with the stage (HD_LATE_LAUNCH)
   int late_launch = 0;
+  // two-pass Ginibre (hd_gin2p.cuh): the K1 dots came from the previous output
+  // pass with right-hand side y while the probe input is x = y * (*xscale)
+  // (lazily normalised): dots scale by it, the sum of squares by its square
+  const double* xscale = nullptr;
+  // ... and k_small_gin's draw dots from the previous fold pass without the
+  // cumulative-sign diagonal (every unmasked row sees D = Dtail of chain B)
+  int ag_dtail = 0;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -1406,6 +1413,16 @@ __device__ __forceinline__ void k_small_dots_impl(const SmallArgs& a) {
     }
   }
   __syncthreads();
+  if (!HAAR && a.xscale) {  // two-pass Ginibre: x = y * xscale
+    const double xs = *a.xscale;
+    #pragma unroll 1
+    for (int t = tid; t < a.kA + a.kB + 1; t += kSmallThreads) {
+      if (t < a.kA) aA[t] *= xs;
+      else if (t < a.kA + a.kB) aB[t - a.kA] *= xs;
+      else m.sc[0] *= xs * xs;
+    }
+    __syncthreads();
+  }
   HD_CLK(a, 11);
   HD_STAMP(a, 2);
   if (tid < kHalf) {
@@ -1667,9 +1684,10 @@ __device__ __forceinline__ void k_small_gin_impl(const SmallArgs& a) {
   __syncthreads();
   {  // both reductions in one pass (see st_sum_slot)
     const int e0 = a.kB, e1 = e0 + (a.pendB >= 0 ? a.pendB + 1 : 0);
+    const double dt = a.ag_dtail ? *a.chB.Dtail : 1.0;
     #pragma unroll 1
     for (int t = tid; t < e1; t += kSmallThreads) {
-      if (t < e0) ag[t] = st_sum_slot(ps, a.nblk, a.slotB_dot + t);
+      if (t < e0) ag[t] = dt * st_sum_slot(ps, a.nblk, a.slotB_dot + t);
       else pB[t - e0] = st_sum_slot(ps, a.nblk, a.slotB_pend + t - e0);
     }
   }
@@ -1725,6 +1743,89 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_gin(const __grid_consta
 template <typename T>
 __global__ void __launch_bounds__(kSmallThreads) k_small_gin_b(const SmallArgs* __restrict__ argv) {
   k_small_gin_impl<T>(argv[blockIdx.y]);
+}
+
+// Two-pass Ginibre (hd_gin2p.cuh), after k_nt<FOLD>: finalise the fold
+// reflector H(p, off) (k_small_fold) AND its compact-WY T column at once: the
+// Gram column W_F^T w_new came out of the same pass for rows > off; the
+// pivot row's term W_F[off, j] * w_new[off] (w_new[off] is fixed here, after
+// the norm) is added from the panel row. No pending column is left behind.
+template <typename T>
+__device__ __forceinline__ void k_small_fold2_impl(const SmallArgs& a) {
+  extern __shared__ double ssm[];
+  const int kv = small_kv(a.kA, 0);
+  const SmallSmem m = small_smem(ssm, kv);
+  double* gram = m.v0;  // reduced Gram dots (rows > off)
+  double* sgA = m.v1;
+  double* rowA = m.v2;  // W_F[off, j]
+  double* gcol = m.v3;  // new G column
+  double* tcol = m.v4;
+  T* rowT = reinterpret_cast<T*>(m.v5);
+  const int tid = threadIdx.x;
+  double* tsA = m.sc + 16;
+  double* ps = tsA + (a.stageA ? (size_t)a.kA * (a.kA | 1) : 0);  // [nslots_in][nblk]
+  int* st = reinterpret_cast<int*>(m.sc + 12);
+  const T* PA = (const T*)a.PA;
+  // ---- phase 1: what earlier launches wrote before griddepcontrol.wait
+  const TView tvA = a.stageA ? st_stage_T(a.chA, a.kA, tsA, tid, kSmallThreads) : TView{a.chA.Tm, a.chA.K};
+  #pragma unroll 1
+  for (int j = tid; j < a.kA; j += kSmallThreads) {
+    cp_async8(sgA + j, a.chA.sig + j);
+    cp_async_elem(rowT + j, PA + paddr(a.off, j, a.chA.K));
+  }
+  if (tid == 0) {
+    cp_async8(m.sc + 8, a.scal + kScEscale);
+    cp_async8(m.sc + 9, a.scal + kScIscale);
+  }
+  pdl_wait();
+  if (!a.late_launch) pdl_launch();
+  st_stage(a.partials, (int64_t)a.nslots_in * a.nblk, ps, tid, kSmallThreads);
+  if (tid == 0) {
+    cp_async8(m.sc + 1, a.head + a.off);
+    cp_async4(st, a.status + kStAbort);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (st[0] != 0) return;
+  #pragma unroll 1
+  for (int t = tid; t <= a.kA; t += kSmallThreads) {
+    if (t < a.kA) {
+      gram[t] = st_sum_slot(ps, a.nblk, a.slotA_pend + t);
+      rowA[t] = (double)rowT[t];
+    } else {
+      m.sc[0] = sqrt(st_sum_slot(ps, a.nblk, a.fold_slot_ss));
+    }
+  }
+  __syncthreads();
+  const double nrm = m.sc[0], piv = m.sc[1];
+  if (tid == 0) {
+    const double sign = st_reflector<T>(a.chA, (T*)a.PA, a.kA, a.off, nrm, piv, a.rule, m.sc[8], m.sc[9],
+                                        a.append != 0);
+    const double zoff = (nrm == 0.0) ? piv : (sign == 0.0 ? 0.0 : nrm);
+    a.scal[kScNrm] = nrm;
+    a.scal[kScCoefCur] = a.append ? zoff : piv;
+    a.scal[kScSign] = sign;
+    m.sc[3] = sign;
+    m.sc[4] = (nrm == 0.0) ? 0.0 : (double)(T)((piv + sign * nrm) * m.sc[8]);  // the stored pivot entry
+    m.sc[5] = (nrm == 0.0) ? 0.0 : m.sc[9] / nrm;                              // sig of the new column
+    m.sc[6] = (nrm == 0.0) ? 0.0 : a.chA.c[a.kA];
+  }
+  __syncthreads();
+  if (a.append && nrm != 0.0) st_D_update(a.chA, a.off, -m.sc[3], tid, kSmallThreads);
+  const double wfix = m.sc[4], signew = m.sc[5], cnew = m.sc[6];
+  const int k = a.kA;
+  #pragma unroll 1
+  for (int j = tid; j < k; j += kSmallThreads) {
+    gcol[j] = sgA[j] * signew * (gram[j] + rowA[j] * wfix);
+    a.chA.G[j + (int64_t)k * a.chA.K] = gcol[j];
+  }
+  if (tid == 0) a.chA.G[k + (int64_t)k * a.chA.K] = (nrm == 0.0) ? 0.0 : 2.0 / cnew;
+  __syncthreads();
+  st_T_column(a.chA, tvA, k, cnew, gcol, tcol, 0, kSmallThreads / 32);
+}
+template <typename T>
+__global__ void __launch_bounds__(kSmallThreads) k_small_fold2(const __grid_constant__ SmallArgs a) {
+  k_small_fold2_impl<T>(a);
 }
 
 // Normalize dynamics: inv = ||y|| > 0 ? 1/||y|| : 1 (bench.cpp:25-28).
@@ -1783,6 +1884,9 @@ struct AppArgs {
   double* scal = nullptr;
   int* status = nullptr;
   int step = 0;
+  // partials layout: [block][nred] (k_ginout epilogue) or, when strided,
+  // group partials [slot0 + r][nblk] (two-pass Ginibre output pass)
+  int strided = 0, slot0 = 0;
 };
 
 __device__ __forceinline__ void k_app_scalars_impl(const AppArgs& a) {
@@ -1793,8 +1897,13 @@ __device__ __forceinline__ void k_app_scalars_impl(const AppArgs& a) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double v0 = 0.0, v1 = 0.0;
   for (int b = threadIdx.x; b < a.nblk; b += kSmallThreads) {
-    v0 += a.partials[(size_t)b * a.nred];
-    if (a.nred > 1) v1 += a.partials[(size_t)b * a.nred + 1];
+    if (a.strided) {
+      v0 += a.partials[(size_t)a.slot0 * a.nblk + b];
+      if (a.nred > 1) v1 += a.partials[(size_t)(a.slot0 + 1) * a.nblk + b];
+    } else {
+      v0 += a.partials[(size_t)b * a.nred];
+      if (a.nred > 1) v1 += a.partials[(size_t)b * a.nred + 1];
+    }
   }
   v0 = warp_sum(v0);
   v1 = warp_sum(v1);

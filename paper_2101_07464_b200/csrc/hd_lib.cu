@@ -8,6 +8,8 @@
 //   GOEOperator::probe       include/lazymat/ensembles.hpp:117-127
 //   run_dynamics             include/lazymat/dynamics.hpp:42-76
 //   check_probe_input        include/lazymat/operators.hpp:44-48
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include "hd_complex.cuh"
@@ -31,6 +33,7 @@
 #include "../../include/hd.h"
 #include "hd_kernels.cuh"
 #include "hd_fused.cuh"
+#include "hd_gin2p.cuh"
 
 using namespace hd;
 
@@ -180,6 +183,8 @@ struct hd_op {
   size_t partsF_cap = 0, partsO_cap = 0;
   double* specbuf = nullptr;    // [K] reduced speculative dots
   FlushBufs fbD, fbF, fbO;      // group partials / per-CTA scratch / tickets
+  FlushBufs fbA[2], fbB;        // two-pass Ginibre: fold passes (ping-pong) and output passes
+  bool gin2p = true;            // two-pass Ginibre / GOE runs (HD_GIN2P=0 disables)
   size_t flush_slots = 0;       // slot capacity of the buffers above
   double* red = nullptr;
   size_t red_cap = 0;
@@ -433,7 +438,7 @@ void ensure_capacity(hd_op* op, int64_t nr, int64_t nl) {
   const size_t groups = ceil_div((int64_t)blocks, kGroup);
   const size_t slots = (size_t)(4 * K + 16);
   if (slots > op->flush_slots) {
-    for (FlushBufs* fb : {&op->fbD, &op->fbF, &op->fbO}) {
+    for (FlushBufs* fb : {&op->fbD, &op->fbF, &op->fbO, &op->fbA[0], &op->fbA[1], &op->fbB}) {
       double* np = dmalloc<double>(slots * groups);
       if (fb->partials && fb == &op->fbO)
         ck(cudaMemcpy(np, fb->partials, sizeof(double) * op->flush_slots * groups, cudaMemcpyDeviceToDevice), "keep");
@@ -755,8 +760,11 @@ const double* inj_at(const hd_op* op, int64_t pos) { return op->inj + (pos - op-
 
 // Append `len` draws (host or device pointer) to the queue.
 void inj_append(hd_op* op, const double* g, int64_t len, bool on_device) {
-  if (op->inj_size + len > op->inj_cap) {
-    const int64_t ncap = std::max<int64_t>(op->inj_cap * 2, op->inj_size + len);
+  // slack of one padded row range: the two-pass kernels bulk-copy whole
+  // sub-tiles of a probe's draws (rows past the dimension are masked)
+  const int64_t slack = op->io_len;
+  if (op->inj_size + len + slack > op->inj_cap) {
+    const int64_t ncap = std::max<int64_t>(op->inj_cap * 2, op->inj_size + len + slack);
     double* np = dmalloc<double>(ncap);
     if (op->inj_size > 0)
       ck(cudaMemcpyAsync(np, op->inj, sizeof(double) * op->inj_size, cudaMemcpyDeviceToDevice, op->stream), "grow");
