@@ -34,15 +34,29 @@
 
 namespace hd {
 
-constexpr int kNtConsumers = 256;                   // 8 consumer warps
+constexpr int kNtConsumers = 352;                   // 11 consumer warps (1-2 epilogue, the rest workers)
 constexpr int kNtThreads = kNtConsumers + 32;       // + 1 producer warp
 constexpr int kNtMaxMaps = 4;
 constexpr int kNtMaxVecs = 5;
 constexpr int kNtMaxStages = 16;
-constexpr int kNtMaxCols = 512;                     // columns of a pass (T-phase: <= 2 per consumer)
+constexpr int kNtMaxCols = 512;                     // columns of an output pass
+constexpr int kNtGinRounds = 16;                    // T-phase column rounds: output pass (>= 512 / (288 / 8))
+constexpr int kNtFoldRounds = 8;                    // ... fold pass (F columns <= 8 x 36 = 288)
 constexpr int kNtBarId = 1;                         // named barrier of the consumer warps
 
 enum NtMode : int { kNtFold = 0, kNtGin = 1 };
+// Compile-time output-pass epilogue (the map and where the T phase's
+// right-hand side comes from): one kernel instance per kind, no runtime
+// branching on the map in the row-serial epilogue.
+enum NtEpi : int {
+  kEkPlain = 0,  // plain / normalize map, T rhs = y
+  kEkSrc = 1,    // plain map, T rhs = a given vector (GOE inner right: the step's x)
+  kEkTanh = 2,
+  kEkAmpInit = 3,
+  kEkAmpX = 4,
+  kEkAmpZ = 5,
+  kEkSpike = 6,
+};
 enum NtRhs : int { kRhsEpi = 0, kRhsSrc = 1 };
 
 // One 3-D TMA box family: panel `panel`, stage columns [scol, scol + cols),
@@ -111,6 +125,7 @@ struct NtArgs {
   Flush out;
   int* status = nullptr;
   int prefetch = 0;
+  unsigned long long* trace = nullptr;  // HD_TRACE=3: [8][grid] cycle counters
 };
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
@@ -153,6 +168,20 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
   }
 }
 
+// mbarrier wait that suspends the thread (suspend-time hint) instead of
+// spinning: the producer warp waits for a stage to drain most of the time.
+__device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITS_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITS_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -165,8 +194,8 @@ __device__ __forceinline__ double ld_vec(const unsigned char* slot, int esz, int
 
 // Warp roles of a k_nt CTA (kNtThreads = 9 warps):
 //   warps [0, E)      epilogue warps: one sub-tile row per thread (rs <= 32 E)
-//   warps [E, 8)      workers: GEMV-N of sub-tile j + 1 and GEMV-T of j - 1
-//   warp 8            producer: the TMA ring
+//   warps [E, 11)     workers: GEMV-N of sub-tile j + 1 and GEMV-T of j - 1
+//   warp 11           producer: the TMA ring
 // In "slot" j the epilogue warps finish sub-tile j while the workers run the
 // N phase of j + 1 and the T phase of j - 1 — one barrier per slot, so the
 // row-serial epilogue is off the critical path.
@@ -175,14 +204,13 @@ __host__ __device__ inline int nt_workers(int rs) { return kNtConsumers - 32 * n
 
 // Shared-memory carve-up (sized per launch): [stages][stage_bytes] | beta1
 // [kP0] | beta3 [kP0] | coefS [C - kP0] | N-phase partials [2][1 or 3][2 WT] |
-// rhs [2][2][rs] | Philox draw batches [2][2 WT] | barriers. The T-phase
+// rhs [2][2][rs] | barriers. The T-phase
 // partials, the scalar partials and the slot row reuse the stages at the end.
 struct NtSmem {
   unsigned char* stages;
   double *b1, *b3, *bs;   // bs is indexed by the stage column (c >= kP0)
   double* red;
   double* rhs;
-  double* draw;
   uint64_t* full;
   uint64_t* empty;
 };
@@ -190,7 +218,7 @@ struct NtSmem {
 __host__ __device__ inline size_t nt_fixed_doubles(int mode, int C, int kP0, int rs) {
   const size_t b = (size_t)((kP0 + 1) & ~1) + (mode == kNtGin ? (size_t)((kP0 + 1) & ~1) + (size_t)((C - kP0 + 1) & ~1) : 0);
   const size_t wt2 = 2 * (size_t)nt_workers(rs);
-  return b + 2 * (mode == kNtGin ? 3 : 1) * wt2 + 4 * (size_t)rs + 2 * wt2;
+  return b + 2 * (mode == kNtGin ? 3 : 1) * wt2 + 4 * (size_t)rs;
 }
 
 __host__ __device__ inline size_t nt_fixed_bytes(int mode, int C, int kP0, int rs, int nst) {
@@ -200,7 +228,7 @@ __host__ __device__ inline size_t nt_fixed_bytes(int mode, int C, int kP0, int r
 // Bytes of the stage ring the final flush reuses: T partials [WT][6], scalar
 // partials [4][kNtConsumers], the slot row.
 __host__ __device__ inline size_t nt_flush_bytes(int nslots) {
-  return sizeof(double) * (6 * (size_t)kNtConsumers + 4 * (size_t)kNtConsumers + (size_t)nslots + 8);
+  return sizeof(double) * (4 * (size_t)kNtConsumers + (size_t)nslots + 8);
 }
 
 __device__ __forceinline__ NtSmem nt_smem(unsigned char* base, int mode, int C, int kP0, int rs, int nst,
@@ -219,20 +247,20 @@ __device__ __forceinline__ NtSmem nt_smem(unsigned char* base, int mode, int C, 
   const int wt2 = 2 * nt_workers(rs);
   m.red = p; p += 2 * (mode == kNtGin ? 3 : 1) * wt2;
   m.rhs = p; p += 4 * rs;
-  m.draw = p; p += 2 * wt2;
   m.full = reinterpret_cast<uint64_t*>(p);
   m.empty = m.full + nst;
   return m;
 }
 
-template <typename T, int MODE>
+template <typename T, int MODE, int RS, int EK>
 __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const NtSmem m = nt_smem(smem, MODE, a.C, a.kP0, a.rs, a.nst, a.stage_bytes);
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const bool producer = (w == kNtConsumers / 32);
-  const int rs = a.rs, C = a.C, nst = a.nst;
-  const int E = nt_ewarps(rs), WT = nt_workers(rs);
+  constexpr int rs = RS;
+  const int C = a.C, nst = a.nst;
+  constexpr int E = (RS <= 32) ? 1 : RS / 32, WT = kNtConsumers - 32 * E;
   const bool epi_thr = !producer && tid < 32 * E;
   const bool worker = !producer && !epi_thr;
   const int wt = tid - 32 * E;  // worker index
@@ -281,7 +309,7 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
     uint32_t ph = (uint32_t)((k / nst) & 1);  // phase of the empty barrier to wait for: use (k / nst) - 1
     if (!abort_all) {
       for (; k < nk; ++k) {
-        if (k >= nst) mbar_wait(m.empty + q, ph ^ 1u);
+        if (k >= nst) mbar_wait_suspend(m.empty + q, ph ^ 1u);
         issue(k, q);
         if (++q == nst) {
           q = 0;
@@ -302,19 +330,28 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
     if (MODE == kNtGin)
       for (int c = kP0 + tid; c < C; c += kNtConsumers) m.bs[c] = a.coefS[c - kP0];
   }
-  // worker T-phase mapping: C >= WT: columns wt, wt + WT, wt + 2 WT; else
-  // G (a power of two) workers per column, column c = wt / G, phase g = wt % G
-  int G = (C >= WT || C == 0) ? 1 : min(WT / C, rs / 2);
-  while (G & (G - 1)) G &= G - 1;
-  const int c0 = (C >= WT) ? wt : wt / G, tg = (C >= WT) ? 0 : wt % G;
-  const int c1 = (C >= WT && wt + WT < C) ? wt + WT : -1;
-  const int c2 = (C >= WT && wt + 2 * WT < C) ? wt + 2 * WT : -1;
-  const bool t_active = worker && C > 0 && c0 < C && a.do_t;
-  double tA0 = 0.0, tA1 = 0.0, tA2 = 0.0, tB0 = 0.0, tB1 = 0.0, tB2 = 0.0;
+  // worker T-phase mapping: 8 consecutive lanes share a column (lane g of the
+  // 8 takes row pairs g, g + 8, ... of the sub-tile: 128 contiguous bytes per
+  // quarter warp, conflict-free, and each right-hand-side pair is loaded once
+  // for all of the thread's columns); the thread's columns are
+  // cb + r NCOL, r < R (NCOL = WT / 8 columns per round)
+  constexpr int NCOL = WT / 8;
+  const int cb = wt >> 3, tg8 = wt & 7;
+  const int Rt = (C > cb) ? (C - cb + NCOL - 1) / NCOL : 0;  // this thread's column rounds
+  const bool t_active = worker && C > 0 && a.do_t;
+  constexpr int RMAX = (MODE == kNtFold) ? kNtFoldRounds : kNtGinRounds;
+  double tA[RMAX], tB[RMAX];
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) {
+    tA[r] = 0.0;
+    tB[r] = 0.0;
+  }
   // worker N-phase mapping: row pair nrp, column group ncg (CG groups)
-  const int RP = rs / 2;
-  const int CG = WT / RP;
+  constexpr int RP = RS / 2;
+  constexpr int CG = WT / RP;
   const int nrp = wt % RP, ncg = wt / RP;
+  constexpr int NP = (RP >= 32) ? CG : WT / 32;         // N-phase partials per row
+  const int npart = (RP >= 32) ? ncg : (wt >> 5);         // this thread's partial index
   const int cga = (int)((int64_t)C * ncg / CG), cgb = (int)((int64_t)C * (ncg + 1) / CG);
   const int nred = (MODE == kNtGin) ? 3 : 1;
   const int red_stride = 2 * WT;  // one partial array: CG x rs = 2 WT doubles
@@ -331,25 +368,6 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
     if (a.rhs_scale) rsc = *a.rhs_scale;
     if (a.epi.sc) esc = *a.epi.sc;
   }
-  const bool need_draw = (MODE == kNtGin) ? (a.g.kind == kSrcPhilox) : (a.spec.kind == kSrcPhilox);
-  const Src<T>& dsrc = (MODE == kNtGin) ? a.g : a.spec;
-  // Philox batches: batch b covers the CTA's sub-tiles [b CG, (b + 1) CG),
-  // one row pair per worker (sub-tile q = wt / RP, pair wt % RP)
-  auto gen_batch = [&](int64_t b) {
-    if (!need_draw || !worker) return;
-    const int64_t k = b * CG + ncg;
-    if (k >= nk) return;
-    const int64_t i = row_of(k) + a.rm.gdelta + 2 * nrp;
-    const double2 v = philox_normal_pair(*dsrc.seedp, dsrc.stream, dsrc.probe, (uint64_t)(i >> 1));
-    double vx = v.x, vy = v.y;
-    if constexpr (sizeof(T) == 4) {
-      vx = (double)(float)vx;
-      vy = (double)(float)vy;
-    }
-    double* d = m.draw + (b & 1) * 2 * WT;
-    d[2 * wt] = vx;
-    d[2 * wt + 1] = vy;
-  };
   auto stage_ptr = [&](int q) { return m.stages + (size_t)q * a.stage_bytes; };
   // ---- N phase of sub-tile k (stage q): workers -> red[k & 1]
   auto nphase = [&](int64_t k, int q, uint32_t ph) {
@@ -378,50 +396,76 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
         ns.y = fma(v.y, b, ns.y);
       }
     }
-    double* red = m.red + (k & 1) * nred * red_stride + ncg * rs + 2 * nrp;  // [cg][rs]
-    *reinterpret_cast<double2*>(red) = n1;
-    if (MODE == kNtGin) {
-      *reinterpret_cast<double2*>(red + red_stride) = n3;
-      *reinterpret_cast<double2*>(red + 2 * red_stride) = ns;
+    // the column groups of one warp (lanes with the same row pair) add up in
+    // a fixed shuffle tree, so the epilogue sums only NP = WT / 32 partials
+    // per row (RS <= 32; RS = 64: one column group per warp, NP = CG)
+#pragma unroll
+    for (int sh = RP; sh < 32; sh <<= 1) {
+      n1.x += __shfl_xor_sync(0xffffffffu, n1.x, sh);
+      n1.y += __shfl_xor_sync(0xffffffffu, n1.y, sh);
+      if (MODE == kNtGin) {
+        n3.x += __shfl_xor_sync(0xffffffffu, n3.x, sh);
+        n3.y += __shfl_xor_sync(0xffffffffu, n3.y, sh);
+        ns.x += __shfl_xor_sync(0xffffffffu, ns.x, sh);
+        ns.y += __shfl_xor_sync(0xffffffffu, ns.y, sh);
+      }
+    }
+    if (RP >= 32 || lane < RP) {
+      double* red = m.red + (k & 1) * nred * red_stride + npart * RS + 2 * nrp;  // [partial][rs]
+      *reinterpret_cast<double2*>(red) = n1;
+      if (MODE == kNtGin) {
+        *reinterpret_cast<double2*>(red + red_stride) = n3;
+        *reinterpret_cast<double2*>(red + 2 * red_stride) = ns;
+      }
     }
   };
   // ---- epilogue of sub-tile k (stage q): epilogue threads, one row each -> rhs[k & 1]
+  unsigned long long epi_tr[2] = {0, 0};  // HD_TRACE=3: epilogue reduction / whole
   auto epilogue = [&](int64_t k, int q, uint32_t ph, int64_t kb, uint32_t bpar) {
-    const int et = tid;
-    if (et >= rs) return;
-    mbar_wait(m.full + q, ph);  // complete (the workers waited for it a slot ago): orders the vector reads
-    const unsigned char* vs = stage_ptr(q) + vec_off;
-    double* rb = m.rhs + (k & 1) * 2 * rs;
+    // LPR lanes per row add the NP column-group partials in fixed order (four
+    // chains each), then combine with a shuffle; lane et < RS runs the row
+    constexpr int LPR = (RS >= 32) ? 1 : 32 / RS;
+    const int et = tid % RS, half = tid / RS;
+    if (tid >= RS * LPR) return;
+    const long long ec0 = (a.trace && tid == 0) ? clock64() : 0;
     const double* red = m.red + (k & 1) * nred * red_stride;
     double r1 = 0.0, r3 = 0.0, rS = 0.0;
-    {  // column-group partials, fixed order (deterministic), two chains each
-      double r1b = 0.0, r3b = 0.0, rSb = 0.0;
-      int g = 0;
-      for (; g + 1 < CG; g += 2) {
-        r1 += red[g * rs + et];
-        r1b += red[(g + 1) * rs + et];
+    {
+      constexpr int per = (NP + LPR - 1) / LPR;
+      const int g0 = half * per, g1 = min(NP, g0 + per);
+      double a1[4] = {0.0, 0.0, 0.0, 0.0}, a3[4] = {0.0, 0.0, 0.0, 0.0}, aS[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+      for (int g = g0; g < g1; ++g) {
+        const int u = (g - g0) & 3;
+        a1[u] += red[g * RS + et];
         if (MODE == kNtGin) {
-          r3 += red[red_stride + g * rs + et];
-          r3b += red[red_stride + (g + 1) * rs + et];
-          rS += red[2 * red_stride + g * rs + et];
-          rSb += red[2 * red_stride + (g + 1) * rs + et];
+          a3[u] += red[red_stride + g * RS + et];
+          aS[u] += red[2 * red_stride + g * RS + et];
         }
       }
-      if (g < CG) {
-        r1 += red[g * rs + et];
-        if (MODE == kNtGin) {
-          r3 += red[red_stride + g * rs + et];
-          rS += red[2 * red_stride + g * rs + et];
+      r1 = (a1[0] + a1[1]) + (a1[2] + a1[3]);
+      r3 = (a3[0] + a3[1]) + (a3[2] + a3[3]);
+      rS = (aS[0] + aS[1]) + (aS[2] + aS[3]);
+      if (LPR > 1) {
+        for (int sh = RS; sh < 32; sh <<= 1) {
+          r1 += __shfl_xor_sync(0xffffffffu, r1, sh);
+          if (MODE == kNtGin) {
+            r3 += __shfl_xor_sync(0xffffffffu, r3, sh);
+            rS += __shfl_xor_sync(0xffffffffu, rS, sh);
+          }
         }
       }
-      r1 += r1b;
-      r3 += r3b;
-      rS += rSb;
     }
+    if (half != 0) return;
+    if (a.trace && tid == 0) epi_tr[0] += clock64() - ec0;
+    const unsigned char* vs = stage_ptr(q) + vec_off;
+    double* rb = m.rhs + (k & 1) * 2 * rs;
+    mbar_wait(m.full + q, ph);  // complete (the workers waited for it a slot ago): orders the vector reads
     const int64_t li = row_of(k) + et;
     const int64_t i = li + a.rm.gdelta;
     const double d = (i < a.Dlen) ? a.D[i] : dtail;
-    const double* draw = m.draw + bpar * 2 * WT + kb * rs + et;
+    (void)kb;
+    (void)bpar;
     if (MODE == kNtFold) {
       const double xv = ld_vec<T>(vs + (size_t)a.vx * rs * 8, sizeof(T), et) * xsc;
       const double p = (i < a.n) ? d * (xv - r1) : 0.0;
@@ -433,7 +477,8 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
       const double g_rhs0 = (i > a.off) ? (double)(T)wv : 0.0;  // Gram RHS (the stored values)
       double g_rhs1 = 0.0;
       if (a.spec.kind != kSrcNone && i < a.n && i >= a.spec.mask_begin) {
-        g_rhs1 = (a.spec.kind == kSrcPhilox) ? *draw : a.spec.inj[i];  // injected: parity mode only
+        // device draws: pre-generated vector (k_draw_fill); injected: parity mode only
+        g_rhs1 = (a.spec.kind == kSrcPhilox) ? ld_vec<T>(vs + (size_t)a.vspec * RS * 8, 8, et) : a.spec.inj[i];
         if constexpr (sizeof(T) == 4) g_rhs1 = (double)(float)g_rhs1;
       }
       e1 += g_rhs0 * g_rhs1;  // new column . next draw
@@ -442,7 +487,7 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
     } else {
       double gv = 0.0;
       if (i < a.n && i >= a.g.mask_begin) {
-        gv = (a.g.kind == kSrcPhilox) ? *draw : a.g.inj[i];  // injected: parity mode only
+        gv = (a.g.kind == kSrcPhilox) ? ld_vec<T>(vs + (size_t)a.vg * RS * 8, 8, et) : a.g.inj[i];
         if constexpr (sizeof(T) == 4) gv = (double)(float)gv;
         gv *= d;
       }
@@ -454,22 +499,23 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
       const Epi<T>& e = a.epi;
       const int64_t vi = i - a.rm.vbase;
       double out = 0.0;
+      constexpr int kind = (EK == kEkAmpInit) ? kEpiAmpInit : (EK == kEkAmpX) ? kEpiAmpX
+                           : (EK == kEkAmpZ) ? kEpiAmpZ : (EK == kEkSpike) ? kEpiSpike : kEpiPlain;
       if (i < a.n) {
-        if (e.yadd) y = (ld_vec<T>(vs + (size_t)a.vyadd * rs * 8, sizeof(T), et) + y) * e.add_scale;
-        if (e.kind >= kEpiAmpInit) {
-          const double stv =
-              (e.state && e.kind != kEpiAmpInit) ? ld_vec<T>(vs + (size_t)a.vstate * rs * 8, sizeof(T), et) : 0.0;
-          const double axv = e.aux ? ld_vec<T>(vs + (size_t)a.vaux * rs * 8, sizeof(T), et) : 0.0;
+        if (e.yadd) y = (ld_vec<T>(vs + (size_t)a.vyadd * RS * 8, sizeof(T), et) + y) * e.add_scale;
+        if constexpr (EK >= kEkAmpInit) {
+          const double stv = (EK != kEkAmpInit) ? ld_vec<T>(vs + (size_t)a.vstate * RS * 8, sizeof(T), et) : 0.0;
+          const double axv = ld_vec<T>(vs + (size_t)a.vaux * RS * 8, sizeof(T), et);
           double q0, q1;
-          const double o = epi_row(e.kind, y, stv, axv, esc, q0, q1);
-          if (e.state) e.state[vi] = (T)o;
-          if (e.kind == kEpiAmpInit || e.kind == kEpiSpike) y = o;
+          const double o = epi_row(kind, y, stv, axv, esc, q0, q1);
+          if (EK != kEkSpike) e.state[vi] = (T)o;
+          if (EK == kEkAmpInit || EK == kEkSpike) y = o;
           out = (double)(T)o;
           e2 += q0;
           e3 += q1;
           bad |= !isfinite(o);
-        } else if (e.kind == kEpiTanhMix) {
-          double xp = e.xprev ? ld_vec<T>(vs + (size_t)a.vxprev * rs * 8, sizeof(T), et) : 0.0;
+        } else if constexpr (EK == kEkTanh) {
+          double xp = e.xprev ? ld_vec<T>(vs + (size_t)a.vxprev * RS * 8, sizeof(T), et) : 0.0;
           if (e.xprev_scale) xp *= *e.xprev_scale;
           const double o = tanh(2.0 * y) + 0.1 * xp;
           e.xnext[vi] = (T)o;
@@ -482,83 +528,48 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
         }
         if (e.y) e.y[vi] = (T)y;
       }
-      const double rhs =
-          (a.rhs_mode == kRhsSrc) ? ((i < a.n) ? ld_vec<T>(vs + (size_t)a.vrhs * rs * 8, sizeof(T), et) * rsc : 0.0)
-                                  : out;
+      double rhs = out;
+      if constexpr (EK == kEkSrc) rhs = (i < a.n) ? ld_vec<T>(vs + (size_t)a.vrhs * RS * 8, sizeof(T), et) * rsc : 0.0;
       e0 += rhs * rhs;  // ||x_{t+1}||^2 (the next probe's K1 sum of squares)
       e1 += uu * rhs;   // new S column . x_{t+1}
       rb[et] = rhs;
     }
+    if (a.trace && tid == 0) epi_tr[1] += clock64() - ec0;
   };
-  // ---- T phase of sub-tile k (stage q): workers; column loads of 2 rows,
-  // the row pair XOR-rotated by the lane (a quarter warp reads 8 distinct
-  // 16-B chunks: conflict-free); small C: G workers per column split the pairs
+  // ---- T phase of sub-tile k (stage q): workers (mapping above)
   auto tphase = [&](int64_t k, int q) {
     if (!t_active) return;
-    const T* sp = reinterpret_cast<const T*>(stage_ptr(q));
-    const double* r0 = m.rhs + (k & 1) * 2 * rs;
-    const T* pc0 = sp + (size_t)c0 * rs;
-    if (G == 1) {
-      const int pm = RP - 1;
-      const T* pc1 = sp + (size_t)(c1 >= 0 ? c1 : 0) * rs;
-      const T* pc2 = sp + (size_t)(c2 >= 0 ? c2 : 0) * rs;
-      double2 a0 = make_double2(0.0, 0.0), a1 = a0, a2 = a0, b0 = a0, b1 = a0, b2 = a0;
-#pragma unroll 4
-      for (int jp = 0; jp < RP; ++jp) {
-        const int o = 2 * ((jp ^ lane) & pm);
-        const double2 x = *reinterpret_cast<const double2*>(r0 + o);
-        double2 z = make_double2(0.0, 0.0);
-        if (MODE == kNtFold) z = *reinterpret_cast<const double2*>(r0 + rs + o);
-        const double2 v = lds_pair(pc0 + o);
-        a0.x = fma(v.x, x.x, a0.x);
-        a0.y = fma(v.y, x.y, a0.y);
-        if (MODE == kNtFold) {
-          b0.x = fma(v.x, z.x, b0.x);
-          b0.y = fma(v.y, z.y, b0.y);
-        }
-        if (c1 >= 0) {
-          const double2 u = lds_pair(pc1 + o);
-          a1.x = fma(u.x, x.x, a1.x);
-          a1.y = fma(u.y, x.y, a1.y);
-          if (MODE == kNtFold) {
-            b1.x = fma(u.x, z.x, b1.x);
-            b1.y = fma(u.y, z.y, b1.y);
-          }
-        }
-        if (c2 >= 0) {
-          const double2 u = lds_pair(pc2 + o);
-          a2.x = fma(u.x, x.x, a2.x);
-          a2.y = fma(u.y, x.y, a2.y);
-          if (MODE == kNtFold) {
-            b2.x = fma(u.x, z.x, b2.x);
-            b2.y = fma(u.y, z.y, b2.y);
-          }
-        }
-      }
-      tA0 += a0.x + a0.y;
-      tA1 += a1.x + a1.y;
-      tA2 += a2.x + a2.y;
-      tB0 += b0.x + b0.y;
-      tB1 += b1.x + b1.y;
-      tB2 += b2.x + b2.y;
-    } else {
-      const int npg = RP / G;  // row pairs per phase (a power of two)
-      double2 a0 = make_double2(0.0, 0.0), b0 = a0;
-      for (int jp = 0; jp < npg; ++jp) {
-        const int o = 2 * (tg * npg + ((jp ^ c0) & (npg - 1)));
-        const double2 x = *reinterpret_cast<const double2*>(r0 + o);
-        const double2 v = lds_pair(pc0 + o);
-        a0.x = fma(v.x, x.x, a0.x);
-        a0.y = fma(v.y, x.y, a0.y);
-        if (MODE == kNtFold) {
-          const double2 z = *reinterpret_cast<const double2*>(r0 + rs + o);
-          b0.x = fma(v.x, z.x, b0.x);
-          b0.y = fma(v.y, z.y, b0.y);
-        }
-      }
-      tA0 += a0.x + a0.y;
-      tB0 += b0.x + b0.y;
+    constexpr int PPL = RP / 8;  // row pairs per lane per column
+    const double* r0 = m.rhs + (k & 1) * 2 * RS + 2 * tg8;
+    double2 x[PPL], z[PPL];
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) {
+      x[u] = *reinterpret_cast<const double2*>(r0 + 16 * u);
+      z[u] = make_double2(0.0, 0.0);
+      if (MODE == kNtFold) z[u] = *reinterpret_cast<const double2*>(r0 + RS + 16 * u);
     }
+    const T* pr = reinterpret_cast<const T*>(stage_ptr(q)) + cb * RS + 2 * tg8;
+    // the thread's column rounds, unrolled to the smallest of 4 / 8 / RMAX
+    // that covers them (the accumulators need compile-time indices)
+#define HD_NT_TROUNDS(RM)                                                         \
+  _Pragma("unroll") for (int r = 0; r < (RM); ++r) {                              \
+    if (r < Rt) {                                                                 \
+      _Pragma("unroll") for (int u = 0; u < PPL; ++u) {                           \
+        const double2 v = lds_pair(pr + 16 * u);                                  \
+        tA[r] = fma(v.y, x[u].y, fma(v.x, x[u].x, tA[r]));                        \
+        if (MODE == kNtFold) tB[r] = fma(v.y, z[u].y, fma(v.x, z[u].x, tB[r]));   \
+      }                                                                           \
+    }                                                                             \
+    pr += NCOL * RS;                                                              \
+  }
+    if (Rt <= 4) {
+      HD_NT_TROUNDS(4)
+    } else if (Rt <= 8) {
+      HD_NT_TROUNDS(8)
+    } else {
+      HD_NT_TROUNDS(RMAX)
+    }
+#undef HD_NT_TROUNDS
   };
   // ---- the slot loop (see the warp roles above)
   if (!producer) named_sync(kNtBarId, kNtConsumers);  // coefficients staged
@@ -568,21 +579,45 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
     uint32_t phN = 0, phE = 0;
     int64_t kbE = 0;                     // epilogue: sub-tile index within its draw batch
     uint32_t bparE = 0;                  // ... and the batch buffer it reads
-    gen_batch(0);
     if (worker) nphase(0, 0, 0);
     qN = (nst > 1) ? 1 : 0;
     phN = (nst > 1) ? 0u : 1u;
     named_sync(kNtBarId, kNtConsumers);
+    // HD_TRACE=3: per-CTA cycle breakdown (epilogue thread 0, worker 0)
+    unsigned long long tr[6] = {0, 0, 0, 0, 0, 0};
+    const bool trace = a.trace && (tid == 0 || wt == 0);
     for (int64_t j = 0; j <= nk; ++j) {
+      long long c0t = trace ? clock64() : 0, c1t = 0, c2t = 0, c3t = 0;
       if (epi_thr && j < nk) epilogue(j, qE, phE, kbE, bparE);
       if (worker) {
         if (j + 1 < nk) {
-          if (kbE + 1 == CG) gen_batch((j + 1) / CG);  // the batch the next epilogue starts (its other buffer)
+          if (trace) {
+            c1t = clock64();
+            mbar_wait(m.full + qN, phN);
+            c2t = clock64();
+          }
           nphase(j + 1, qN, phN);
         }
+        if (trace) c3t = clock64();
         if (j >= 1) tphase(j - 1, qT);
       }
+      const long long c4t = trace ? clock64() : 0;
       named_sync(kNtBarId, kNtConsumers);  // red of j + 1, rhs of j ready; stage of j - 1 free
+      if (trace) {
+        const long long c5t = clock64();
+        if (tid == 0) {
+          tr[0] += c4t - c0t;  // epilogue
+          tr[1] += c5t - c4t;  // epilogue warp at the barrier
+        } else {
+          if (c1t) {
+            tr[2] += c1t - c0t;  // draw batches
+            tr[3] += c2t - c1t;  // waiting for the stage
+            tr[4] += c3t - c2t;  // N phase
+          }
+          tr[5] += c4t - c3t;    // T phase
+          tr[1] += c5t - c4t;    // workers at the barrier
+        }
+      }
       if (j >= 1) {
         if (tid == 0) mbar_arrive(m.empty + qT);
         if (++qT == nst) qT = 0;
@@ -600,21 +635,27 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
         phN ^= 1u;
       }
     }
+    if (trace) {
+      if (tid == 0) {
+        a.trace[0 * gridDim.x + blockIdx.x] += tr[0];
+        a.trace[1 * gridDim.x + blockIdx.x] += tr[1];
+        a.trace[8 * gridDim.x + blockIdx.x] += epi_tr[0];
+        a.trace[9 * gridDim.x + blockIdx.x] += epi_tr[1];
+      } else {
+        a.trace[6 * gridDim.x + blockIdx.x] += tr[1];
+        a.trace[2 * gridDim.x + blockIdx.x] += tr[2];
+        a.trace[3 * gridDim.x + blockIdx.x] += tr[3];
+        a.trace[4 * gridDim.x + blockIdx.x] += tr[4];
+        a.trace[5 * gridDim.x + blockIdx.x] += tr[5];
+      }
+      if (tid == 0) a.trace[7 * gridDim.x + blockIdx.x] += (unsigned long long)nk;
+    }
   }
   // ---- partial sums -> slot row (fixed order) -> group flush; the stages
   // are free now: [T partials: 6 x 256][scalar partials: 4 x 256][slot row]
   __syncthreads();
-  double* part = reinterpret_cast<double*>(m.stages);
-  double* sc = part + 6 * kNtConsumers;
+  double* sc = reinterpret_cast<double*>(m.stages);
   double* acc = sc + 4 * kNtConsumers;
-  if (worker) {
-    part[6 * wt + 0] = tA0;
-    part[6 * wt + 1] = tA1;
-    part[6 * wt + 2] = tA2;
-    part[6 * wt + 3] = tB0;
-    part[6 * wt + 4] = tB1;
-    part[6 * wt + 5] = tB2;
-  }
   if (!producer) {
     sc[tid] = e0;
     sc[kNtConsumers + tid] = e1;
@@ -623,21 +664,23 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
   }
   for (int sl = tid; sl < a.nslots; sl += kNtThreads) acc[sl] = 0.0;
   __syncthreads();
-  if (C > 0 && a.do_t) {
-    for (int c = tid; c < C; c += kNtThreads) {
-      double s0 = 0.0, s1 = 0.0;
-      if (C >= WT) {
-        const int t = c % WT, u = c / WT;
-        s0 = part[6 * t + u];
-        s1 = part[6 * t + 3 + u];
-      } else {
-        for (int g = 0; g < G; ++g) {  // fixed order: deterministic
-          s0 += part[6 * (c * G + g) + 0];
-          s1 += part[6 * (c * G + g) + 3];
-        }
+  if (worker && C > 0 && a.do_t) {  // each column's 8 lanes add up (fixed shuffle tree), lane g = 0 stores
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) {
+      double va = tA[r], vb = tB[r];
+      va += __shfl_xor_sync(0xffffffffu, va, 1);
+      va += __shfl_xor_sync(0xffffffffu, va, 2);
+      va += __shfl_xor_sync(0xffffffffu, va, 4);
+      if (MODE == kNtFold) {
+        vb += __shfl_xor_sync(0xffffffffu, vb, 1);
+        vb += __shfl_xor_sync(0xffffffffu, vb, 2);
+        vb += __shfl_xor_sync(0xffffffffu, vb, 4);
       }
-      acc[(c < kP0) ? a.slot_t0 + c : a.slot_t1 + (c - kP0)] = s0;
-      if (MODE == kNtFold && a.slot_t2 >= 0) acc[a.slot_t2 + c] = s1;
+      const int c = cb + r * NCOL;
+      if (tg8 == 0 && r < Rt && c < C) {
+        acc[(c < kP0) ? a.slot_t0 + c : a.slot_t1 + (c - kP0)] = va;
+        if (MODE == kNtFold && a.slot_t2 >= 0) acc[a.slot_t2 + c] = vb;
+      }
     }
   }
   if (tid < 4) {  // scalar reductions of the epilogue threads, fixed order
@@ -655,9 +698,26 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
   flush_row(acc, a.nslots, a.out);
 }
 
-template <typename T, int MODE>
+// The device draw of one probe (Philox4x32-10 + Box-Muller, the stream every
+// streaming kernel regenerates: philox_normal_pair) written once for rows
+// [0, rows) of a (local) dimension, global row = local row + gdelta; the two
+// passes that need it read it as a bulk-copied vector instead of each
+// regenerating the fp64 transcendentals inside their streams.
+__global__ void __launch_bounds__(256) k_draw_fill(const unsigned long long* seedp, uint32_t stream, uint32_t probe,
+                                                   int64_t rows, int64_t gdelta, double* out) {
+  pdl_wait();
+  pdl_launch();
+  const uint64_t seed = *seedp;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 2 * q < rows; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = 2 * q + gdelta;  // gdelta is even (tile-aligned)
+    const double2 v = philox_normal_pair(seed, stream, probe, (uint64_t)(i >> 1));
+    *reinterpret_cast<double2*>(out + 2 * q) = v;
+  }
+}
+
+template <typename T, int MODE, int RS, int EK>
 __global__ void __launch_bounds__(kNtThreads, 1) k_nt(const __grid_constant__ NtArgs<T> a) {
-  k_nt_impl<T, MODE>(a);
+  k_nt_impl<T, MODE, RS, EK>(a);
 }
 
 }  // namespace hd

@@ -184,6 +184,7 @@ struct hd_op {
   double* specbuf = nullptr;    // [K] reduced speculative dots
   FlushBufs fbD, fbF, fbO;      // group partials / per-CTA scratch / tickets
   FlushBufs fbA[2], fbB;        // two-pass Ginibre: fold passes (ping-pong) and output passes
+  double* drawbuf[2] = {nullptr, nullptr};  // two-pass Ginibre: device draws of a probe (io_len each)
   bool gin2p = true;            // two-pass Ginibre / GOE runs (HD_GIN2P=0 disables)
   size_t flush_slots = 0;       // slot capacity of the buffers above
   double* red = nullptr;
@@ -245,6 +246,7 @@ struct hd_op {
   std::vector<double> trace_acc;        // accumulated phase durations (ns)
   int64_t trace_n = 0;
   unsigned long long* trace2 = nullptr;  // HD_TRACE=2: [probe][16] stage stamps of two-pass runs
+  unsigned long long* trace3 = nullptr;  // HD_TRACE=3: k_nt cycle breakdown [fold, gin][8][SMs]
   int64_t trace2_cap = 0, trace2_used = 0;
   // graph cache (hd_run from a fresh state)
   cudaGraphExec_t graph = nullptr;
@@ -454,6 +456,8 @@ void ensure_capacity(hd_op* op, int64_t nr, int64_t nl) {
     op->flush_slots = slots;
     op->layout_gen++;
   }
+  if (op->ens != HD_HAAR && !op->drawbuf[0])  // two-pass Ginibre draw buffers (before any graph capture)
+    for (double*& b : op->drawbuf) b = dmalloc<double>(std::max<int64_t>(op->io_len, 2));
   op->partials = op->fbD.partials;
   op->partsF = op->fbF.partials;
   op->partsO = op->fbO.partials;

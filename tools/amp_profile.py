@@ -30,3 +30,4 @@ if prof:
                           "TBps": round(v["alg_bytes"] / (v["ms"] * 1e-3) / 1e12, 2) if v["ms"] else 0}
                       for k, v in st.items()}
 print(json.dumps(out, indent=0))
+del op  # hd_destroy prints the HD_TRACE=3 breakdown
