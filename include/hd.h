@@ -190,9 +190,12 @@ int hd_reseed(hd_op* op, uint64_t seed);
  * the run is issued once for all operators (gridDim.y = count); the launch
  * sequence is recorded and captured in one CUDA graph on the first call for a
  * given operator set and replayed afterwards. Asynchronous on args->stream;
- * the operators must be idle. Results equal `count` separate hd_run calls
- * bitwise. Non-finite steps are not reported (each operator's status words
- * hold them). */
+ * the operators must be idle. Each trial equals a separate hd_run call up to
+ * the rounding of its re-associated GEMV-T partial sums (a batched launch
+ * gives each trial its share of the SMs, so the warp -> tile split differs:
+ * <= 1e-11 relative, tests/test_gpu_batch.py), and repeated batched calls are
+ * bitwise identical. Non-finite steps are not reported (each operator's status
+ * words hold them). */
 typedef struct hd_batch_item {
   const void* x1;  /* device x_1 (op dtype) */
   void* out;       /* device x_{T+1}        */

@@ -91,7 +91,8 @@ def traffic(full_json, out, t=91, n=1_000_000):
     for d in json.load(open(full_json)):
         name = d.get("Kernel Name", "")
         for key, k in kind.items():
-            if key in name and "dram_bytes" in d:
+            # the capture holds probes t and t + 1: keep the first (probe t), whose bytes alg[k] describes
+            if key in name and "dram_bytes" in d and k not in res:
                 us = float(d["gpu__time_duration.sum"]) / (1e3 if d["units"]["gpu__time_duration.sum"] == "nsecond" else 1)
                 res[k] = {"probe_t": t, "dram_bytes": d["dram_bytes"], "alg_bytes": alg[k],
                           "ratio": d["dram_bytes"] / alg[k], "ncu_us": us,
