@@ -449,6 +449,33 @@ class Runner:
         return {"survey_formula_GBps": survey_bytes_ginibre(m, n, self.probe_sides) / per_gpu / (ms_step / 1e3) / 1e9}
 
 
+def dist_selftest(args):
+    """The multi-rank host logic of the bench on CPU (gloo): every rank plans
+    its row slab of config 5's n the way the sharded operator does
+    (hd_shard_plan), times a fake step, and rank 0 prints the whole-job line
+    fields computed from the max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2101_07464_b200 import lazymat
+
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    n = args.n5 * world
+    cap = args.T5
+    head = -(-(cap + 1) // 256) * 256
+    lo, hi = lazymat.shard_plan(n, world, rank, head)
+    slabs = [None] * world
+    dist.all_gather_object(slabs, (lo, hi))
+    ms = max_over_ranks(10.0 + rank, dist, torch.device("cpu"))
+    if rank == 0:
+        covered = sorted(slabs)
+        ok = covered[0][0] == 0 and covered[-1][1] == n and all(a[1] == b[0] for a, b in zip(covered, covered[1:]))
+        print(json.dumps({"selftest": "ok" if ok else "bad slabs", "world": world, "slabs": covered, "ms": ms,
+                          "value": whole_job_value(world, eu_goe(n, args.T5) / world, 1, ms)}), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -473,7 +500,22 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--cpu-baselines", action="store_true",
                     help="time the reference CPU path (oracle) on every BASELINE config and exit")
+    ap.add_argument("--dist-selftest", action="store_true",
+                    help="CPU check of the multi-rank plumbing (gloo): spawn, shard plan, max-over-ranks; no GPU")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` launches its own N ranks (one per GPU, torchrun)
+        import socket
+
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    if args.dist_selftest:
+        dist_selftest(args)
+        return
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     if args.workload is None:
         args.workload = "config5" if (world_env > 1 and not args.trials) else "config4"

@@ -1873,7 +1873,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_norm_b(const NormArgs* 
 // Reduction stage of the app maps (kEpiAmp*, kEpiSpike): the per-block
 // partial sums of the output pass, summed in fixed order (deterministic),
 // turned into the scalar the next probe's epilogue reads.
-enum AppStage : int { kAppTh = 0, kAppOns = 1, kAppSpike = 2, kAppSpikeInit = 3 };
+enum AppStage : int { kAppTh = 0, kAppOns = 1, kAppSpike = 2, kAppSpikeInit = 3, kAppSum = 4 };
 struct AppArgs {
   const double* partials = nullptr;  // [nblk][nred]
   int nblk = 0, nred = 1, stage = 0;
@@ -1934,9 +1934,12 @@ __device__ __forceinline__ void k_app_scalars_impl(const AppArgs& a) {
     a.scal[kScAppA] = a.alpha * ux;
     if (a.out) a.out[0] = ux;
     bad = !isfinite(inv) || !isfinite(ux);
-  } else {  // kAppSpikeInit: theta <u, x_1>
+  } else if (a.stage == kAppSpikeInit) {  // theta <u, x_1>
     a.scal[kScAppA] = a.alpha * s0;
     a.scal[kScInv] = 1.0;
+  } else {  // kAppSum: this shard's sums, for the exchange (row-sharded runs)
+    a.out[0] = s0;
+    a.out[1] = s1;
   }
   if (bad) {
     atomicMin(a.status + kStBadStep, a.step);

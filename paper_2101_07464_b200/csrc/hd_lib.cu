@@ -259,6 +259,7 @@ struct hd_op {
   size_t appv_bytes[6] = {0, 0, 0, 0, 0, 0};
   double* app_out = nullptr;
   int64_t app_out_cap = 0;
+  double* app_red = nullptr;  // row-sharded runs: the map's sums, exchanged
   cudaGraphExec_t app_graph = nullptr;
   std::string app_graph_key;
   Counters app_graph_end;

@@ -748,7 +748,8 @@ def spiked_power(op, u, x1, T: int, theta: float = 2.0, use_graph: bool = True, 
     """Power method on Q + theta u u^T with Q a device GOE operator (BASELINE
     config 5): x_{t+1} = (Q x_t + theta <u, x_t> u) / ||.||. One device-resident
     CUDA graph (hd_run_spiked). Returns (x_{T+1}, overlaps <u, x_{t+1}>)."""
-    n = op.cols
+    lo, hi = op.shard_range("cols")  # a row shard takes and returns its own rows
+    n = hi - lo
     ptrs, keep, on_dev, stream, torch = _app_io(op, [u, x1], [n, n])
     a = N.hd_spiked_args()
     a.u, a.x1 = ptrs

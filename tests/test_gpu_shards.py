@@ -199,3 +199,40 @@ def test_sharded_faults_and_reference_draws(orc, lm, ens, kw):
     assert not errs, errs
     for t in range(T):
         assert rel(np.concatenate([outs[0][t], outs[1][t]]), want[t]) < 1e-10, t
+
+
+@pytest.mark.parametrize("S", [2, 3])
+def test_sharded_spiked_power_run_matches_oracle(orc, lm, S):
+    # config 5's workload row-sharded (virtual shards, one host thread each):
+    # the GOE probes exchange their partial dots, the spike's <u, g> and ||g||^2
+    # travel through the same exchange, every shard derives the same scalars
+    n, T, seed = 2400, 14, 71
+    u = orc.RandomSource(seed, 1).normal_vector(n)
+    u /= np.linalg.norm(u)
+    x1 = orc.RandomSource(seed, 2).normal_vector(n)
+    x1 /= np.linalg.norm(x1)
+    xr, ovr = orc.Operator("goe", n=n, sigma=n ** -0.5, seed=seed).spiked_power(u, x1, T)
+    draws = orc.draws_for(seed, [n] * (2 * T))
+    ex = lm.Exchange.local(S)
+    outs, errs = [None] * S, []
+
+    def worker(r):
+        try:
+            op = lm.GOEOperator(n, seed, sigma=n ** -0.5, draws="injected", capacity=T, shard=(r, S), exchange=ex)
+            op.push_draws(draws)
+            lo, hi = op.shard_range("cols")
+            outs[r] = lm.spiked_power(op, u[lo:hi], x1[lo:hi], T)
+        except Exception as e:  # noqa: BLE001
+            errs.append((r, e))
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(S)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    if errs:
+        raise errs[0][1]
+    x = np.concatenate([outs[r][0] for r in range(S)])
+    assert rel(x, xr) < 1e-9
+    for r in range(S):
+        assert np.max(np.abs(outs[r][1] - ovr)) < 1e-9

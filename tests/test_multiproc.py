@@ -101,3 +101,25 @@ def test_two_rank_shard_plan_and_nccl_id():
         for (a, b), (c, d) in zip(ranges, ranges[1:]):
             assert b == c and a < b and b % 256 == 0
     assert ids0[0] == ids0[1] == ids1[0] and len(ids0[0]) == 128
+
+
+def test_bench_self_spawns_ranks_and_plans_config5_slabs():
+    # `python bench.py --gpus 2` launches its own 2 ranks (torch.distributed.run);
+    # the CPU self-test runs the multi-rank plumbing over gloo: each rank's row
+    # slab of config 5's n (hd_shard_plan), max-over-ranks timing, whole-job value
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dist-selftest",
+                          "--n5", "1000000", "--T5", "16"], capture_output=True, text=True, timeout=600, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["selftest"] == "ok" and line["world"] == 2
+    assert line["ms"] == 11.0  # the slowest rank's time
+    (lo0, hi0), (lo1, hi1) = line["slabs"]
+    assert lo0 == 0 and hi0 == lo1 and hi1 == 2_000_000 and hi0 % 256 == 0
