@@ -217,8 +217,8 @@ struct NtSmem {
 
 __host__ __device__ inline size_t nt_fixed_doubles(int mode, int C, int kP0, int rs) {
   const size_t b = (size_t)((kP0 + 1) & ~1) + (mode == kNtGin ? (size_t)((kP0 + 1) & ~1) + (size_t)((C - kP0 + 1) & ~1) : 0);
-  const size_t wt2 = 2 * (size_t)nt_workers(rs);
-  return b + 2 * (mode == kNtGin ? 3 : 1) * wt2 + 4 * (size_t)rs;
+  const size_t np_rs = (size_t)(nt_workers(rs) / 32) * rs;  // NP partials x rs rows per array
+  return b + 2 * (mode == kNtGin ? 3 : 1) * np_rs + 4 * (size_t)rs;
 }
 
 __host__ __device__ inline size_t nt_fixed_bytes(int mode, int C, int kP0, int rs, int nst) {
@@ -244,8 +244,8 @@ __device__ __forceinline__ NtSmem nt_smem(unsigned char* base, int mode, int C, 
     m.bs = p - kP0;
     p += (C - kP0 + 1) & ~1;
   }
-  const int wt2 = 2 * nt_workers(rs);
-  m.red = p; p += 2 * (mode == kNtGin ? 3 : 1) * wt2;
+  const int np_rs = (nt_workers(rs) / 32) * rs;
+  m.red = p; p += 2 * (mode == kNtGin ? 3 : 1) * np_rs;
   m.rhs = p; p += 4 * rs;
   m.full = reinterpret_cast<uint64_t*>(p);
   m.empty = m.full + nst;
@@ -354,7 +354,7 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
   const int npart = (RP >= 32) ? ncg : (wt >> 5);         // this thread's partial index
   const int cga = (int)((int64_t)C * ncg / CG), cgb = (int)((int64_t)C * (ncg + 1) / CG);
   const int nred = (MODE == kNtGin) ? 3 : 1;
-  const int red_stride = 2 * WT;  // one partial array: CG x rs = 2 WT doubles
+  const int red_stride = NP * RS;  // one partial array: NP x rs doubles
   // epilogue scalar accumulators
   double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
   bool bad = false;
