@@ -32,6 +32,10 @@
 
 #include "hd_kernels.cuh"
 
+#ifndef HD_NT_TRACE
+#define HD_NT_TRACE 0  // 1: HD_TRACE=3 per-slot cycle counters in k_nt (A/B builds only)
+#endif
+
 namespace hd {
 
 constexpr int kNtConsumers = 352;                   // 11 consumer warps (1-2 epilogue, the rest workers)
@@ -216,7 +220,7 @@ struct NtSmem {
 };
 
 __host__ __device__ inline size_t nt_fixed_doubles(int mode, int C, int kP0, int rs) {
-  const size_t b = (size_t)((kP0 + 1) & ~1) + (mode == kNtGin ? (size_t)((kP0 + 1) & ~1) + (size_t)((C - kP0 + 1) & ~1) : 0);
+  const size_t b = (size_t)((kP0 + 1) & ~1) * (mode == kNtGin ? 2 : 1) + (mode == kNtGin ? (size_t)((C - kP0 + 1) & ~1) : 0);
   const size_t np_rs = (size_t)(nt_workers(rs) / 32) * rs;  // NP partials x rs rows per array
   return b + 2 * (mode == kNtGin ? 3 : 1) * np_rs + 4 * (size_t)rs;
 }
@@ -236,13 +240,15 @@ __device__ __forceinline__ NtSmem nt_smem(unsigned char* base, int mode, int C, 
   NtSmem m;
   m.stages = base;
   double* p = reinterpret_cast<double*>(base + (size_t)nst * stage_bytes);
-  m.b1 = p; p += (kP0 + 1) & ~1;
+  m.b1 = p;  // fold: beta1 [kP0]; output pass: (beta1, beta3) pairs [kP0][2]
   m.b3 = p;
   m.bs = p;
   if (mode == kNtGin) {
-    p += (kP0 + 1) & ~1;
+    p += 2 * (size_t)((kP0 + 1) & ~1);
     m.bs = p - kP0;
     p += (C - kP0 + 1) & ~1;
+  } else {
+    p += (kP0 + 1) & ~1;
   }
   const int np_rs = (nt_workers(rs) / 32) * rs;
   m.red = p; p += 2 * (mode == kNtGin ? 3 : 1) * np_rs;
@@ -324,8 +330,12 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
   const int kP0 = a.kP0;
   if (!producer) {
     for (int c = tid; c < kP0; c += kNtConsumers) {
-      m.b1[c] = a.beta1[c];
-      if (MODE == kNtGin) m.b3[c] = a.beta3[c];
+      if (MODE == kNtGin) {
+        m.b1[2 * c] = a.beta1[c];
+        m.b1[2 * c + 1] = a.beta3[c];
+      } else {
+        m.b1[c] = a.beta1[c];
+      }
     }
     if (MODE == kNtGin)
       for (int c = kP0 + tid; c < C; c += kNtConsumers) m.bs[c] = a.coefS[c - kP0];
@@ -378,13 +388,16 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
 #pragma unroll 4
     for (int c = cga; c < ce; ++c) {  // one 2-row load per column, coefficients broadcast
       const double2 v = lds_pair(sp + c * rs);
-      const double b = m.b1[c];
-      n1.x = fma(v.x, b, n1.x);
-      n1.y = fma(v.y, b, n1.y);
       if (MODE == kNtGin) {
-        const double b3 = m.b3[c];
-        n3.x = fma(v.x, b3, n3.x);
-        n3.y = fma(v.y, b3, n3.y);
+        const double2 b = *reinterpret_cast<const double2*>(m.b1 + 2 * c);  // (beta1, beta3)
+        n1.x = fma(v.x, b.x, n1.x);
+        n1.y = fma(v.y, b.x, n1.y);
+        n3.x = fma(v.x, b.y, n3.x);
+        n3.y = fma(v.y, b.y, n3.y);
+      } else {
+        const double b = m.b1[c];
+        n1.x = fma(v.x, b, n1.x);
+        n1.y = fma(v.y, b, n1.y);
       }
     }
     if (MODE == kNtGin) {
@@ -427,7 +440,8 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
     constexpr int LPR = (RS >= 32) ? 1 : 32 / RS;
     const int et = tid % RS, half = tid / RS;
     if (tid >= RS * LPR) return;
-    const long long ec0 = (a.trace && tid == 0) ? clock64() : 0;
+    const bool etr = HD_NT_TRACE && a.trace && tid == 0;
+    const long long ec0 = etr ? clock64() : 0;
     const double* red = m.red + (k & 1) * nred * red_stride;
     double r1 = 0.0, r3 = 0.0, rS = 0.0;
     {
@@ -457,7 +471,7 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
       }
     }
     if (half != 0) return;
-    if (a.trace && tid == 0) epi_tr[0] += clock64() - ec0;
+    if (etr) epi_tr[0] += clock64() - ec0;
     const unsigned char* vs = stage_ptr(q) + vec_off;
     double* rb = m.rhs + (k & 1) * 2 * rs;
     mbar_wait(m.full + q, ph);  // complete (the workers waited for it a slot ago): orders the vector reads
@@ -534,7 +548,7 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
       e1 += uu * rhs;   // new S column . x_{t+1}
       rb[et] = rhs;
     }
-    if (a.trace && tid == 0) epi_tr[1] += clock64() - ec0;
+    if (etr) epi_tr[1] += clock64() - ec0;
   };
   // ---- T phase of sub-tile k (stage q): workers (mapping above)
   auto tphase = [&](int64_t k, int q) {
@@ -585,7 +599,7 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
     named_sync(kNtBarId, kNtConsumers);
     // HD_TRACE=3: per-CTA cycle breakdown (epilogue thread 0, worker 0)
     unsigned long long tr[6] = {0, 0, 0, 0, 0, 0};
-    const bool trace = a.trace && (tid == 0 || wt == 0);
+    const bool trace = HD_NT_TRACE && a.trace && (tid == 0 || wt == 0);
     for (int64_t j = 0; j <= nk; ++j) {
       long long c0t = trace ? clock64() : 0, c1t = 0, c2t = 0, c3t = 0;
       if (epi_thr && j < nk) epilogue(j, qE, phE, kbE, bparE);
