@@ -717,21 +717,39 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
 // [0, rows) of a (local) dimension, global row = local row + gdelta; the two
 // passes that need it read it as a bulk-copied vector instead of each
 // regenerating the fp64 transcendentals inside their streams.
-__global__ void __launch_bounds__(256) k_draw_fill(const unsigned long long* seedp, uint32_t stream, uint32_t probe,
-                                                   int64_t rows, int64_t gdelta, double* out) {
+struct DrawArgs {
+  const unsigned long long* seedp = nullptr;
+  uint32_t stream = 0, probe = 0;
+  int64_t rows = 0, gdelta = 0;
+  double* out = nullptr;
+};
+
+__device__ __forceinline__ void k_draw_fill_impl(const DrawArgs& a) {
   pdl_wait();
   pdl_launch();
-  const uint64_t seed = *seedp;
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 2 * q < rows; q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = 2 * q + gdelta;  // gdelta is even (tile-aligned)
-    const double2 v = philox_normal_pair(seed, stream, probe, (uint64_t)(i >> 1));
-    *reinterpret_cast<double2*>(out + 2 * q) = v;
+  const uint64_t seed = *a.seedp;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 2 * q < a.rows; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = 2 * q + a.gdelta;  // gdelta is even (tile-aligned)
+    const double2 v = philox_normal_pair(seed, a.stream, a.probe, (uint64_t)(i >> 1));
+    *reinterpret_cast<double2*>(a.out + 2 * q) = v;
   }
+}
+__global__ void __launch_bounds__(256) k_draw_fill(const __grid_constant__ DrawArgs a) { k_draw_fill_impl(a); }
+// batched twin: one launch serves gridDim.y operators (hd_batch_run)
+__global__ void __launch_bounds__(256) k_draw_fill_b(const DrawArgs* __restrict__ argv) {
+  k_draw_fill_impl(argv[blockIdx.y]);
 }
 
 template <typename T, int MODE, int RS, int EK>
 __global__ void __launch_bounds__(kNtThreads, 1) k_nt(const __grid_constant__ NtArgs<T> a) {
   k_nt_impl<T, MODE, RS, EK>(a);
+}
+// batched twin: operator blockIdx.y's arguments — tensor maps included (the
+// TMA unit reads a 64-B aligned descriptor from global memory) — from the
+// device table of hd_batch_run
+template <typename T, int MODE, int RS, int EK>
+__global__ void __launch_bounds__(kNtThreads, 1) k_nt_b(const NtArgs<T>* __restrict__ argv) {
+  k_nt_impl<T, MODE, RS, EK>(argv[blockIdx.y]);
 }
 
 }  // namespace hd

@@ -1827,6 +1827,10 @@ template <typename T>
 __global__ void __launch_bounds__(kSmallThreads) k_small_fold2(const __grid_constant__ SmallArgs a) {
   k_small_fold2_impl<T>(a);
 }
+template <typename T>
+__global__ void __launch_bounds__(kSmallThreads) k_small_fold2_b(const SmallArgs* __restrict__ argv) {
+  k_small_fold2_impl<T>(argv[blockIdx.y]);
+}
 
 // Normalize dynamics: inv = ||y|| > 0 ? 1/||y|| : 1 (bench.cpp:25-28).
 struct NormArgs {

@@ -185,7 +185,7 @@ struct hd_op {
   FlushBufs fbD, fbF, fbO;      // group partials / per-CTA scratch / tickets
   FlushBufs fbA[2], fbB;        // two-pass Ginibre: fold passes (ping-pong) and output passes
   double* drawbuf[2] = {nullptr, nullptr};  // two-pass Ginibre: device draws of a probe (io_len each)
-  bool gin2p = true;            // two-pass Ginibre / GOE runs (HD_GIN2P=0 disables)
+  int gin2p = 1;                // two-pass Ginibre / GOE runs: 1 auto, 2 forced (HD_GIN2P=1), 0 off (HD_GIN2P=0)
   size_t flush_slots = 0;       // slot capacity of the buffers above
   double* red = nullptr;
   size_t red_cap = 0;
