@@ -103,7 +103,10 @@ struct KStat {
 struct PendingEv {
   cudaEvent_t a, b;
   std::string kind;
+  double bytes;
+  std::string note;
 };
+thread_local std::string g_prof_note;  // HD_PROF_LOG: shape of the next launch (launch_nt)
 
 // host-side counters, snapshotted per step so a failed probe / aborted run
 // can restore the exact reference state (operators.hpp:44-48: a failed probe
@@ -505,7 +508,8 @@ struct LaunchScope {
     if (op->prof) {
       cudaEvent_t b = get_event(op);
       cudaEventRecord(b, s);
-      op->evq.push_back({a, b, kind});
+      op->evq.push_back({a, b, kind, bytes, g_prof_note});
+      g_prof_note.clear();
       KStat& st = op->stats[kind];
       st.launches++;
       st.bytes += bytes;
@@ -516,13 +520,19 @@ struct LaunchScope {
 void drain_events(hd_op* op) {
   if (op->evq.empty()) return;
   cudaStreamSynchronize(op->stream);
+  // HD_PROF_LOG=path: one line per launch (kind, algorithmic bytes, ms) — a
+  // diagnostic of profiling runs (hd_set_profiling), never on by default
+  static const char* log_path = std::getenv("HD_PROF_LOG");
+  FILE* lf = log_path ? std::fopen(log_path, "a") : nullptr;
   for (auto& e : op->evq) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e.a, e.b);
     op->stats[e.kind].ms += ms;
+    if (lf) std::fprintf(lf, "%s %.0f %.6f %s\n", e.kind.c_str(), e.bytes, (double)ms, e.note.c_str());
     op->evpool.push_back(e.a);
     op->evpool.push_back(e.b);
   }
+  if (lf) std::fclose(lf);
   op->evq.clear();
 }
 
