@@ -38,14 +38,20 @@
 
 namespace hd {
 
-constexpr int kNtConsumers = 352;                   // 11 consumer warps (1-2 epilogue, the rest workers)
+#ifndef HD_NT_CONSUMERS
+#define HD_NT_CONSUMERS 352  // consumer threads of a k_nt CTA (A/B builds: 480)
+#endif
+constexpr int kNtConsumers = HD_NT_CONSUMERS;       // consumer warps: 1-2 epilogue, the rest workers
 constexpr int kNtThreads = kNtConsumers + 32;       // + 1 producer warp
 constexpr int kNtMaxMaps = 4;
 constexpr int kNtMaxVecs = 5;
 constexpr int kNtMaxStages = 16;
 constexpr int kNtMaxCols = 512;                     // columns of an output pass
-constexpr int kNtGinRounds = 16;                    // T-phase column rounds: output pass (>= 512 / (288 / 8))
-constexpr int kNtFoldRounds = 8;                    // ... fold pass (F columns <= 8 x 36 = 288)
+constexpr int kNtMaxFoldCols = 288;                 // columns of a fold pass
+// T-phase column rounds per worker thread (8 lanes per column, WT / 8 columns
+// per round; WT >= kNtConsumers - 64 workers)
+constexpr int kNtGinRounds = (kNtMaxCols * 8 + (kNtConsumers - 64) - 1) / (kNtConsumers - 64);
+constexpr int kNtFoldRounds = (kNtMaxFoldCols * 8 + (kNtConsumers - 64) - 1) / (kNtConsumers - 64);
 constexpr int kNtBarId = 1;                         // named barrier of the consumer warps
 
 enum NtMode : int { kNtFold = 0, kNtGin = 1 };
@@ -129,19 +135,28 @@ struct NtArgs {
   Flush out;
   int* status = nullptr;
   int prefetch = 0;
+  int evict = 0;      // L2 policy of the panel boxes (nt_l2_policy)
   unsigned long long* trace = nullptr;  // HD_TRACE=3: [8][grid] cycle counters
 };
 
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
+                                            uint64_t pol) {
   asm volatile(
-      "{\n"
-      ".reg .b64 pol;\n"
-      "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3, %4}], [%5], pol;\n"
-      "}\n" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
+}
+
+// L2 policy of the panel boxes: evict_first (panel bytes are read once per
+// pass) or evict_normal (NtArgs::evict, HD_NT_EVICT A/B knob)
+__device__ __forceinline__ uint64_t nt_l2_policy(int evict) {
+  uint64_t pol;
+  if (evict == 0)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
 }
 
 // mbarrier wait that backs off between probes: the producer warp waits for
@@ -284,6 +299,7 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
   __syncthreads();
   const size_t vec_off = (size_t)C * rs * sizeof(T);  // vector slots after the panel columns (8 B each)
   auto row_of = [&](int64_t k) { return a.rm.tile0 * kTile + ((int64_t)blockIdx.x + k * gridDim.x) * rs; };
+  const uint64_t l2pol = nt_l2_policy(a.evict);
   auto issue = [&](int64_t k, int q) {  // producer lane 0: sub-tile k into stage q
     unsigned char* st = m.stages + (size_t)q * a.stage_bytes;
     const int64_t li = row_of(k);  // local panel row
@@ -291,7 +307,7 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_arrive_expect_tx(m.full + q, (uint32_t)a.tx_bytes);
     for (int b = 0; b < a.nmaps; ++b)
-      tma_load_3d(st + (size_t)a.mi[b].scol * rs * sizeof(T), &a.maps[b], rin, a.mi[b].pcol, tile, m.full + q);
+      tma_load_3d(st + (size_t)a.mi[b].scol * rs * sizeof(T), &a.maps[b], rin, a.mi[b].pcol, tile, m.full + q, l2pol);
     const int64_t vi = li + a.rm.gdelta - a.rm.vbase;  // vector index of the sub-tile's first row
     for (int v = 0; v < a.nvec; ++v)
       bulk_g2s(st + vec_off + (size_t)v * rs * 8, static_cast<const unsigned char*>(a.vec[v]) + vi * a.vesz[v],
