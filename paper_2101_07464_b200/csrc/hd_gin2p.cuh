@@ -221,13 +221,17 @@ __device__ __forceinline__ double ld_vec(const unsigned char* slot, int esz, int
 __host__ __device__ inline int nt_ewarps(int rs) { return rs <= 32 ? 1 : rs / 32; }
 __host__ __device__ inline int nt_workers(int rs) { return kNtConsumers - 32 * nt_ewarps(rs); }
 
-// Shared-memory carve-up (sized per launch): [stages][stage_bytes] | beta1
-// [kP0] | beta3 [kP0] | coefS [C - kP0] | N-phase partials [2][1 or 3][2 WT] |
-// rhs [2][2][rs] | barriers. The T-phase
-// partials, the scalar partials and the slot row reuse the stages at the end.
+// N-phase coefficient entries (one per column)
+__host__ __device__ inline int nt_coef_len(int C, int rs) { (void)rs; return C; }
+
+// Shared-memory carve-up (sized per launch): [stages][stage_bytes] | N-phase
+// coefficients (fold: beta1 [cl]; output pass: pairs [cl][2], O columns
+// (beta1, -beta3), S columns (0, coefS); cl = nt_coef_len) | N-phase partials
+// [2][1 or 2][NP][rs] | rhs [2][2][rs] | barriers. The T-phase partials, the
+// scalar partials and the slot row reuse the stages at the end.
 struct NtSmem {
   unsigned char* stages;
-  double *b1, *b3, *bs;   // bs is indexed by the stage column (c >= kP0)
+  double* cf;
   double* red;
   double* rhs;
   uint64_t* full;
@@ -235,9 +239,10 @@ struct NtSmem {
 };
 
 __host__ __device__ inline size_t nt_fixed_doubles(int mode, int C, int kP0, int rs) {
-  const size_t b = (size_t)((kP0 + 1) & ~1) * (mode == kNtGin ? 2 : 1) + (mode == kNtGin ? (size_t)((C - kP0 + 1) & ~1) : 0);
+  (void)kP0;
+  const size_t b = (size_t)((nt_coef_len(C, rs) + 1) & ~1) * (mode == kNtGin ? 2 : 1);
   const size_t np_rs = (size_t)(nt_workers(rs) / 32) * rs;  // NP partials x rs rows per array
-  return b + 2 * (mode == kNtGin ? 3 : 1) * np_rs + 4 * (size_t)rs;
+  return b + 2 * (mode == kNtGin ? 2 : 1) * np_rs + 4 * (size_t)rs;
 }
 
 __host__ __device__ inline size_t nt_fixed_bytes(int mode, int C, int kP0, int rs, int nst) {
@@ -255,18 +260,11 @@ __device__ __forceinline__ NtSmem nt_smem(unsigned char* base, int mode, int C, 
   NtSmem m;
   m.stages = base;
   double* p = reinterpret_cast<double*>(base + (size_t)nst * stage_bytes);
-  m.b1 = p;  // fold: beta1 [kP0]; output pass: (beta1, beta3) pairs [kP0][2]
-  m.b3 = p;
-  m.bs = p;
-  if (mode == kNtGin) {
-    p += 2 * (size_t)((kP0 + 1) & ~1);
-    m.bs = p - kP0;
-    p += (C - kP0 + 1) & ~1;
-  } else {
-    p += (kP0 + 1) & ~1;
-  }
+  (void)kP0;
+  m.cf = p;
+  p += (size_t)((nt_coef_len(C, rs) + 1) & ~1) * (mode == kNtGin ? 2 : 1);
   const int np_rs = (nt_workers(rs) / 32) * rs;
-  m.red = p; p += 2 * (mode == kNtGin ? 3 : 1) * np_rs;
+  m.red = p; p += 2 * (mode == kNtGin ? 2 : 1) * np_rs;
   m.rhs = p; p += 4 * rs;
   m.full = reinterpret_cast<uint64_t*>(p);
   m.empty = m.full + nst;
@@ -345,16 +343,19 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
   // ------------------------------------------------------------ consumers
   const int kP0 = a.kP0;
   if (!producer) {
-    for (int c = tid; c < kP0; c += kNtConsumers) {
+    // one coefficient entry per column: n1 = W beta1 (O or F columns),
+    // nm = S coefS - W_O beta3 (output pass: one sum over both panels)
+    const int cl = nt_coef_len(C, RS);
+    for (int c = tid; c < cl; c += kNtConsumers) {
       if (MODE == kNtGin) {
-        m.b1[2 * c] = a.beta1[c];
-        m.b1[2 * c + 1] = a.beta3[c];
+        double2 v = make_double2(0.0, 0.0);
+        if (c < kP0) v = make_double2(a.beta1[c], -a.beta3[c]);
+        else if (c < C) v.y = a.coefS[c - kP0];
+        reinterpret_cast<double2*>(m.cf)[c] = v;
       } else {
-        m.b1[c] = a.beta1[c];
+        m.cf[c] = (c < C) ? a.beta1[c] : 0.0;
       }
     }
-    if (MODE == kNtGin)
-      for (int c = kP0 + tid; c < C; c += kNtConsumers) m.bs[c] = a.coefS[c - kP0];
   }
   // worker T-phase mapping: 8 consecutive lanes share a column (lane g of the
   // 8 takes row pairs g, g + 8, ... of the sub-tile: 128 contiguous bytes per
@@ -372,14 +373,15 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
     tA[r] = 0.0;
     tB[r] = 0.0;
   }
-  // worker N-phase mapping: row pair nrp, column group ncg (CG groups)
+  // worker N-phase mapping: row pair nrp, column group ncg (CG groups) of
+  // contiguous columns [cga, cgb)
   constexpr int RP = RS / 2;
   constexpr int CG = WT / RP;
   const int nrp = wt % RP, ncg = wt / RP;
   constexpr int NP = (RP >= 32) ? CG : WT / 32;         // N-phase partials per row
   const int npart = (RP >= 32) ? ncg : (wt >> 5);         // this thread's partial index
   const int cga = (int)((int64_t)C * ncg / CG), cgb = (int)((int64_t)C * (ncg + 1) / CG);
-  const int nred = (MODE == kNtGin) ? 3 : 1;
+  constexpr int nred = (MODE == kNtGin) ? 2 : 1;
   const int red_stride = NP * RS;  // one partial array: NP x rs doubles
   // epilogue scalar accumulators
   double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
@@ -399,30 +401,20 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
   auto nphase = [&](int64_t k, int q, uint32_t ph) {
     mbar_wait(m.full + q, ph);
     const T* sp = reinterpret_cast<const T*>(stage_ptr(q)) + 2 * nrp;
-    double2 n1 = make_double2(0.0, 0.0), n3 = make_double2(0.0, 0.0), ns = make_double2(0.0, 0.0);
-    const int ce = min(cgb, kP0);
+    double2 n1 = make_double2(0.0, 0.0), nm = make_double2(0.0, 0.0);
 #pragma unroll 4
-    for (int c = cga; c < ce; ++c) {  // one 2-row load per column, coefficients broadcast
-      const double2 v = lds_pair(sp + c * rs);
+    for (int c = cga; c < cgb; ++c) {  // one 2-row load per column, coefficients broadcast
+      const double2 v = lds_pair(sp + c * RS);
       if (MODE == kNtGin) {
-        const double2 b = *reinterpret_cast<const double2*>(m.b1 + 2 * c);  // (beta1, beta3)
+        const double2 b = reinterpret_cast<const double2*>(m.cf)[c];
         n1.x = fma(v.x, b.x, n1.x);
         n1.y = fma(v.y, b.x, n1.y);
-        n3.x = fma(v.x, b.y, n3.x);
-        n3.y = fma(v.y, b.y, n3.y);
+        nm.x = fma(v.x, b.y, nm.x);
+        nm.y = fma(v.y, b.y, nm.y);
       } else {
-        const double b = m.b1[c];
+        const double b = m.cf[c];
         n1.x = fma(v.x, b, n1.x);
         n1.y = fma(v.y, b, n1.y);
-      }
-    }
-    if (MODE == kNtGin) {
-#pragma unroll 4
-      for (int c = max(cga, kP0); c < cgb; ++c) {
-        const double2 v = lds_pair(sp + c * rs);
-        const double b = m.bs[c];
-        ns.x = fma(v.x, b, ns.x);
-        ns.y = fma(v.y, b, ns.y);
       }
     }
     // the column groups of one warp (lanes with the same row pair) add up in
@@ -433,19 +425,14 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
       n1.x += __shfl_xor_sync(0xffffffffu, n1.x, sh);
       n1.y += __shfl_xor_sync(0xffffffffu, n1.y, sh);
       if (MODE == kNtGin) {
-        n3.x += __shfl_xor_sync(0xffffffffu, n3.x, sh);
-        n3.y += __shfl_xor_sync(0xffffffffu, n3.y, sh);
-        ns.x += __shfl_xor_sync(0xffffffffu, ns.x, sh);
-        ns.y += __shfl_xor_sync(0xffffffffu, ns.y, sh);
+        nm.x += __shfl_xor_sync(0xffffffffu, nm.x, sh);
+        nm.y += __shfl_xor_sync(0xffffffffu, nm.y, sh);
       }
     }
     if (RP >= 32 || lane < RP) {
       double* red = m.red + (k & 1) * nred * red_stride + npart * RS + 2 * nrp;  // [partial][rs]
       *reinterpret_cast<double2*>(red) = n1;
-      if (MODE == kNtGin) {
-        *reinterpret_cast<double2*>(red + red_stride) = n3;
-        *reinterpret_cast<double2*>(red + 2 * red_stride) = ns;
-      }
+      if (MODE == kNtGin) *reinterpret_cast<double2*>(red + red_stride) = nm;
     }
   };
   // ---- epilogue of sub-tile k (stage q): epilogue threads, one row each -> rhs[k & 1]
@@ -459,30 +446,23 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
     const bool etr = HD_NT_TRACE && a.trace && tid == 0;
     const long long ec0 = etr ? clock64() : 0;
     const double* red = m.red + (k & 1) * nred * red_stride;
-    double r1 = 0.0, r3 = 0.0, rS = 0.0;
+    double r1 = 0.0, rm = 0.0;
     {
       constexpr int per = (NP + LPR - 1) / LPR;
       const int g0 = half * per, g1 = min(NP, g0 + per);
-      double a1[4] = {0.0, 0.0, 0.0, 0.0}, a3[4] = {0.0, 0.0, 0.0, 0.0}, aS[4] = {0.0, 0.0, 0.0, 0.0};
+      double a1[4] = {0.0, 0.0, 0.0, 0.0}, am[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll 4
       for (int g = g0; g < g1; ++g) {
         const int u = (g - g0) & 3;
         a1[u] += red[g * RS + et];
-        if (MODE == kNtGin) {
-          a3[u] += red[red_stride + g * RS + et];
-          aS[u] += red[2 * red_stride + g * RS + et];
-        }
+        if (MODE == kNtGin) am[u] += red[red_stride + g * RS + et];
       }
       r1 = (a1[0] + a1[1]) + (a1[2] + a1[3]);
-      r3 = (a3[0] + a3[1]) + (a3[2] + a3[3]);
-      rS = (aS[0] + aS[1]) + (aS[2] + aS[3]);
+      rm = (am[0] + am[1]) + (am[2] + am[3]);
       if (LPR > 1) {
         for (int sh = RS; sh < 32; sh <<= 1) {
           r1 += __shfl_xor_sync(0xffffffffu, r1, sh);
-          if (MODE == kNtGin) {
-            r3 += __shfl_xor_sync(0xffffffffu, r3, sh);
-            rS += __shfl_xor_sync(0xffffffffu, rS, sh);
-          }
+          if (MODE == kNtGin) rm += __shfl_xor_sync(0xffffffffu, rm, sh);
         }
       }
     }
@@ -525,7 +505,7 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
       a.Sw[paddr(li, a.newjS, a.KS)] = (T)u;
       const double uu = (double)(T)u;
       const double cs = (i < a.csplen) ? d * a.csp[i] : 0.0;
-      double y = a.sigma * (rS + cc * u + (cs - r3));  // k_ginout's order
+      double y = a.sigma * (rm + cc * u + cs);  // rm = S coefS - W_O beta3
       const Epi<T>& e = a.epi;
       const int64_t vi = i - a.rm.vbase;
       double out = 0.0;
