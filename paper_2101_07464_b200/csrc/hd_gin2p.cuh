@@ -136,6 +136,7 @@ struct NtArgs {
   int* status = nullptr;
   int prefetch = 0;
   int evict = 0;      // L2 policy of the panel boxes (nt_l2_policy)
+  int deal = 0;       // sub-tile order (k_nt_impl: 0 round robin, 1 by tile)
   unsigned long long* trace = nullptr;  // HD_TRACE=3: [8][grid] cycle counters
 };
 
@@ -218,7 +219,7 @@ __device__ __forceinline__ double ld_vec(const unsigned char* slot, int esz, int
 // In "slot" j the epilogue warps finish sub-tile j while the workers run the
 // N phase of j + 1 and the T phase of j - 1 — one barrier per slot, so the
 // row-serial epilogue is off the critical path.
-__host__ __device__ inline int nt_ewarps(int rs) { return rs <= 32 ? 1 : rs / 32; }
+__host__ __device__ inline int nt_ewarps(int rs) { return rs <= 32 ? 1 : 2; }
 __host__ __device__ inline int nt_workers(int rs) { return kNtConsumers - 32 * nt_ewarps(rs); }
 
 // N-phase coefficient entries (one per column)
@@ -279,14 +280,24 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
   const bool producer = (w == kNtConsumers / 32);
   constexpr int rs = RS;
   const int C = a.C, nst = a.nst;
-  constexpr int E = (RS <= 32) ? 1 : RS / 32, WT = kNtConsumers - 32 * E;
+  // sub-tiles taller than 64 rows (narrow passes: the per-slot costs spread
+  // over more bytes) run as NB blocks of RB = 64 rows through the same thread
+  // mappings; the blocks of a slot are independent (instruction-level overlap)
+  constexpr int RB = (RS > 64) ? 64 : RS, NB = RS / RB;
+  constexpr int E = (RB <= 32) ? 1 : 2, WT = kNtConsumers - 32 * E;
   const bool epi_thr = !producer && tid < 32 * E;
   const bool worker = !producer && !epi_thr;
   const int wt = tid - 32 * E;  // worker index
   // sub-tiles dealt round robin: at any moment the CTAs stream neighbouring
   // sub-tiles, so each column's contiguous 2 KB tile segment is read by
   // neighbouring CTAs close together in time (DRAM row-buffer locality)
-  const int64_t nk = (a.nsub > (int64_t)blockIdx.x) ? (a.nsub - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  // deal 0: sub-tile s = blockIdx.x + k gridDim.x; deal 1: whole tiles dealt
+  // round robin, a CTA streams the 256 / RS sub-tiles of its tile in order
+  constexpr int SPT = kTile / RS;
+  const int64_t ntl = a.nsub / SPT;
+  const int64_t nk = (a.deal == 0)
+                         ? ((a.nsub > (int64_t)blockIdx.x) ? (a.nsub - blockIdx.x + gridDim.x - 1) / gridDim.x : 0)
+                         : ((ntl > (int64_t)blockIdx.x) ? (ntl - blockIdx.x + gridDim.x - 1) / gridDim.x : 0) * SPT;
   if (tid == 0) {
     for (int q = 0; q < nst; ++q) {
       mbar_init(m.full + q, 1);
@@ -296,7 +307,11 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
   }
   __syncthreads();
   const size_t vec_off = (size_t)C * rs * sizeof(T);  // vector slots after the panel columns (8 B each)
-  auto row_of = [&](int64_t k) { return a.rm.tile0 * kTile + ((int64_t)blockIdx.x + k * gridDim.x) * rs; };
+  auto row_of = [&](int64_t k) {
+    const int64_t sidx = (a.deal == 0) ? (int64_t)blockIdx.x + k * gridDim.x
+                                       : ((int64_t)blockIdx.x + (k / SPT) * gridDim.x) * SPT + (k % SPT);
+    return a.rm.tile0 * kTile + sidx * rs;
+  };
   const uint64_t l2pol = nt_l2_policy(a.evict);
   auto issue = [&](int64_t k, int q) {  // producer lane 0: sub-tile k into stage q
     unsigned char* st = m.stages + (size_t)q * a.stage_bytes;
@@ -375,7 +390,7 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
   }
   // worker N-phase mapping: row pair nrp, column group ncg (CG groups) of
   // contiguous columns [cga, cgb)
-  constexpr int RP = RS / 2;
+  constexpr int RP = RB / 2;
   constexpr int CG = WT / RP;
   const int nrp = wt % RP, ncg = wt / RP;
   constexpr int NP = (RP >= 32) ? CG : WT / 32;         // N-phase partials per row
@@ -401,81 +416,100 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
   auto nphase = [&](int64_t k, int q, uint32_t ph) {
     mbar_wait(m.full + q, ph);
     const T* sp = reinterpret_cast<const T*>(stage_ptr(q)) + 2 * nrp;
-    double2 n1 = make_double2(0.0, 0.0), nm = make_double2(0.0, 0.0);
+    double2 n1[NB], nm[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      n1[b] = make_double2(0.0, 0.0);
+      nm[b] = make_double2(0.0, 0.0);
+    }
 #pragma unroll 4
-    for (int c = cga; c < cgb; ++c) {  // one 2-row load per column, coefficients broadcast
-      const double2 v = lds_pair(sp + c * RS);
+    for (int c = cga; c < cgb; ++c) {  // one 2-row load per column and block, coefficients broadcast
       if (MODE == kNtGin) {
-        const double2 b = reinterpret_cast<const double2*>(m.cf)[c];
-        n1.x = fma(v.x, b.x, n1.x);
-        n1.y = fma(v.y, b.x, n1.y);
-        nm.x = fma(v.x, b.y, nm.x);
-        nm.y = fma(v.y, b.y, nm.y);
+        const double2 cf = reinterpret_cast<const double2*>(m.cf)[c];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          const double2 v = lds_pair(sp + c * RS + b * RB);
+          n1[b].x = fma(v.x, cf.x, n1[b].x);
+          n1[b].y = fma(v.y, cf.x, n1[b].y);
+          nm[b].x = fma(v.x, cf.y, nm[b].x);
+          nm[b].y = fma(v.y, cf.y, nm[b].y);
+        }
       } else {
-        const double b = m.cf[c];
-        n1.x = fma(v.x, b, n1.x);
-        n1.y = fma(v.y, b, n1.y);
+        const double cf = m.cf[c];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          const double2 v = lds_pair(sp + c * RS + b * RB);
+          n1[b].x = fma(v.x, cf, n1[b].x);
+          n1[b].y = fma(v.y, cf, n1[b].y);
+        }
       }
     }
     // the column groups of one warp (lanes with the same row pair) add up in
     // a fixed shuffle tree, so the epilogue sums only NP = WT / 32 partials
-    // per row (RS <= 32; RS = 64: one column group per warp, NP = CG)
+    // per row (RB <= 32; RB = 64: one column group per warp, NP = CG)
 #pragma unroll
-    for (int sh = RP; sh < 32; sh <<= 1) {
-      n1.x += __shfl_xor_sync(0xffffffffu, n1.x, sh);
-      n1.y += __shfl_xor_sync(0xffffffffu, n1.y, sh);
-      if (MODE == kNtGin) {
-        nm.x += __shfl_xor_sync(0xffffffffu, nm.x, sh);
-        nm.y += __shfl_xor_sync(0xffffffffu, nm.y, sh);
+    for (int b = 0; b < NB; ++b) {
+#pragma unroll
+      for (int sh = RP; sh < 32; sh <<= 1) {
+        n1[b].x += __shfl_xor_sync(0xffffffffu, n1[b].x, sh);
+        n1[b].y += __shfl_xor_sync(0xffffffffu, n1[b].y, sh);
+        if (MODE == kNtGin) {
+          nm[b].x += __shfl_xor_sync(0xffffffffu, nm[b].x, sh);
+          nm[b].y += __shfl_xor_sync(0xffffffffu, nm[b].y, sh);
+        }
       }
-    }
-    if (RP >= 32 || lane < RP) {
-      double* red = m.red + (k & 1) * nred * red_stride + npart * RS + 2 * nrp;  // [partial][rs]
-      *reinterpret_cast<double2*>(red) = n1;
-      if (MODE == kNtGin) *reinterpret_cast<double2*>(red + red_stride) = nm;
+      if (RP >= 32 || lane < RP) {
+        double* red = m.red + (k & 1) * nred * red_stride + npart * RS + b * RB + 2 * nrp;  // [partial][rs]
+        *reinterpret_cast<double2*>(red) = n1[b];
+        if (MODE == kNtGin) *reinterpret_cast<double2*>(red + red_stride) = nm[b];
+      }
     }
   };
   // ---- epilogue of sub-tile k (stage q): epilogue threads, one row each -> rhs[k & 1]
   unsigned long long epi_tr[2] = {0, 0};  // HD_TRACE=3: epilogue reduction / whole
-  auto epilogue = [&](int64_t k, int q, uint32_t ph, int64_t kb, uint32_t bpar) {
+  auto epilogue = [&](int64_t k, int q, uint32_t ph) {
     // LPR lanes per row add the NP column-group partials in fixed order (four
-    // chains each), then combine with a shuffle; lane et < RS runs the row
-    constexpr int LPR = (RS >= 32) ? 1 : 32 / RS;
-    const int et = tid % RS, half = tid / RS;
-    if (tid >= RS * LPR) return;
+    // chains each), then combine with a shuffle; lane et < RB runs row et of
+    // each of the NB blocks
+    constexpr int LPR = (RB >= 32) ? 1 : 32 / RB;
+    const int et0 = tid % RB, half = tid / RB;
+    if (tid >= RB * LPR) return;
     const bool etr = HD_NT_TRACE && a.trace && tid == 0;
     const long long ec0 = etr ? clock64() : 0;
     const double* red = m.red + (k & 1) * nred * red_stride;
+#pragma unroll
+    for (int blk = 0; blk < NB; ++blk) {
+    const int et = et0 + blk * RB;
     double r1 = 0.0, rm = 0.0;
     {
       constexpr int per = (NP + LPR - 1) / LPR;
-      const int g0 = half * per, g1 = min(NP, g0 + per);
+      const int g0 = half * per;
       double a1[4] = {0.0, 0.0, 0.0, 0.0}, am[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll 4
-      for (int g = g0; g < g1; ++g) {
-        const int u = (g - g0) & 3;
-        a1[u] += red[g * RS + et];
-        if (MODE == kNtGin) am[u] += red[red_stride + g * RS + et];
+#pragma unroll
+      for (int jg = 0; jg < per; ++jg) {  // compile-time chain index jg & 3
+        const int g = g0 + jg;
+        if (g < NP) {
+          a1[jg & 3] += red[g * RS + et];
+          if (MODE == kNtGin) am[jg & 3] += red[red_stride + g * RS + et];
+        }
       }
       r1 = (a1[0] + a1[1]) + (a1[2] + a1[3]);
       rm = (am[0] + am[1]) + (am[2] + am[3]);
       if (LPR > 1) {
-        for (int sh = RS; sh < 32; sh <<= 1) {
+        for (int sh = RB; sh < 32; sh <<= 1) {
           r1 += __shfl_xor_sync(0xffffffffu, r1, sh);
           if (MODE == kNtGin) rm += __shfl_xor_sync(0xffffffffu, rm, sh);
         }
       }
     }
-    if (half != 0) return;
+    if (LPR > 1 && half != 0) continue;  // (NB == 1 when LPR > 1)
     if (etr) epi_tr[0] += clock64() - ec0;
     const unsigned char* vs = stage_ptr(q) + vec_off;
     double* rb = m.rhs + (k & 1) * 2 * rs;
-    mbar_wait(m.full + q, ph);  // complete (the workers waited for it a slot ago): orders the vector reads
+    if (blk == 0) mbar_wait(m.full + q, ph);  // complete (the workers waited for it a slot ago): orders the vector reads
     const int64_t li = row_of(k) + et;
     const int64_t i = li + a.rm.gdelta;
     const double d = (i < a.Dlen) ? a.D[i] : dtail;
-    (void)kb;
-    (void)bpar;
     if (MODE == kNtFold) {
       const double xv = ld_vec<T>(vs + (size_t)a.vx * rs * 8, sizeof(T), et) * xsc;
       const double p = (i < a.n) ? d * (xv - r1) : 0.0;
@@ -544,13 +578,16 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
       e1 += uu * rhs;   // new S column . x_{t+1}
       rb[et] = rhs;
     }
+    }  // blocks
     if (etr) epi_tr[1] += clock64() - ec0;
   };
   // ---- T phase of sub-tile k (stage q): workers (mapping above)
   auto tphase = [&](int64_t k, int q) {
     if (!t_active) return;
-    constexpr int PPL = RP / 8;  // row pairs per lane per column
-    const double* r0 = m.rhs + (k & 1) * 2 * RS + 2 * tg8;
+    constexpr int PPL = RP / 8;  // row pairs per lane per column and block
+#pragma unroll 1
+    for (int blk = 0; blk < NB; ++blk) {
+    const double* r0 = m.rhs + (k & 1) * 2 * RS + blk * RB + 2 * tg8;
     double2 x[PPL], z[PPL];
 #pragma unroll
     for (int u = 0; u < PPL; ++u) {
@@ -558,7 +595,7 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
       z[u] = make_double2(0.0, 0.0);
       if (MODE == kNtFold) z[u] = *reinterpret_cast<const double2*>(r0 + RS + 16 * u);
     }
-    const T* pr = reinterpret_cast<const T*>(stage_ptr(q)) + cb * RS + 2 * tg8;
+    const T* pr = reinterpret_cast<const T*>(stage_ptr(q)) + cb * RS + blk * RB + 2 * tg8;
     // the thread's column rounds, unrolled to the smallest of 4 / 8 / RMAX
     // that covers them (the accumulators need compile-time indices)
 #define HD_NT_TROUNDS(RM)                                                         \
@@ -579,70 +616,72 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
     } else {
       HD_NT_TROUNDS(RMAX)
     }
+    }  // blocks
 #undef HD_NT_TROUNDS
   };
-  // ---- the slot loop (see the warp roles above)
+  // ---- the slot loop (see the warp roles above): one named barrier per slot;
+  // each role runs its own loop (32-bit counters, stage indices advanced
+  // without divisions)
   if (!producer) named_sync(kNtBarId, kNtConsumers);  // coefficients staged
   if (!producer && !abort_all && nk > 0) {
-    // stage / phase of sub-tile k, advanced without divisions
-    int qN = 0, qE = 0, qT = 0;          // stages of N (k + 1), epilogue (k), T (k - 1)
-    uint32_t phN = 0, phE = 0;
-    int64_t kbE = 0;                     // epilogue: sub-tile index within its draw batch
-    uint32_t bparE = 0;                  // ... and the batch buffer it reads
-    if (worker) nphase(0, 0, 0);
-    qN = (nst > 1) ? 1 : 0;
-    phN = (nst > 1) ? 0u : 1u;
-    named_sync(kNtBarId, kNtConsumers);
+    const int nki = (int)nk;
     // HD_TRACE=3: per-CTA cycle breakdown (epilogue thread 0, worker 0)
     unsigned long long tr[6] = {0, 0, 0, 0, 0, 0};
     const bool trace = HD_NT_TRACE && a.trace && (tid == 0 || wt == 0);
-    for (int64_t j = 0; j <= nk; ++j) {
-      long long c0t = trace ? clock64() : 0, c1t = 0, c2t = 0, c3t = 0;
-      if (epi_thr && j < nk) epilogue(j, qE, phE, kbE, bparE);
-      if (worker) {
-        if (j + 1 < nk) {
+    if (worker) {
+      nphase(0, 0, 0);
+      int qN = (nst > 1) ? 1 : 0, qT = 0;  // stages of N (j + 1) and T (j - 1)
+      uint32_t phN = (nst > 1) ? 0u : 1u;
+      named_sync(kNtBarId, kNtConsumers);
+      for (int j = 0; j <= nki; ++j) {
+        const long long c0t = trace ? clock64() : 0;
+        long long c2t = c0t;
+        if (j + 1 < nki) {
           if (trace) {
-            c1t = clock64();
             mbar_wait(m.full + qN, phN);
             c2t = clock64();
           }
           nphase(j + 1, qN, phN);
         }
-        if (trace) c3t = clock64();
-        if (j >= 1) tphase(j - 1, qT);
-      }
-      const long long c4t = trace ? clock64() : 0;
-      named_sync(kNtBarId, kNtConsumers);  // red of j + 1, rhs of j ready; stage of j - 1 free
-      if (trace) {
-        const long long c5t = clock64();
-        if (tid == 0) {
-          tr[0] += c4t - c0t;  // epilogue
-          tr[1] += c5t - c4t;  // epilogue warp at the barrier
-        } else {
-          if (c1t) {
-            tr[2] += c1t - c0t;  // draw batches
-            tr[3] += c2t - c1t;  // waiting for the stage
-            tr[4] += c3t - c2t;  // N phase
-          }
-          tr[5] += c4t - c3t;    // T phase
-          tr[1] += c5t - c4t;    // workers at the barrier
+        const long long c3t = trace ? clock64() : 0;
+        if (j >= 1) {
+          tphase(j - 1, qT);
+          if (++qT == nst) qT = 0;
+        }
+        const long long c4t = trace ? clock64() : 0;
+        named_sync(kNtBarId, kNtConsumers);  // red of j + 1, rhs of j ready; stage of j - 1 free
+        if (trace) {
+          tr[3] += c2t - c0t;          // waiting for the stage
+          tr[4] += c3t - c2t;          // N phase
+          tr[5] += c4t - c3t;          // T phase
+          tr[1] += clock64() - c4t;    // workers at the barrier
+        }
+        if (++qN == nst) {
+          qN = 0;
+          phN ^= 1u;
         }
       }
-      if (j >= 1) {
-        if (tid == 0) mbar_arrive(m.empty + qT);
-        if (++qT == nst) qT = 0;
-      }
-      if (++qE == nst) {
-        qE = 0;
-        phE ^= 1u;
-      }
-      if (++kbE == CG) {
-        kbE = 0;
-        bparE ^= 1u;
-      }
-      if (++qN == nst) {
-        qN = 0;
-        phN ^= 1u;
+    } else {  // epilogue warps; thread 0 frees the stages
+      named_sync(kNtBarId, kNtConsumers);
+      int qE = 0, qT = 0;  // stages of the epilogue (j) and of T (j - 1)
+      uint32_t phE = 0;
+      for (int j = 0; j <= nki; ++j) {
+        const long long c0t = trace ? clock64() : 0;
+        if (j < nki) epilogue(j, qE, phE);
+        const long long c4t = trace ? clock64() : 0;
+        named_sync(kNtBarId, kNtConsumers);
+        if (trace) {
+          tr[0] += c4t - c0t;          // epilogue
+          tr[1] += clock64() - c4t;    // epilogue warp at the barrier
+        }
+        if (j >= 1) {
+          if (tid == 0) mbar_arrive(m.empty + qT);
+          if (++qT == nst) qT = 0;
+        }
+        if (++qE == nst) {
+          qE = 0;
+          phE ^= 1u;
+        }
       }
     }
     if (trace) {
@@ -651,14 +690,13 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
         a.trace[1 * gridDim.x + blockIdx.x] += tr[1];
         a.trace[8 * gridDim.x + blockIdx.x] += epi_tr[0];
         a.trace[9 * gridDim.x + blockIdx.x] += epi_tr[1];
+        a.trace[7 * gridDim.x + blockIdx.x] += (unsigned long long)nk;
       } else {
         a.trace[6 * gridDim.x + blockIdx.x] += tr[1];
-        a.trace[2 * gridDim.x + blockIdx.x] += tr[2];
         a.trace[3 * gridDim.x + blockIdx.x] += tr[3];
         a.trace[4 * gridDim.x + blockIdx.x] += tr[4];
         a.trace[5 * gridDim.x + blockIdx.x] += tr[5];
       }
-      if (tid == 0) a.trace[7 * gridDim.x + blockIdx.x] += (unsigned long long)nk;
     }
   }
   // ---- partial sums -> slot row (fixed order) -> group flush; the stages
@@ -697,7 +735,7 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
     const int slot = tid == 0 ? a.slot_r0 : tid == 1 ? a.slot_r1 : tid == 2 ? a.slot_r2 : a.slot_r3;
     if (slot >= 0) {
       double v = 0.0;
-      for (int t = 0; t < rs; ++t) v += sc[tid * kNtConsumers + t];
+      for (int t = 0; t < RB; ++t) v += sc[tid * kNtConsumers + t];
       acc[slot] = v;
     }
   }
