@@ -48,10 +48,6 @@ constexpr int kNtMaxVecs = 5;
 constexpr int kNtMaxStages = 16;
 constexpr int kNtMaxCols = 512;                     // columns of an output pass
 constexpr int kNtMaxFoldCols = 288;                 // columns of a fold pass
-// T-phase column rounds per worker thread (8 lanes per column, WT / 8 columns
-// per round; WT >= kNtConsumers - 64 workers)
-constexpr int kNtGinRounds = (kNtMaxCols * 8 + (kNtConsumers - 64) - 1) / (kNtConsumers - 64);
-constexpr int kNtFoldRounds = (kNtMaxFoldCols * 8 + (kNtConsumers - 64) - 1) / (kNtConsumers - 64);
 constexpr int kNtBarId = 1;                         // named barrier of the consumer warps
 
 enum NtMode : int { kNtFold = 0, kNtGin = 1 };
@@ -219,20 +215,30 @@ __device__ __forceinline__ double ld_vec(const unsigned char* slot, int esz, int
 // In "slot" j the epilogue warps finish sub-tile j while the workers run the
 // N phase of j + 1 and the T phase of j - 1 — one barrier per slot, so the
 // row-serial epilogue is off the critical path.
-__host__ __device__ inline int nt_ewarps(int rs) { return rs <= 32 ? 1 : 2; }
-__host__ __device__ inline int nt_workers(int rs) { return kNtConsumers - 32 * nt_ewarps(rs); }
+__host__ __device__ constexpr int nt_ewarps(int rs) { return rs <= 32 ? 1 : 2; }
+__host__ __device__ constexpr int nt_workers(int rs) { return kNtConsumers - 32 * nt_ewarps(rs); }
+// Column capacity of a pass with sub-tiles of rs rows (the stage-size rule
+// keeps C * rs * 8 B near 56 KB): the per-thread register arrays below are
+// sized from it, and nt_shape takes a shorter sub-tile for a wider pass.
+__host__ __device__ constexpr int nt_max_cols(int mode, int rs) {
+  return (mode == kNtFold && 8192 / rs > kNtMaxFoldCols) ? kNtMaxFoldCols : 8192 / rs;
+}
+// N-phase column groups (workers per row pair) and the columns one worker
+// thread owns at most; T-phase columns per round (8 lanes each) and rounds
+__host__ __device__ constexpr int nt_ngroups(int rs) { return nt_workers(rs) / ((rs > 64 ? 64 : rs) / 2); }
+__host__ __device__ constexpr int nt_ncols(int mode, int rs) {
+  return (nt_max_cols(mode, rs) + nt_ngroups(rs) - 1) / nt_ngroups(rs);
+}
+__host__ __device__ constexpr int nt_trounds(int mode, int rs) {
+  return (nt_max_cols(mode, rs) + nt_workers(rs) / 8 - 1) / (nt_workers(rs) / 8);
+}
 
-// N-phase coefficient entries (one per column)
-__host__ __device__ inline int nt_coef_len(int C, int rs) { (void)rs; return C; }
 
 // Shared-memory carve-up (sized per launch): [stages][stage_bytes] | N-phase
-// coefficients (fold: beta1 [cl]; output pass: pairs [cl][2], O columns
-// (beta1, -beta3), S columns (0, coefS); cl = nt_coef_len) | N-phase partials
-// [2][1 or 2][NP][rs] | rhs [2][2][rs] | barriers. The T-phase partials, the
-// scalar partials and the slot row reuse the stages at the end.
+// partials [2][1 or 2][NP][rs] | rhs [2][2][rs] | barriers. The T-phase
+// partials, the scalar partials and the slot row reuse the stages at the end.
 struct NtSmem {
   unsigned char* stages;
-  double* cf;
   double* red;
   double* rhs;
   uint64_t* full;
@@ -241,9 +247,9 @@ struct NtSmem {
 
 __host__ __device__ inline size_t nt_fixed_doubles(int mode, int C, int kP0, int rs) {
   (void)kP0;
-  const size_t b = (size_t)((nt_coef_len(C, rs) + 1) & ~1) * (mode == kNtGin ? 2 : 1);
+  (void)C;
   const size_t np_rs = (size_t)(nt_workers(rs) / 32) * rs;  // NP partials x rs rows per array
-  return b + 2 * (mode == kNtGin ? 2 : 1) * np_rs + 4 * (size_t)rs;
+  return 2 * (mode == kNtGin ? 2 : 1) * np_rs + 4 * (size_t)rs;
 }
 
 __host__ __device__ inline size_t nt_fixed_bytes(int mode, int C, int kP0, int rs, int nst) {
@@ -262,8 +268,7 @@ __device__ __forceinline__ NtSmem nt_smem(unsigned char* base, int mode, int C, 
   m.stages = base;
   double* p = reinterpret_cast<double*>(base + (size_t)nst * stage_bytes);
   (void)kP0;
-  m.cf = p;
-  p += (size_t)((nt_coef_len(C, rs) + 1) & ~1) * (mode == kNtGin ? 2 : 1);
+  (void)C;
   const int np_rs = (nt_workers(rs) / 32) * rs;
   m.red = p; p += 2 * (mode == kNtGin ? 2 : 1) * np_rs;
   m.rhs = p; p += 4 * rs;
@@ -357,21 +362,6 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
   }
   // ------------------------------------------------------------ consumers
   const int kP0 = a.kP0;
-  if (!producer) {
-    // one coefficient entry per column: n1 = W beta1 (O or F columns),
-    // nm = S coefS - W_O beta3 (output pass: one sum over both panels)
-    const int cl = nt_coef_len(C, RS);
-    for (int c = tid; c < cl; c += kNtConsumers) {
-      if (MODE == kNtGin) {
-        double2 v = make_double2(0.0, 0.0);
-        if (c < kP0) v = make_double2(a.beta1[c], -a.beta3[c]);
-        else if (c < C) v.y = a.coefS[c - kP0];
-        reinterpret_cast<double2*>(m.cf)[c] = v;
-      } else {
-        m.cf[c] = (c < C) ? a.beta1[c] : 0.0;
-      }
-    }
-  }
   // worker T-phase mapping: 8 consecutive lanes share a column (lane g of the
   // 8 takes row pairs g, g + 8, ... of the sub-tile: 128 contiguous bytes per
   // quarter warp, conflict-free, and each right-hand-side pair is loaded once
@@ -381,7 +371,7 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
   const int cb = wt >> 3, tg8 = wt & 7;
   const int Rt = (C > cb) ? (C - cb + NCOL - 1) / NCOL : 0;  // this thread's column rounds
   const bool t_active = worker && C > 0 && a.do_t;
-  constexpr int RMAX = (MODE == kNtFold) ? kNtFoldRounds : kNtGinRounds;
+  constexpr int RMAX = nt_trounds(MODE, RS);
   double tA[RMAX], tB[RMAX];
 #pragma unroll
   for (int r = 0; r < RMAX; ++r) {
@@ -396,6 +386,30 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
   constexpr int NP = (RP >= 32) ? CG : WT / 32;         // N-phase partials per row
   const int npart = (RP >= 32) ? ncg : (wt >> 5);         // this thread's partial index
   const int cga = (int)((int64_t)C * ncg / CG), cgb = (int)((int64_t)C * (ncg + 1) / CG);
+  const int kc = cgb - cga;  // <= KN
+  constexpr int KN = nt_ncols(MODE, RS);
+  // the thread's N-phase coefficients, in registers for the whole launch:
+  // n1 = W beta1 (O or F columns), nm = S coefS - W_O beta3 (output pass: one
+  // sum over both panels: O columns (beta1, -beta3), S columns (0, coefS))
+  double cfa[KN], cfb[KN];
+#pragma unroll
+  for (int r = 0; r < KN; ++r) {
+    const int c = cga + r;
+    cfa[r] = 0.0;
+    cfb[r] = 0.0;
+    if (worker && r < kc) {
+      if (MODE == kNtGin) {
+        if (c < kP0) {
+          cfa[r] = a.beta1[c];
+          cfb[r] = -a.beta3[c];
+        } else {
+          cfb[r] = a.coefS[c - kP0];
+        }
+      } else {
+        cfa[r] = a.beta1[c];
+      }
+    }
+  }
   constexpr int nred = (MODE == kNtGin) ? 2 : 1;
   const int red_stride = NP * RS;  // one partial array: NP x rs doubles
   // epilogue scalar accumulators
@@ -422,25 +436,19 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
       n1[b] = make_double2(0.0, 0.0);
       nm[b] = make_double2(0.0, 0.0);
     }
-#pragma unroll 4
-    for (int c = cga; c < cgb; ++c) {  // one 2-row load per column and block, coefficients broadcast
-      if (MODE == kNtGin) {
-        const double2 cf = reinterpret_cast<const double2*>(m.cf)[c];
+    const T* sc0 = sp + cga * RS;
+#pragma unroll
+    for (int r = 0; r < KN; ++r) {  // one 2-row load per column and block, coefficients in registers
+      if (r < kc) {
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
-          const double2 v = lds_pair(sp + c * RS + b * RB);
-          n1[b].x = fma(v.x, cf.x, n1[b].x);
-          n1[b].y = fma(v.y, cf.x, n1[b].y);
-          nm[b].x = fma(v.x, cf.y, nm[b].x);
-          nm[b].y = fma(v.y, cf.y, nm[b].y);
-        }
-      } else {
-        const double cf = m.cf[c];
-#pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          const double2 v = lds_pair(sp + c * RS + b * RB);
-          n1[b].x = fma(v.x, cf, n1[b].x);
-          n1[b].y = fma(v.y, cf, n1[b].y);
+          const double2 v = lds_pair(sc0 + r * RS + b * RB);
+          n1[b].x = fma(v.x, cfa[r], n1[b].x);
+          n1[b].y = fma(v.y, cfa[r], n1[b].y);
+          if (MODE == kNtGin) {
+            nm[b].x = fma(v.x, cfb[r], nm[b].x);
+            nm[b].y = fma(v.y, cfb[r], nm[b].y);
+          }
         }
       }
     }
@@ -622,7 +630,6 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
   // ---- the slot loop (see the warp roles above): one named barrier per slot;
   // each role runs its own loop (32-bit counters, stage indices advanced
   // without divisions)
-  if (!producer) named_sync(kNtBarId, kNtConsumers);  // coefficients staged
   if (!producer && !abort_all && nk > 0) {
     const int nki = (int)nk;
     // HD_TRACE=3: per-CTA cycle breakdown (epilogue thread 0, worker 0)
