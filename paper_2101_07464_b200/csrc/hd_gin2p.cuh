@@ -132,6 +132,7 @@ struct NtArgs {
   int* status = nullptr;
   int prefetch = 0;
   int evict = 0;      // L2 policy of the panel boxes (nt_l2_policy)
+  int sched = 1;      // slot schedule (k_nt_impl): 0 T of j - 1 in slot j, 1 T of j in slot j
   int deal = 0;       // sub-tile order (k_nt_impl: 0 round robin, 1 by tile)
   unsigned long long* trace = nullptr;  // HD_TRACE=3: [8][grid] cycle counters
 };
@@ -243,6 +244,7 @@ struct NtSmem {
   double* rhs;
   uint64_t* full;
   uint64_t* empty;
+  uint64_t* rdy;  // [2] rhs of sub-tile j ready (sched 1)
 };
 
 __host__ __device__ inline size_t nt_fixed_doubles(int mode, int C, int kP0, int rs) {
@@ -253,7 +255,7 @@ __host__ __device__ inline size_t nt_fixed_doubles(int mode, int C, int kP0, int
 }
 
 __host__ __device__ inline size_t nt_fixed_bytes(int mode, int C, int kP0, int rs, int nst) {
-  return sizeof(double) * nt_fixed_doubles(mode, C, kP0, rs) + 2 * (size_t)nst * sizeof(uint64_t) + 128;
+  return sizeof(double) * nt_fixed_doubles(mode, C, kP0, rs) + (2 * (size_t)nst + 2) * sizeof(uint64_t) + 128;
 }
 
 // Bytes of the stage ring the final flush reuses: T partials [WT][6], scalar
@@ -274,6 +276,7 @@ __device__ __forceinline__ NtSmem nt_smem(unsigned char* base, int mode, int C, 
   m.rhs = p; p += 4 * rs;
   m.full = reinterpret_cast<uint64_t*>(p);
   m.empty = m.full + nst;
+  m.rdy = m.empty + nst;
   return m;
 }
 
@@ -308,6 +311,8 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
       mbar_init(m.full + q, 1);
       mbar_init(m.empty + q, 1);
     }
+    mbar_init(m.rdy, E);
+    mbar_init(m.rdy + 1, E);
     mbar_fence_init();
   }
   __syncthreads();
@@ -635,7 +640,62 @@ __device__ __forceinline__ void k_nt_impl(const NtArgs<T>& a) {
     // HD_TRACE=3: per-CTA cycle breakdown (epilogue thread 0, worker 0)
     unsigned long long tr[6] = {0, 0, 0, 0, 0, 0};
     const bool trace = HD_NT_TRACE && a.trace && (tid == 0 || wt == 0);
-    if (worker) {
+    if (a.sched == 1 && worker) {
+      // slot j: N of j + 1, then (once the epilogue warps publish it) the T
+      // phase of j from its rhs: a stage is held for two slots, not three
+      nphase(0, 0, 0);
+      int qN = (nst > 1) ? 1 : 0, qT = 0;  // stages of N (j + 1) and T (j)
+      uint32_t phN = (nst > 1) ? 0u : 1u;
+      named_sync(kNtBarId, kNtConsumers);
+      for (int j = 0; j < nki; ++j) {
+        const long long c0t = trace ? clock64() : 0;
+        long long c2t = c0t;
+        if (j + 1 < nki) {
+          if (trace) {
+            mbar_wait(m.full + qN, phN);
+            c2t = clock64();
+          }
+          nphase(j + 1, qN, phN);
+        }
+        const long long c3t = trace ? clock64() : 0;
+        mbar_wait(m.rdy + (j & 1), (uint32_t)(j >> 1) & 1u);
+        tphase(j, qT);
+        if (++qT == nst) qT = 0;
+        const long long c4t = trace ? clock64() : 0;
+        named_sync(kNtBarId, kNtConsumers);  // red of j + 1 ready; stage of j free
+        if (trace) {
+          tr[3] += c2t - c0t;
+          tr[4] += c3t - c2t;
+          tr[5] += c4t - c3t;
+          tr[1] += clock64() - c4t;
+        }
+        if (++qN == nst) {
+          qN = 0;
+          phN ^= 1u;
+        }
+      }
+    } else if (a.sched == 1) {  // epilogue warps; thread 0 frees the stages
+      named_sync(kNtBarId, kNtConsumers);
+      int qE = 0;
+      uint32_t phE = 0;
+      for (int j = 0; j < nki; ++j) {
+        const long long c0t = trace ? clock64() : 0;
+        epilogue(j, qE, phE);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(m.rdy + (j & 1));
+        const long long c4t = trace ? clock64() : 0;
+        named_sync(kNtBarId, kNtConsumers);
+        if (trace) {
+          tr[0] += c4t - c0t;
+          tr[1] += clock64() - c4t;
+        }
+        if (tid == 0) mbar_arrive(m.empty + qE);
+        if (++qE == nst) {
+          qE = 0;
+          phE ^= 1u;
+        }
+      }
+    } else if (worker) {
       nphase(0, 0, 0);
       int qN = (nst > 1) ? 1 : 0, qT = 0;  // stages of N (j + 1) and T (j - 1)
       uint32_t phN = (nst > 1) ? 0u : 1u;
