@@ -156,14 +156,14 @@ def gin_case(orc):
     return x1, ref, {"f64": env64, "f32": stepnoise_envelope(orc, make, T3, x1, ref, 6e-8)}
 
 
-@pytest.mark.parametrize("two_pass", ["auto", "1"])
+@pytest.mark.parametrize("two_pass", ["auto", "0"])
 def test_config3_ginibre_1e5_T100_every_iterate_f64(lm, gin_case, env_flags, two_pass):
     # every iterate within max(1e-9, 10 x the oracle's envelope at fp64
     # rounding): the north star's 1e-9 while the run is well conditioned, the
-    # oracle's own chaos bound once it is not; at this n the three-pass probes
-    # are the default, HD_GIN2P=1 forces the two-pass sequence
-    if two_pass == "1":
-        env_flags(HD_GIN2P="1")
+    # oracle's own chaos bound once it is not; fp64 runs take the two-pass
+    # sequence by default, HD_GIN2P=0 the three-pass probes
+    if two_pass == "0":
+        env_flags(HD_GIN2P="0")
     x1, ref, env = gin_case
     tol = np.maximum(1e-9, 10.0 * env["f64"])
     op = lm.GinibreOperator(N3, N3, N3 ** -0.5, SEED3, draws="reference", capacity=T3)
@@ -191,12 +191,14 @@ def test_config3_ginibre_1e5_T100_f32_within_its_horizon(lm, gin_case):
     assert np.all(np.isfinite(traj)) and np.max(np.abs(norms - 1.0)) < 1e-5
 
 
-@pytest.mark.parametrize("two_pass", ["auto", "1"])
+@pytest.mark.parametrize("two_pass", ["auto", "0"])
 def test_config3_batched_trial_matches_oracle_on_philox_draws(orc, lm, env_flags, two_pass):
     import torch
 
-    if two_pass == "1":  # the batched twins of the two-pass kernels (tensor maps in the argument table)
-        env_flags(HD_GIN2P="1")
+    # auto: the batched twins of the two-pass kernels (tensor maps in the
+    # argument table); HD_GIN2P=0: the batched three-pass kernels
+    if two_pass == "0":
+        env_flags(HD_GIN2P="0")
 
     B, seeds = 4, [SEED3 + b for b in range(4)]
     ops = [lm.GinibreOperator(N3, N3, N3 ** -0.5, s, capacity=T3) for s in seeds]
