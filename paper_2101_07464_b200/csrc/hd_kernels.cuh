@@ -66,7 +66,10 @@ __device__ __forceinline__ void flush_row(const double* acc, int nslots, const F
 // refills the slot. No inter-warp synchronisation in the streaming loop;
 // per-warp slot rows keep the GEMV-T sums deterministic.
 constexpr int kCW = 4;
-constexpr int kRing = 3;
+#ifndef HD_KRING
+#define HD_KRING 3
+#endif
+constexpr int kRing = HD_KRING;
 constexpr int kMaxWarps = 8;
 
 template <typename T>

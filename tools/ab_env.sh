@@ -2,6 +2,8 @@
 # On the GPU box: alternate variants of the config-4 AMP run (tools/amp_profile.py)
 # given as "LABEL:ENV=V,ENV=V" arguments, REPS rounds -> gpurun_out/ab_env.txt
 # e.g. tools/ab_env.sh "base:HD_LIB=ab/A.so" "new:HD_LIB=ab/B.so,HD_NT_EVICT=1"
+# AB_BENCH="--workload config2": time bench.py with those arguments instead
+# (its ms_per_step).
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 out=gpurun_out/ab_env.txt
@@ -9,7 +11,11 @@ out=gpurun_out/ab_env.txt
 for i in $(seq ${REPS:-2}); do
   for v in "$@"; do
     label=${v%%:*}; envs=${v#*:}
-    ms=$(env $(echo "$envs" | tr ',' ' ') AP_PROF=0 python tools/amp_profile.py 2>&1 | grep '"ms"' | tr -dc '0-9.')
+    if [ -n "$AB_BENCH" ]; then
+      ms=$(env $(echo "$envs" | tr ',' ' ') python bench.py $AB_BENCH --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; print(json.loads(sys.stdin.read())['ms_per_step'])")
+    else
+      ms=$(env $(echo "$envs" | tr ',' ' ') AP_PROF=0 python tools/amp_profile.py 2>&1 | grep '"ms"' | tr -dc '0-9.')
+    fi
     echo "$label $ms" >> $out
   done
 done
