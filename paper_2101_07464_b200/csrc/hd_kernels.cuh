@@ -168,9 +168,12 @@ struct DotArgs {
 // Columns per chunk: 4 for fp64, 8 for fp32, so a chunk is 8 KB either way
 // and the per-chunk costs (barrier wait, butterfly, slot update) are spread
 // over the same bytes (fp32: 3.0 -> see DESIGN.md §4.2a).
+#ifndef HD_CW64
+#define HD_CW64 4  // fp64 columns per chunk (A/B builds: 2)
+#endif
 template <typename T>
 __host__ __device__ constexpr int chunk_cols() {
-  return sizeof(T) == 8 ? 4 : 8;
+  return sizeof(T) == 8 ? HD_CW64 : 8;
 }
 
 template <typename T>
@@ -182,7 +185,11 @@ __host__ __device__ constexpr size_t ring_bytes() {
 // for col0 + u < lim (fixed butterfly order: deterministic).
 template <int CW>
 __device__ __forceinline__ void add_chunk_sums(const double* d, int lane, int col0, int lim, double* dst) {
-  if constexpr (CW == 4) {
+  if constexpr (CW == 2) {
+    const double f = warp_sum2(d[0], d[1], lane);
+    const int u = lane >> 4;
+    if ((lane & 15) == 0 && col0 + u < lim) dst[col0 + u] += f;
+  } else if constexpr (CW == 4) {
     const double f = warp_sum4(d[0], d[1], d[2], d[3], lane);
     const int u = lane >> 3;
     if ((lane & 7) == 0 && col0 + u < lim) dst[col0 + u] += f;
