@@ -37,6 +37,10 @@ enum FusedSlot { kScDold = 7, kScNrm2e = 8 };
 // update x_{t+1} for the lane's rows, then stream the FOLD chain: GEMV-N
 // p = D_old (x_t − P_F β_F) and GEMV-T P_F^T x_{t+1} from the same chunks; the
 // new fold column p[off+1:]·2^-e is written and dotted with x_{t+1}.
+#ifndef HD_GEN_IN_F
+#define HD_GEN_IN_F 1  // the next tile's draw is generated during the fold-chain chunks (config 2: 15.37 -> 15.25 ms; 0: during the other chain's)
+#endif
+
 template <typename T>
 struct FusedArgs {
   // other chain
@@ -263,9 +267,9 @@ __device__ __forceinline__ void k_haar2p_impl(const FusedArgs<T>& a) {
       __syncwarp();
       if (lane == 0 && it + kRing < nst) issue(it + kRing);
       if (spec) add_chunk_sums<kCW>(d, lane, col0, a.ncolsO, acc + a.slot_spec);
-      if (gen_next && c < 4) gen(next, c);
+      if (!HD_GEN_IN_F && gen_next && c < 4) gen(next, c);
     }
-    if (gen_next)
+    if (!HD_GEN_IN_F && gen_next)
       for (int q = nchO; q < 4; ++q) gen(next, q);
     // ---- y = D_O z - acc and the update x_{t+1} (rows >= n stay zero)
 #pragma unroll
@@ -349,7 +353,10 @@ __device__ __forceinline__ void k_haar2p_impl(const FusedArgs<T>& a) {
       __syncwarp();
       if (lane == 0 && it + kRing < nst) issue(it + kRing);
       add_chunk_sums<kCW>(d, lane, col0, a.ncolsF, acc + a.slot_aF);
+      if (HD_GEN_IN_F && gen_next && c < 4) gen(next, c);
     }
+    if (HD_GEN_IN_F && gen_next)
+      for (int q = nchF; q < 4; ++q) gen(next, q);
     // ---- the new fold column: rows > off from p (row off: the stage wrote
     // the pivot entry), its exact ||p[off:]||^2 and its dot with x_{t+1}
 #pragma unroll
