@@ -158,6 +158,20 @@ struct BatchRec {
 };
 struct BatchPlan;
 
+// Shape and schedule knobs of the two-pass kernels (hd_gin2p_host.inc), read
+// from the environment when an operator is created (A/B measurements, tests):
+// HD_NT_STAGE_KB, HD_NT_MAX_RS, HD_NT_MIN_STAGES, HD_NT_SCHED, HD_NT_L2PROMO,
+// HD_NT_EVICT, HD_NT_DEAL.
+struct NtKnobs {
+  int stage_kb = 56;   // target stage size; 48 -> 56 KB: config 4 2.689 -> 2.661 s
+  int max_rs = 256;    // tallest sub-tile (16..256 rows)
+  int min_stages = 4;  // below this stage count a shorter sub-tile is taken
+  int sched = -1;      // slot schedule: -1 auto (two-slot at 4 stages), 0 / 1 forced
+  int l2promo = -1;    // L2 promotion bytes of the boxes: -1 auto (the column segment)
+  int evict = 0;       // panel boxes evict_first (0) or evict_normal (1)
+  int deal = 0;        // sub-tiles round robin (0) or by tile (1)
+};
+
 struct hd_op {
   hd_config cfg{};
   int ens = 0;
@@ -188,6 +202,7 @@ struct hd_op {
   FlushBufs fbD, fbF, fbO;      // group partials / per-CTA scratch / tickets
   FlushBufs fbA[2], fbB;        // two-pass Ginibre: fold passes (ping-pong) and output passes
   double* drawbuf[2] = {nullptr, nullptr};  // two-pass Ginibre: device draws of a probe (io_len each)
+  NtKnobs nt;                   // two-pass kernel shapes (HD_NT_* environment)
   int gin2p = 1;                // two-pass Ginibre / GOE runs: 1 auto, 2 forced (HD_GIN2P=1), 0 off (HD_GIN2P=0)
   size_t flush_slots = 0;       // slot capacity of the buffers above
   double* red = nullptr;
