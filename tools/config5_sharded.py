@@ -1,10 +1,12 @@
 """BASELINE config 5 — spiked GOE power method x <- (Q x + theta <u,x> u)/||.||,
 inner sigma = 1/sqrt(n), theta = 2, T = 256 GOE steps — with the operator
 row-sharded across the ranks of a torchrun job (one GPU each): every rank
-owns a row slab (lazymat.shard_plan), the probes exchange over NCCL
-(lazymat.nccl_exchange) and the spike dot / norms are torch.distributed
-all-reduces. Quoted at n = 1e8 on 8 GPUs; C5_N sets n (default 1.25e7 per
-rank, i.e. weak scaling to 1e8 at 8 ranks).
+owns a row slab (lazymat.shard_plan) and runs the whole dynamics device-
+resident (lazymat.spiked_power -> hd_run_spiked): the probes' partial dots and
+the map's sums (<u, x>, ||g||^2) travel in the operator's NCCL exchange
+(lazymat.nccl_exchange), so the loop has no torch.distributed calls and no
+per-probe host synchronisation. Quoted at n = 1e8 on 8 GPUs; C5_N sets n
+(default 1.25e7 per rank, i.e. weak scaling to 1e8 at 8 ranks).
 
   torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/config5_sharded.py
 """
@@ -21,7 +23,7 @@ from paper_2101_07464_b200 import lazymat
 
 
 def main():
-    dist.init_process_group("nccl")
+    dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
     rank, world = dist.get_rank(), dist.get_world_size()
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
     n = int(float(os.environ.get("C5_N", 12_500_000 * world)))
@@ -37,21 +39,12 @@ def main():
     u, x = (u / u.norm())[lo:hi].clone(), (x / x.norm())[lo:hi].clone()
     torch.cuda.empty_cache()
 
-    def gsum(t):
-        dist.all_reduce(t)
-        return t
-
-    ov = torch.empty(T, dtype=torch.float64, device="cuda")
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
     e0.record()
-    for t in range(T):
-        gx = op.probe(x, "right")
-        gx += theta * gsum(torch.dot(u, x).reshape(1)) * u
-        x = gx / torch.sqrt(gsum(torch.dot(gx, gx).reshape(1)))
-        ov[t] = gsum(torch.dot(u, x).reshape(1))[0]
+    x, ov = lazymat.spiked_power(op, u, x, T, theta=theta)
     e1.record()
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
