@@ -201,11 +201,16 @@ def test_sharded_faults_and_reference_draws(orc, lm, ens, kw):
         assert rel(np.concatenate([outs[0][t], outs[1][t]]), want[t]) < 1e-10, t
 
 
+@pytest.mark.parametrize("two_pass", ["auto", "0"])
 @pytest.mark.parametrize("S", [2, 3])
-def test_sharded_spiked_power_run_matches_oracle(orc, lm, S):
+def test_sharded_spiked_power_run_matches_oracle(orc, lm, S, two_pass, monkeypatch):
     # config 5's workload row-sharded (virtual shards, one host thread each):
     # the GOE probes exchange their partial dots, the spike's <u, g> and ||g||^2
-    # travel through the same exchange, every shard derives the same scalars
+    # travel through the same exchange, every shard derives the same scalars;
+    # fp64 runs take the two-pass kernels (one exchange per pass),
+    # HD_GIN2P=0 the three-pass probes
+    if two_pass == "0":
+        monkeypatch.setenv("HD_GIN2P", "0")
     n, T, seed = 2400, 14, 71
     u = orc.RandomSource(seed, 1).normal_vector(n)
     u /= np.linalg.norm(u)
@@ -214,14 +219,16 @@ def test_sharded_spiked_power_run_matches_oracle(orc, lm, S):
     xr, ovr = orc.Operator("goe", n=n, sigma=n ** -0.5, seed=seed).spiked_power(u, x1, T)
     draws = orc.draws_for(seed, [n] * (2 * T))
     ex = lm.Exchange.local(S)
-    outs, errs = [None] * S, []
+    outs, errs, kinds = [None] * S, [], [None] * S
 
     def worker(r):
         try:
             op = lm.GOEOperator(n, seed, sigma=n ** -0.5, draws="injected", capacity=T, shard=(r, S), exchange=ex)
             op.push_draws(draws)
+            op.set_profiling(True)
             lo, hi = op.shard_range("cols")
             outs[r] = lm.spiked_power(op, u[lo:hi], x1[lo:hi], T)
+            kinds[r] = set(op.kernel_stats())
         except Exception as e:  # noqa: BLE001
             errs.append((r, e))
 
@@ -236,3 +243,4 @@ def test_sharded_spiked_power_run_matches_oracle(orc, lm, S):
     assert rel(x, xr) < 1e-9
     for r in range(S):
         assert np.max(np.abs(outs[r][1] - ovr)) < 1e-9
+        assert ("gin2p" in kinds[r]) == (two_pass == "auto")
