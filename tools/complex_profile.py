@@ -1,8 +1,9 @@
 import os, sys
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, json
 from paper_2101_07464_b200 import lazymat
-n, T = 1_000_000, 30
+n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 1_000_000
+T = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 op = lazymat.HaarOperator(n, seed=1, dtype="c128", capacity=T)
 op.set_profiling(True)
 x = torch.randn(n, dtype=torch.complex128, device="cuda"); x /= x.norm()
