@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include "hd_complex.cuh"
+#include "hd_complex_fused.cuh"
 #include "hd_refrng.hpp"
 #include "hd_shard.cuh"
 

@@ -143,3 +143,103 @@ def test_complex_user_dynamics(orc, lm):
     traj = lm.run_dynamics(op, spec)
     for t in range(T + 1):
         assert rel(traj[t].cpu().numpy(), want[t]) < 1e-9, t
+
+
+# ---- fused Haar probe (csrc/hd_complex_fused.cuh): four panel passes, the fold
+# member's Gram column from the k x k Gram matrix and the t x k head corner
+@pytest.mark.parametrize("n,T,cap", [(5000, 120, 4), (1300, 200, 64)])
+def test_complex_haar_long_chain_vs_oracle(orc, lm, n, T, cap):
+    # long chains, capacity doubling on the way (W, T, G and D grow), mixed sides
+    seed = 11 + n
+    rng = np.random.default_rng(seed)
+    ref = orc.COperator("haar", n=n, seed=seed)
+    op = lm.HaarOperator(n, seed=seed, dtype="c128", draws="injected", capacity=cap)
+    op.push_draws(orc.complex_draws_for(seed, [n] * T).view(np.complex128))
+    aux = orc.RandomSource(seed + 1)
+    x = aux.normal_complex_vector(n)
+    x /= np.linalg.norm(x)
+    worst = 0.0
+    for t in range(T):
+        s = "right" if rng.random() < 0.7 else "left"
+        got, want = op.probe(x, s), ref.probe(x, s)
+        worst = max(worst, rel(got, want))
+        # the iterate plus a fresh component: Q^H (Q x) alone would fold onto an exactly
+        # zero tail (a reflector built from rounding noise, in the reference too)
+        x = want / np.linalg.norm(want) + 0.5 * aux.normal_complex_vector(n) / np.sqrt(n)
+    assert worst < 1e-10, worst
+
+
+@pytest.mark.parametrize("skip", [False, True])
+def test_complex_haar_fused_matches_generic_sequence(orc, lm, monkeypatch, skip):
+    n, T, seed = 3001, 40, 23
+    draws = orc.complex_draws_for(seed, [n] * T).view(np.complex128)
+    ref = orc.COperator("haar", n=n, seed=seed, skip_reflector=skip)
+    ops = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("HD_CX_FUSED", flag)  # read at hd_create
+        ops[flag] = lm.HaarOperator(n, seed=seed, dtype="c128", draws="injected", capacity=T, skip_reflector=skip)
+        ops[flag].push_draws(draws)
+    aux = orc.RandomSource(seed + 1)
+    x = aux.normal_complex_vector(n)
+    for t in range(T):
+        s = "left" if t % 5 == 3 else "right"
+        a, b, want = ops["1"].probe(x, s), ops["0"].probe(x, s), ref.probe(x, s)
+        assert rel(a, b) < 1e-11, (t, rel(a, b))
+        assert rel(a, want) < 1e-10, (t, rel(a, want))
+        x = want / np.linalg.norm(want) + 0.5 * aux.normal_complex_vector(n) / np.sqrt(n)
+    assert ops["1"].launch_count() < ops["0"].launch_count() / 2
+
+
+def test_complex_haar_fused_reset_and_budget_edge(orc, lm):
+    # every probe of the budget (the last tail has one row), then a reset run
+    n, seed = 37, 5
+    op = lm.HaarOperator(n, seed=seed, dtype="c128", draws="injected", capacity=2)
+    for rep in range(2):
+        ref = orc.COperator("haar", n=n, seed=seed)
+        op.push_draws(orc.complex_draws_for(seed, [n] * n).view(np.complex128))
+        aux = orc.RandomSource(seed + rep)
+        for t in range(n):
+            x = aux.normal_complex_vector(n)
+            s = "right" if t % 2 else "left"
+            assert rel(op.probe(x, s), ref.probe(x, s)) < 1e-10, (rep, t)
+        with pytest.raises(lm.BudgetExhausted):
+            op.probe(x, "right")
+        op.reset()
+
+
+def test_complex_haar_flagged_device_input_leaves_the_operator_untouched(orc, lm):
+    # device inputs are validated by a device flag the state-changing kernels test; a
+    # rejected probe must not advance the operator (operators.hpp:44-48)
+    import torch
+
+    n, seed, T = 700, 31, 9
+    draws = orc.complex_draws_for(seed, [n] * T).view(np.complex128)
+    ref = orc.COperator("haar", n=n, seed=seed)
+    op = lm.HaarOperator(n, seed=seed, dtype="c128", draws="injected", capacity=4)
+    op.push_draws(draws)
+    aux = orc.RandomSource(seed + 1)
+    for t in range(T):
+        x = aux.normal_complex_vector(n)
+        if t in (0, 4, 5):
+            bad = x.copy()
+            bad[(7 * t) % n] = complex(0.0, np.inf)
+            before = op.remaining_probes
+            with pytest.raises(ValueError, match="non-finite"):
+                op.probe(torch.from_numpy(bad).cuda(), "right")
+            assert op.remaining_probes == before
+        s = "left" if t % 3 == 1 else "right"
+        got = op.probe(torch.from_numpy(x).cuda(), s).cpu().numpy()
+        assert rel(got, ref.probe(x, s)) < 1e-10, t
+
+
+def test_complex_haar_two_rows_per_thread_variant(orc, lm, monkeypatch):
+    monkeypatch.setenv("HD_CX_NROWS", "2")
+    n, seed, T = 2500, 41, 24
+    ref = orc.COperator("haar", n=n, seed=seed)
+    op = lm.HaarOperator(n, seed=seed, dtype="c128", draws="injected", capacity=T)
+    op.push_draws(orc.complex_draws_for(seed, [n] * T).view(np.complex128))
+    aux = orc.RandomSource(seed + 1)
+    for t in range(T):
+        x = aux.normal_complex_vector(n)
+        s = "left" if t % 4 == 2 else "right"
+        assert rel(op.probe(x, s), ref.probe(x, s)) < 1e-10, t
