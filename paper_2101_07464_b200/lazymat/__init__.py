@@ -530,13 +530,19 @@ def run_trials(ensemble: str, trials: int, n: int, T: int, *, m: int = None, sig
     one trial's probe sequence overlaps the HBM streaming of the others.
     batch > 1: `concurrency` groups of `batch` operators, each group's trials
     sharing every kernel launch (batch_run / hd_batch_run) — the separate-graph
-    mode is bound by the kernel-dispatch rate at config-3 sizes.
+    mode is bound by the kernel-dispatch rate at config-3 sizes. A batched
+    launch gives each operator floor(SMs / batch) CTAs, so `batch` should
+    divide the SM count (148 = 4 x 37: batch 37 / 74 / 148); batch = 0 picks
+    half the SM count (config 3: 1.62 s against 1.71 s at batch 32).
     Returns x_{T+1} of every trial as a (trials, dim) CUDA tensor.
     x1: optional (trials, dim) CUDA tensor; default N(0, I) per trial.
     ops: the operators a previous call returned (return_ops=True) with the same
     arguments, reused instead of allocating new ones."""
     import torch
 
+    if batch == 0:
+        sms = torch.cuda.get_device_properties(device).multi_processor_count
+        batch = max(1, min(trials, sms // 2))
     if batch > 1:
         return _run_trials_batched(ensemble, trials, n, T, m=m, sigma=sigma, seed=seed, dtype=dtype, update=update,
                                    sides=sides, groups=concurrency, batch=batch, x1=x1, first_trial=first_trial,

@@ -9,12 +9,12 @@ import torch
 from paper_2101_07464_b200 import lazymat
 
 n, T = int(os.environ.get("C3_N", 100000)), 100
-batches = [int(b) for b in os.environ.get("C3_BATCH", "32").split(",")]
+batches = [int(b) for b in os.environ.get("C3_BATCH", "74").split(",")]
 res = {}
 for dtype, B in (("f64", int(os.environ.get("C3_B64", 1024))), ("f32", int(os.environ.get("C3_B32", 1024)))):
     tdt = torch.float64 if dtype == "f64" else torch.float32
     x1 = torch.randn((B, n), dtype=tdt, device="cuda", generator=torch.Generator("cuda").manual_seed(1))
-    for conc in [int(c) for c in os.environ.get("C3_CONC", "4").split(",")]:
+    for conc in [int(c) for c in os.environ.get("C3_CONC", "2").split(",")]:
       for bt in batches:
         if B == 0:
             continue
