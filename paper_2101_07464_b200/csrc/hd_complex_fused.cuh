@@ -59,45 +59,18 @@ __device__ __forceinline__ c2 warp_csum(c2 a) {
   return a;
 }
 
-__global__ void __launch_bounds__(kCxThreads) kc_gemv_t2(TJob j0, TJob j1) {
-  pdl_wait();
-  pdl_launch();
-  __shared__ c2 wp[kCxWarps][kTColGroup];
-  __shared__ double red[32];
-  const bool second = (int)blockIdx.x >= j0.nb;
-  TJob J;  // field-wise select (no dynamic indexing of the parameter space)
-  J.W = second ? j1.W : j0.W;
-  J.ld = second ? j1.ld : j0.ld;
-  J.k = second ? j1.k : j0.k;
-  J.v = second ? j1.v : j0.v;
-  J.r0 = second ? j1.r0 : j0.r0;
-  J.r1 = second ? j1.r1 : j0.r1;
-  J.part = second ? j1.part : j0.part;
-  J.npart = second ? j1.npart : j0.npart;
-  const int bb = second ? (int)blockIdx.x - j0.nb : (int)blockIdx.x;
+// part_row[j] = sum over this CTA's rows of conj(W[row, j]) v[row], j < k: every thread
+// holds kTRows rows of the right-hand side; two columns per step (eight independent
+// loads), warp-shuffle then cross-warp reduction through shared memory
+__device__ __forceinline__ void gemv_t_cols(const c2* W, int64_t ld, int k, const int64_t* row, const c2* v,
+                                            c2* part_row, c2 (*wp)[kTColGroup]) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t b0 = J.r0 + (int64_t)bb * kTBlockRows;
-  c2 v[kTRows];
-  int64_t row[kTRows];
-  double n2 = 0.0;
-#pragma unroll
-  for (int r = 0; r < kTRows; ++r) {
-    const int64_t i = b0 + r * kCxThreads + threadIdx.x;
-    const bool ok = i < J.r1;
-    row[r] = ok ? i : J.r1 - 1;  // clamped: loads stay unconditional, the product is zero
-    v[r] = ok ? J.v[i] : cmk(0.0, 0.0);
-    n2 += cnorm2(v[r]);
-  }
-  if (J.npart) {
-    n2 = block_sum<kCxThreads>(n2, red);
-    if (threadIdx.x == 0) J.npart[bb] = n2;
-  }
-  for (int g0 = 0; g0 < J.k; g0 += kTColGroup) {
-    const int gk = min(kTColGroup, J.k - g0);
+  for (int g0 = 0; g0 < k; g0 += kTColGroup) {
+    const int gk = min(kTColGroup, k - g0);
     int j = 0;
-    for (; j + 1 < gk; j += 2) {  // two columns per step: eight independent loads
-      const c2* ca = J.W + (size_t)(g0 + j) * J.ld;
-      const c2* cb = ca + J.ld;
+    for (; j + 1 < gk; j += 2) {
+      const c2* ca = W + (size_t)(g0 + j) * ld;
+      const c2* cb = ca + ld;
       c2 la[kTRows], lb[kTRows];
 #pragma unroll
       for (int r = 0; r < kTRows; ++r) {
@@ -118,7 +91,7 @@ __global__ void __launch_bounds__(kCxThreads) kc_gemv_t2(TJob j0, TJob j1) {
       }
     }
     if (j < gk) {
-      const c2* ca = J.W + (size_t)(g0 + j) * J.ld;
+      const c2* ca = W + (size_t)(g0 + j) * ld;
       c2 sa = cmk(0.0, 0.0);
 #pragma unroll
       for (int r = 0; r < kTRows; ++r) sa = cadd(sa, cconjmul(ca[row[r]], v[r]));
@@ -130,10 +103,45 @@ __global__ void __launch_bounds__(kCxThreads) kc_gemv_t2(TJob j0, TJob j1) {
       c2 s = wp[0][c];
 #pragma unroll
       for (int w = 1; w < kCxWarps; ++w) s = cadd(s, wp[w][c]);
-      J.part[(size_t)bb * J.k + g0 + c] = s;
+      part_row[g0 + c] = s;
     }
     __syncthreads();
   }
+}
+
+__global__ void __launch_bounds__(kCxThreads) kc_gemv_t2(TJob j0, TJob j1) {
+  pdl_wait();
+  pdl_launch();
+  __shared__ c2 wp[kCxWarps][kTColGroup];
+  __shared__ double red[32];
+  const bool second = (int)blockIdx.x >= j0.nb;
+  TJob J;  // field-wise select (no dynamic indexing of the parameter space)
+  J.W = second ? j1.W : j0.W;
+  J.ld = second ? j1.ld : j0.ld;
+  J.k = second ? j1.k : j0.k;
+  J.v = second ? j1.v : j0.v;
+  J.r0 = second ? j1.r0 : j0.r0;
+  J.r1 = second ? j1.r1 : j0.r1;
+  J.part = second ? j1.part : j0.part;
+  J.npart = second ? j1.npart : j0.npart;
+  const int bb = second ? (int)blockIdx.x - j0.nb : (int)blockIdx.x;
+  const int64_t b0 = J.r0 + (int64_t)bb * kTBlockRows;
+  c2 v[kTRows];
+  int64_t row[kTRows];
+  double n2 = 0.0;
+#pragma unroll
+  for (int r = 0; r < kTRows; ++r) {
+    const int64_t i = b0 + r * kCxThreads + threadIdx.x;
+    const bool ok = i < J.r1;
+    row[r] = ok ? i : J.r1 - 1;  // clamped: loads stay unconditional, the product is zero
+    v[r] = ok ? J.v[i] : cmk(0.0, 0.0);
+    n2 += cnorm2(v[r]);
+  }
+  if (J.npart) {
+    n2 = block_sum<kCxThreads>(n2, red);
+    if (threadIdx.x == 0) J.npart[bb] = n2;
+  }
+  gemv_t_cols(J.W, J.ld, J.k, row, v, J.part + (size_t)bb * J.k, wp);
 }
 
 // out0[j] = sum_b part0[b, j], out1[j] = sum_b part1[b, j], nrm2 = sum_b npart[b]:
@@ -236,6 +244,98 @@ __device__ __forceinline__ void append_member(const ChainRef& ch, int k, const c
   for (int64_t i = off + threadIdx.x; i < ch.Dlen; i += blockDim.x) ch.Dhead[i] = cmul(ch.Dhead[i], s);
 }
 
+// beta[i] = sum_{j <= i} conj(T[j, i]) a[j] (T^H a): a warp per output (column i of T
+// is contiguous), two outputs in flight. All threads of the CTA.
+__device__ __forceinline__ void tmul_herm(const c2* T, int64_t K, int k, const c2* a, c2* beta) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = wid; i < k; i += 2 * nw) {
+    const int i2 = i + nw;
+    const bool two = i2 < k;
+    const c2* c1 = T + (size_t)i * K;
+    const c2* c2p = T + (size_t)(two ? i2 : i) * K;
+    c2 s1 = cmk(0.0, 0.0), s2 = cmk(0.0, 0.0);
+    const int jmax = two ? i2 : i;
+    for (int j = lane; j <= jmax; j += 32) {
+      const c2 av = a[j];
+      if (j <= i) s1 = cadd(s1, cconjmul(c1[j], av));
+      if (two) s2 = cadd(s2, cconjmul(c2p[j], av));
+    }
+    s1 = warp_csum(s1);
+    s2 = warp_csum(s2);
+    if (lane == 0) {
+      beta[i] = s1;
+      if (two) beta[i2] = s2;
+    }
+  }
+}
+
+// beta[i] = sum_{j >= i} T[i, j] a[j] (T a): a warp per output, lanes over the columns
+__device__ __forceinline__ void tmul_plain(const c2* T, int64_t K, int k, const c2* a, c2* beta) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = wid; i < k; i += 2 * nw) {
+    const int i2 = i + nw;
+    const bool two = i2 < k;
+    c2 s1 = cmk(0.0, 0.0), sb = cmk(0.0, 0.0);
+    for (int j = i + lane; j < k; j += 32) {
+      const c2 av = a[j];
+      s1 = cadd(s1, cmul(T[(size_t)j * K + i], av));
+      if (two && j >= i2) sb = cadd(sb, cmul(T[(size_t)j * K + i2], av));
+    }
+    s1 = warp_csum(s1);
+    sb = warp_csum(sb);
+    if (lane == 0) {
+      beta[i] = s1;
+      if (two) beta[i2] = sb;
+    }
+  }
+}
+
+// The fold member (built from p at offset off, scalars in scal) joins chain F without a
+// panel pass for its Gram column: on rows >= off the diagonal D_F is the scalar d = D_tail, so
+//   W^H p[off:] = d (a - G beta - W_head^H (p_head / D_head)),  a = W^H x, beta = T^H a,
+// and the column is p[off:] / nrm + phase e_off. aF is overwritten with the Gram column.
+// All threads of the CTA.
+__device__ __forceinline__ void append_fold_member(const ChainRef& F, int k, int64_t off, const c2* p, c2* aF,
+                                                   const c2* betaF, const double* scal) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double nrm = scal[0];
+  const c2 ph = cmk(scal[4], scal[5]);
+  const c2 dt = *F.Dtail;  // D_F on rows >= off (before this member's s)
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {  // a_j - (G beta)_j
+    c2 a0 = cmk(0.0, 0.0), a1 = cmk(0.0, 0.0);
+    int l = 0;
+#pragma unroll 4
+    for (; l + 1 < k; l += 2) {
+      a0 = cadd(a0, cmul(F.G[(size_t)l * F.K + j], betaF[l]));
+      a1 = cadd(a1, cmul(F.G[(size_t)(l + 1) * F.K + j], betaF[l + 1]));
+    }
+    if (l < k) a0 = cadd(a0, cmul(F.G[(size_t)l * F.K + j], betaF[l]));
+    aF[j] = csub(aF[j], cadd(a0, a1));
+  }
+  __syncthreads();
+  // minus the head corner W_head^H (p_head / D_head), a warp per column
+  for (int j = wid; j < k; j += nw) {
+    const c2* col = F.W + (size_t)j * F.ld;
+    c2 acc = cmk(0.0, 0.0);
+    for (int64_t i = lane; i < off; i += 32) {
+      const c2 d = F.d_at(i);
+      const c2 xv = cscale(cconjmul(d, p[i]), 1.0 / cnorm2(d));  // p / D
+      acc = cadd(acc, cconjmul(col[i], xv));
+    }
+    acc = warp_csum(acc);
+    if (lane == 0) {
+      c2 v = cmk(0.0, 0.0);
+      if (nrm > 0.0) {
+        const c2 S = cmul(dt, csub(aF[j], acc));  // W[:, j]^H p[off:]
+        v = cadd(cscale(S, 1.0 / nrm), cmul(ph, cconj(col[off])));
+      }
+      aF[j] = v;
+    }
+  }
+  __syncthreads();
+  append_member(F, k, aF, scal, off);
+}
+
 constexpr int kSmallThreads = 512;
 
 struct SmallA {
@@ -253,29 +353,8 @@ struct SmallA {
 __global__ void __launch_bounds__(kSmallThreads) kc_small_a(SmallA A) {
   pdl_wait();
   pdl_launch();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if (threadIdx.x == 0) reflector_scalars(*A.nrm2g, A.g[A.off], A.scal2);
-  // beta_F[i] = sum_{j <= i} conj(T[j, i]) a[j]: a warp per output (column i of T is
-  // contiguous), two outputs in flight
-  for (int i = wid; i < A.kF; i += 2 * nw) {
-    const int i2 = i + nw;
-    const bool two = i2 < A.kF;
-    const c2* c1 = A.TF + (size_t)i * A.KF;
-    const c2* c2p = A.TF + (size_t)(two ? i2 : i) * A.KF;
-    c2 s1 = cmk(0.0, 0.0), s2 = cmk(0.0, 0.0);
-    const int jmax = two ? i2 : i;
-    for (int j = lane; j <= jmax; j += 32) {
-      const c2 av = A.aF[j];
-      if (j <= i) s1 = cadd(s1, cconjmul(c1[j], av));
-      if (two) s2 = cadd(s2, cconjmul(c2p[j], av));
-    }
-    s1 = warp_csum(s1);
-    s2 = warp_csum(s2);
-    if (lane == 0) {
-      A.betaF[i] = s1;
-      if (two) A.betaF[i2] = s2;
-    }
-  }
+  tmul_herm(A.TF, A.KF, A.kF, A.aF, A.betaF);
 }
 
 struct NFold {
@@ -432,23 +511,7 @@ __global__ void __launch_bounds__(kSmallThreads) kc_small_b(SmallB A) {
     }
   }
   __syncthreads();
-  // beta_O[i] = sum_{j >= i} T_O[i, j] a_O[j]: a warp per output, lanes over the columns
-  for (int i = wid; i < A.kO1; i += 2 * nw) {
-    const int i2 = i + nw;
-    const bool two = i2 < A.kO1;
-    c2 s1 = cmk(0.0, 0.0), sb = cmk(0.0, 0.0);
-    for (int j = i + lane; j < A.kO1; j += 32) {
-      const c2 av = A.aO[j];
-      s1 = cadd(s1, cmul(A.O.T[(size_t)j * A.O.K + i], av));
-      if (two && j >= i2) sb = cadd(sb, cmul(A.O.T[(size_t)j * A.O.K + i2], av));
-    }
-    s1 = warp_csum(s1);
-    sb = warp_csum(sb);
-    if (lane == 0) {
-      A.betaO[i] = s1;
-      if (two) A.betaO[i2] = sb;
-    }
-  }
+  tmul_plain(A.O.T, A.O.K, A.kO1, A.aO, A.betaO);
 }
 
 struct NOther {
@@ -479,44 +542,7 @@ __global__ void __launch_bounds__(kCxThreads) kc_nother(NOther A) {
   if (A.bad && *A.bad) return;
   if (blockIdx.x == 0) {
     if (!A.appendF) return;
-    const int k = A.kF;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const double nrm = A.scal[0];
-    const c2 ph = cmk(A.scal[4], A.scal[5]);
-    const c2 dt = *A.F.Dtail;  // D_F on rows >= off (before this member's s)
-    for (int j = threadIdx.x; j < k; j += blockDim.x) {  // a_j - (G beta)_j
-      c2 a0 = cmk(0.0, 0.0), a1 = cmk(0.0, 0.0);
-      int l = 0;
-#pragma unroll 4
-      for (; l + 1 < k; l += 2) {
-        a0 = cadd(a0, cmul(A.F.G[(size_t)l * A.F.K + j], A.betaF[l]));
-        a1 = cadd(a1, cmul(A.F.G[(size_t)(l + 1) * A.F.K + j], A.betaF[l + 1]));
-      }
-      if (l < k) a0 = cadd(a0, cmul(A.F.G[(size_t)l * A.F.K + j], A.betaF[l]));
-      A.aF[j] = csub(A.aF[j], cadd(a0, a1));
-    }
-    __syncthreads();
-    // minus the head corner W_head^H (p_head / D_head), a warp per column
-    for (int j = wid; j < k; j += nw) {
-      const c2* col = A.F.W + (size_t)j * A.F.ld;
-      c2 acc = cmk(0.0, 0.0);
-      for (int64_t i = lane; i < A.off; i += 32) {
-        const c2 d = A.F.d_at(i);
-        const c2 xv = cscale(cconjmul(d, A.p[i]), 1.0 / cnorm2(d));  // p / D
-        acc = cadd(acc, cconjmul(col[i], xv));
-      }
-      acc = warp_csum(acc);
-      if (lane == 0) {
-        c2 v = cmk(0.0, 0.0);
-        if (nrm > 0.0) {
-          const c2 S = cmul(dt, csub(A.aF[j], acc));  // W[:, j]^H p[off:]
-          v = cadd(cscale(S, 1.0 / nrm), cmul(ph, cconj(col[A.off])));
-        }
-        A.aF[j] = v;
-      }
-    }
-    __syncthreads();
-    append_member(A.F, k, A.aF, A.scal, A.off);
+    append_fold_member(A.F, A.kF, A.off, A.p, A.aF, A.betaF, A.scal);
     return;
   }
   const int64_t i0 = ((int64_t)(blockIdx.x - 1) * kCxThreads + threadIdx.x) * R;

@@ -14,6 +14,7 @@
 
 #include "hd_complex.cuh"
 #include "hd_complex_fused.cuh"
+#include "hd_complex_gin.cuh"
 #include "hd_refrng.hpp"
 #include "hd_shard.cuh"
 

@@ -243,3 +243,62 @@ def test_complex_haar_two_rows_per_thread_variant(orc, lm, monkeypatch):
         x = aux.normal_complex_vector(n)
         s = "left" if t % 4 == 2 else "right"
         assert rel(op.probe(x, s), ref.probe(x, s)) < 1e-10, t
+
+
+# ---- fused Ginibre / GOE probes (csrc/hd_complex_gin.cuh)
+@pytest.mark.parametrize("m,n,T,cap", [(2600, 1900, 90, 3), (1500, 3100, 120, 200)])
+def test_complex_ginibre_long_run_vs_oracle(orc, lm, m, n, T, cap):
+    seed = 3 + m
+    rng = np.random.default_rng(seed)
+    sides = ["right" if rng.random() < 0.55 else "left" for _ in range(T)]
+    ref = orc.COperator("ginibre", m=m, n=n, sigma=0.9 / np.sqrt(m), seed=seed)
+    op = lm.GinibreOperator(m, n, 0.9 / np.sqrt(m), seed, dtype="c128", draws="injected", capacity=cap)
+    op.push_draws(orc.complex_draws_for(seed, [m if s == "right" else n for s in sides]).view(np.complex128))
+    aux = orc.RandomSource(seed + 2)
+    worst = 0.0
+    for t, s in enumerate(sides):
+        x = aux.normal_complex_vector(n if s == "right" else m)
+        worst = max(worst, rel(op.probe(x, s), ref.probe(x, s)))
+    assert worst < 1e-10, worst
+    assert op.probe_counts() == (sides.count("right"), sides.count("left"))
+
+
+@pytest.mark.parametrize("skip", [False, True])
+def test_complex_ginibre_fused_matches_generic_sequence(orc, lm, monkeypatch, skip):
+    m, n, T, seed = 1100, 900, 30, 19
+    sides = ["left" if t % 3 == 1 else "right" for t in range(T)]
+    draws = orc.complex_draws_for(seed, [m if s == "right" else n for s in sides]).view(np.complex128)
+    ref = orc.COperator("ginibre", m=m, n=n, sigma=1.0, seed=seed, skip_reflector=skip)
+    ops = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("HD_CX_FUSED", flag)  # read at hd_create
+        ops[flag] = lm.GinibreOperator(m, n, 1.0, seed, dtype="c128", draws="injected", capacity=8,
+                                       skip_reflector=skip)
+        ops[flag].push_draws(draws)
+    aux = orc.RandomSource(seed + 1)
+    for t, s in enumerate(sides):
+        x = aux.normal_complex_vector(n if s == "right" else m)
+        a, b, want = ops["1"].probe(x, s), ops["0"].probe(x, s), ref.probe(x, s)
+        assert rel(a, b) < 1e-11, (t, rel(a, b))
+        assert rel(a, want) < 1e-10, (t, rel(a, want))
+    assert ops["1"].launch_count() < ops["0"].launch_count() / 3
+
+
+def test_complex_goe_device_inputs_and_flagged_probe(orc, lm):
+    import torch
+
+    n, seed, T = 500, 13, 14
+    inner = orc.COperator("ginibre", m=n, n=n, sigma=1.0, seed=seed)
+    op = lm.GOEOperator(n, seed, dtype="c128", draws="injected", capacity=4)
+    op.push_draws(orc.complex_draws_for(seed, [n] * (2 * T)).view(np.complex128))
+    aux = orc.RandomSource(4)
+    for t in range(T):
+        x = aux.normal_complex_vector(n)
+        if t in (0, 6):
+            bad = x.copy()
+            bad[t] = complex(np.nan, 1.0)
+            with pytest.raises(ValueError, match="non-finite"):
+                op.probe(torch.from_numpy(bad).cuda(), "right")
+        want = (inner.probe(x, "right") + inner.probe(x, "left")) * 0.7071067811865475244
+        got = op.probe(torch.from_numpy(x).cuda(), "right").cpu().numpy()
+        assert rel(got, want) < 1e-10, t

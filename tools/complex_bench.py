@@ -7,7 +7,9 @@ from paper_2101_07464_b200 import lazymat
 
 res = {}
 TH = int(sys.argv[1]) if len(sys.argv) > 1 else 30
-for ens, n, T in [("haar", 1_000_000, TH), ("ginibre", 100_000, 40)]:
+NG = int(float(sys.argv[2])) if len(sys.argv) > 2 else 100_000
+TG = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+for ens, n, T in [("haar", 1_000_000, TH), ("ginibre", NG, TG)]:
     op = (lazymat.HaarOperator(n, seed=1, dtype="c128", capacity=T) if ens == "haar"
           else lazymat.GinibreOperator(n, n, n ** -0.5, 1, dtype="c128", capacity=T))
     x = torch.randn(n, dtype=torch.complex128, device="cuda")
