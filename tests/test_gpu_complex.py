@@ -302,3 +302,45 @@ def test_complex_goe_device_inputs_and_flagged_probe(orc, lm):
         want = (inner.probe(x, "right") + inner.probe(x, "left")) * 0.7071067811865475244
         got = op.probe(torch.from_numpy(x).cuda(), "right").cpu().numpy()
         assert rel(got, want) < 1e-10, t
+
+
+def test_complex_fused_large_n_properties(lm, monkeypatch):
+    # size-independent properties at a size the oracle does not reach (n = 2^20 + 77 rows:
+    # ragged last row block; device Philox draws; device tensors in and out)
+    import torch
+
+    n, T = (1 << 20) + 77, 10
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    rnd = lambda k: torch.complex(torch.randn(k, dtype=torch.float64, device="cuda", generator=gen),  # noqa: E731
+                                  torch.randn(k, dtype=torch.float64, device="cuda", generator=gen))
+    haar = lm.HaarOperator(n, seed=9, dtype="c128", capacity=2 * T + 2)
+    monkeypatch.setenv("HD_CX_FUSED", "0")
+    generic = lm.HaarOperator(n, seed=9, dtype="c128", capacity=2 * T + 2)
+    monkeypatch.delenv("HD_CX_FUSED")
+    for t in range(T):
+        x, w = rnd(n), rnd(n)
+        s = "left" if t % 3 == 2 else "right"
+        opp = "left" if s == "right" else "right"
+        y = haar.probe(x, s)
+        assert abs(float(y.norm() / x.norm()) - 1.0) < 1e-12  # unitary
+        assert float((y - generic.probe(x, s)).norm() / y.norm()) < 1e-12
+        z = haar.probe(w, opp)  # the same lazily sampled Q from the other side
+        assert float((z - generic.probe(w, opp)).norm() / z.norm()) < 1e-12
+        lhs, rhs = torch.vdot(w, y), torch.vdot(z, x)
+        assert abs(complex(lhs - rhs)) < 1e-10 * float(x.norm() * w.norm())
+    m2, n2 = 700_001, 400_003
+    gin = lm.GinibreOperator(m2, n2, m2 ** -0.5, 3, dtype="c128", capacity=2 * T)
+    monkeypatch.setenv("HD_CX_FUSED", "0")
+    gin0 = lm.GinibreOperator(m2, n2, m2 ** -0.5, 3, dtype="c128", capacity=2 * T)
+    monkeypatch.delenv("HD_CX_FUSED")
+    for t in range(T):
+        x, w = rnd(n2), rnd(m2)
+        y = gin.probe(x, "right")
+        assert float((y - gin0.probe(x, "right")).norm() / y.norm()) < 1e-12
+        z = gin.probe(w, "left")
+        assert float((z - gin0.probe(w, "left")).norm() / z.norm()) < 1e-12
+        lhs, rhs = torch.vdot(w, y), torch.vdot(z, x)  # the same lazily sampled matrix from both sides
+        assert abs(complex(lhs - rhs)) < 1e-10 * (abs(complex(lhs)) + float(x.norm() * w.norm()) * m2 ** -0.5)
+        y2 = gin.probe(x, "right")  # repeated probe: the same matrix
+        assert float((y2 - y).norm() / y.norm()) < 1e-11
+        gin0.probe(x, "right")
