@@ -341,6 +341,7 @@ def test_complex_fused_large_n_properties(lm, monkeypatch):
         assert float((z - gin0.probe(w, "left")).norm() / z.norm()) < 1e-12
         lhs, rhs = torch.vdot(w, y), torch.vdot(z, x)  # the same lazily sampled matrix from both sides
         assert abs(complex(lhs - rhs)) < 1e-10 * (abs(complex(lhs)) + float(x.norm() * w.norm()) * m2 ** -0.5)
-        y2 = gin.probe(x, "right")  # repeated probe: the same matrix
-        assert float((y2 - y).norm() / y.norm()) < 1e-11
-        gin0.probe(x, "right")
+    # a repeated probe answers from the same matrix (last: its fold tail is rounding noise, so the
+    # reflector it appends is implementation-specific, in the reference too)
+    y2 = gin.probe(x, "right")
+    assert float((y2 - y).norm() / y.norm()) < 1e-11
