@@ -34,8 +34,7 @@
 namespace hd {
 namespace cx {
 
-constexpr int kTRows = 4;                           // rows per thread (GEMV-T)
-constexpr int kTBlockRows = kCxThreads * kTRows;    // rows per CTA
+constexpr int kTRows = 4;  // most rows per thread of the GEMV-T kernels (templated: 2 or 4; rows per CTA = R * kCxThreads)
 constexpr int kTColGroup = 128;                     // columns per shared-memory round
 constexpr int kCxWarps = kCxThreads / 32;
 
@@ -62,6 +61,7 @@ __device__ __forceinline__ c2 warp_csum(c2 a) {
 // part_row[j] = sum over this CTA's rows of conj(W[row, j]) v[row], j < k: every thread
 // holds kTRows rows of the right-hand side; two columns per step (eight independent
 // loads), warp-shuffle then cross-warp reduction through shared memory
+template <int R>
 __device__ __forceinline__ void gemv_t_cols(const c2* W, int64_t ld, int k, const int64_t* row, const c2* v,
                                             c2* part_row, c2 (*wp)[kTColGroup]) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -71,15 +71,15 @@ __device__ __forceinline__ void gemv_t_cols(const c2* W, int64_t ld, int k, cons
     for (; j + 1 < gk; j += 2) {
       const c2* ca = W + (size_t)(g0 + j) * ld;
       const c2* cb = ca + ld;
-      c2 la[kTRows], lb[kTRows];
+      c2 la[R], lb[R];
 #pragma unroll
-      for (int r = 0; r < kTRows; ++r) {
+      for (int r = 0; r < R; ++r) {
         la[r] = ca[row[r]];
         lb[r] = cb[row[r]];
       }
       c2 sa = cmk(0.0, 0.0), sb = cmk(0.0, 0.0);
 #pragma unroll
-      for (int r = 0; r < kTRows; ++r) {
+      for (int r = 0; r < R; ++r) {
         sa = cadd(sa, cconjmul(la[r], v[r]));
         sb = cadd(sb, cconjmul(lb[r], v[r]));
       }
@@ -94,7 +94,7 @@ __device__ __forceinline__ void gemv_t_cols(const c2* W, int64_t ld, int k, cons
       const c2* ca = W + (size_t)(g0 + j) * ld;
       c2 sa = cmk(0.0, 0.0);
 #pragma unroll
-      for (int r = 0; r < kTRows; ++r) sa = cadd(sa, cconjmul(ca[row[r]], v[r]));
+      for (int r = 0; r < R; ++r) sa = cadd(sa, cconjmul(ca[row[r]], v[r]));
       sa = warp_csum(sa);
       if (lane == 0) wp[wid][j] = sa;
     }
@@ -109,6 +109,7 @@ __device__ __forceinline__ void gemv_t_cols(const c2* W, int64_t ld, int k, cons
   }
 }
 
+template <int R>
 __global__ void __launch_bounds__(kCxThreads) kc_gemv_t2(TJob j0, TJob j1) {
   pdl_wait();
   pdl_launch();
@@ -125,12 +126,12 @@ __global__ void __launch_bounds__(kCxThreads) kc_gemv_t2(TJob j0, TJob j1) {
   J.part = second ? j1.part : j0.part;
   J.npart = second ? j1.npart : j0.npart;
   const int bb = second ? (int)blockIdx.x - j0.nb : (int)blockIdx.x;
-  const int64_t b0 = J.r0 + (int64_t)bb * kTBlockRows;
-  c2 v[kTRows];
-  int64_t row[kTRows];
+  const int64_t b0 = J.r0 + (int64_t)bb * (R * kCxThreads);
+  c2 v[R];
+  int64_t row[R];
   double n2 = 0.0;
 #pragma unroll
-  for (int r = 0; r < kTRows; ++r) {
+  for (int r = 0; r < R; ++r) {
     const int64_t i = b0 + r * kCxThreads + threadIdx.x;
     const bool ok = i < J.r1;
     row[r] = ok ? i : J.r1 - 1;  // clamped: loads stay unconditional, the product is zero
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(kCxThreads) kc_gemv_t2(TJob j0, TJob j1) {
     n2 = block_sum<kCxThreads>(n2, red);
     if (threadIdx.x == 0) J.npart[bb] = n2;
   }
-  gemv_t_cols(J.W, J.ld, J.k, row, v, J.part + (size_t)bb * J.k, wp);
+  gemv_t_cols<R>(J.W, J.ld, J.k, row, v, J.part + (size_t)bb * J.k, wp);
 }
 
 // out0[j] = sum_b part0[b, j], out1[j] = sum_b part1[b, j], nrm2 = sum_b npart[b]:
@@ -555,6 +556,96 @@ __global__ void __launch_bounds__(kCxThreads) kc_nother(NOther A) {
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int64_t i = i0 + r;
+    if (i < A.n) {
+      const c2 pv = A.p[i];
+      const c2 z = (i < A.off) ? pv : (i == A.off ? cmk(A.scal[0], 0.0) : cmk(0.0, 0.0));
+      A.y[i] = csub(cmul(A.d.at(i), z), acc[r]);
+      if (A.colF) A.colF[i] = column_entry(pv, i, A.off, A.scal);
+    }
+  }
+}
+
+
+// ---- the other chain's GEMV-N with the NEXT probe's draw dots from the same bytes.
+// A Haar probe's draw never depends on x, so when the next probe keeps its side the
+// dots W_O'^H g'[off + 1:] and ||g'[off + 1:]||^2 it needs (kc_gemv_t2's second job) are
+// taken here, from the columns this pass streams anyway: three panel passes per probe.
+// Rows per thread / CTA as in the GEMV-T kernel (the shuffle reduction per column is
+// amortised over kTRows rows).
+constexpr int kSpecCols = 8;  // columns per shared-memory reduction round (kc_nother_spec)
+
+struct SpecOut {
+  const c2* g = nullptr;     // the next probe's draw
+  int64_t off = 0;           // its offset: rows below are masked
+  c2* part = nullptr;        // (grid - 1) x k block partials
+  double* npart = nullptr;   // (grid - 1) partial ||g[off:]||^2
+};
+
+// grid = 1 + ceil(n / (R kCxThreads)); CTA 0 appends the fold member. R rows per thread:
+// fewer rows = more CTAs (finer waves), more rows = fewer shared-memory partials per byte
+template <int R>
+__global__ void __launch_bounds__(kCxThreads, 4) kc_nother_spec(NOther A, SpecOut S) {
+  pdl_wait();
+  pdl_launch();
+  if (A.bad && *A.bad) return;
+  if (blockIdx.x == 0) {
+    if (A.appendF) append_fold_member(A.F, A.kF, A.off, A.p, A.aF, A.betaF, A.scal);
+    return;
+  }
+  // per-thread column partials go to shared memory; one warp per column reduces them
+  // every kSpecCols columns (no shuffle chain inside the streaming loop)
+  __shared__ c2 tp[kSpecCols][kCxThreads];
+  __shared__ double red[32];
+  const int bb = (int)blockIdx.x - 1;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t b0 = (int64_t)bb * (R * kCxThreads);
+  int row[R];  // offsets from the CTA's first row (clamped: loads stay unconditional)
+  c2 gv[R], acc[R];
+  double n2 = 0.0;
+  const int nrem = (int)min((int64_t)(R * kCxThreads), A.n - b0);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int o = r * kCxThreads + threadIdx.x;
+    const bool ok = o < nrem;
+    row[r] = ok ? o : nrem - 1;
+    gv[r] = (ok && b0 + o >= S.off) ? S.g[b0 + o] : cmk(0.0, 0.0);
+    n2 += cnorm2(gv[r]);
+    acc[r] = cmk(0.0, 0.0);
+  }
+  n2 = block_sum<kCxThreads>(n2, red);
+  if (threadIdx.x == 0) S.npart[bb] = n2;
+  c2* part_row = S.part + (size_t)bb * A.k;
+  const c2* Wb = A.W + b0;
+  for (int g0 = 0; g0 < A.k; g0 += kSpecCols) {
+    const int gk = min(kSpecCols, A.k - g0);
+#pragma unroll 2
+    for (int j = 0; j < gk; ++j) {
+      const c2* ca = Wb + (size_t)(g0 + j) * A.ld;
+      c2 la[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) la[r] = ca[row[r]];
+      const c2 ba = __ldg(A.beta + g0 + j);
+      c2 sa = cmk(0.0, 0.0);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        acc[r] = cadd(acc[r], cmul(la[r], ba));
+        sa = cadd(sa, cconjmul(la[r], gv[r]));
+      }
+      tp[j][threadIdx.x] = sa;
+    }
+    __syncthreads();
+    for (int c = wid; c < gk; c += kCxWarps) {
+      c2 t = cmk(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < kCxThreads / 32; ++q) t = cadd(t, tp[c][q * 32 + lane]);
+      t = warp_csum(t);
+      if (lane == 0) part_row[g0 + c] = t;
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int64_t i = b0 + r * kCxThreads + threadIdx.x;
     if (i < A.n) {
       const c2 pv = A.p[i];
       const c2 z = (i < A.off) ? pv : (i == A.off ? cmk(A.scal[0], 0.0) : cmk(0.0, 0.0));

@@ -41,6 +41,7 @@ struct TJobs3 {
   TJobD j[3];
 };
 
+template <int R>
 __global__ void __launch_bounds__(kCxThreads) kc_gemv_t3(TJobs3 A) {
   pdl_wait();
   pdl_launch();
@@ -56,11 +57,11 @@ __global__ void __launch_bounds__(kCxThreads) kc_gemv_t3(TJobs3 A) {
     }
   }
   const TJobD J = jid == 0 ? A.j[0] : (jid == 1 ? A.j[1] : A.j[2]);
-  const int64_t b0 = J.r0 + (int64_t)bb * kTBlockRows;
-  c2 v[kTRows];
-  int64_t row[kTRows];
+  const int64_t b0 = J.r0 + (int64_t)bb * (R * kCxThreads);
+  c2 v[R];
+  int64_t row[R];
 #pragma unroll
-  for (int r = 0; r < kTRows; ++r) {
+  for (int r = 0; r < R; ++r) {
     const int64_t i = b0 + r * kCxThreads + threadIdx.x;
     const bool ok = i < J.r1;
     row[r] = ok ? i : J.r1 - 1;
@@ -68,7 +69,7 @@ __global__ void __launch_bounds__(kCxThreads) kc_gemv_t3(TJobs3 A) {
     if (ok && J.use_d) t = cmul(J.d.at(i), t);
     v[r] = t;
   }
-  gemv_t_cols(J.W, J.ld, J.k, row, v, J.part + (size_t)bb * J.k, wp);
+  gemv_t_cols<R>(J.W, J.ld, J.k, row, v, J.part + (size_t)bb * J.k, wp);
 }
 
 struct RJob {

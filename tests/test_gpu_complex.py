@@ -345,3 +345,36 @@ def test_complex_fused_large_n_properties(lm, monkeypatch):
     # reflector it appends is implementation-specific, in the reference too)
     y2 = gin.probe(x, "right")
     assert float((y2 - y).norm() / y.norm()) < 1e-11
+
+
+def test_complex_haar_speculative_draw_dots(orc, lm, monkeypatch):
+    # the last pass of a fused Haar probe takes the next draw's dots (three panel passes per
+    # probe when the side repeats): with the draws queued ahead, one at a time (no
+    # speculation possible), and with HD_CX_SPEC=0 — all against the oracle
+    n, T, seed = 2600, 36, 77
+    draws = orc.complex_draws_for(seed, [n] * T).view(np.complex128).reshape(T, n)
+    sides = ["left" if t % 7 in (3, 4) else "right" for t in range(T)]
+    ref = orc.COperator("haar", n=n, seed=seed)
+    ahead = lm.HaarOperator(n, seed=seed, dtype="c128", draws="injected", capacity=6)
+    ahead.push_draws(draws.reshape(-1))
+    single = lm.HaarOperator(n, seed=seed, dtype="c128", draws="injected", capacity=6)
+    monkeypatch.setenv("HD_CX_SPEC", "0")
+    off = lm.HaarOperator(n, seed=seed, dtype="c128", draws="injected", capacity=6)
+    off.push_draws(draws.reshape(-1))
+    aux = orc.RandomSource(seed + 1)
+    for t, s in enumerate(sides):
+        x = aux.normal_complex_vector(n)
+        single.push_draws(draws[t])
+        want = ref.probe(x, s)
+        for name, op in (("ahead", ahead), ("single", single), ("off", off)):
+            assert rel(op.probe(x, s), want) < 1e-10, (name, t)
+    # the speculative pass replaces the draw's GEMV-T job: fewer algorithmic bytes
+    ahead.set_profiling(True)
+    off.set_profiling(True)
+    ahead.reset(), off.reset()
+    for op in (ahead, off):
+        op.push_draws(draws.reshape(-1))
+        for t in range(T):
+            op.probe(aux.normal_complex_vector(n), "right")
+    b = lambda op: sum(v["alg_bytes"] for v in op.kernel_stats().values())  # noqa: E731
+    assert b(ahead) < 0.85 * b(off)
