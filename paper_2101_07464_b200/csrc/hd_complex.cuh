@@ -287,12 +287,22 @@ __global__ void kc_scale(c2* y, int64_t n, double s, const c2* add, double add_s
   y[i] = cscale(v, s);
 }
 
+// A non-finite entry raises the device flag (tested by the state-changing fused kernels)
+// and its host-mapped mirror (read by the host after the probe's synchronisation)
+__device__ __forceinline__ void raise_bad(int* flag, int* hflag) {
+  atomicOr(flag, 1);
+  if (hflag) {
+    *reinterpret_cast<volatile int*>(hflag) = 1;
+    __threadfence_system();
+  }
+}
+
 // 1 if any entry is non-finite
-__global__ void kc_check_finite(const c2* x, int64_t n, int* flag) {
+__global__ void kc_check_finite(const c2* x, int64_t n, int* flag, int* hflag) {
   pdl_wait();  // programmatic dependent launch (as the real path)
   pdl_launch();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    if (!isfinite(x[i].x) || !isfinite(x[i].y)) atomicOr(flag, 1);
+    if (!isfinite(x[i].x) || !isfinite(x[i].y)) raise_bad(flag, hflag);
 }
 
 }  // namespace cx

@@ -47,6 +47,8 @@ struct TJob {
   int nb = 0;                // row blocks of this job
   c2* part = nullptr;        // nb x k
   double* npart = nullptr;   // nb: ||v||^2 over the block's rows (or null)
+  int* flag = nullptr;       // non-null: v is a device input to validate (raise_bad on a non-finite entry)
+  int* hflag = nullptr;
 };
 
 __device__ __forceinline__ c2 warp_csum(c2 a) {
@@ -125,6 +127,8 @@ __global__ void __launch_bounds__(kCxThreads) kc_gemv_t2(TJob j0, TJob j1) {
   J.r1 = second ? j1.r1 : j0.r1;
   J.part = second ? j1.part : j0.part;
   J.npart = second ? j1.npart : j0.npart;
+  J.flag = second ? j1.flag : j0.flag;
+  J.hflag = second ? j1.hflag : j0.hflag;
   const int bb = second ? (int)blockIdx.x - j0.nb : (int)blockIdx.x;
   const int64_t b0 = J.r0 + (int64_t)bb * (R * kCxThreads);
   c2 v[R];
@@ -136,6 +140,7 @@ __global__ void __launch_bounds__(kCxThreads) kc_gemv_t2(TJob j0, TJob j1) {
     const bool ok = i < J.r1;
     row[r] = ok ? i : J.r1 - 1;  // clamped: loads stay unconditional, the product is zero
     v[r] = ok ? J.v[i] : cmk(0.0, 0.0);
+    if (J.flag && !(isfinite(v[r].x) && isfinite(v[r].y))) raise_bad(J.flag, J.hflag);
     n2 += cnorm2(v[r]);
   }
   if (J.npart) {

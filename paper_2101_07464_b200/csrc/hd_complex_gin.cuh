@@ -35,6 +35,8 @@ struct TJobD {
   int64_t r0 = 0, r1 = 0;
   int nb = 0;
   c2* part = nullptr;  // nb x k
+  int* flag = nullptr;  // non-null: v is a device input to validate
+  int* hflag = nullptr;
 };
 
 struct TJobs3 {
@@ -66,6 +68,7 @@ __global__ void __launch_bounds__(kCxThreads) kc_gemv_t3(TJobs3 A) {
     const bool ok = i < J.r1;
     row[r] = ok ? i : J.r1 - 1;
     c2 t = ok ? J.v[i] : cmk(0.0, 0.0);
+    if (J.flag && !(isfinite(t.x) && isfinite(t.y))) raise_bad(J.flag, J.hflag);
     if (ok && J.use_d) t = cmul(J.d.at(i), t);
     v[r] = t;
   }
