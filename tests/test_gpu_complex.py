@@ -378,3 +378,30 @@ def test_complex_haar_speculative_draw_dots(orc, lm, monkeypatch):
             op.probe(aux.normal_complex_vector(n), "right")
     b = lambda op: sum(v["alg_bytes"] for v in op.kernel_stats().values())  # noqa: E731
     assert b(ahead) < 0.85 * b(off)
+
+
+@pytest.mark.parametrize("ens", ["haar", "ginibre", "goe"])
+def test_complex_philox_rejected_probe_does_not_shift_the_stream(lm, ens):
+    # production draws: a rejected device input must leave counters, the early-drawn next
+    # draw and its speculative dots as they were — the twin that never saw it stays identical
+    import torch
+
+    n, T = 3000, 12
+    mk = {"haar": lambda: lm.HaarOperator(n, seed=5, dtype="c128", capacity=4),
+          "ginibre": lambda: lm.GinibreOperator(n + 100, n, 0.03, 5, dtype="c128", capacity=4),
+          "goe": lambda: lm.GOEOperator(n, 5, dtype="c128", capacity=4)}[ens]
+    a, b = mk(), mk()
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    for t in range(T):
+        side = "left" if (ens != "goe" and t % 4 == 1) else "right"
+        k = n + 100 if (ens == "ginibre" and side == "left") else n
+        x = torch.complex(torch.randn(k, dtype=torch.float64, device="cuda", generator=gen),
+                          torch.randn(k, dtype=torch.float64, device="cuda", generator=gen))
+        if t in (0, 5, 6):
+            bad = x.clone()
+            bad[t * 3] = complex(float("inf"), 0.0)
+            with pytest.raises(ValueError, match="non-finite"):
+                a.probe(bad, side)
+        ya, yb = a.probe(x, side), b.probe(x, side)
+        assert float((ya - yb).norm() / yb.norm()) < 1e-14, (ens, t)
+    assert a.remaining_probes == b.remaining_probes
