@@ -1,6 +1,6 @@
 // Fused complex-field Haar probe (haar.hpp:40-67 with
-// Scalar = complex<double>): four panel passes in seven launches instead of
-// the generic sequence's five passes in 22 (hd_complex.cuh).
+// Scalar = complex<double>): three to four panel passes in seven launches
+// instead of the generic sequence's five passes in 22 (hd_complex.cuh).
 //
 //   kc_gemv_t2   one grid, two GEMV-T jobs: a_F = W_F^H x over all rows and the
 //                fresh draw's dots W_O^H g[off:] (they do not depend on x) with
@@ -25,8 +25,12 @@
 //                  W^H p[off:] = d (a - G beta - W_head^H (p_head / D_head)),
 //                with G = W_F^H W_F kept per chain (k x k) and the head a t x k
 //                corner; T_F / G_F columns, D_F update (needed by the next probe)
-// Device inputs are validated by a flag the state-changing kernels test
-// (`bad`), so a probe is one enqueue and one synchronisation.
+//   kc_nother_spec  kc_nother that also takes the NEXT probe's draw dots with chain
+//                O' from the columns it streams (a Haar draw never depends on x): the
+//                next probe's second kc_gemv_t2 job disappears when its side repeats
+// Device inputs are validated inside the first GEMV-T job that streams them: a
+// non-finite entry raises a flag the state-changing kernels test (`bad`) and its
+// host-mapped mirror, so a probe is one enqueue and one synchronisation.
 #pragma once
 
 #include "hd_complex.cuh"
@@ -34,8 +38,8 @@
 namespace hd {
 namespace cx {
 
-constexpr int kTRows = 4;  // most rows per thread of the GEMV-T kernels (templated: 2 or 4; rows per CTA = R * kCxThreads)
-constexpr int kTColGroup = 128;                     // columns per shared-memory round
+constexpr int kTRows = 4;        // most rows per thread of the GEMV-T kernels (template R = 2 or 4; a CTA holds R * kCxThreads rows)
+constexpr int kTColGroup = 128;  // columns per shared-memory round
 constexpr int kCxWarps = kCxThreads / 32;
 
 struct TJob {
