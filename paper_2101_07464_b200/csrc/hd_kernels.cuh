@@ -1102,6 +1102,7 @@ constexpr int kSmallThreads = 1024;
 constexpr int kHalf = kSmallThreads / 2;
 
 struct SmallArgs {
+  int head_late = 0;  // k_small_gin: read head after griddepcontrol.wait (paired launch)
   const double* partials = nullptr;  // [slot][nblk] group partials
   int nblk = 0;
   double* scal = nullptr;
@@ -1680,8 +1681,11 @@ __device__ __forceinline__ void k_small_gin_impl(const SmallArgs& a) {
     for (int j = w; j < a.kB; j += kSmallThreads / 32)
       #pragma unroll 1
       for (int64_t i = lane; i < nr; i += 32) cp_async_elem(cs + j * nr + i, PB + paddr(i, j, a.chB.K));
-  #pragma unroll 1
-  for (int q = tid; q < a.nS; q += kSmallThreads) a.coefS[q] = a.head[q];
+  // head = p[0..off] of the fold pass: two launches old when the fold stage ran in between,
+  // the immediate predecessor's output when the two stages share a launch (head_late)
+  if (!a.head_late)
+    #pragma unroll 1
+    for (int q = tid; q < a.nS; q += kSmallThreads) a.coefS[q] = a.head[q];
   if (tid == 0) m.sc[0] = (a.pendB >= 0) ? a.chB.c[a.pendB] : 0.0;
   pdl_wait();
   if (!a.late_launch) pdl_launch();
@@ -1689,6 +1693,9 @@ __device__ __forceinline__ void k_small_gin_impl(const SmallArgs& a) {
     cp_async_wait_all();
     return;
   }
+  if (a.head_late)
+    #pragma unroll 1
+    for (int q = tid; q < a.nS; q += kSmallThreads) a.coefS[q] = a.head[q];
   st_stage(a.partials, (int64_t)a.nslots_in * a.nblk, ps, tid, kSmallThreads);
   cp_async_wait_all();
   __syncthreads();
@@ -1840,6 +1847,29 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_fold2(const __grid_cons
 template <typename T>
 __global__ void __launch_bounds__(kSmallThreads) k_small_fold2_b(const SmallArgs* __restrict__ argv) {
   k_small_fold2_impl<T>(argv[blockIdx.y]);
+}
+
+// The two single-CTA stages between the passes of a two-pass Ginibre probe in ONE
+// launch of two CTAs: CTA 0 the fold stage (chain F, the reflector scalars), CTA 1 the
+// output-side stage (chain O, the coefficients; its draw dots were taken a probe earlier).
+// They share no data: the fold stage touches chain F / scal / the fold pass's partials,
+// the output-side stage chain O / csp / head / beta1, beta3, coefS.
+struct SmallPair {
+  SmallArgs f, g;
+};
+template <typename T>
+__global__ void __launch_bounds__(kSmallThreads) k_small_fold2_gin(const __grid_constant__ SmallPair a) {
+  if (blockIdx.x == 0)
+    k_small_fold2_impl<T>(a.f);
+  else
+    k_small_gin_impl<T>(a.g);
+}
+template <typename T>
+__global__ void __launch_bounds__(kSmallThreads) k_small_fold2_gin_b(const SmallPair* __restrict__ argv) {
+  if (blockIdx.x == 0)
+    k_small_fold2_impl<T>(argv[blockIdx.y].f);
+  else
+    k_small_gin_impl<T>(argv[blockIdx.y].g);
 }
 
 // Normalize dynamics: inv = ||y|| > 0 ? 1/||y|| : 1 (bench.cpp:25-28).
