@@ -94,3 +94,27 @@ def test_poisoned_philox_deterministic(lm, ens):
         outs.append(torch.stack(tr))
     assert torch.isfinite(outs[0]).all()
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("ens,m,n,cap", [("haar", 0, 2311, 3), ("ginibre", 1500, 2100, 2), ("ginibre", 900, 640, 40)])
+def test_poisoned_complex_probe_sequences(orc, lm, ens, m, n, cap):
+    # the fused complex sequences (csrc/hd_complex_fused.cuh, hd_complex_gin.cuh): partial
+    # buffers, Gram matrices, speculative dots and panel growth under poisoned allocations
+    T, seed = 30, 23
+    rng = np.random.default_rng(seed)
+    sides = ["right" if rng.random() < 0.6 else "left" for _ in range(T)]
+    if ens == "haar":
+        ref = orc.COperator("haar", n=n, seed=seed)
+        op = lm.HaarOperator(n, seed=seed, dtype="c128", draws="injected", capacity=cap)
+        lens = [n] * T
+    else:
+        ref = orc.COperator("ginibre", m=m, n=n, sigma=0.8, seed=seed)
+        op = lm.GinibreOperator(m, n, 0.8, seed, dtype="c128", draws="injected", capacity=cap)
+        lens = [m if s == "right" else n for s in sides]
+    op.push_draws(orc.complex_draws_for(seed, lens).view(np.complex128))
+    aux = orc.RandomSource(seed + 1)
+    for t, s in enumerate(sides):
+        x = aux.normal_complex_vector(n if (s == "right" or ens == "haar") else m)
+        got = op.probe(x, s)
+        assert np.all(np.isfinite(got.view(np.float64))), t
+        assert rel(got, ref.probe(x, s)) < 1e-10, (t, s)
