@@ -1103,6 +1103,11 @@ constexpr int kHalf = kSmallThreads / 2;
 
 struct SmallArgs {
   int head_late = 0;  // k_small_gin: read head after griddepcontrol.wait (paired launch)
+  // k_small_dots: the normalize map's scalar of the previous step, inv = 1 / ||y||, is taken
+  // from this stage's own ||rhs||^2 slot (rhs = y) and published in scal[kScInv] instead
+  // of a k_small_norm launch (same rule and abort as k_small_norm_impl)
+  int norm_from_ss = 0;
+  int norm_step = 0;
   const double* partials = nullptr;  // [slot][nblk] group partials
   int nblk = 0;
   double* scal = nullptr;
@@ -1424,8 +1429,23 @@ __device__ __forceinline__ void k_small_dots_impl(const SmallArgs& a) {
     }
   }
   __syncthreads();
-  if (!HAAR && a.xscale) {  // two-pass Ginibre: x = y * xscale
-    const double xs = *a.xscale;
+  if (!HAAR && (a.xscale || a.norm_from_ss)) {  // two-pass Ginibre: x = y * xscale
+    double xs;
+    if (a.norm_from_ss) {
+      const double nrm = sqrt(m.sc[0]);
+      xs = nrm > 0.0 ? 1.0 / nrm : 1.0;
+      if (tid == 0) {
+        a.scal[kScInv] = xs;
+        if (!isfinite(xs)) {
+          atomicMin(a.status + kStBadStep, a.norm_step);
+          atomicOr(a.status + kStAbort, 1);
+        }
+      }
+      if (!isfinite(xs)) return;  // uniform: every thread reads the same sum
+    } else {
+      xs = *a.xscale;
+    }
+    __syncthreads();  // every thread has read m.sc[0] before it is rescaled
     #pragma unroll 1
     for (int t = tid; t < a.kA + a.kB + 1; t += kSmallThreads) {
       if (t < a.kA) aA[t] *= xs;

@@ -261,6 +261,11 @@ struct hd_op {
   int64_t pend_fdim = 0, pend_dim1 = 0;
   void* pend_traj_dev = nullptr;
   bool pend_final_deferred = false;  // device x_{T+1} copied out by hd_wait (two-pass runs)
+  // normalize runs on the two-pass Ginibre sequence: the previous step's 1 / ||y|| is left to
+  // the next probe's k_small_dots (flush_norm launches k_small_norm if that stage is not taken)
+  bool norm_defer = false;
+  const double* norm_parts = nullptr;
+  int norm_nblk = 0, norm_step = 0;
   cudaStream_t pend_stream = nullptr;
   unsigned long long* trace = nullptr;  // HD_TRACE=1: phase stamps of k_small_dots
   std::vector<double> trace_acc;        // accumulated phase durations (ns)
