@@ -823,16 +823,22 @@ struct DrawArgs {
   uint32_t stream = 0, probe = 0;
   int64_t rows = 0, gdelta = 0;
   double* out = nullptr;
+  // nprobe > 1: the draws of probes probe .. probe + nprobe - 1 in one launch (small
+  // operators keep a block of future draws: hd_gin2p_host.inc), `rows` apart in out
+  int nprobe = 1;
 };
 
 __device__ __forceinline__ void k_draw_fill_impl(const DrawArgs& a) {
   pdl_wait();
   pdl_launch();
   const uint64_t seed = *a.seedp;
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 2 * q < a.rows; q += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t half = a.rows / 2;  // rows is a multiple of the tile height
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < half * a.nprobe; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pi = (a.nprobe > 1) ? w / half : 0;
+    const int64_t q = w - pi * half;
     const int64_t i = 2 * q + a.gdelta;  // gdelta is even (tile-aligned)
-    const double2 v = philox_normal_pair(seed, a.stream, a.probe, (uint64_t)(i >> 1));
-    *reinterpret_cast<double2*>(a.out + 2 * q) = v;
+    const double2 v = philox_normal_pair(seed, a.stream, a.probe + (uint32_t)pi, (uint64_t)(i >> 1));
+    *reinterpret_cast<double2*>(a.out + pi * a.rows + 2 * q) = v;
   }
 }
 __global__ void __launch_bounds__(256) k_draw_fill(const __grid_constant__ DrawArgs a) { k_draw_fill_impl(a); }

@@ -108,6 +108,7 @@ struct PendingEv {
   double bytes;
   std::string note;
 };
+constexpr int kDrawBlock = 16;  // probes per block of the small-operator draw cache
 thread_local std::string g_prof_note;  // HD_PROF_LOG: shape of the next launch (launch_nt)
 
 // host-side counters, snapshotted per step so a failed probe / aborted run
@@ -204,6 +205,9 @@ struct hd_op {
   FlushBufs fbD, fbF, fbO;      // group partials / per-CTA scratch / tickets
   FlushBufs fbA[2], fbB;        // two-pass Ginibre: fold passes (ping-pong) and output passes
   double* drawbuf[2] = {nullptr, nullptr};  // two-pass Ginibre: device draws of a probe (io_len each)
+  // small square operators: two blocks of kDrawBlock future draws each, one k_draw_fill
+  // launch per block instead of one per probe (ensure_draw)
+  double* drawcache = nullptr;
   NtKnobs nt;                   // two-pass kernel shapes (HD_NT_* environment)
   int gin2p = 1;                // two-pass Ginibre / GOE runs: 1 auto, 2 forced (HD_GIN2P=1), 0 off (HD_GIN2P=0)
   size_t flush_slots = 0;       // slot capacity of the buffers above
@@ -484,6 +488,9 @@ void ensure_capacity(hd_op* op, int64_t nr, int64_t nl) {
   }
   if (op->ens != HD_HAAR && !op->drawbuf[0])  // two-pass Ginibre draw buffers (before any graph capture)
     for (double*& b : op->drawbuf) b = dmalloc<double>(std::max<int64_t>(op->io_len, 2));
+  if (op->ens != HD_HAAR && !op->drawcache && op->m == op->n && op->ex == nullptr && op->cfg.draw_mode == HD_DRAWS_PHILOX &&
+      op->io_len * 8 * 2 * kDrawBlock <= (int64_t(16) << 20))
+    op->drawcache = dmalloc<double>(2 * kDrawBlock * op->io_len);
   op->partials = op->fbD.partials;
   op->partsF = op->fbF.partials;
   op->partsO = op->fbO.partials;
